@@ -1,0 +1,347 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 RBD greedy loop (BASELINE.json metric: effective HBM
+GB/s = X bytes x greedy steps / time).
+
+One bench "step" = one full rbd::decompose of the workload (default C1, the
+BASELINE config the metric is quoted on). `value` is device-resident (X in
+HBM before the timed region); `e2e` goes through the reference-facing host
+entry (numpy X in pinned memory -> H2D -> loop -> D2H of Y and T).
+
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+For N > 1 launch under torchrun; C1 does not shard (replicas only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    p.add_argument("--workload", default="C1-image-like")
+    p.add_argument("--cpu-seconds", type=float, default=15.0)
+    p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    return p.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def peak_hbm():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic():
+    path = os.path.join(ROOT, "profiles", "sweep_traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
+def make_workload(name, device):
+    import torch
+    from paper_1503_05947_b200 import configs
+    w = configs.WORKLOADS[name]
+    if name.startswith("C1"):
+        Xd = configs.c1_matrix(n=w.n, seed=w.seed, device=device)
+    elif name.startswith("C0"):
+        Xh = configs.c0_matrix()
+        Xd = torch.as_tensor(Xh.T.copy(), device=device).t()
+    else:
+        rank = {"C2-tall": 1024, "C3-sharded": 2048, "C4-out-of-sample": 512}[name]
+        key = name.split("-")[0]
+        Xd = configs.low_rank_matrix_torch(w.m, w.n, rank, configs.spectrum(key, rank),
+                                           {"C2": 1e-8, "C3": 1e-10, "C4": 1e-6}[key], w.seed,
+                                           device=device)
+    torch.cuda.synchronize(device)
+    colmax = float(Xd.norm(dim=0).max())
+    return w, Xd, configs.eps_for(w, colmax)
+
+
+def cpu_baseline_sample(X_host, w, eps, seconds, nthreads):
+    """Oracle (restated reference path, two X passes per step) on the first
+    greedy steps of the same workload, bounded to ~`seconds` of CPU work."""
+    import oracle
+    t0 = time.perf_counter()
+    oracle.decompose(X_host, w.d_max, eps, nthreads=nthreads, max_steps=2)
+    per = max((time.perf_counter() - t0) / 2.0, 1e-4)
+    steps = int(max(2, min(w.d_max, seconds / per)))
+    t0 = time.perf_counter()
+    r = oracle.decompose(X_host, w.d_max, eps, nthreads=nthreads, max_steps=steps)
+    dt = time.perf_counter() - t0
+    return r.d, dt
+
+
+def run_reference(args):
+    rank, world, local = dist_env()
+    if rank != 0:
+        return
+    import torch
+    from paper_1503_05947_b200 import configs
+    w = configs.WORKLOADS[args.workload]
+    dev = torch.device("cuda", local) if torch.cuda.is_available() else torch.device("cpu")
+    _, Xd, eps = make_workload(args.workload, dev)
+    X = np.asfortranarray(Xd.cpu().numpy())
+    del Xd
+    cores = os.cpu_count() or 1
+    import oracle
+    # bounded sample per step: the first S greedy steps of the full workload
+    t0 = time.perf_counter()
+    oracle.decompose(X, w.d_max, eps, nthreads=cores, max_steps=2)
+    per = max((time.perf_counter() - t0) / 2.0, 1e-4)
+    S = int(max(2, min(w.d_max, 6.0 / per)))
+    for _ in range(args.warmup):
+        oracle.decompose(X, w.d_max, eps, nthreads=cores, max_steps=S)
+    t0 = time.perf_counter()
+    done = 0
+    for _ in range(args.steps):
+        r = oracle.decompose(X, w.d_max, eps, nthreads=cores, max_steps=S)
+        done += r.d
+    dt = time.perf_counter() - t0
+    bytes_per = w.m * w.n * 8
+    val = bytes_per * done / dt / 1e9
+    sample = f"first {S} greedy steps of {w.name} per bench step ({w.m}x{w.n} fp64)"
+    line = {
+        "impl": "reference", "metric": "rbd_effective_hbm_gbs", "value": val, "unit": "GB/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": w.name, "m": w.m, "n": w.n, "d_max": w.d_max, "eps_R": eps},
+        "cpu_baseline": {"value": val, "unit": "GB/s", "cores": cores, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": val, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_b200(args):
+    import torch
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    import paper_1503_05947_b200 as rbd
+    from paper_1503_05947_b200._lib import load_library
+    import ctypes as C
+
+    w, Xd, eps = make_workload(args.workload, dev)
+    ctx = rbd.Context(local)
+    lib = load_library()
+    m, n = Xd.shape
+    bytes_per_gstep = m * n * 8
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    for _ in range(max(args.warmup, 0)):
+        g = rbd.decompose(Xd, d_max=w.d_max, eps_r=eps, ctx=ctx)
+    stream = torch.cuda.ExternalStream(ctx.stream, device=dev)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    clocks = ClockSampler(local)
+    barrier()
+    torch.cuda.synchronize(dev)
+    clocks.start()
+    launches0 = ctx.launches
+    e0.record(stream)
+    ds = []
+    loop_ms = []
+    for _ in range(args.steps):
+        g = rbd.decompose(Xd, d_max=w.d_max, eps_r=eps, ctx=ctx)
+        ds.append(g.d)
+        loop_ms.append(g.result.loop_ms)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    barrier()
+    clk = clocks.stop()
+    launches = ctx.launches - launches0
+    ms = e0.elapsed_time(e1)
+    t_max = ms
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_max = float(t.item())
+    total_bytes = bytes_per_gstep * sum(ds) * world
+    value = total_bytes / (t_max / 1e3) / 1e9
+
+    # ---- roofline of the dominant kernel (fused sweep K2), CUDA events ----
+    y = torch.randn(m, dtype=torch.float64, device=dev)
+    y /= y.norm()
+    torch.cuda.synchronize(dev)
+    ms_sweep = C.c_double()
+    xc = Xd
+    from paper_1503_05947_b200._lib import check
+    check(lib.rbd_time_sweep(ctx.handle, C.c_void_p(xc.data_ptr()), m, n, xc.stride(1),
+                             C.c_void_p(y.data_ptr()), 20, C.byref(ms_sweep)))
+    peak, peak_src = peak_hbm()
+    ach = bytes_per_gstep / (ms_sweep.value / 1e3) / 1e9
+    traffic = ncu_traffic()
+    roofline = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+                "frac": ach / peak, "traffic": (traffic or {}).get("bytes_per_launch"),
+                "kernel": "k_sweep<2,MODE_DOT,stream> (K2 fused sweep)",
+                "algorithmic_bytes_per_launch": bytes_per_gstep,
+                "ms_per_launch": ms_sweep.value, "peak_source": peak_src,
+                "in_loop_share": None}
+    # share of the greedy loop spent in the sweep (for the ncu cross-check)
+    avg_loop = float(np.mean(loop_ms)) if loop_ms else None
+    if avg_loop:
+        roofline["in_loop_share"] = ms_sweep.value * float(np.mean(ds)) / avg_loop
+
+    # ---- e2e through the reference-facing host entry (pinned host X) ----
+    e2e = None
+    if not args.no_e2e:
+        Xh_t = torch.empty((n, m), dtype=torch.float64, pin_memory=True)
+        Xh_t.copy_(Xd.t())
+        Xh = Xh_t.numpy().T  # (m, n) Fortran view, pinned
+        assert Xh.flags["F_CONTIGUOUS"]
+        g2 = rbd.decompose(Xh, d_max=w.d_max, eps_r=eps, ctx=ctx)  # warm-up (buffers, graph)
+        barrier()
+        torch.cuda.synchronize(dev)
+        e0.record(stream)
+        t0 = time.perf_counter()
+        d2 = []
+        for _ in range(max(1, args.steps)):
+            g2 = rbd.decompose(Xh, d_max=w.d_max, eps_r=eps, ctx=ctx)
+            d2.append(g2.d)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        wall = time.perf_counter() - t0
+        ms2 = e0.elapsed_time(e1)
+        t2 = max(ms2, wall * 1e3)
+        if world > 1:
+            import torch.distributed as dist
+            t = torch.tensor([t2], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            t2 = float(t.item())
+        dmean = float(np.mean(d2))
+        e2e = {"value": bytes_per_gstep * sum(d2) * world / (t2 / 1e3) / 1e9, "unit": "GB/s",
+               "h2d_bytes_per_step": m * n * 8,
+               "d2h_bytes_per_step": int(8 * (m * dmean + dmean * n + 2 * dmean)),
+               "ms_per_step": t2 / len(d2), "entry": "rbd_decompose_host (numpy, pinned)"}
+
+    # ---- CPU baseline: oracle port, one thread, bounded sample (rank 0, N=1) ----
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        X_host = np.asfortranarray(Xd.cpu().numpy())
+        steps, dt = cpu_baseline_sample(X_host, w, eps, args.cpu_seconds, 1)
+        cpu = {"value": bytes_per_gstep * steps / dt / 1e9, "unit": "GB/s", "cores": 1,
+               "kind": "port",
+               "sample": f"first {steps} greedy steps of {w.name} ({m}x{n} fp64), single-thread "
+                         f"oracle restating decompose.cpp (two X passes per step), {dt:.1f}s"}
+
+    if rank == 0:
+        line = {
+            "metric": "rbd_effective_hbm_gbs", "value": value, "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": w.name, "m": m, "n": n, "d_max": w.d_max, "eps_R": eps,
+                       "d_reached": int(np.mean(ds)), "parallelism": f"replicas{world}",
+                       "l2": "inputs larger than L2 (X 627 MB vs 126 MB L2)",
+                       "describe": w.describe},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clk, "loop_ms_mean": float(np.mean(loop_ms)),
+            "d_per_step": ds,
+        }
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

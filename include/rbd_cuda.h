@@ -1,0 +1,169 @@
+/* rbd_cuda.h — C ABI of the B200-native RBD greedy loop (arXiv 1503.05947).
+ *
+ * This is the drop-in boundary under the reference's C++ API
+ * (proj/include/rbd/decompose.hpp:61-77, workspace.hpp:34-54). Every entry
+ * point takes plain pointers and sizes; no torch or Eigen types cross it.
+ * The C++ mirror of the reference API (include/rbd/*.hpp) and the Python
+ * package (paper_1503_05947_b200) are thin layers over these functions.
+ *
+ * Layouts (all fp64):
+ *   X      m x n column-major, leading dimension ldx >= m  (reference types.hpp:9-10)
+ *   Y      m x cap column-major, leading dimension m          (RbdModel::Y)
+ *   T      cap x n ROW-major: T[k*n + j] = row k of the reference's d x n T
+ *          (the reference writes T row-major in its model file, io.cpp:563-564)
+ * Device pointers are CUDA device addresses on the context's device; host
+ * pointers are ordinary (pageable or pinned) host memory.
+ *
+ * Errors: every function returns an rbd_status (0 = ok). The message of the
+ * last failure on the calling thread is returned by rbd_last_error(). Status
+ * codes map one-to-one onto the reference's rbd::Error subclasses
+ * (proj/include/rbd/errors.hpp:9-77).
+ *
+ * Threading: one rbd_ctx per host thread; calls on distinct contexts are
+ * reentrant. Results are deterministic: the same inputs and config give
+ * bit-identical Y, T, selected and history (test_decompose.cpp:128-137),
+ * including across 1/2/4/8 column shards (summation order depends on m only).
+ */
+#ifndef RBD_CUDA_H
+#define RBD_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RBD_ABI_VERSION 1
+
+typedef enum {
+  RBD_OK = 0,
+  RBD_ERR_INVALID_ARGUMENT = 1,   /* rbd::InvalidArgument   errors.hpp:62-65 */
+  RBD_ERR_INCOMPATIBLE_WEIGHT = 2,/* rbd::IncompatibleWeight errors.hpp:21-24 */
+  RBD_ERR_DEGENERATE_INPUT = 3,   /* rbd::DegenerateInput   errors.hpp:27-30 */
+  RBD_ERR_INDEX_OUT_OF_RANGE = 4, /* rbd::IndexOutOfRange   errors.hpp:39-42 */
+  RBD_ERR_DIMENSION_MISMATCH = 5, /* rbd::DimensionMismatch errors.hpp:15-18 */
+  RBD_ERR_NOT_POSITIVE = 6,       /* rbd::NotPositive       errors.hpp:33-36 */
+  RBD_ERR_NO_CONVERGENCE = 7,     /* rbd::NoConvergence     errors.hpp:45-48 */
+  RBD_ERR_CUDA = 100,             /* CUDA runtime failure (maps to rbd::Error) */
+  RBD_ERR_NCCL = 101,             /* NCCL failure (maps to rbd::Error) */
+  RBD_ERR_OUT_OF_MEMORY = 102     /* device allocation failure (maps to rbd::Error) */
+} rbd_status;
+
+typedef enum { RBD_START_FIXED_COLUMN = 0, RBD_START_SEEDED_RANDOM = 1 } rbd_start_kind;
+typedef enum { RBD_WEIGHT_IDENTITY = 0, RBD_WEIGHT_DIAGONAL = 1, RBD_WEIGHT_SPARSE_SPD = 2 } rbd_weight_kind;
+
+/* Mirrors rbd::RbdConfig + rbd::StartSpec (decompose.hpp:14-36). */
+typedef struct {
+  int64_t d_max;            /* 1 <= d_max <= n, checked at decompose time          */
+  double eps_R;             /* absolute stop tolerance on E_cur                    */
+  int32_t start_kind;       /* rbd_start_kind (default fixed column)               */
+  int32_t reorthogonalize;  /* force the second orthogonalisation pass             */
+  int64_t start_column;     /* fixed start column (default 0)                      */
+  uint64_t start_seed;      /* seed for RBD_START_SEEDED_RANDOM                    */
+  double breakdown_tol;     /* < 0: use eps_R (reference default -1.0)             */
+  int32_t weight_kind;      /* rbd_weight_kind; only IDENTITY runs on this path    */
+  int64_t weight_dim;       /* dimension of a non-identity weight (compat check)   */
+} rbd_config_t;
+
+typedef struct rbd_ctx_s* rbd_ctx_t;
+typedef struct rbd_ws_s* rbd_ws_t;
+
+/* Result counters of a decomposition (the rest goes to caller buffers). */
+typedef struct {
+  int64_t d;            /* accepted basis vectors (RbdModel::d)               */
+  int32_t breakdown;    /* 1 if the loop ended on an orthogonalisation breakdown */
+  int32_t reserved;
+  double breakdown_tol; /* effective breakdown tolerance (decompose.cpp:73-74) */
+  double max_col_norm;  /* max_j ||x_j|| (noise-floor input, decompose.cpp:70) */
+  double init_ms;       /* device time of the K1 init pass (CUDA events)      */
+  double loop_ms;       /* device time from the first greedy step to the stop  */
+  int64_t launches;     /* kernels launched by this call                       */
+} rbd_result_t;
+
+const char* rbd_last_error(void);
+int rbd_abi_version(void);
+void rbd_config_default(rbd_config_t* cfg);
+
+/* Context: owns the device, a stream, scratch buffers and captured graphs. */
+int rbd_ctx_create(int device, rbd_ctx_t* out);
+int rbd_ctx_destroy(rbd_ctx_t ctx);
+/* Use an external stream (e.g. torch's current stream); NULL = context stream. */
+int rbd_ctx_set_stream(rbd_ctx_t ctx, void* cuda_stream);
+/* Number of kernel launches issued by this context since creation (evidence). */
+int64_t rbd_ctx_launch_count(rbd_ctx_t ctx);
+int rbd_ctx_synchronize(rbd_ctx_t ctx);
+/* The cudaStream_t the context launches on (for event timing by callers). */
+void* rbd_ctx_stream(rbd_ctx_t ctx);
+
+/* rbd::decompose (decompose.cpp:53-111) on device-resident X.
+ * dY: m x d_max (ld m), dT: d_max x n row-major, both device buffers.
+ * h_selected / h_history: host arrays of length d_max. */
+int rbd_decompose_device(rbd_ctx_t ctx, const double* dX, int64_t m, int64_t n, int64_t ldx,
+                         const rbd_config_t* cfg, double* dY, double* dT, int64_t* h_selected,
+                         double* h_history, rbd_result_t* result);
+
+/* rbd::decompose with HOST buffers: X is uploaded, Y/T downloaded inside the
+ * call (the reference-facing, end-to-end entry). hY: m x d_max col-major,
+ * hT: d_max x n row-major (rows >= result->d are left untouched). */
+int rbd_decompose_host(rbd_ctx_t ctx, const double* hX, int64_t m, int64_t n, int64_t ldx,
+                       const rbd_config_t* cfg, double* hY, double* hT, int64_t* h_selected,
+                       double* h_history, rbd_result_t* result);
+
+/* rbd::mgs_project (decompose.cpp:12-33) on device vectors: orthonormalise dv
+ * against the k orthonormal columns of dB (ld ldb). On success *ok = 1 and
+ * dxi/norm hold the unit vector and pre-normalisation norm; *ok = 0 on
+ * breakdown (the reference's std::nullopt). */
+int rbd_mgs_project(rbd_ctx_t ctx, const double* dv, int64_t m, const double* dB, int64_t k,
+                    int64_t ldb, double breakdown_tol, int reorthogonalize, double* dxi,
+                    double* norm, int* ok);
+
+/* ErrorWorkspace, identity weight (workspace.hpp:18-54). The workspace keeps
+ * a pointer to dX (not owned, workspace.hpp:15-17) and up to cap T rows. */
+int rbd_ws_init(rbd_ctx_t ctx, const double* dX, int64_t m, int64_t n, int64_t ldx, int64_t cap,
+                rbd_ws_t* out);
+int rbd_ws_destroy(rbd_ws_t ws);
+int rbd_ws_extend(rbd_ws_t ws, const double* dxi);          /* workspace.cpp:43-60 */
+int rbd_ws_scan(rbd_ws_t ws, double* e_cur, int64_t* argmax); /* workspace.cpp:101-125 */
+int rbd_ws_error_sq(rbd_ws_t ws, int64_t j, const double* h_c, int64_t clen, double* out); /* :84-99 */
+int64_t rbd_ws_d(rbd_ws_t ws);
+int rbd_ws_read(rbd_ws_t ws, double* h_col_sq, double* h_residual_sq, double* h_yax /* d x n row-major */);
+
+/* Out-of-sample compression (decompose.cpp:113-117, batched) plus the
+ * identity error indicator err_j = max(||x_j||^2 - ||t_j||^2, 0) (Eq. 3,
+ * workspace.cpp:88-97). dY m x d (ld ldy), dXn m x N (ld ldx);
+ * dTn d x N column-major (ld d), d_err length N (may be NULL). */
+int rbd_project_batch(rbd_ctx_t ctx, const double* dY, int64_t m, int64_t d, int64_t ldy,
+                      const double* dXn, int64_t N, int64_t ldx, double* dTn, double* d_err);
+/* rbd::reconstruct (decompose.cpp:119-123): dv = Y c (dc length d). */
+int rbd_reconstruct(rbd_ctx_t ctx, const double* dY, int64_t m, int64_t d, int64_t ldy,
+                    const double* dc, double* dv);
+/* Host-buffer variants (upload, kernel, download inside the call). */
+int rbd_project_host(rbd_ctx_t ctx, const double* hY, int64_t m, int64_t d, const double* hXn,
+                     int64_t N, double* hTn, double* h_err);
+int rbd_reconstruct_host(rbd_ctx_t ctx, const double* hY, int64_t m, int64_t d,
+                         const double* hc, double* hv);
+
+/* Measurement hook: run the fused sweep kernel (K2) `reps` times back to back
+ * on dX with vector dy and return the mean device time per launch (CUDA
+ * events on the context stream). Used by bench.py for the roofline figure. */
+int rbd_time_sweep(rbd_ctx_t ctx, const double* dX, int64_t m, int64_t n, int64_t ldx,
+                   const double* dy, int reps, double* ms_per_launch);
+
+/* ---- multi-GPU (one process per GPU; X sharded by contiguous column blocks,
+ *      Y replicated) ---- */
+#define RBD_UNIQUE_ID_BYTES 128
+int rbd_comm_unique_id(char out[RBD_UNIQUE_ID_BYTES]);
+int rbd_ctx_init_comm(rbd_ctx_t ctx, int rank, int world, const char id[RBD_UNIQUE_ID_BYTES]);
+/* Sharded decompose: this rank owns global columns [col_offset, col_offset+n_local)
+ * of an m x n_global X. dT_local: d_max x n_local row-major. selected holds
+ * GLOBAL column indices; Y/selected/history are identical on every rank. */
+int rbd_decompose_sharded(rbd_ctx_t ctx, const double* dX_local, int64_t m, int64_t n_local,
+                          int64_t ldx, int64_t col_offset, int64_t n_global,
+                          const rbd_config_t* cfg, double* dY, double* dT_local,
+                          int64_t* h_selected, double* h_history, rbd_result_t* result);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RBD_CUDA_H */

@@ -1,0 +1,227 @@
+"""TEST INFRASTRUCTURE ONLY — the CPU oracle of the RBD greedy loop.
+
+ctypes wrapper over ``oracle/build/liborc.so`` (oracle/rbd_oracle.cpp, a
+plain-loop restatement of /root/reference/proj/src/decompose.cpp:12-125 and
+workspace.cpp:9-125, identity path). Only tests/, __graft_entry__.smoke() and
+bench.py's CPU-baseline legs may import this package; the product package
+never does.
+
+Parity pinning: the reference cannot be compiled here (Eigen 3.4 absent), so
+the restatement is pinned by the reference's own known-answer values and
+property tests, ported in tests/test_oracle_pins.py.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+from typing import List, Optional
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "build", "liborc.so")
+
+ORC_OK = 0
+ERRORS = {1: "InvalidArgument", 2: "IncompatibleWeight", 3: "DegenerateInput",
+          4: "IndexOutOfRange", 5: "DimensionMismatch"}
+
+
+class OracleError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{ERRORS.get(code, code)}: {msg}")
+        self.code = code
+        self.kind = ERRORS.get(code, str(code))
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            import subprocess
+            subprocess.run(["make", "-s", "-C", HERE], check=True)
+        L = C.CDLL(LIB_PATH)
+        P, I64, D, I = C.c_void_p, C.c_int64, C.c_double, C.c_int
+        L.orc_last_error.restype = C.c_char_p
+        L.orc_decompose_steps.argtypes = [P, I64, I64, I64, I64, D, I, I64, C.c_uint64, I, D, I, I64,
+                                          P, P, P, P, P]
+        L.orc_decompose_steps.restype = I
+        L.orc_mgs_project.argtypes = [P, I64, P, I64, I64, D, I, P, P]
+        L.orc_mgs_project.restype = I
+        L.orc_ws_init.argtypes = [P, I64, I64, I64]
+        L.orc_ws_init.restype = P
+        L.orc_ws_free.argtypes = [P]
+        L.orc_ws_extend.argtypes = [P, P]
+        L.orc_ws_d.argtypes = [P]
+        L.orc_ws_d.restype = I64
+        L.orc_ws_col_sq.argtypes = [P, P]
+        L.orc_ws_residual.argtypes = [P, P]
+        L.orc_ws_yax_row.argtypes = [P, I64, P]
+        L.orc_ws_error_sq.argtypes = [P, I64, P, I64, P]
+        L.orc_ws_error_sq.restype = I
+        L.orc_ws_scan.argtypes = [P, P, P]
+        L.orc_project.argtypes = [P, I64, I64, P, P]
+        L.orc_reconstruct.argtypes = [P, I64, I64, P, P]
+        L.orc_project_batch.argtypes = [P, I64, I64, P, I64, I64, I, P, P]
+        L.orc_random_matrix.argtypes = [I64, I64, C.c_uint64, P]
+        L.orc_random_low_rank.argtypes = [I64, I64, I64, C.c_uint64, P]
+        L.orc_gen_grid_matrix.argtypes = [I, I64, P]
+        L.orc_gen_grid_matrix.restype = I
+        L.orc_acceptance3_count.restype = I64
+        L.orc_seeded_start.argtypes = [C.c_uint64, I64]
+        L.orc_seeded_start.restype = I64
+        _lib = L
+    return _lib
+
+
+def _p(a: np.ndarray):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+@dataclass
+class OracleModel:
+    Y: np.ndarray                 # m x d
+    T: np.ndarray                 # d x n
+    selected: List[int]
+    residual_history: List[float]
+    d: int = 0
+
+
+def decompose(x, d_max: int, eps_r: float = 0.0, start_column: int = 0,
+              start_seed: Optional[int] = None, reorthogonalize: bool = False,
+              breakdown_tol: float = -1.0, nthreads: int = 1,
+              max_steps: Optional[int] = None) -> OracleModel:
+    """rbd::decompose restated (decompose.cpp:53-111)."""
+    xa = np.asfortranarray(np.asarray(x, dtype=np.float64))
+    m, n = xa.shape if xa.ndim == 2 else (0, 0)
+    cap = max(1, min(int(d_max), max(n, 1)))
+    Y = np.zeros((m, cap), order="F")
+    T = np.zeros((cap, max(n, 1)))
+    sel = np.zeros(cap, dtype=np.int64)
+    hist = np.zeros(cap)
+    d = C.c_int64(0)
+    rc = lib().orc_decompose_steps(
+        _p(xa), m, n, max(m, 1), int(d_max), float(eps_r), 1 if start_seed is not None else 0,
+        int(start_column), int(start_seed or 0) & 0xFFFFFFFFFFFFFFFF, 1 if reorthogonalize else 0,
+        float(breakdown_tol), int(nthreads), int(max_steps if max_steps is not None else 2**62),
+        _p(Y), _p(T), _p(sel), _p(hist), C.byref(d))
+    if rc != ORC_OK:
+        raise OracleError(rc, lib().orc_last_error().decode())
+    k = d.value
+    return OracleModel(Y[:, :k].copy(order="F"), T[:k, :n].copy(), [int(s) for s in sel[:k]],
+                       [float(h) for h in hist[:k]], k)
+
+
+def mgs_project(v, basis, breakdown_tol: float, reorthogonalize: bool = False):
+    v = np.ascontiguousarray(np.asarray(v, dtype=np.float64))
+    m = v.shape[0]
+    if basis is None or np.asarray(basis).size == 0:
+        B, k = np.zeros((m, 1), order="F"), 0
+    else:
+        B = np.asfortranarray(np.asarray(basis, dtype=np.float64))
+        k = B.shape[1]
+    xi = np.zeros(m)
+    nrm = C.c_double()
+    ok = lib().orc_mgs_project(_p(v), m, _p(B), k, m, float(breakdown_tol),
+                               1 if reorthogonalize else 0, _p(xi), C.byref(nrm))
+    if not ok:
+        return None
+    return xi, nrm.value
+
+
+class Workspace:
+    """ErrorWorkspace, identity weight (workspace.cpp:9-125)."""
+
+    def __init__(self, x):
+        self.x = np.asfortranarray(np.asarray(x, dtype=np.float64))
+        self.m, self.n = self.x.shape
+        self.h = lib().orc_ws_init(_p(self.x), self.m, self.n, self.m)
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().orc_ws_free(self.h)
+            self.h = None
+
+    @property
+    def d(self):
+        return lib().orc_ws_d(self.h)
+
+    def extend(self, xi):
+        xi = np.ascontiguousarray(np.asarray(xi, dtype=np.float64))
+        lib().orc_ws_extend(self.h, _p(xi))
+
+    def col_sq(self):
+        out = np.zeros(self.n)
+        lib().orc_ws_col_sq(self.h, _p(out))
+        return out
+
+    def residual(self):
+        out = np.zeros(self.n)
+        lib().orc_ws_residual(self.h, _p(out))
+        return out
+
+    def yax_row(self, k):
+        out = np.zeros(self.n)
+        lib().orc_ws_yax_row(self.h, int(k), _p(out))
+        return out
+
+    def error_sq(self, j, c):
+        c = np.ascontiguousarray(np.asarray(c, dtype=np.float64).reshape(-1))
+        out = C.c_double()
+        rc = lib().orc_ws_error_sq(self.h, int(j), _p(c) if c.size else None, c.shape[0],
+                                   C.byref(out))
+        if rc != ORC_OK:
+            raise OracleError(rc, lib().orc_last_error().decode())
+        return out.value
+
+    def scan(self):
+        e = C.c_double()
+        j = C.c_int64()
+        lib().orc_ws_scan(self.h, C.byref(e), C.byref(j))
+        return e.value, j.value
+
+
+def project_batch(Y, Xn, nthreads: int = 1):
+    Ya = np.asfortranarray(np.asarray(Y, dtype=np.float64))
+    Xa = np.asfortranarray(np.asarray(Xn, dtype=np.float64))
+    m, d = Ya.shape
+    N = Xa.shape[1]
+    Tn = np.zeros((d, N), order="F")
+    err = np.zeros(N)
+    lib().orc_project_batch(_p(Ya), m, d, _p(Xa), N, m, int(nthreads), _p(Tn), _p(err))
+    return Tn, err
+
+
+def random_matrix(m, n, seed):
+    """testutil::random_matrix (helpers.hpp:14-21), bit-identical draws."""
+    out = np.zeros((m, n), order="F")
+    lib().orc_random_matrix(m, n, int(seed), _p(out))
+    return out
+
+
+def random_low_rank(m, n, r, seed):
+    out = np.zeros((m, n), order="F")
+    lib().orc_random_low_rank(m, n, r, int(seed), _p(out))
+    return out
+
+
+GRID_FUNCS = {"rank1": 0, "rank2": 1, "rank3": 2, "composite": 3}
+
+
+def gen_grid_matrix(name: str, n_points: int = 101):
+    out = np.zeros((n_points, n_points), order="F")
+    rc = lib().orc_gen_grid_matrix(GRID_FUNCS[name], n_points, _p(out))
+    if rc != ORC_OK:
+        raise OracleError(rc, lib().orc_last_error().decode())
+    return out
+
+
+def acceptance3_count() -> int:
+    return int(lib().orc_acceptance3_count())
+
+
+def seeded_start(seed: int, n: int) -> int:
+    return int(lib().orc_seeded_start(int(seed) & 0xFFFFFFFFFFFFFFFF, int(n)))

@@ -1,0 +1,18 @@
+"""paper_1503_05947_b200 — B200-native Reduced Basis Decomposition greedy loop.
+
+A drop-in for the hot path of the reference (arXiv 1503.05947, proj/): the
+``decompose`` greedy loop and out-of-sample ``project``, executed by
+hand-written sm_100a CUDA kernels behind the C ABI ``include/rbd_cuda.h``.
+"""
+from ._lib import (CudaError, DegenerateInput, DimensionMismatch, IncompatibleWeight,
+                   IndexOutOfRange, InvalidArgument, NoConvergence, NotPositive, RbdError,
+                   Context, default_context, load_library)
+from .api import (Model, Workspace, decompose, make_config, mgs_project, project, project_batch,
+                  reconstruct)
+
+__all__ = [
+    "RbdError", "InvalidArgument", "IncompatibleWeight", "DegenerateInput", "IndexOutOfRange",
+    "DimensionMismatch", "NotPositive", "NoConvergence", "CudaError", "Context",
+    "default_context", "load_library", "Model", "Workspace", "decompose", "make_config",
+    "mgs_project", "project", "project_batch", "reconstruct",
+]

@@ -1,0 +1,345 @@
+"""Python mirror of the reference's RBD API (proj/python/bindings.cpp:41-178,
+proj/include/rbd/decompose.hpp:61-77, workspace.hpp:34-54), executed on B200
+through the C ABI (include/rbd_cuda.h).
+
+Host arrays (numpy) go through the reference-facing host entry points
+(upload -> CUDA loop -> download inside the call); torch CUDA tensors go
+through the device-resident entry points. There is no CPU compute path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Optional
+
+import numpy as np
+
+from . import _lib
+from ._lib import (Config, Context, DimensionMismatch, InvalidArgument, Result, check,
+                   default_config, default_context, load_library)
+
+try:  # torch is plumbing (device memory / streams); optional for host calls
+    import torch
+except Exception:  # pragma: no cover
+    torch = None
+
+
+def _is_torch_cuda(x) -> bool:
+    return torch is not None and isinstance(x, torch.Tensor) and x.is_cuda
+
+
+def _dp(a: np.ndarray):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def _col_major_np(x) -> np.ndarray:
+    return np.asfortranarray(np.asarray(x, dtype=np.float64))
+
+
+def _col_major_torch(x):
+    if x.dtype != torch.float64:
+        x = x.to(torch.float64)
+    if x.dim() != 2:
+        raise InvalidArgument("decompose: X must be a 2-D matrix")
+    m = x.shape[0]
+    if x.stride(0) == 1 and x.stride(1) >= max(m, 1):
+        return x, x.stride(1)
+    xc = x.t().contiguous().t()
+    return xc, m
+
+
+def make_config(d_max: int, eps_r: float = 0.0, start_column: int = 0,
+                reorthogonalize: bool = False, breakdown_tol: float = -1.0,
+                start_seed: Optional[int] = None, diag=None, sparse=None) -> Config:
+    """config_from_args (bindings.cpp:27-37) + RbdConfig defaults (decompose.hpp:25-36)."""
+    if diag is not None and sparse is not None:
+        raise InvalidArgument("pass at most one of diag and sparse")
+    cfg = default_config(int(d_max))
+    cfg.eps_R = float(eps_r)
+    cfg.reorthogonalize = 1 if reorthogonalize else 0
+    cfg.breakdown_tol = float(breakdown_tol)
+    if start_seed is not None:
+        cfg.start_kind = 1
+        cfg.start_seed = int(start_seed) & 0xFFFFFFFFFFFFFFFF
+    else:
+        cfg.start_kind = 0
+        cfg.start_column = int(start_column)
+    if diag is not None:
+        cfg.weight_kind = 1
+        cfg.weight_dim = int(np.asarray(diag).shape[0])
+    elif sparse is not None:
+        cfg.weight_kind = 2
+        cfg.weight_dim = int(sparse.shape[0])
+    return cfg
+
+
+class Model:
+    """RbdModel (decompose.hpp:39-46): X ~= Y T with Y'Y = I.
+
+    ``Y`` is m x d, ``T`` is d x n (numpy for host calls, torch CUDA tensors for
+    device calls); ``selected`` and ``residual_history`` are Python lists.
+    """
+
+    def __init__(self, Y, T, d, selected, residual_history, result: Result, ctx: Context):
+        self._Y = Y
+        self._T = T
+        self.d = int(d)
+        self.selected = list(int(s) for s in selected)
+        self.residual_history = list(float(h) for h in residual_history)
+        self.result = result
+        self._ctx = ctx
+
+    @property
+    def Y(self):
+        return self._Y[:, : self.d]
+
+    @property
+    def T(self):
+        return self._T[: self.d]
+
+    @property
+    def on_device(self) -> bool:
+        return _is_torch_cuda(self._Y)
+
+    def project(self, v):
+        """Reduced coordinates c = Y'v (decompose.cpp:113-117)."""
+        return project(self, v)
+
+    def reconstruct(self, c):
+        """Y c (decompose.cpp:119-123)."""
+        return reconstruct(self, c)
+
+    def compress(self):
+        """Y T (decompose.cpp:125)."""
+        if self.on_device:
+            return self.Y @ self.T
+        return self.Y @ self.T
+
+
+def decompose(x, d_max: int, eps_r: float = 0.0, diag=None, sparse=None, start_column: int = 0,
+              reorthogonalize: bool = False, breakdown_tol: float = -1.0,
+              start_seed: Optional[int] = None, ctx: Optional[Context] = None) -> Model:
+    """rbd.decompose (bindings.cpp:69-78) -> rbd::decompose (decompose.cpp:53-111).
+
+    numpy input: end-to-end host entry (rbd_decompose_host).
+    torch CUDA input: device-resident entry (rbd_decompose_device).
+    """
+    cfg = make_config(d_max, eps_r, start_column, reorthogonalize, breakdown_tol, start_seed,
+                      diag, sparse)
+    lib = load_library()
+    res = Result()
+    if _is_torch_cuda(x):
+        dev = x.device.index or 0
+        ctx = ctx or default_context(dev)
+        xc, ldx = _col_major_torch(x)
+        m, n = xc.shape
+        cap = max(1, min(int(d_max), n)) if n > 0 else 1
+        Y = torch.empty((cap, max(m, 1)), dtype=torch.float64, device=x.device).t()
+        T = torch.empty((cap, max(n, 1)), dtype=torch.float64, device=x.device)
+        sel = np.zeros(cap, dtype=np.int64)
+        hist = np.zeros(cap, dtype=np.float64)
+        torch.cuda.current_stream(x.device).synchronize()
+        check(lib.rbd_decompose_device(ctx.handle, C.c_void_p(xc.data_ptr()), m, n, ldx,
+                                       C.byref(cfg), C.c_void_p(Y.data_ptr()),
+                                       C.c_void_p(T.data_ptr()), _dp(sel), _dp(hist),
+                                       C.byref(res)))
+        d = res.d
+        return Model(Y, T, d, sel[:d], hist[:d], res, ctx)
+    ctx = ctx or default_context(0)
+    xa = _col_major_np(x)
+    if xa.ndim != 2:
+        raise InvalidArgument("decompose: X must be a 2-D matrix")
+    m, n = xa.shape
+    cap = max(1, min(int(d_max), n)) if n > 0 else 1
+    Y = np.zeros((m, cap), dtype=np.float64, order="F")
+    T = np.zeros((cap, n), dtype=np.float64)
+    sel = np.zeros(cap, dtype=np.int64)
+    hist = np.zeros(cap, dtype=np.float64)
+    check(lib.rbd_decompose_host(ctx.handle, _dp(xa), m, n, max(m, 1), C.byref(cfg), _dp(Y),
+                                 _dp(T), _dp(sel), _dp(hist), C.byref(res)))
+    d = res.d
+    return Model(Y, T, d, sel[:d], hist[:d], res, ctx)
+
+
+def project(model: Model, v):
+    """rbd::project (decompose.cpp:113-117): c = Y'v; DimensionMismatch if len(v) != m."""
+    lib = load_library()
+    ctx = model._ctx
+    if model.on_device:
+        vv = v if _is_torch_cuda(v) else torch.as_tensor(np.asarray(v, dtype=np.float64),
+                                                          device=model._Y.device)
+        vv = vv.reshape(-1).to(torch.float64).contiguous()
+        m = model._Y.shape[0]
+        if vv.numel() != m:
+            raise DimensionMismatch("project: vector length != m")
+        out = torch.empty(model.d, dtype=torch.float64, device=vv.device)
+        torch.cuda.current_stream(vv.device).synchronize()
+        check(lib.rbd_project_batch(ctx.handle, C.c_void_p(model._Y.data_ptr()), m, model.d,
+                                    model._Y.stride(1), C.c_void_p(vv.data_ptr()), 1, m,
+                                    C.c_void_p(out.data_ptr()), None))
+        ctx.synchronize()
+        return out
+    vv = np.ascontiguousarray(np.asarray(v, dtype=np.float64).reshape(-1))
+    Y = np.asfortranarray(model.Y)
+    m = Y.shape[0]
+    if vv.shape[0] != m:
+        raise DimensionMismatch("project: vector length != m")
+    out = np.zeros(model.d, dtype=np.float64)
+    check(lib.rbd_project_host(ctx.handle, _dp(Y), m, model.d, _dp(vv), 1, _dp(out), None))
+    return out
+
+
+def reconstruct(model: Model, c):
+    """rbd::reconstruct (decompose.cpp:119-123): Y c; DimensionMismatch if len(c) != d."""
+    lib = load_library()
+    ctx = model._ctx
+    if model.on_device:
+        cc = c if _is_torch_cuda(c) else torch.as_tensor(np.asarray(c, dtype=np.float64),
+                                                          device=model._Y.device)
+        cc = cc.reshape(-1).to(torch.float64).contiguous()
+        if cc.numel() != model.d:
+            raise DimensionMismatch("reconstruct: coefficient length != d")
+        m = model._Y.shape[0]
+        out = torch.empty(m, dtype=torch.float64, device=cc.device)
+        torch.cuda.current_stream(cc.device).synchronize()
+        check(lib.rbd_reconstruct(ctx.handle, C.c_void_p(model._Y.data_ptr()), m, model.d,
+                                  model._Y.stride(1), C.c_void_p(cc.data_ptr()),
+                                  C.c_void_p(out.data_ptr())))
+        ctx.synchronize()
+        return out
+    cc = np.ascontiguousarray(np.asarray(c, dtype=np.float64).reshape(-1))
+    if cc.shape[0] != model.d:
+        raise DimensionMismatch("reconstruct: coefficient length != d")
+    Y = np.asfortranarray(model.Y)
+    out = np.zeros(Y.shape[0], dtype=np.float64)
+    check(lib.rbd_reconstruct_host(ctx.handle, _dp(Y), Y.shape[0], model.d, _dp(cc), _dp(out)))
+    return out
+
+
+def project_batch(Y, Xn, with_error: bool = True, ctx: Optional[Context] = None):
+    """Batched out-of-sample compression: T_new = Y'X_new (d x N) and the identity
+    error indicator err_j = max(||x_j||^2 - ||t_j||^2, 0) (Eq. 3). Device tensors
+    (column-major views) or numpy arrays."""
+    lib = load_library()
+    if _is_torch_cuda(Y):
+        ctx = ctx or default_context(Y.device.index or 0)
+        Yc, ldy = _col_major_torch(Y)
+        Xc, ldx = _col_major_torch(Xn)
+        m, d = Yc.shape
+        if Xc.shape[0] != m:
+            raise DimensionMismatch("project: vector length != m")
+        N = Xc.shape[1]
+        Tn = torch.empty((N, d), dtype=torch.float64, device=Y.device).t()
+        err = torch.empty(N, dtype=torch.float64, device=Y.device) if with_error else None
+        torch.cuda.current_stream(Y.device).synchronize()
+        check(lib.rbd_project_batch(ctx.handle, C.c_void_p(Yc.data_ptr()), m, d, ldy,
+                                    C.c_void_p(Xc.data_ptr()), N, ldx, C.c_void_p(Tn.data_ptr()),
+                                    C.c_void_p(err.data_ptr()) if err is not None else None))
+        ctx.synchronize()
+        return Tn, err
+    ctx = ctx or default_context(0)
+    Ya = _col_major_np(Y)
+    Xa = _col_major_np(Xn)
+    m, d = Ya.shape
+    if Xa.shape[0] != m:
+        raise DimensionMismatch("project: vector length != m")
+    N = Xa.shape[1]
+    Tn = np.zeros((d, N), dtype=np.float64, order="F")
+    err = np.zeros(N, dtype=np.float64)
+    check(lib.rbd_project_host(ctx.handle, _dp(Ya), m, d, _dp(Xa), N, _dp(Tn),
+                               _dp(err) if with_error else None))
+    return Tn, (err if with_error else None)
+
+
+def mgs_project(v, basis, breakdown_tol: float, reorthogonalize: bool = False,
+                ctx: Optional[Context] = None):
+    """rbd::mgs_project (decompose.cpp:12-33) on device tensors.
+
+    Returns (xi, residual_norm) or None on breakdown (std::nullopt).
+    ``basis`` is an m x k column-major CUDA tensor (k may be 0)."""
+    if not _is_torch_cuda(v):
+        raise InvalidArgument("mgs_project: pass torch CUDA tensors (device entry point)")
+    lib = load_library()
+    ctx = ctx or default_context(v.device.index or 0)
+    vv = v.reshape(-1).to(torch.float64).contiguous()
+    m = vv.numel()
+    if basis is None or basis.numel() == 0:
+        k, ldb, bptr = 0, m, None
+    else:
+        B, ldb = _col_major_torch(basis)
+        if B.shape[0] != m:
+            raise DimensionMismatch("mgs_project: vector length != basis row count")
+        k, bptr = B.shape[1], C.c_void_p(B.data_ptr())
+    xi = torch.empty(m, dtype=torch.float64, device=v.device)
+    norm = C.c_double()
+    ok = C.c_int()
+    torch.cuda.current_stream(v.device).synchronize()
+    check(lib.rbd_mgs_project(ctx.handle, C.c_void_p(vv.data_ptr()), m, bptr, k, ldb,
+                              float(breakdown_tol), 1 if reorthogonalize else 0,
+                              C.c_void_p(xi.data_ptr()), C.byref(norm), C.byref(ok)))
+    if not ok.value:
+        return None
+    return xi, norm.value
+
+
+class Workspace:
+    """ErrorWorkspace (workspace.hpp:18-30), identity weight, on device.
+
+    workspace_init (workspace.cpp:9-41) at construction; extend(xi)
+    (workspace.cpp:43-60); scan() (workspace.cpp:101-125); error_sq(j, c)
+    (workspace.cpp:84-99)."""
+
+    def __init__(self, x, cap: Optional[int] = None, ctx: Optional[Context] = None):
+        if not _is_torch_cuda(x):
+            raise InvalidArgument("Workspace: pass a torch CUDA tensor")
+        self._lib = load_library()
+        self.ctx = ctx or default_context(x.device.index or 0)
+        self._x, ldx = _col_major_torch(x)
+        self.m, self.n = self._x.shape
+        cap = cap if cap is not None else self.n
+        h = C.c_void_p()
+        torch.cuda.current_stream(x.device).synchronize()
+        check(self._lib.rbd_ws_init(self.ctx.handle, C.c_void_p(self._x.data_ptr()), self.m,
+                                    self.n, ldx, cap, C.byref(h)))
+        self.handle = h
+
+    def close(self):
+        if getattr(self, "handle", None):
+            self._lib.rbd_ws_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def d(self) -> int:
+        return int(self._lib.rbd_ws_d(self.handle))
+
+    def extend(self, xi):
+        xv = xi.reshape(-1).to(torch.float64).contiguous()
+        if xv.numel() != self.m:
+            raise DimensionMismatch("workspace_extend: dimensions changed since init")
+        torch.cuda.current_stream(xv.device).synchronize()
+        check(self._lib.rbd_ws_extend(self.handle, C.c_void_p(xv.data_ptr())))
+
+    def scan(self):
+        e = C.c_double()
+        j = C.c_int64()
+        check(self._lib.rbd_ws_scan(self.handle, C.byref(e), C.byref(j)))
+        return e.value, j.value
+
+    def error_sq(self, j: int, c) -> float:
+        cc = np.ascontiguousarray(np.asarray(c, dtype=np.float64).reshape(-1))
+        out = C.c_double()
+        check(self._lib.rbd_ws_error_sq(self.handle, int(j), _dp(cc) if cc.size else None,
+                                        cc.shape[0], C.byref(out)))
+        return out.value
+
+    def read(self):
+        col_sq = np.zeros(self.n)
+        resid = np.zeros(self.n)
+        yax = np.zeros((max(self.d, 1), self.n))
+        check(self._lib.rbd_ws_read(self.handle, _dp(col_sq), _dp(resid), _dp(yax)))
+        return col_sq, resid, yax[: self.d]

@@ -1,0 +1,1008 @@
+// rbd_capi.cu — host runtime of the B200 RBD path behind the C ABI in
+// include/rbd_cuda.h: context, scratch management, the CUDA-graph-captured
+// greedy step loop, the workspace API and out-of-sample projection.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "rbd_cuda.h"
+#include "rbd_device.cuh"
+#include "rbd_project.cuh"
+
+using namespace rbdk;
+
+void rbd_comm_release(rbd_ctx_t ctx);
+
+namespace {
+
+thread_local std::string g_err;
+
+int set_err(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CU(call)                                                                          \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      return set_err(e_ == cudaErrorMemoryAllocation ? RBD_ERR_OUT_OF_MEMORY : RBD_ERR_CUDA, \
+                     std::string(#call) + ": " + cudaGetErrorString(e_));                 \
+  } while (0)
+
+#define TRY(expr)            \
+  do {                       \
+    int s_ = (expr);         \
+    if (s_ != RBD_OK) return s_; \
+  } while (0)
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+
+int ensure(DevBuf& b, size_t bytes) {
+  if (bytes == 0) bytes = 16;
+  if (b.bytes >= bytes) return RBD_OK;
+  if (b.p) cudaFree(b.p);
+  b.p = nullptr;
+  b.bytes = 0;
+  cudaError_t e = cudaMalloc(&b.p, bytes);
+  if (e != cudaSuccess)
+    return set_err(RBD_ERR_OUT_OF_MEMORY, std::string("cudaMalloc(") + std::to_string(bytes) +
+                                              "): " + cudaGetErrorString(e));
+  b.bytes = bytes;
+  return RBD_OK;
+}
+
+void release(DevBuf& b) {
+  if (b.p) cudaFree(b.p);
+  b.p = nullptr;
+  b.bytes = 0;
+}
+
+template <typename T>
+T* ptr(DevBuf& b) {
+  return static_cast<T*>(b.p);
+}
+
+long long cdiv(long long a, long long b) { return (a + b - 1) / b; }
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+struct GraphKey {
+  const void* X = nullptr;
+  const void* Y = nullptr;
+  const void* T = nullptr;
+  long long m = 0, n = 0, ldx = 0, d_max = 0;
+  const void* bufs[8] = {};
+  cudaStream_t stream = nullptr;
+  int steps = 0;
+  bool operator==(const GraphKey& o) const {
+    if (X != o.X || Y != o.Y || T != o.T || m != o.m || n != o.n || ldx != o.ldx ||
+        d_max != o.d_max || stream != o.stream || steps != o.steps)
+      return false;
+    for (int i = 0; i < 8; ++i)
+      if (bufs[i] != o.bufs[i]) return false;
+    return true;
+  }
+};
+
+}  // namespace
+
+struct rbd_ctx_s {
+  int device = 0;
+  int nsm = 148;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;
+  DevBuf partial, rec, counter, state, colsq, resid, w, c, p, nrm, hist, sel, out_rec, scratch1;
+  DevBuf hX, hY, hT;  // cached device copies for the host entry
+  DevState* h_state = nullptr;  // pinned
+  Rec* h_rec = nullptr;         // pinned
+  cudaGraphExec_t gexec = nullptr;
+  GraphKey gkey;
+  long long graph_nodes = 0;
+  long long launches = 0;
+  int occ_sweep2 = 2, occ_sweep1 = 2;
+  // multi-GPU
+  void* comm = nullptr;
+  int rank = 0, world = 1;
+};
+
+struct rbd_ws_s {
+  rbd_ctx_t ctx;
+  const double* X;
+  long long m, n, ldx, cap, d;
+  DevBuf T, colsq, resid, partial, rec, counter, out, tmp;
+};
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// Launch helpers (each increments the context's launch counter)
+// ---------------------------------------------------------------------------
+int sweep_grid(rbd_ctx_t ctx, long long m, long long ncols_max, int vec) {
+  const long long tiles = cdiv(m, kChunk) * cdiv(std::max<long long>(ncols_max, 1), kCols);
+  const long long cap = (long long)ctx->nsm * (vec == 2 ? ctx->occ_sweep2 : ctx->occ_sweep1);
+  return (int)std::max<long long>(1, std::min(tiles, cap));
+}
+
+int launch_sweep(rbd_ctx_t ctx, const SweepArgs& a, int vec, int mode, bool stream_a,
+                 long long ncols_max) {
+  const int grid = sweep_grid(ctx, a.m, ncols_max, vec);
+  if (vec == 2) {
+    if (mode == MODE_INIT)
+      k_sweep<2, MODE_INIT, true><<<grid, kThreads, 0, ctx->stream>>>(a);
+    else if (stream_a)
+      k_sweep<2, MODE_DOT, true><<<grid, kThreads, 0, ctx->stream>>>(a);
+    else
+      k_sweep<2, MODE_DOT, false><<<grid, kThreads, 0, ctx->stream>>>(a);
+  } else {
+    if (mode == MODE_INIT)
+      k_sweep<1, MODE_INIT, true><<<grid, kThreads, 0, ctx->stream>>>(a);
+    else if (stream_a)
+      k_sweep<1, MODE_DOT, true><<<grid, kThreads, 0, ctx->stream>>>(a);
+    else
+      k_sweep<1, MODE_DOT, false><<<grid, kThreads, 0, ctx->stream>>>(a);
+  }
+  ctx->launches++;
+  CU(cudaGetLastError());
+  return RBD_OK;
+}
+
+int finalize_grid(rbd_ctx_t ctx, long long n) {
+  return (int)std::max<long long>(1, std::min<long long>(cdiv(n, kThreads), (long long)ctx->nsm * 4));
+}
+
+long long gemv_grid(long long m) { return cdiv(m, kGemvRows); }
+
+// ---------------------------------------------------------------------------
+// K1: init pass over X (col_sq, residual, flags, max col_sq)
+// ---------------------------------------------------------------------------
+int enqueue_init(rbd_ctx_t ctx, const double* X, long long m, long long n, long long ldx,
+                 double* partial, double* colsq, double* resid, DevState* st) {
+  const int vec = (ldx % 2 == 0 && aligned16(X)) ? 2 : 1;
+  SweepArgs a{};
+  a.A = X;
+  a.lda = ldx;
+  a.m = m;
+  a.ncols = n;
+  a.partial = partial;
+  a.pstride = n;
+  a.st = st;
+  a.gate = GATE_NONE;
+  TRY(launch_sweep(ctx, a, vec, MODE_INIT, true, n));
+  const int g = (int)std::max<long long>(1, std::min<long long>(cdiv(n, 256), 1024));
+  k_init_finish<<<g, 256, 0, ctx->stream>>>(partial, cdiv(m, kChunk), n, colsq, resid, st);
+  ctx->launches++;
+  CU(cudaGetLastError());
+  return RBD_OK;
+}
+
+// ---------------------------------------------------------------------------
+// One extension (K4) on device state: x from X[:, st->jlocal] (or v), first
+// coefficients c, basis B = Y[:, 0:st->d] (ld m); result y written to
+// ybase + (use_d ? st->d*m : 0).
+// ---------------------------------------------------------------------------
+struct ExtBufs {
+  const double* B;
+  long long m;
+  long long dcap;       // max basis size (grid sizing of the reorth sweep)
+  const double* X;
+  long long ldx;
+  const double* v;
+  const double* c;
+  double* w;
+  double* p;
+  double* nrm;
+  double* partial;      // >= S * dcap doubles
+  double* ybase;
+  int use_d;
+  long long* selected;
+  DevState* st;
+};
+
+int enqueue_extension(rbd_ctx_t ctx, const ExtBufs& b) {
+  const long long gb = gemv_grid(b.m);
+  ExtArgs e{};
+  e.B = b.B;
+  e.ldb = b.m;
+  e.m = b.m;
+  e.X = b.X;
+  e.ldx = b.ldx;
+  e.v = b.v;
+  e.c = b.c;
+  e.w = b.w;
+  e.nrm_part = b.nrm;
+  e.st = b.st;
+  e.gate = GATE_LIVE;
+  e.pass = 1;
+  k_ext_gemv_n<<<(unsigned)gb, kThreads, 0, ctx->stream>>>(e);
+  ctx->launches++;
+  k_ext_decide<<<1, kThreads, 0, ctx->stream>>>(b.nrm, gb, b.st);
+  ctx->launches++;
+  // reorth pass: p = B' w (chunked dots over the basis columns), w -= B p
+  const int vec = (b.m % 2 == 0 && aligned16(b.B) && aligned16(b.w)) ? 2 : 1;
+  SweepArgs s{};
+  s.A = b.B;
+  s.lda = b.m;
+  s.m = b.m;
+  s.ncols = b.dcap;
+  s.v = b.w;
+  s.partial = b.partial;
+  s.pstride = b.dcap;
+  s.st = b.st;
+  s.gate = GATE_REORTH;
+  s.csel = 1;
+  TRY(launch_sweep(ctx, s, vec, MODE_DOT, false, b.dcap));
+  k_coef_combine<<<(unsigned)std::max<long long>(1, cdiv(b.dcap, 256)), 256, 0, ctx->stream>>>(
+      b.partial, cdiv(b.m, kChunk), b.dcap, b.p, b.st, GATE_REORTH);
+  ctx->launches++;
+  e.c = b.p;
+  e.gate = GATE_REORTH;
+  e.pass = 2;
+  k_ext_gemv_n<<<(unsigned)gb, kThreads, 0, ctx->stream>>>(e);
+  ctx->launches++;
+  k_ext_finish<<<1, kThreads, 0, ctx->stream>>>(b.nrm, gb, b.st, b.selected);
+  ctx->launches++;
+  const int ng = (int)std::max<long long>(1, std::min<long long>(cdiv(b.m, 256), (long long)ctx->nsm * 8));
+  k_normalize<<<ng, 256, 0, ctx->stream>>>(b.w, b.ybase, b.m, b.m, b.st, b.use_d);
+  ctx->launches++;
+  CU(cudaGetLastError());
+  return RBD_OK;
+}
+
+struct LoopBufs {
+  const double* X;
+  long long m, n, ldx, d_max;
+  double* Y;
+  double* T;
+};
+
+// One greedy step: extension (K4) + fused sweep (K2) + finalize/argmax (K3).
+int enqueue_step(rbd_ctx_t ctx, const LoopBufs& L) {
+  DevState* st = ptr<DevState>(ctx->state);
+  ExtBufs b{};
+  b.B = L.Y;
+  b.m = L.m;
+  b.dcap = L.d_max;
+  b.X = L.X;
+  b.ldx = L.ldx;
+  b.c = ptr<double>(ctx->c);
+  b.w = ptr<double>(ctx->w);
+  b.p = ptr<double>(ctx->p);
+  b.nrm = ptr<double>(ctx->nrm);
+  b.partial = ptr<double>(ctx->partial);
+  b.ybase = L.Y;
+  b.use_d = 1;
+  b.selected = ptr<long long>(ctx->sel);
+  b.st = st;
+  TRY(enqueue_extension(ctx, b));
+
+  const int vec = (L.ldx % 2 == 0 && L.m % 2 == 0 && aligned16(L.X) && aligned16(L.Y)) ? 2 : 1;
+  SweepArgs s{};
+  s.A = L.X;
+  s.lda = L.ldx;
+  s.m = L.m;
+  s.ncols = L.n;
+  s.vbase = L.Y;
+  s.vstride = L.m;
+  s.vsel = 1;
+  s.partial = ptr<double>(ctx->partial);
+  s.pstride = L.n;
+  s.st = st;
+  s.gate = GATE_LIVE;
+  TRY(launch_sweep(ctx, s, vec, MODE_DOT, true, L.n));
+
+  FinalizeArgs f{};
+  f.partial = ptr<double>(ctx->partial);
+  f.S = cdiv(L.m, kChunk);
+  f.n = L.n;
+  f.T = L.T;
+  f.r = ptr<double>(ctx->resid);
+  f.col_sq = ptr<double>(ctx->colsq);
+  f.st = st;
+  f.rec = ptr<Rec>(ctx->rec);
+  f.counter = ptr<unsigned>(ctx->counter);
+  f.history = ptr<double>(ctx->hist);
+  f.cbuf = ptr<double>(ctx->c);
+  f.mode = 0;
+  k_finalize<<<finalize_grid(ctx, L.n), kThreads, 0, ctx->stream>>>(f);
+  ctx->launches++;
+  CU(cudaGetLastError());
+  return RBD_OK;
+}
+
+int ensure_loop_buffers(rbd_ctx_t ctx, long long m, long long n, long long d_max) {
+  const long long S = cdiv(m, kChunk);
+  TRY(ensure(ctx->partial, sizeof(double) * S * std::max(n, d_max)));
+  TRY(ensure(ctx->rec, sizeof(Rec) * (size_t)ctx->nsm * 8));
+  TRY(ensure(ctx->counter, 64));
+  TRY(ensure(ctx->state, sizeof(DevState)));
+  TRY(ensure(ctx->colsq, sizeof(double) * n));
+  TRY(ensure(ctx->resid, sizeof(double) * n));
+  TRY(ensure(ctx->w, sizeof(double) * m));
+  TRY(ensure(ctx->c, sizeof(double) * (d_max + 1)));
+  TRY(ensure(ctx->p, sizeof(double) * (d_max + 1)));
+  TRY(ensure(ctx->nrm, sizeof(double) * gemv_grid(m)));
+  TRY(ensure(ctx->hist, sizeof(double) * d_max));
+  TRY(ensure(ctx->sel, sizeof(long long) * d_max));
+  TRY(ensure(ctx->out_rec, sizeof(Rec) * 16));
+  return RBD_OK;
+}
+
+constexpr int kGraphSteps = 8;
+
+int get_step_graph(rbd_ctx_t ctx, const LoopBufs& L) {
+  GraphKey k;
+  k.X = L.X;
+  k.Y = L.Y;
+  k.T = L.T;
+  k.m = L.m;
+  k.n = L.n;
+  k.ldx = L.ldx;
+  k.d_max = L.d_max;
+  k.stream = ctx->stream;
+  k.steps = kGraphSteps;
+  DevBuf* bl[8] = {&ctx->partial, &ctx->rec, &ctx->state, &ctx->colsq,
+                   &ctx->resid,   &ctx->w,   &ctx->c,     &ctx->nrm};
+  for (int i = 0; i < 8; ++i) k.bufs[i] = bl[i]->p;
+  if (ctx->gexec && ctx->gkey == k) return RBD_OK;
+  if (ctx->gexec) {
+    cudaGraphExecDestroy(ctx->gexec);
+    ctx->gexec = nullptr;
+  }
+  const long long before = ctx->launches;
+  CU(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+  int rc = RBD_OK;
+  for (int s = 0; s < kGraphSteps && rc == RBD_OK; ++s) rc = enqueue_step(ctx, L);
+  cudaGraph_t g = nullptr;
+  cudaError_t ec = cudaStreamEndCapture(ctx->stream, &g);
+  ctx->launches = before;  // captured launches are counted per replay
+  if (rc != RBD_OK) {
+    if (g) cudaGraphDestroy(g);
+    return rc;
+  }
+  if (ec != cudaSuccess) return set_err(RBD_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(ec));
+  size_t nn = 0;
+  cudaGraphGetNodes(g, nullptr, &nn);
+  ctx->graph_nodes = (long long)nn;
+  cudaError_t ei = cudaGraphInstantiate(&ctx->gexec, g, 0);
+  cudaGraphDestroy(g);
+  if (ei != cudaSuccess) return set_err(RBD_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(ei));
+  ctx->gkey = k;
+  return RBD_OK;
+}
+
+// Validation shared by the single- and multi-GPU entries: reference order of
+// decompose.cpp:56-64 after the K1 flags are known.
+int validate_after_init(const rbd_config_t* cfg, long long m, long long n, const DevState& hs) {
+  if (hs.flags_nonfinite)
+    return set_err(RBD_ERR_INVALID_ARGUMENT, "decompose: matrix has non-finite entries");
+  if (cfg->d_max < 1 || cfg->d_max > n)
+    return set_err(RBD_ERR_INVALID_ARGUMENT, "decompose: d_max must satisfy 1 <= d_max <= n");
+  if (!(cfg->eps_R >= 0.0)) return set_err(RBD_ERR_INVALID_ARGUMENT, "decompose: eps_R must be >= 0");
+  if (cfg->weight_kind != RBD_WEIGHT_IDENTITY) {
+    if (cfg->weight_dim != 0 && cfg->weight_dim != m)
+      return set_err(RBD_ERR_INCOMPATIBLE_WEIGHT, "decompose: weight dimension != m");
+    return set_err(RBD_ERR_INVALID_ARGUMENT,
+                   "decompose: only the identity weight runs on the B200 path (diagonal/SPD "
+                   "weights are out of scope, SURVEY.md §8(f1))");
+  }
+  if (!hs.flags_nonzero)
+    return set_err(RBD_ERR_DEGENERATE_INPUT, "decompose: zero matrix, no basis can be built");
+  return RBD_OK;
+}
+
+int start_column(const rbd_config_t* cfg, long long n, long long* out) {
+  // decompose.cpp:37-49
+  if (cfg->start_kind == RBD_START_FIXED_COLUMN) {
+    if (cfg->start_column < 0 || cfg->start_column >= n)
+      return set_err(RBD_ERR_INDEX_OUT_OF_RANGE, "start column index out of range");
+    *out = cfg->start_column;
+  } else {
+    std::mt19937_64 rng(cfg->start_seed);
+    *out = (long long)std::uniform_int_distribution<long>(0, (long)n - 1)(rng);
+  }
+  return RBD_OK;
+}
+
+double breakdown_tolerance(const rbd_config_t* cfg, long long m, double max_colsq) {
+  // decompose.cpp:70-74
+  const double max_col_norm = std::sqrt(max_colsq);
+  const double noise_floor = max_col_norm * std::sqrt(static_cast<double>(m)) *
+                             std::numeric_limits<double>::epsilon() * 16.0;
+  return std::max(cfg->breakdown_tol < 0.0 ? cfg->eps_R : cfg->breakdown_tol, noise_floor);
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+const char* rbd_last_error(void) { return g_err.c_str(); }
+int rbd_abi_version(void) { return RBD_ABI_VERSION; }
+
+void rbd_config_default(rbd_config_t* cfg) {
+  std::memset(cfg, 0, sizeof(*cfg));
+  cfg->d_max = 1;             // decompose.hpp:26
+  cfg->eps_R = 0.0;           // :27
+  cfg->start_kind = RBD_START_FIXED_COLUMN;
+  cfg->start_column = 0;      // :28
+  cfg->reorthogonalize = 0;   // :30
+  cfg->breakdown_tol = -1.0;  // :35
+  cfg->weight_kind = RBD_WEIGHT_IDENTITY;
+}
+
+int rbd_ctx_create(int device, rbd_ctx_t* out) {
+  if (!out) return set_err(RBD_ERR_INVALID_ARGUMENT, "rbd_ctx_create: null output");
+  int ndev = 0;
+  CU(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev)
+    return set_err(RBD_ERR_INVALID_ARGUMENT, "rbd_ctx_create: no such CUDA device");
+  CU(cudaSetDevice(device));
+  auto* ctx = new rbd_ctx_s();
+  ctx->device = device;
+  cudaDeviceGetAttribute(&ctx->nsm, cudaDevAttrMultiProcessorCount, device);
+  cudaError_t e = cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    delete ctx;
+    return set_err(RBD_ERR_CUDA, std::string("stream create: ") + cudaGetErrorString(e));
+  }
+  ctx->stream = ctx->own_stream;
+  cudaMallocHost(&ctx->h_state, sizeof(DevState));
+  cudaMallocHost(&ctx->h_rec, sizeof(Rec) * 4);
+  int o = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_sweep<2, MODE_DOT, true>, kThreads, 0) ==
+          cudaSuccess && o > 0)
+    ctx->occ_sweep2 = o;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_sweep<1, MODE_DOT, true>, kThreads, 0) ==
+          cudaSuccess && o > 0)
+    ctx->occ_sweep1 = o;
+  *out = ctx;
+  return RBD_OK;
+}
+
+int rbd_ctx_destroy(rbd_ctx_t ctx) {
+  if (!ctx) return RBD_OK;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
+  DevBuf* bl[] = {&ctx->partial, &ctx->rec,  &ctx->counter, &ctx->state, &ctx->colsq,
+                  &ctx->resid,   &ctx->w,    &ctx->c,       &ctx->p,     &ctx->nrm,
+                  &ctx->hist,    &ctx->sel,  &ctx->out_rec, &ctx->scratch1,
+                  &ctx->hX,      &ctx->hY,   &ctx->hT};
+  for (DevBuf* b : bl) release(*b);
+  if (ctx->h_state) cudaFreeHost(ctx->h_state);
+  if (ctx->h_rec) cudaFreeHost(ctx->h_rec);
+  if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+  rbd_comm_release(ctx);
+  delete ctx;
+  return RBD_OK;
+}
+
+int rbd_ctx_set_stream(rbd_ctx_t ctx, void* s) {
+  if (!ctx) return set_err(RBD_ERR_INVALID_ARGUMENT, "null context");
+  ctx->stream = s ? static_cast<cudaStream_t>(s) : ctx->own_stream;
+  return RBD_OK;
+}
+
+int64_t rbd_ctx_launch_count(rbd_ctx_t ctx) { return ctx ? ctx->launches : 0; }
+
+int rbd_ctx_synchronize(rbd_ctx_t ctx) {
+  CU(cudaStreamSynchronize(ctx->stream));
+  return RBD_OK;
+}
+
+void* rbd_ctx_stream(rbd_ctx_t ctx) { return ctx ? (void*)ctx->stream : nullptr; }
+
+int rbd_decompose_device(rbd_ctx_t ctx, const double* dX, int64_t m, int64_t n, int64_t ldx,
+                         const rbd_config_t* cfg, double* dY, double* dT, int64_t* h_selected,
+                         double* h_history, rbd_result_t* result) {
+  if (!ctx || !cfg) return set_err(RBD_ERR_INVALID_ARGUMENT, "decompose: null context/config");
+  if (m < 1 || n < 1) return set_err(RBD_ERR_INVALID_ARGUMENT, "decompose: matrix must be non-empty");
+  if (ldx < m) return set_err(RBD_ERR_DIMENSION_MISMATCH, "decompose: ldx < m");
+  CU(cudaSetDevice(ctx->device));
+  const long long d_cap = std::max<long long>(1, std::min<long long>(cfg->d_max, n));
+  TRY(ensure_loop_buffers(ctx, m, n, d_cap));
+  DevState* st = ptr<DevState>(ctx->state);
+
+  const long long launches0 = ctx->launches;
+  cudaEvent_t ev0, ev1, ev2;
+  CU(cudaEventCreate(&ev0));
+  CU(cudaEventCreate(&ev1));
+  CU(cudaEventCreate(&ev2));
+  struct EvGuard {
+    cudaEvent_t a, b, c;
+    ~EvGuard() {
+      cudaEventDestroy(a);
+      cudaEventDestroy(b);
+      cudaEventDestroy(c);
+    }
+  } evg{ev0, ev1, ev2};
+  // ---- K1 ----
+  CU(cudaMemsetAsync(st, 0, sizeof(DevState), ctx->stream));
+  CU(cudaEventRecord(ev0, ctx->stream));
+  TRY(enqueue_init(ctx, dX, m, n, ldx, ptr<double>(ctx->partial), ptr<double>(ctx->colsq),
+                   ptr<double>(ctx->resid), st));
+  CU(cudaEventRecord(ev1, ctx->stream));
+  CU(cudaMemsetAsync(ctx->counter.p, 0, 64, ctx->stream));
+  CU(cudaMemcpyAsync(ctx->h_state, st, sizeof(DevState), cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  DevState hs = *ctx->h_state;
+  double init_ms = 0.0;
+  {
+    float t = 0.f;
+    cudaEventElapsedTime(&t, ev0, ev1);
+    init_ms = t;
+  }
+  TRY(validate_after_init(cfg, m, n, hs));
+  double max_colsq;
+  {
+    unsigned long long b = hs.max_colsq_bits;
+    std::memcpy(&max_colsq, &b, sizeof(double));
+  }
+  const double tol = breakdown_tolerance(cfg, m, max_colsq);
+  long long j0 = 0;
+  TRY(start_column(cfg, n, &j0));
+
+  // ---- loop state ----
+  hs.d = 0;
+  hs.jstar = j0;
+  hs.jlocal = j0;
+  hs.d_max = cfg->d_max;
+  hs.e_cur = std::numeric_limits<double>::infinity();
+  hs.eps_R = cfg->eps_R;
+  hs.breakdown_tol = tol;
+  hs.done = !(0 < cfg->d_max && hs.e_cur > cfg->eps_R) ? 1 : 0;
+  hs.breakdown = 0;
+  hs.reorth = 0;
+  hs.cfg_reorth = cfg->reorthogonalize ? 1 : 0;
+  *ctx->h_state = hs;
+  CU(cudaMemcpyAsync(st, ctx->h_state, sizeof(DevState), cudaMemcpyHostToDevice, ctx->stream));
+
+  LoopBufs L{dX, m, n, ldx, cfg->d_max, dY, dT};
+  TRY(get_step_graph(ctx, L));
+  CU(cudaEventRecord(ev1, ctx->stream));
+  // Replay G-step graphs; the done flag is polled one graph behind so the
+  // device never waits for the host.
+  volatile int* hdone = &ctx->h_state->done;
+  long long launched = 0;
+  bool pending = false;
+  cudaEvent_t ev;
+  CU(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  int rc = RBD_OK;
+  while (launched < cfg->d_max) {
+    cudaError_t e = cudaGraphLaunch(ctx->gexec, ctx->stream);
+    if (e != cudaSuccess) {
+      rc = set_err(RBD_ERR_CUDA, std::string("graph launch: ") + cudaGetErrorString(e));
+      break;
+    }
+    ctx->launches += ctx->graph_nodes;
+    launched += kGraphSteps;
+    if (pending) {
+      cudaEventSynchronize(ev);
+      if (*hdone) break;
+    }
+    cudaMemcpyAsync((void*)&ctx->h_state->done, &st->done, sizeof(int), cudaMemcpyDeviceToHost,
+                    ctx->stream);
+    cudaEventRecord(ev, ctx->stream);
+    pending = true;
+  }
+  cudaEventDestroy(ev);
+  if (rc != RBD_OK) return rc;
+  CU(cudaEventRecord(ev2, ctx->stream));
+  CU(cudaMemcpyAsync(ctx->h_state, st, sizeof(DevState), cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  hs = *ctx->h_state;
+  const long long d = hs.d;
+  if (d == 0)
+    return set_err(RBD_ERR_DEGENERATE_INPUT,
+                   "decompose: start column is numerically zero, no basis built");
+  if (h_selected)
+    CU(cudaMemcpyAsync(h_selected, ctx->sel.p, sizeof(long long) * d, cudaMemcpyDeviceToHost, ctx->stream));
+  if (h_history)
+    CU(cudaMemcpyAsync(h_history, ctx->hist.p, sizeof(double) * d, cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  if (result) {
+    float t_loop = 0.f;
+    cudaEventElapsedTime(&t_loop, ev1, ev2);
+    result->d = d;
+    result->breakdown = hs.breakdown;
+    result->breakdown_tol = tol;
+    result->max_col_norm = std::sqrt(max_colsq);
+    result->init_ms = init_ms;
+    result->loop_ms = t_loop;
+    result->launches = ctx->launches - launches0;
+  }
+  return RBD_OK;
+}
+
+int rbd_decompose_host(rbd_ctx_t ctx, const double* hX, int64_t m, int64_t n, int64_t ldx,
+                       const rbd_config_t* cfg, double* hY, double* hT, int64_t* h_selected,
+                       double* h_history, rbd_result_t* result) {
+  if (!ctx || !cfg) return set_err(RBD_ERR_INVALID_ARGUMENT, "decompose: null context/config");
+  if (m < 1 || n < 1) return set_err(RBD_ERR_INVALID_ARGUMENT, "decompose: matrix must be non-empty");
+  if (ldx < m) return set_err(RBD_ERR_DIMENSION_MISMATCH, "decompose: ldx < m");
+  CU(cudaSetDevice(ctx->device));
+  const long long d_cap = std::max<long long>(1, std::min<long long>(cfg->d_max, n));
+  const long long ldd = (m % 2 == 0) ? m : m + 1;  // keep columns 16-byte aligned on device
+  TRY(ensure(ctx->hX, sizeof(double) * ldd * n));
+  TRY(ensure(ctx->hY, sizeof(double) * m * d_cap));
+  TRY(ensure(ctx->hT, sizeof(double) * d_cap * n));
+  double* dX = ptr<double>(ctx->hX);
+  double* dY = ptr<double>(ctx->hY);
+  double* dT = ptr<double>(ctx->hT);
+  cudaError_t e = cudaMemcpy2DAsync(dX, sizeof(double) * ldd, hX, sizeof(double) * ldx,
+                                    sizeof(double) * m, n, cudaMemcpyHostToDevice, ctx->stream);
+  if (e != cudaSuccess) return set_err(RBD_ERR_CUDA, std::string("H2D X: ") + cudaGetErrorString(e));
+  rbd_result_t r{};
+  int rc = rbd_decompose_device(ctx, dX, m, n, ldd, cfg, dY, dT, h_selected, h_history, &r);
+  // dY was allocated with d_cap columns; the device call writes at most d_cap
+  if (rc == RBD_OK) {
+    if (hY) e = cudaMemcpyAsync(hY, dY, sizeof(double) * m * r.d, cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess && hT)
+      e = cudaMemcpyAsync(hT, dT, sizeof(double) * r.d * n, cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) rc = set_err(RBD_ERR_CUDA, std::string("D2H model: ") + cudaGetErrorString(e));
+    if (result) *result = r;
+  }
+  return rc;
+}
+
+int rbd_mgs_project(rbd_ctx_t ctx, const double* dv, int64_t m, const double* dB, int64_t k,
+                    int64_t ldb, double breakdown_tol, int reorthogonalize, double* dxi,
+                    double* norm, int* ok) {
+  if (!ctx) return set_err(RBD_ERR_INVALID_ARGUMENT, "null context");
+  if (m < 1) return set_err(RBD_ERR_DIMENSION_MISMATCH, "mgs_project: vector length != basis row count");
+  if (k > 0 && ldb < m) return set_err(RBD_ERR_DIMENSION_MISMATCH, "mgs_project: ldb < m");
+  CU(cudaSetDevice(ctx->device));
+  // the extension kernels read the basis with ld m; repack when ldb != m
+  const double* B = dB;
+  DevBuf packed;
+  const long long S = cdiv(m, kChunk);
+  TRY(ensure(ctx->scratch1, sizeof(DevState) + sizeof(double) * (3 * (k + 1) + m + gemv_grid(m) +
+                                                                  S * std::max<long long>(k, 1))));
+  if (k > 0 && ldb != m) {
+    TRY(ensure(packed, sizeof(double) * m * k));
+    CU(cudaMemcpy2DAsync(packed.p, sizeof(double) * m, dB, sizeof(double) * ldb, sizeof(double) * m,
+                         k, cudaMemcpyDeviceToDevice, ctx->stream));
+    B = ptr<double>(packed);
+  }
+  char* base = static_cast<char*>(ctx->scratch1.p);
+  DevState* st = reinterpret_cast<DevState*>(base);
+  double* c = reinterpret_cast<double*>(base + sizeof(DevState));
+  double* p = c + (k + 1);
+  double* w = p + (k + 1);
+  double* nrm = w + m;
+  double* partial = nrm + gemv_grid(m);
+  DevState hs{};
+  hs.d = k;
+  hs.d_max = k + 1;
+  hs.breakdown_tol = breakdown_tol;
+  hs.cfg_reorth = reorthogonalize ? 1 : 0;
+  *ctx->h_state = hs;
+  CU(cudaMemcpyAsync(st, ctx->h_state, sizeof(DevState), cudaMemcpyHostToDevice, ctx->stream));
+  k_norm2_single<<<1, kThreads, 0, ctx->stream>>>(dv, m, st);
+  ctx->launches++;
+  if (k > 0) {
+    const int vec = (m % 2 == 0 && aligned16(B) && aligned16(dv)) ? 2 : 1;
+    SweepArgs s{};
+    s.A = B;
+    s.lda = m;
+    s.m = m;
+    s.ncols = k;
+    s.v = dv;
+    s.partial = partial;
+    s.pstride = k;
+    s.st = st;
+    s.gate = GATE_NONE;
+    TRY(launch_sweep(ctx, s, vec, MODE_DOT, false, k));
+    k_coef_combine<<<(unsigned)cdiv(k, 256), 256, 0, ctx->stream>>>(partial, S, k, c, st, GATE_NONE);
+    ctx->launches++;
+  }
+  ExtBufs b{};
+  b.B = B;
+  b.m = m;
+  b.dcap = std::max<long long>(k, 1);
+  b.X = nullptr;
+  b.v = dv;
+  b.c = c;
+  b.w = w;
+  b.p = p;
+  b.nrm = nrm;
+  b.partial = partial;
+  b.ybase = dxi;
+  b.use_d = 0;
+  b.selected = nullptr;
+  b.st = st;
+  TRY(enqueue_extension(ctx, b));
+  CU(cudaMemcpyAsync(ctx->h_state, st, sizeof(DevState), cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  release(packed);
+  hs = *ctx->h_state;
+  if (ok) *ok = hs.breakdown ? 0 : 1;
+  if (norm) *norm = hs.wnorm;
+  return RBD_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Workspace API
+// ---------------------------------------------------------------------------
+int rbd_ws_init(rbd_ctx_t ctx, const double* dX, int64_t m, int64_t n, int64_t ldx, int64_t cap,
+                rbd_ws_t* out) {
+  if (!ctx || !out) return set_err(RBD_ERR_INVALID_ARGUMENT, "null argument");
+  if (m < 1 || n < 1) return set_err(RBD_ERR_INVALID_ARGUMENT, "workspace_init: empty matrix");
+  if (ldx < m) return set_err(RBD_ERR_DIMENSION_MISMATCH, "workspace_init: ldx < m");
+  CU(cudaSetDevice(ctx->device));
+  auto* ws = new rbd_ws_s();
+  ws->ctx = ctx;
+  ws->X = dX;
+  ws->m = m;
+  ws->n = n;
+  ws->ldx = ldx;
+  ws->cap = std::max<int64_t>(cap, 1);
+  ws->d = 0;
+  const long long S = cdiv(m, kChunk);
+  int rc = RBD_OK;
+  if ((rc = ensure(ws->T, sizeof(double) * ws->cap * n)) ||
+      (rc = ensure(ws->colsq, sizeof(double) * n)) || (rc = ensure(ws->resid, sizeof(double) * n)) ||
+      (rc = ensure(ws->partial, sizeof(double) * S * n)) ||
+      (rc = ensure(ws->rec, sizeof(Rec) * (size_t)ctx->nsm * 8)) ||
+      (rc = ensure(ws->counter, 64)) || (rc = ensure(ws->out, 64)) ||
+      (rc = ensure(ws->tmp, sizeof(DevState) + 64))) {
+    rbd_ws_destroy(ws);
+    return rc;
+  }
+  cudaMemsetAsync(ws->counter.p, 0, 64, ctx->stream);
+  cudaMemsetAsync(ws->tmp.p, 0, sizeof(DevState), ctx->stream);
+  rc = enqueue_init(ctx, dX, m, n, ldx, ptr<double>(ws->partial), ptr<double>(ws->colsq),
+                    ptr<double>(ws->resid), ptr<DevState>(ws->tmp));
+  if (rc == RBD_OK && cudaStreamSynchronize(ctx->stream) != cudaSuccess)
+    rc = set_err(RBD_ERR_CUDA, "workspace_init: kernel failure");
+  if (rc != RBD_OK) {
+    rbd_ws_destroy(ws);
+    return rc;
+  }
+  *out = ws;
+  return RBD_OK;
+}
+
+int rbd_ws_destroy(rbd_ws_t ws) {
+  if (!ws) return RBD_OK;
+  DevBuf* bl[] = {&ws->T, &ws->colsq, &ws->resid, &ws->partial, &ws->rec, &ws->counter, &ws->out, &ws->tmp};
+  for (DevBuf* b : bl) release(*b);
+  delete ws;
+  return RBD_OK;
+}
+
+int64_t rbd_ws_d(rbd_ws_t ws) { return ws ? ws->d : 0; }
+
+int rbd_ws_extend(rbd_ws_t ws, const double* dxi) {
+  if (!ws) return set_err(RBD_ERR_INVALID_ARGUMENT, "null workspace");
+  if (ws->d >= ws->cap) return set_err(RBD_ERR_INVALID_ARGUMENT, "workspace_extend: capacity exhausted");
+  rbd_ctx_t ctx = ws->ctx;
+  CU(cudaSetDevice(ctx->device));
+  const int vec = (ws->ldx % 2 == 0 && aligned16(ws->X) && aligned16(dxi)) ? 2 : 1;
+  SweepArgs s{};
+  s.A = ws->X;
+  s.lda = ws->ldx;
+  s.m = ws->m;
+  s.ncols = ws->n;
+  s.v = dxi;
+  s.partial = ptr<double>(ws->partial);
+  s.pstride = ws->n;
+  s.st = nullptr;
+  s.gate = GATE_NONE;
+  TRY(launch_sweep(ctx, s, vec, MODE_DOT, true, ws->n));
+  FinalizeArgs f{};
+  f.partial = ptr<double>(ws->partial);
+  f.S = cdiv(ws->m, kChunk);
+  f.n = ws->n;
+  f.T = ptr<double>(ws->T);
+  f.krow = ws->d;
+  f.r = ptr<double>(ws->resid);
+  f.col_sq = ptr<double>(ws->colsq);
+  f.st = nullptr;
+  f.mode = 1;
+  k_finalize<<<finalize_grid(ctx, ws->n), kThreads, 0, ctx->stream>>>(f);
+  ctx->launches++;
+  CU(cudaGetLastError());
+  CU(cudaStreamSynchronize(ctx->stream));
+  ws->d += 1;
+  return RBD_OK;
+}
+
+int rbd_ws_scan(rbd_ws_t ws, double* e_cur, int64_t* argmax) {
+  if (!ws) return set_err(RBD_ERR_INVALID_ARGUMENT, "null workspace");
+  rbd_ctx_t ctx = ws->ctx;
+  CU(cudaSetDevice(ctx->device));
+  const int g = finalize_grid(ctx, ws->n);
+  k_scan_only<<<g, kThreads, 0, ctx->stream>>>(ptr<double>(ws->resid), ws->n, ptr<Rec>(ws->rec),
+                                                ptr<unsigned>(ws->counter), ptr<Rec>(ws->out));
+  ctx->launches++;
+  CU(cudaGetLastError());
+  CU(cudaMemcpyAsync(ctx->h_rec, ws->out.p, sizeof(Rec), cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  if (e_cur) *e_cur = ctx->h_rec->v;
+  if (argmax) *argmax = ctx->h_rec->j;
+  return RBD_OK;
+}
+
+int rbd_ws_error_sq(rbd_ws_t ws, int64_t j, const double* h_c, int64_t clen, double* out) {
+  if (!ws) return set_err(RBD_ERR_INVALID_ARGUMENT, "null workspace");
+  if (j < 0 || j >= ws->n) return set_err(RBD_ERR_INDEX_OUT_OF_RANGE, "error_sq: column index out of range");
+  if (clen != ws->d) return set_err(RBD_ERR_DIMENSION_MISMATCH, "error_sq: coefficient length != d");
+  rbd_ctx_t ctx = ws->ctx;
+  CU(cudaSetDevice(ctx->device));
+  double* dc = reinterpret_cast<double*>(static_cast<char*>(ws->tmp.p) + sizeof(DevState));
+  DevBuf cbuf;
+  if (clen > 0) {
+    TRY(ensure(cbuf, sizeof(double) * clen));
+    CU(cudaMemcpyAsync(cbuf.p, h_c, sizeof(double) * clen, cudaMemcpyHostToDevice, ctx->stream));
+  }
+  k_error_sq<<<1, kThreads, 0, ctx->stream>>>(ptr<double>(ws->T), ws->n, ws->d, j, ptr<double>(cbuf),
+                                              ptr<double>(ws->colsq), dc);
+  ctx->launches++;
+  CU(cudaGetLastError());
+  CU(cudaMemcpyAsync(out, dc, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  release(cbuf);
+  return RBD_OK;
+}
+
+int rbd_ws_read(rbd_ws_t ws, double* h_col_sq, double* h_residual_sq, double* h_yax) {
+  if (!ws) return set_err(RBD_ERR_INVALID_ARGUMENT, "null workspace");
+  rbd_ctx_t ctx = ws->ctx;
+  CU(cudaSetDevice(ctx->device));
+  if (h_col_sq) CU(cudaMemcpyAsync(h_col_sq, ws->colsq.p, sizeof(double) * ws->n, cudaMemcpyDeviceToHost, ctx->stream));
+  if (h_residual_sq)
+    CU(cudaMemcpyAsync(h_residual_sq, ws->resid.p, sizeof(double) * ws->n, cudaMemcpyDeviceToHost, ctx->stream));
+  if (h_yax && ws->d > 0)
+    CU(cudaMemcpyAsync(h_yax, ws->T.p, sizeof(double) * ws->d * ws->n, cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  return RBD_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Out-of-sample compression (K5) and reconstruct
+// ---------------------------------------------------------------------------
+int rbd_project_batch(rbd_ctx_t ctx, const double* dY, int64_t m, int64_t d, int64_t ldy,
+                      const double* dXn, int64_t N, int64_t ldx, double* dTn, double* d_err) {
+  if (!ctx) return set_err(RBD_ERR_INVALID_ARGUMENT, "null context");
+  if (m < 1 || d < 1 || N < 0) return set_err(RBD_ERR_DIMENSION_MISMATCH, "project: bad sizes");
+  if (ldy < m || ldx < m) return set_err(RBD_ERR_DIMENSION_MISMATCH, "project: vector length != m");
+  if (N == 0) return RBD_OK;
+  CU(cudaSetDevice(ctx->device));
+  long long nl = 0;
+  int rc = rbdk::launch_project_f64(dY, m, d, ldy, dXn, N, ldx, dTn, d_err, ctx->stream, &nl);
+  ctx->launches += nl;
+  if (rc != 0) return set_err(RBD_ERR_CUDA, std::string("project kernel: ") + cudaGetErrorString((cudaError_t)rc));
+  return RBD_OK;
+}
+
+int rbd_reconstruct(rbd_ctx_t ctx, const double* dY, int64_t m, int64_t d, int64_t ldy,
+                    const double* dc, double* dv) {
+  if (!ctx) return set_err(RBD_ERR_INVALID_ARGUMENT, "null context");
+  if (ldy < m) return set_err(RBD_ERR_DIMENSION_MISMATCH, "reconstruct: ldy < m");
+  CU(cudaSetDevice(ctx->device));
+  long long nl = 0;
+  int rc = rbdk::launch_reconstruct_f64(dY, m, d, ldy, dc, dv, ctx->stream, &nl);
+  ctx->launches += nl;
+  if (rc != 0) return set_err(RBD_ERR_CUDA, std::string("reconstruct kernel: ") + cudaGetErrorString((cudaError_t)rc));
+  return RBD_OK;
+}
+
+}  // extern "C"
+
+extern "C" {
+
+int rbd_project_host(rbd_ctx_t ctx, const double* hY, int64_t m, int64_t d, const double* hXn,
+                     int64_t N, double* hTn, double* h_err) {
+  if (!ctx) return set_err(RBD_ERR_INVALID_ARGUMENT, "null context");
+  if (m < 1 || d < 1 || N < 0) return set_err(RBD_ERR_DIMENSION_MISMATCH, "project: bad sizes");
+  if (N == 0) return RBD_OK;
+  CU(cudaSetDevice(ctx->device));
+  DevBuf bY, bX, bT, bE;
+  auto fin = [&](int rc) {
+    release(bY);
+    release(bX);
+    release(bT);
+    release(bE);
+    return rc;
+  };
+  int rc;
+  if ((rc = ensure(bY, sizeof(double) * m * d)) || (rc = ensure(bX, sizeof(double) * m * N)) ||
+      (rc = ensure(bT, sizeof(double) * d * N)) || (rc = ensure(bE, sizeof(double) * N)))
+    return fin(rc);
+  if (cudaMemcpyAsync(bY.p, hY, sizeof(double) * m * d, cudaMemcpyHostToDevice, ctx->stream) ||
+      cudaMemcpyAsync(bX.p, hXn, sizeof(double) * m * N, cudaMemcpyHostToDevice, ctx->stream))
+    return fin(set_err(RBD_ERR_CUDA, "project_host: H2D failed"));
+  rc = rbd_project_batch(ctx, ptr<double>(bY), m, d, m, ptr<double>(bX), N, m, ptr<double>(bT),
+                         h_err ? ptr<double>(bE) : nullptr);
+  if (rc) return fin(rc);
+  if (hTn && cudaMemcpyAsync(hTn, bT.p, sizeof(double) * d * N, cudaMemcpyDeviceToHost, ctx->stream))
+    return fin(set_err(RBD_ERR_CUDA, "project_host: D2H failed"));
+  if (h_err && cudaMemcpyAsync(h_err, bE.p, sizeof(double) * N, cudaMemcpyDeviceToHost, ctx->stream))
+    return fin(set_err(RBD_ERR_CUDA, "project_host: D2H failed"));
+  if (cudaStreamSynchronize(ctx->stream)) return fin(set_err(RBD_ERR_CUDA, "project_host: sync failed"));
+  return fin(RBD_OK);
+}
+
+int rbd_reconstruct_host(rbd_ctx_t ctx, const double* hY, int64_t m, int64_t d, const double* hc,
+                         double* hv) {
+  if (!ctx) return set_err(RBD_ERR_INVALID_ARGUMENT, "null context");
+  if (m < 1 || d < 0) return set_err(RBD_ERR_DIMENSION_MISMATCH, "reconstruct: bad sizes");
+  CU(cudaSetDevice(ctx->device));
+  DevBuf bY, bc, bv;
+  auto fin = [&](int rc) {
+    release(bY);
+    release(bc);
+    release(bv);
+    return rc;
+  };
+  int rc;
+  if ((rc = ensure(bY, sizeof(double) * m * std::max<int64_t>(d, 1))) ||
+      (rc = ensure(bc, sizeof(double) * std::max<int64_t>(d, 1))) || (rc = ensure(bv, sizeof(double) * m)))
+    return fin(rc);
+  if (d > 0 && (cudaMemcpyAsync(bY.p, hY, sizeof(double) * m * d, cudaMemcpyHostToDevice, ctx->stream) ||
+                cudaMemcpyAsync(bc.p, hc, sizeof(double) * d, cudaMemcpyHostToDevice, ctx->stream)))
+    return fin(set_err(RBD_ERR_CUDA, "reconstruct_host: H2D failed"));
+  rc = rbd_reconstruct(ctx, ptr<double>(bY), m, d, m, ptr<double>(bc), ptr<double>(bv));
+  if (rc) return fin(rc);
+  if (cudaMemcpyAsync(hv, bv.p, sizeof(double) * m, cudaMemcpyDeviceToHost, ctx->stream) ||
+      cudaStreamSynchronize(ctx->stream))
+    return fin(set_err(RBD_ERR_CUDA, "reconstruct_host: D2H failed"));
+  return fin(RBD_OK);
+}
+
+int rbd_time_sweep(rbd_ctx_t ctx, const double* dX, int64_t m, int64_t n, int64_t ldx,
+                   const double* dy, int reps, double* ms_per_launch) {
+  if (!ctx || reps < 1) return set_err(RBD_ERR_INVALID_ARGUMENT, "time_sweep: bad arguments");
+  CU(cudaSetDevice(ctx->device));
+  TRY(ensure(ctx->partial, sizeof(double) * cdiv(m, kChunk) * n));
+  const int vec = (ldx % 2 == 0 && aligned16(dX) && aligned16(dy)) ? 2 : 1;
+  SweepArgs s{};
+  s.A = dX;
+  s.lda = ldx;
+  s.m = m;
+  s.ncols = n;
+  s.v = dy;
+  s.partial = ptr<double>(ctx->partial);
+  s.pstride = n;
+  s.gate = GATE_NONE;
+  TRY(launch_sweep(ctx, s, vec, MODE_DOT, true, n));  // warm-up
+  cudaEvent_t a, b;
+  CU(cudaEventCreate(&a));
+  CU(cudaEventCreate(&b));
+  cudaEventRecord(a, ctx->stream);
+  for (int r = 0; r < reps; ++r) {
+    int rc = launch_sweep(ctx, s, vec, MODE_DOT, true, n);
+    if (rc) {
+      cudaEventDestroy(a);
+      cudaEventDestroy(b);
+      return rc;
+    }
+  }
+  cudaEventRecord(b, ctx->stream);
+  cudaError_t e = cudaEventSynchronize(b);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, a, b);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  if (e != cudaSuccess) return set_err(RBD_ERR_CUDA, std::string("time_sweep: ") + cudaGetErrorString(e));
+  *ms_per_launch = ms / reps;
+  return RBD_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,659 @@
+// rbd_device.cuh — device-side data structures and kernels of the B200 RBD
+// greedy loop. Written for sm_100a (B200); see DESIGN.md for the data layout
+// and the roofline of each kernel.
+//
+// Kernel map (reference function each one replaces):
+//   k_sweep<MODE_INIT>   K1  workspace_init col_sq + allFinite + zero test
+//                            (workspace.cpp:21-23, decompose.cpp:57,63,70)
+//   k_sweep<MODE_DOT>    K2  T.row(d) = xi'X and workspace_extend's X'xi
+//                            (decompose.cpp:93, workspace.cpp:51) — one X pass,
+//                            chunk partials; also Y'w for the reorth pass
+//   k_finalize           K3  residual_sq -= row^2, clamp, residual_scan argmax,
+//                            stop test (workspace.cpp:52-53,107-113,123;
+//                            decompose.cpp:87,98-101)
+//   k_ext_gemv_n / k_ext_* K4 mgs_project (decompose.cpp:12-33) as CGS with the
+//                            stored coefficients T[:,j*] plus the reference's
+//                            conditional second pass
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace rbdk {
+
+// ---- tiling constants (the per-column summation order depends on these and
+//      on m only, never on n, the grid or the number of GPUs) ----
+constexpr int kThreads = 256;      // sweep CTA size
+constexpr int kChunk = 4096;       // rows per sweep tile (32 KiB per column in fp64)
+constexpr int kCols = 4;           // columns per sweep tile
+constexpr int kWarps = kThreads / 32;
+constexpr int kGemvRows = 64;      // rows per GEMV-N CTA
+constexpr int kGemvSplit = 4;      // l-splits per row in GEMV-N (kThreads = 64*4)
+constexpr int kCoefTile = 2048;    // coefficients staged in smem per pass
+
+enum Gate : int { GATE_NONE = 0, GATE_LIVE = 1, GATE_REORTH = 2 };
+enum SweepMode : int { MODE_INIT = 0, MODE_DOT = 1 };
+
+// Device-resident loop state. Every per-step kernel reads it, so one captured
+// CUDA graph of G steps is valid for any step index.
+struct DevState {
+  long long d;            // accepted basis vectors so far (the reference's d)
+  long long jstar;        // global index of the column to extend with next
+  long long jlocal;       // local index of that column on this rank (-1: not owned)
+  long long d_max;
+  double e_cur;           // last E_cur
+  double eps_R;
+  double breakdown_tol;
+  double xnorm2;          // ||x_{j*}||^2 (entry norm^2, decompose.cpp:18)
+  double w1n2;            // ||w||^2 after the first pass
+  double wnorm;           // final norm (MgsResult::residual_norm)
+  int done;               // loop finished
+  int breakdown;          // finished by an orthogonalisation breakdown
+  int reorth;             // second pass active this step
+  int cfg_reorth;         // RbdConfig::reorthogonalize
+  unsigned flags_nonfinite;
+  unsigned flags_nonzero;
+  unsigned long long max_colsq_bits;  // max_j col_sq (as ordered bits, >= 0)
+  int rank_owner;         // multi-GPU: rank owning jstar
+  int pad;
+};
+
+struct Rec {            // max-loc record: value desc, index asc (workspace.cpp:109)
+  double v;
+  long long j;
+};
+
+__device__ __forceinline__ bool rec_better(double av, long long aj, double bv, long long bj) {
+  return av > bv || (av == bv && aj < bj);
+}
+
+__device__ __forceinline__ bool gate_skip(const DevState* st, int gate) {
+  if (gate == GATE_NONE) return false;
+  if (st->done) return true;
+  if (gate == GATE_REORTH && !st->reorth) return true;
+  return false;
+}
+
+// Streaming load (X is read once per step and must not evict Y/T/r from L2).
+__device__ __forceinline__ double2 ld_stream2(const double* p) {
+  return __ldcs(reinterpret_cast<const double2*>(p));
+}
+__device__ __forceinline__ double ld_stream1(const double* p) { return __ldcs(p); }
+__device__ __forceinline__ double2 ld_keep2(const double* p) {
+  return __ldg(reinterpret_cast<const double2*>(p));
+}
+__device__ __forceinline__ double ld_keep1(const double* p) { return __ldg(p); }
+
+__device__ __forceinline__ bool is_nonfinite(double x) {
+  return (__double_as_longlong(x) & 0x7ff0000000000000LL) == 0x7ff0000000000000LL;
+}
+
+// ---------------------------------------------------------------------------
+// K1/K2: chunked column dot products.  partial[s*pstride + j] =
+//   sum over rows of chunk s of A(i,j)*v(i)   (MODE_DOT)
+//   sum over rows of chunk s of A(i,j)^2      (MODE_INIT, plus flags)
+// A is m x ncols column-major (lda). Tiles = (chunk s, column group g); the
+// grid is persistent (grid-stride over tiles).
+// ---------------------------------------------------------------------------
+struct SweepArgs {
+  const double* A;
+  long long lda;
+  long long m;
+  long long ncols;        // static column count (csel == 0)
+  const double* v;        // vector (vsel == 0)
+  const double* vbase;    // vsel == 1: v = vbase + st->d * vstride
+  long long vstride;
+  double* partial;
+  long long pstride;
+  DevState* st;
+  int gate;
+  int vsel;
+  int csel;               // 1: ncols = st->d (reorth pass over Y)
+};
+
+template <int VEC, int MODE, bool STREAM>
+__global__ void __launch_bounds__(kThreads, 2) k_sweep(SweepArgs a) {
+  if (gate_skip(a.st, a.gate)) return;
+  const long long m = a.m;
+  const long long ncols = a.csel ? a.st->d : a.ncols;
+  const double* __restrict__ v = a.vsel ? a.vbase + a.st->d * a.vstride : a.v;
+  const long long S = (m + kChunk - 1) / kChunk;
+  const long long G = (ncols + kCols - 1) / kCols;
+  const long long ntiles = S * G;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  constexpr int U = kChunk / (VEC * kThreads);  // element groups per thread per column
+  constexpr int UB = (VEC == 2) ? 4 : 8;         // batch of groups loaded together
+  __shared__ double red[kWarps][kCols];
+  unsigned nonfinite = 0, nonzero = 0;
+
+  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const long long s = tile / G;
+    const long long g = tile - s * G;
+    const long long row0 = s * kChunk;
+    const long long col0 = g * kCols;
+    const bool full = (row0 + kChunk <= m) && (col0 + kCols <= ncols);
+    double acc[kCols];
+#pragma unroll
+    for (int c = 0; c < kCols; ++c) acc[c] = 0.0;
+    const double* Ac[kCols];
+#pragma unroll
+    for (int c = 0; c < kCols; ++c) {
+      const long long cc = (col0 + c < ncols) ? col0 + c : col0;  // clamp (unused cols)
+      Ac[c] = a.A + cc * a.lda + row0;
+    }
+    const double* vr = (MODE == MODE_DOT) ? v + row0 : nullptr;
+
+    if (full) {
+#pragma unroll 1
+      for (int ub = 0; ub < U; ub += UB) {
+        if constexpr (VEC == 2) {
+          double2 yv[UB];
+          double2 xv[UB][kCols];
+#pragma unroll
+          for (int u = 0; u < UB; ++u) {
+            const int e = (tid + (ub + u) * kThreads) * 2;
+            if constexpr (MODE == MODE_DOT) yv[u] = ld_keep2(vr + e);
+#pragma unroll
+            for (int c = 0; c < kCols; ++c)
+              xv[u][c] = STREAM ? ld_stream2(Ac[c] + e) : ld_keep2(Ac[c] + e);
+          }
+#pragma unroll
+          for (int u = 0; u < UB; ++u)
+#pragma unroll
+            for (int c = 0; c < kCols; ++c) {
+              if constexpr (MODE == MODE_DOT) {
+                acc[c] = fma(xv[u][c].x, yv[u].x, acc[c]);
+                acc[c] = fma(xv[u][c].y, yv[u].y, acc[c]);
+              } else {
+                acc[c] = fma(xv[u][c].x, xv[u][c].x, acc[c]);
+                acc[c] = fma(xv[u][c].y, xv[u][c].y, acc[c]);
+                nonfinite |= is_nonfinite(xv[u][c].x) | is_nonfinite(xv[u][c].y);
+                nonzero |= (xv[u][c].x != 0.0) | (xv[u][c].y != 0.0);
+              }
+            }
+        } else {
+          double yv[UB];
+          double xv[UB][kCols];
+#pragma unroll
+          for (int u = 0; u < UB; ++u) {
+            const int e = tid + (ub + u) * kThreads;
+            if constexpr (MODE == MODE_DOT) yv[u] = ld_keep1(vr + e);
+#pragma unroll
+            for (int c = 0; c < kCols; ++c)
+              xv[u][c] = STREAM ? ld_stream1(Ac[c] + e) : ld_keep1(Ac[c] + e);
+          }
+#pragma unroll
+          for (int u = 0; u < UB; ++u)
+#pragma unroll
+            for (int c = 0; c < kCols; ++c) {
+              if constexpr (MODE == MODE_DOT) {
+                acc[c] = fma(xv[u][c], yv[u], acc[c]);
+              } else {
+                acc[c] = fma(xv[u][c], xv[u][c], acc[c]);
+                nonfinite |= is_nonfinite(xv[u][c]);
+                nonzero |= (xv[u][c] != 0.0);
+              }
+            }
+        }
+      }
+    } else {
+      // Edge tile: identical arithmetic order, out-of-range rows contribute +0.
+      const long long rows = (m - row0 < kChunk) ? m - row0 : kChunk;
+#pragma unroll 1
+      for (int u = 0; u < U; ++u) {
+        if constexpr (VEC == 2) {
+          const long long e = (long long)(tid + u * kThreads) * 2;
+          double y0 = 0.0, y1 = 0.0;
+          if constexpr (MODE == MODE_DOT) {
+            if (e < rows) y0 = vr[e];
+            if (e + 1 < rows) y1 = vr[e + 1];
+          }
+#pragma unroll
+          for (int c = 0; c < kCols; ++c) {
+            if (col0 + c >= ncols) continue;
+            const double x0 = (e < rows) ? Ac[c][e] : 0.0;
+            const double x1 = (e + 1 < rows) ? Ac[c][e + 1] : 0.0;
+            if constexpr (MODE == MODE_DOT) {
+              acc[c] = fma(x0, y0, acc[c]);
+              acc[c] = fma(x1, y1, acc[c]);
+            } else {
+              acc[c] = fma(x0, x0, acc[c]);
+              acc[c] = fma(x1, x1, acc[c]);
+              nonfinite |= is_nonfinite(x0) | is_nonfinite(x1);
+              nonzero |= (x0 != 0.0) | (x1 != 0.0);
+            }
+          }
+        } else {
+          const long long e = tid + (long long)u * kThreads;
+          double y0 = 0.0;
+          if constexpr (MODE == MODE_DOT) {
+            if (e < rows) y0 = vr[e];
+          }
+#pragma unroll
+          for (int c = 0; c < kCols; ++c) {
+            if (col0 + c >= ncols) continue;
+            const double x0 = (e < rows) ? Ac[c][e] : 0.0;
+            if constexpr (MODE == MODE_DOT) {
+              acc[c] = fma(x0, y0, acc[c]);
+            } else {
+              acc[c] = fma(x0, x0, acc[c]);
+              nonfinite |= is_nonfinite(x0);
+              nonzero |= (x0 != 0.0);
+            }
+          }
+        }
+      }
+    }
+    // CTA reduction in a fixed order: xor-butterfly in the warp, then warps 0..7.
+#pragma unroll
+    for (int c = 0; c < kCols; ++c) {
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], off);
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int c = 0; c < kCols; ++c) red[warp][c] = acc[c];
+    }
+    __syncthreads();
+    if (tid < kCols && col0 + tid < ncols) {
+      double sum = red[0][tid];
+#pragma unroll
+      for (int w = 1; w < kWarps; ++w) sum += red[w][tid];
+      a.partial[s * a.pstride + col0 + tid] = sum;
+    }
+    __syncthreads();
+  }
+  if constexpr (MODE == MODE_INIT) {
+    const int any_nf = __syncthreads_or(nonfinite);
+    const int any_nz = __syncthreads_or(nonzero);
+    if (tid == 0) {
+      if (any_nf) atomicOr(&a.st->flags_nonfinite, 1u);
+      if (any_nz) atomicOr(&a.st->flags_nonzero, 1u);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Block-level helpers
+// ---------------------------------------------------------------------------
+template <int NT>
+__device__ __forceinline__ double block_sum_fixed(double x, double* sm) {
+  // deterministic: xor-butterfly per warp, then warps in order
+  for (int off = 16; off > 0; off >>= 1) x += __shfl_xor_sync(0xffffffffu, x, off);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) sm[warp] = x;
+  __syncthreads();
+  double s = sm[0];
+#pragma unroll
+  for (int w = 1; w < NT / 32; ++w) s += sm[w];
+  __syncthreads();
+  return s;
+}
+
+__device__ __forceinline__ void warp_argmax(double& v, long long& j) {
+  for (int off = 16; off > 0; off >>= 1) {
+    const double ov = __shfl_xor_sync(0xffffffffu, v, off);
+    const long long oj = __shfl_xor_sync(0xffffffffu, j, off);
+    if (rec_better(ov, oj, v, j)) {
+      v = ov;
+      j = oj;
+    }
+  }
+}
+
+template <int NT>
+__device__ __forceinline__ void block_argmax(double& v, long long& j, Rec* sm) {
+  warp_argmax(v, j);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) sm[warp] = Rec{v, j};
+  __syncthreads();
+  v = sm[0].v;
+  j = sm[0].j;
+#pragma unroll
+  for (int w = 1; w < NT / 32; ++w)
+    if (rec_better(sm[w].v, sm[w].j, v, j)) {
+      v = sm[w].v;
+      j = sm[w].j;
+    }
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// K1 finish: col_sq = sum of chunk partials, residual_sq = col_sq, max col_sq.
+// ---------------------------------------------------------------------------
+__global__ void k_init_finish(const double* __restrict__ partial, long long S, long long n,
+                              double* __restrict__ col_sq, double* __restrict__ resid,
+                              DevState* st) {
+  __shared__ double sm[kWarps];
+  double mx = 0.0;
+  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < n;
+       j += (long long)gridDim.x * blockDim.x) {
+    double t = 0.0;
+    for (long long s = 0; s < S; ++s) t += partial[s * n + j];
+    t = t > 0.0 ? t : 0.0;  // workspace.cpp:37 cwiseMax(0); NaN stays NaN-free only if finite
+    col_sq[j] = t;
+    resid[j] = t;
+    if (t == t && t > mx) mx = t;
+  }
+  // max is order independent; publish as ordered bits (values >= 0)
+  for (int off = 16; off > 0; off >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double b = sm[0];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) b = fmax(b, sm[w]);
+    atomicMax(&st->max_colsq_bits, (unsigned long long)__double_as_longlong(b));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K3: finalize one greedy step.
+//   t_j = sum_s partial[s*n + j]      (fixed order: chunk 0..S-1)
+//   T[k*n + j] = t_j                  (decompose.cpp:93)
+//   r_j = max(r_j - t_j^2, 0)         (workspace.cpp:52-53)
+//   argmax over r (value desc, index asc), E_cur = sqrt(max(best, 0))
+// mode 0: full decompose step (state update in the last CTA)
+// mode 1: workspace extend only (no argmax)
+// mode 2: multi-GPU step: local record -> rec_out, no state update
+// ---------------------------------------------------------------------------
+struct FinalizeArgs {
+  const double* partial;
+  long long S;
+  long long n;
+  double* T;            // row-major, row stride n
+  long long krow;       // row index (mode 1); modes 0/2 use st->d
+  double* r;
+  const double* col_sq;
+  DevState* st;
+  Rec* rec;             // per-CTA records (gridDim.x)
+  unsigned* counter;    // last-CTA-done counter (self-resetting)
+  double* history;      // device history (mode 0)
+  double* cbuf;         // next-step coefficients T[0:d, j*] (mode 0)
+  Rec* rec_out;         // mode 2: this rank's record
+  long long col_offset; // global index of local column 0
+  int mode;
+};
+
+__device__ void finalize_state(const FinalizeArgs& a, double best, long long arg) {
+  DevState* st = a.st;
+  const long long k = st->d;
+  const double e_cur = sqrt(best > 0.0 ? best : 0.0);  // workspace.cpp:123
+  a.history[k] = e_cur;                                 // decompose.cpp:99
+  st->e_cur = e_cur;
+  st->d = k + 1;                                        // :96
+  st->jstar = arg;                                      // :101
+  st->done = !((k + 1) < st->d_max && e_cur > st->eps_R) ? 1 : 0;  // :87
+}
+
+__global__ void __launch_bounds__(kThreads) k_finalize(FinalizeArgs a) {
+  if (a.mode != 1 && a.st->done) return;
+  __shared__ Rec smr[kWarps];
+  __shared__ int is_last;
+  const long long n = a.n;
+  const long long k = (a.mode == 1) ? a.krow : a.st->d;
+  double* Trow = a.T + k * n;
+  double bv = -1.0;  // residual_scan starts best at -1 (workspace.cpp:105)
+  long long bj = 0x7fffffffffffffffLL;
+  for (long long j = blockIdx.x * (long long)kThreads + threadIdx.x; j < n;
+       j += (long long)gridDim.x * kThreads) {
+    double t = 0.0;
+    for (long long s = 0; s < a.S; ++s) t += a.partial[s * n + j];
+    Trow[j] = t;
+    const double sq = __dmul_rn(t, t);
+    double rj = __dsub_rn(a.r[j], sq);
+    rj = rj > 0.0 ? rj : 0.0;
+    a.r[j] = rj;
+    if (rec_better(rj, j, bv, bj)) {
+      bv = rj;
+      bj = j;
+    }
+  }
+  if (a.mode == 1) return;
+  __threadfence();  // publish this CTA's T/r writes before the done-counter
+  block_argmax<kThreads>(bv, bj, smr);
+  if (threadIdx.x == 0) {
+    a.rec[blockIdx.x] = Rec{bv, bj};
+    __threadfence();
+    const unsigned prev = atomicAdd(a.counter, 1u);
+    is_last = (prev == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  bv = -1.0;
+  bj = 0x7fffffffffffffffLL;
+  for (unsigned b = threadIdx.x; b < gridDim.x; b += kThreads) {
+    const Rec rr{__ldcg(&a.rec[b].v), __ldcg(&a.rec[b].j)};
+    if (rec_better(rr.v, rr.j, bv, bj)) {
+      bv = rr.v;
+      bj = rr.j;
+    }
+  }
+  block_argmax<kThreads>(bv, bj, smr);
+  if (threadIdx.x == 0) *a.counter = 0u;
+  if (a.mode == 2) {
+    if (threadIdx.x == 0) a.rec_out[0] = Rec{bv, bj + a.col_offset};
+    return;
+  }
+  // single GPU: state update + gather of the next step's coefficients
+  if (threadIdx.x == 0) {
+    finalize_state(a, bv, bj);
+    a.st->jlocal = bj;
+    a.st->xnorm2 = a.col_sq[bj];
+  }
+  __syncthreads();
+  if (!a.st->done) {
+    for (long long l = threadIdx.x; l <= k; l += kThreads) a.cbuf[l] = __ldcg(&a.T[l * n + bj]);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K4: extension.  w = x - B c (pass 1) / w = w - B p (pass 2), B = Y[:, 0:k].
+// CTA = 64 rows x 4 coefficient splits; per-row order fixed (split s takes
+// l = s, s+4, ...; the 4 split sums are combined ((s0+s1)+(s2+s3))).
+// Each CTA writes sum_rows w^2 to nrm_part[blockIdx.x].
+// ---------------------------------------------------------------------------
+struct ExtArgs {
+  const double* B;      // basis (Y), ld ldb
+  long long ldb;
+  long long m;
+  const double* X;      // pass 1 source: x = X + st->jlocal*ldx (if X != nullptr)
+  long long ldx;
+  const double* v;      // pass 1 source otherwise (may alias w)
+  const double* c;      // coefficients (length k)
+  double* w;            // m scratch
+  double* nrm_part;     // one per CTA
+  DevState* st;
+  int gate;
+  int pass;             // 1 or 2
+};
+
+__global__ void __launch_bounds__(kThreads) k_ext_gemv_n(ExtArgs a) {
+  if (gate_skip(a.st, a.gate)) return;
+  const long long k = a.st->d;
+  const long long m = a.m;
+  __shared__ double cs[kCoefTile];
+  __shared__ double part[kGemvSplit][kGemvRows];
+  __shared__ double sm[kWarps];
+  const int r = threadIdx.x % kGemvRows;
+  const int sp = threadIdx.x / kGemvRows;
+  const long long i = (long long)blockIdx.x * kGemvRows + r;
+  const bool valid = i < m;
+  double acc = 0.0;
+  for (long long l0 = 0; l0 < k; l0 += kCoefTile) {
+    const int nl = (int)((k - l0) < kCoefTile ? (k - l0) : kCoefTile);
+    __syncthreads();
+    for (int t = threadIdx.x; t < nl; t += kThreads) cs[t] = a.c[l0 + t];
+    __syncthreads();
+    if (valid) {
+      const double* Bp = a.B + i + (l0 + sp) * a.ldb;
+      const long long step = (long long)kGemvSplit * a.ldb;
+      int l = sp;
+      // 8 independent loads in flight per thread
+      for (; l + 7 * kGemvSplit < nl; l += 8 * kGemvSplit) {
+        double yv[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) yv[q] = ld_keep1(Bp + q * step);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc = fma(yv[q], cs[l + q * kGemvSplit], acc);
+        Bp += 8 * step;
+      }
+      for (; l < nl; l += kGemvSplit) {
+        acc = fma(ld_keep1(Bp), cs[l], acc);
+        Bp += step;
+      }
+    }
+  }
+  part[sp][r] = acc;
+  __syncthreads();
+  double wsq = 0.0;
+  if (threadIdx.x < kGemvRows) {
+    if (valid) {
+      const double proj = (part[0][r] + part[1][r]) + (part[2][r] + part[3][r]);
+      double x;
+      if (a.pass == 1 && a.X != nullptr)
+        x = a.X[a.st->jlocal * a.ldx + i];
+      else if (a.pass == 1)
+        x = a.v[i];
+      else
+        x = a.w[i];
+      const double wi = x - proj;
+      a.w[i] = wi;
+      wsq = wi * wi;
+    }
+  }
+  const double s = block_sum_fixed<kThreads>(threadIdx.x < kGemvRows ? wsq : 0.0, sm);
+  if (threadIdx.x == 0) a.nrm_part[blockIdx.x] = s;
+}
+
+// Deterministic single-CTA sum of nparts values.
+__device__ __forceinline__ double sum_parts(const double* p, long long np, double* sm) {
+  double s = 0.0;
+  for (long long b = threadIdx.x; b < np; b += kThreads) s += p[b];
+  return block_sum_fixed<kThreads>(s, sm);
+}
+
+// After pass 1: decide the second pass exactly as decompose.cpp:28 does.
+__global__ void __launch_bounds__(kThreads) k_ext_decide(const double* nrm_part, long long np,
+                                                         DevState* st) {
+  if (st->done) return;
+  __shared__ double sm[kWarps];
+  const double w1n2 = sum_parts(nrm_part, np, sm);
+  if (threadIdx.x == 0) {
+    st->w1n2 = w1n2;
+    const double entry_norm = sqrt(st->xnorm2);
+    st->reorth = (st->d > 0) && (st->cfg_reorth || sqrt(w1n2) < 0.5 * entry_norm) ? 1 : 0;
+  }
+}
+
+// Second-pass coefficients p[l] = sum_s partial[s*pstride + l] (fixed order).
+__global__ void k_coef_combine(const double* __restrict__ partial, long long S, long long pstride,
+                               double* __restrict__ p, DevState* st, int gate) {
+  if (gate_skip(st, gate)) return;
+  const long long k = st->d;
+  for (long long l = blockIdx.x * (long long)blockDim.x + threadIdx.x; l < k;
+       l += (long long)gridDim.x * blockDim.x) {
+    double t = 0.0;
+    for (long long s = 0; s < S; ++s) t += partial[s * pstride + l];
+    p[l] = t;
+  }
+}
+
+// Norm + breakdown test (decompose.cpp:29-30); on success record selected.
+__global__ void __launch_bounds__(kThreads) k_ext_finish(const double* nrm_part, long long np,
+                                                         DevState* st, long long* selected) {
+  if (st->done) return;
+  __shared__ double sm[kWarps];
+  const int re = st->reorth;
+  const double wn2 = re ? sum_parts(nrm_part, np, sm) : st->w1n2;
+  if (threadIdx.x == 0) {
+    const double norm = sqrt(wn2);
+    st->wnorm = norm;
+    if (norm < st->breakdown_tol || norm == 0.0) {
+      st->done = 1;
+      st->breakdown = 1;
+    } else if (selected != nullptr) {
+      selected[st->d] = st->jstar;  // decompose.cpp:94
+    }
+  }
+}
+
+// y = w / norm into the output column (decompose.cpp:31,92).
+__global__ void k_normalize(const double* __restrict__ w, double* __restrict__ ybase,
+                            long long ystride, long long m, DevState* st, int use_d) {
+  if (st->done) return;
+  const double norm = st->wnorm;
+  double* y = ybase + (use_d ? st->d * ystride : 0);
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m;
+       i += (long long)gridDim.x * blockDim.x)
+    y[i] = w[i] / norm;
+}
+
+// Entry norm for standalone mgs_project: xnorm2 = ||v||^2 (fixed order).
+__global__ void __launch_bounds__(kThreads) k_norm2_single(const double* v, long long m,
+                                                           DevState* st) {
+  __shared__ double sm[kWarps];
+  double s = 0.0;
+  for (long long i = threadIdx.x; i < m; i += kThreads) s = fma(v[i], v[i], s);
+  s = block_sum_fixed<kThreads>(s, sm);
+  if (threadIdx.x == 0) st->xnorm2 = s;
+}
+
+// Workspace scan (residual_scan identity, workspace.cpp:101-125) into out.
+__global__ void __launch_bounds__(kThreads) k_scan_only(const double* r, long long n, Rec* rec,
+                                                        unsigned* counter, Rec* out) {
+  __shared__ Rec smr[kWarps];
+  __shared__ int is_last;
+  double bv = -1.0;
+  long long bj = 0x7fffffffffffffffLL;
+  for (long long j = blockIdx.x * (long long)kThreads + threadIdx.x; j < n;
+       j += (long long)gridDim.x * kThreads)
+    if (rec_better(r[j], j, bv, bj)) {
+      bv = r[j];
+      bj = j;
+    }
+  block_argmax<kThreads>(bv, bj, smr);
+  if (threadIdx.x == 0) {
+    rec[blockIdx.x] = Rec{bv, bj};
+    __threadfence();
+    is_last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  bv = -1.0;
+  bj = 0x7fffffffffffffffLL;
+  for (unsigned b = threadIdx.x; b < gridDim.x; b += kThreads) {
+    const Rec rr{__ldcg(&rec[b].v), __ldcg(&rec[b].j)};
+    if (rec_better(rr.v, rr.j, bv, bj)) {
+      bv = rr.v;
+      bj = rr.j;
+    }
+  }
+  block_argmax<kThreads>(bv, bj, smr);
+  if (threadIdx.x == 0) {
+    *counter = 0u;
+    if (bj == 0x7fffffffffffffffLL) bj = 0;
+    out[0] = Rec{sqrt(bv > 0.0 ? bv : 0.0), bj};
+  }
+}
+
+// Identity error_sq (workspace.cpp:84-99) for one column from the T rows.
+__global__ void k_error_sq(const double* T, long long n, long long d, long long j,
+                           const double* c, const double* col_sq, double* out) {
+  __shared__ double sm[kWarps];
+  double cross = 0.0, quad = 0.0;
+  for (long long k = threadIdx.x; k < d; k += kThreads) {
+    cross = fma(c[k], T[k * n + j], cross);
+    quad = fma(c[k], c[k], quad);
+  }
+  cross = block_sum_fixed<kThreads>(cross, sm);
+  quad = block_sum_fixed<kThreads>(quad, sm);
+  if (threadIdx.x == 0) {
+    const double e2 = col_sq[j] - 2.0 * cross + quad;
+    out[0] = e2 > 0.0 ? e2 : 0.0;
+  }
+}
+
+}  // namespace rbdk
