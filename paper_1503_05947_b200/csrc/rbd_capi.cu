@@ -16,6 +16,7 @@
 #include "rbd_cuda.h"
 #include "rbd_device.cuh"
 #include "rbd_project.cuh"
+#include "rbd_persistent.cuh"
 
 using namespace rbdk;
 
@@ -105,6 +106,7 @@ struct rbd_ctx_s {
   cudaStream_t stream = nullptr;
   DevBuf partial, rec, counter, state, colsq, resid, w, c, p, nrm, hist, sel, out_rec, scratch1;
   DevBuf hX, hY, hT;  // cached device copies for the host entry
+  DevBuf ppart;       // fused-extension partials
   DevState* h_state = nullptr;  // pinned
   Rec* h_rec = nullptr;         // pinned
   cudaGraphExec_t gexec = nullptr;
@@ -112,6 +114,11 @@ struct rbd_ctx_s {
   long long graph_nodes = 0;
   long long launches = 0;
   int occ_sweep2 = 2, occ_sweep1 = 2;
+  int fused_grid_cap = 296;
+  int persist_occ2 = 0, persist_occ1 = 0;  // co-resident CTAs/SM of the persistent kernel
+  int path = 0;                            // 0 persistent, 1 graph of per-phase kernels
+  DevBuf bar;                              // grid-barrier words
+  DevBuf ctl, gcnt, ygcnt;                 // persistent loop: ctl words, p double buffer, group records
   // multi-GPU
   void* comm = nullptr;
   int rank = 0, world = 1;
@@ -321,6 +328,161 @@ int enqueue_step(rbd_ctx_t ctx, const LoopBufs& L) {
   return RBD_OK;
 }
 
+bool use_fused(long long d_max) { return d_max <= kFMaxCoef; }
+
+int fused_grid(rbd_ctx_t ctx, long long m) {
+  return (int)std::max<long long>(1, std::min<long long>(cdiv(m, kFRows), ctx->fused_grid_cap));
+}
+
+size_t fused_smem(long long dcap) { return sizeof(double) * 3 * (size_t)std::max<long long>(dcap, 1); }
+size_t persist_smem(long long dcap) { return sizeof(double) * 2 * (size_t)std::max<long long>(dcap, 1); }
+
+// Materialise a pending column / clear the pending flag (used after the loop).
+int enqueue_fused_ext(rbd_ctx_t ctx, const LoopBufs& L) {
+  DevState* st = ptr<DevState>(ctx->state);
+  FusedArgs fa{};
+  fa.Y = L.Y;
+  fa.m = L.m;
+  fa.X = L.X;
+  fa.ldx = L.ldx;
+  fa.c = ptr<double>(ctx->c);
+  fa.p = ptr<double>(ctx->p);
+  fa.w = ptr<double>(ctx->w);
+  fa.ppart = ptr<double>(ctx->ppart);
+  fa.pstride = L.d_max;
+  fa.npart = ptr<double>(ctx->nrm);
+  fa.st = st;
+  fa.dcap = L.d_max;
+  const int ga = fused_grid(ctx, L.m);
+  k_ext_fused<<<ga, kThreads, fused_smem(L.d_max), ctx->stream>>>(fa);
+  ctx->launches++;
+  ReduceArgs ra{};
+  ra.ppart = ptr<double>(ctx->ppart);
+  ra.pstride = L.d_max;
+  ra.nparts = ga;
+  ra.npart = ptr<double>(ctx->nrm);
+  ra.p = ptr<double>(ctx->p);
+  ra.st = st;
+  ra.selected = ptr<long long>(ctx->sel);
+  k_ext_reduce<<<(unsigned)std::max<long long>(1, cdiv(L.d_max, 32)), kThreads, 0, ctx->stream>>>(ra);
+  ctx->launches++;
+  CU(cudaGetLastError());
+  return RBD_OK;
+}
+
+// One greedy step on the fused path: A (extension pass, one Y read), B
+// (reduce + reorth decision + breakdown), C (fused X sweep on w1), D
+// (normalise/correct T row, residuals, argmax, state).
+int enqueue_step_fused(rbd_ctx_t ctx, const LoopBufs& L) {
+  DevState* st = ptr<DevState>(ctx->state);
+  TRY(enqueue_fused_ext(ctx, L));
+  const int vec = (L.ldx % 2 == 0 && aligned16(L.X) && aligned16(ctx->w.p)) ? 2 : 1;
+  SweepArgs s{};
+  s.A = L.X;
+  s.lda = L.ldx;
+  s.m = L.m;
+  s.ncols = L.n;
+  s.v = ptr<double>(ctx->w);
+  s.partial = ptr<double>(ctx->partial);
+  s.pstride = L.n;
+  s.st = st;
+  s.gate = GATE_LIVE;
+  TRY(launch_sweep(ctx, s, vec, MODE_DOT, true, L.n));
+  Finalize2Args f{};
+  f.partial = ptr<double>(ctx->partial);
+  f.S = cdiv(L.m, kChunk);
+  f.n = L.n;
+  f.T = L.T;
+  f.p = ptr<double>(ctx->p);
+  f.r = ptr<double>(ctx->resid);
+  f.col_sq = ptr<double>(ctx->colsq);
+  f.st = st;
+  f.rec = ptr<Rec>(ctx->rec);
+  f.counter = ptr<unsigned>(ctx->counter);
+  f.history = ptr<double>(ctx->hist);
+  f.cbuf = ptr<double>(ctx->c);
+  f.mode = 0;
+  const int g = (int)std::max<long long>(1, std::min<long long>(cdiv(L.n, kF2Cols), (long long)ctx->nsm * 4));
+  k_finalize_fused<<<g, kThreads, 0, ctx->stream>>>(f);
+  ctx->launches++;
+  CU(cudaGetLastError());
+  return RBD_OK;
+}
+
+int persistent_grid(rbd_ctx_t ctx, int vec, long long d_max) {
+  int occ = 0;
+  const size_t smem = persist_smem(d_max);
+  if (vec == 2)
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_rbd_persistent<2>, kThreads, smem);
+  else
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_rbd_persistent<1>, kThreads, smem);
+  occ = std::min(occ, 2);
+  return occ * ctx->nsm;
+}
+
+// The whole greedy loop in one cooperative launch (single GPU).
+int launch_persistent(rbd_ctx_t ctx, const LoopBufs& L) {
+  const int vec = (L.ldx % 2 == 0 && L.m % 2 == 0 && aligned16(L.X) && aligned16(L.Y) &&
+                   aligned16(ctx->w.p)) ? 2 : 1;
+  const int grid = persistent_grid(ctx, vec, L.d_max);
+  if (grid < 1) return set_err(RBD_ERR_CUDA, "persistent kernel: zero occupancy");
+  const long long S = cdiv(L.m, kChunk);
+  const long long ngx = cdiv(L.n, kCols);
+  TRY(ensure(ctx->ppart, sizeof(double) * (size_t)std::max<long long>(grid, S) * L.d_max));
+  TRY(ensure(ctx->ctl, sizeof(StepCtl)));
+  TRY(ensure(ctx->gcnt, sizeof(double) * (size_t)(L.d_max + 1)));   // p_k
+  TRY(ensure(ctx->ygcnt, sizeof(Rec) * (size_t)grid));              // CTA records
+  CU(cudaMemsetAsync(ctx->ctl.p, 0, sizeof(StepCtl), ctx->stream));
+  (void)ngx;
+  TRY(ensure(ctx->nrm, sizeof(double) * std::max<long long>(gemv_grid(L.m), grid)));
+  TRY(ensure(ctx->rec, sizeof(Rec) * (size_t)std::max(grid, ctx->nsm * 8)));
+  PersistArgs a{};
+  a.X = L.X;
+  a.ldx = L.ldx;
+  a.m = L.m;
+  a.n = L.n;
+  a.Y = L.Y;
+  a.T = L.T;
+  a.w = ptr<double>(ctx->w);
+  a.p = ptr<double>(ctx->gcnt);
+  a.ppart = ptr<double>(ctx->ppart);
+  a.npart = ptr<double>(ctx->nrm);
+  a.partial = ptr<double>(ctx->partial);
+  a.r = ptr<double>(ctx->resid);
+  a.col_sq = ptr<double>(ctx->colsq);
+  a.rec = ptr<Rec>(ctx->ygcnt);
+  a.history = ptr<double>(ctx->hist);
+  a.selected = ptr<long long>(ctx->sel);
+  a.st = ptr<DevState>(ctx->state);
+  a.bar = ptr<unsigned>(ctx->bar);
+  a.d_max = L.d_max;
+  a.ctl = ptr<StepCtl>(ctx->ctl);
+  a.phase_ns = nullptr;
+  if (getenv("RBD_PHASE_TIMING")) {
+    TRY(ensure(ctx->scratch1, 256));
+    cudaMemsetAsync(ctx->scratch1.p, 0, 128, ctx->stream);
+    a.phase_ns = ptr<unsigned long long>(ctx->scratch1);
+  }
+  void* args[] = {&a};
+  const size_t smem = persist_smem(L.d_max);
+  cudaError_t e = vec == 2 ? cudaLaunchCooperativeKernel((void*)k_rbd_persistent<2>, grid, kThreads,
+                                                         args, smem, ctx->stream)
+                           : cudaLaunchCooperativeKernel((void*)k_rbd_persistent<1>, grid, kThreads,
+                                                         args, smem, ctx->stream);
+  ctx->launches++;
+  if (e != cudaSuccess)
+    return set_err(RBD_ERR_CUDA, std::string("persistent launch: ") + cudaGetErrorString(e));
+  if (a.phase_ns) {
+    unsigned long long h[10];
+    cudaMemcpyAsync(h, a.phase_ns, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream);
+    cudaStreamSynchronize(ctx->stream);
+    const char* nm[10] = {"P1 ext", "bar1", "P2 queue", "bar2", "state", "claim wait",
+                          "Y tiles", "X tiles", "fin spin", "fin/other"};
+    for (int i = 0; i < 10; ++i) fprintf(stderr, "[phase] %-16s %10.3f ms\n", nm[i], h[i] / 1e6);
+  }
+  return RBD_OK;
+}
+
 int ensure_loop_buffers(rbd_ctx_t ctx, long long m, long long n, long long d_max) {
   const long long S = cdiv(m, kChunk);
   TRY(ensure(ctx->partial, sizeof(double) * S * std::max(n, d_max)));
@@ -336,6 +498,8 @@ int ensure_loop_buffers(rbd_ctx_t ctx, long long m, long long n, long long d_max
   TRY(ensure(ctx->hist, sizeof(double) * d_max));
   TRY(ensure(ctx->sel, sizeof(long long) * d_max));
   TRY(ensure(ctx->out_rec, sizeof(Rec) * 16));
+  TRY(ensure(ctx->ppart, sizeof(double) * (size_t)ctx->fused_grid_cap * d_max));
+  TRY(ensure(ctx->nrm, sizeof(double) * std::max<long long>(gemv_grid(m), ctx->fused_grid_cap)));
   return RBD_OK;
 }
 
@@ -353,7 +517,7 @@ int get_step_graph(rbd_ctx_t ctx, const LoopBufs& L) {
   k.stream = ctx->stream;
   k.steps = kGraphSteps;
   DevBuf* bl[8] = {&ctx->partial, &ctx->rec, &ctx->state, &ctx->colsq,
-                   &ctx->resid,   &ctx->w,   &ctx->c,     &ctx->nrm};
+                   &ctx->resid,   &ctx->w,   &ctx->c,     &ctx->ppart};
   for (int i = 0; i < 8; ++i) k.bufs[i] = bl[i]->p;
   if (ctx->gexec && ctx->gkey == k) return RBD_OK;
   if (ctx->gexec) {
@@ -363,7 +527,8 @@ int get_step_graph(rbd_ctx_t ctx, const LoopBufs& L) {
   const long long before = ctx->launches;
   CU(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
   int rc = RBD_OK;
-  for (int s = 0; s < kGraphSteps && rc == RBD_OK; ++s) rc = enqueue_step(ctx, L);
+  for (int s = 0; s < kGraphSteps && rc == RBD_OK; ++s)
+    rc = use_fused(L.d_max) ? enqueue_step_fused(ctx, L) : enqueue_step(ctx, L);
   cudaGraph_t g = nullptr;
   cudaError_t ec = cudaStreamEndCapture(ctx->stream, &g);
   ctx->launches = before;  // captured launches are counted per replay
@@ -469,6 +634,15 @@ int rbd_ctx_create(int device, rbd_ctx_t* out) {
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_sweep<1, MODE_DOT, true>, kThreads, 0) ==
           cudaSuccess && o > 0)
     ctx->occ_sweep1 = o;
+  cudaFuncSetAttribute(k_ext_fused, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)fused_smem(kFMaxCoef));
+  ctx->fused_grid_cap = 2 * ctx->nsm;
+  cudaFuncSetAttribute(k_rbd_persistent<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)fused_smem(kFMaxCoef));
+  cudaFuncSetAttribute(k_rbd_persistent<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)fused_smem(kFMaxCoef));
+  if (const char* pth = getenv("RBD_PATH")) ctx->path = (std::string(pth) == "graph") ? 1 : 0;
+  if (ensure(ctx->bar, 64) == RBD_OK) cudaMemset(ctx->bar.p, 0, 64);
   *out = ctx;
   return RBD_OK;
 }
@@ -481,7 +655,8 @@ int rbd_ctx_destroy(rbd_ctx_t ctx) {
   DevBuf* bl[] = {&ctx->partial, &ctx->rec,  &ctx->counter, &ctx->state, &ctx->colsq,
                   &ctx->resid,   &ctx->w,    &ctx->c,       &ctx->p,     &ctx->nrm,
                   &ctx->hist,    &ctx->sel,  &ctx->out_rec, &ctx->scratch1,
-                  &ctx->hX,      &ctx->hY,   &ctx->hT};
+                  &ctx->hX,      &ctx->hY,   &ctx->hT,      &ctx->ppart, &ctx->bar,
+                  &ctx->ctl,     &ctx->gcnt, &ctx->ygcnt};
   for (DevBuf* b : bl) release(*b);
   if (ctx->h_state) cudaFreeHost(ctx->h_state);
   if (ctx->h_rec) cudaFreeHost(ctx->h_rec);
@@ -572,35 +747,41 @@ int rbd_decompose_device(rbd_ctx_t ctx, const double* dX, int64_t m, int64_t n, 
   CU(cudaMemcpyAsync(st, ctx->h_state, sizeof(DevState), cudaMemcpyHostToDevice, ctx->stream));
 
   LoopBufs L{dX, m, n, ldx, cfg->d_max, dY, dT};
-  TRY(get_step_graph(ctx, L));
-  CU(cudaEventRecord(ev1, ctx->stream));
-  // Replay G-step graphs; the done flag is polled one graph behind so the
-  // device never waits for the host.
-  volatile int* hdone = &ctx->h_state->done;
-  long long launched = 0;
-  bool pending = false;
-  cudaEvent_t ev;
-  CU(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-  int rc = RBD_OK;
-  while (launched < cfg->d_max) {
-    cudaError_t e = cudaGraphLaunch(ctx->gexec, ctx->stream);
-    if (e != cudaSuccess) {
-      rc = set_err(RBD_ERR_CUDA, std::string("graph launch: ") + cudaGetErrorString(e));
-      break;
+  if (ctx->path == 0 && use_fused(cfg->d_max)) {
+    CU(cudaEventRecord(ev1, ctx->stream));
+    TRY(launch_persistent(ctx, L));
+  } else {
+    TRY(get_step_graph(ctx, L));
+    CU(cudaEventRecord(ev1, ctx->stream));
+    // Replay G-step graphs; the done flag is polled one graph behind so the
+    // device never waits for the host.
+    volatile int* hdone = &ctx->h_state->done;
+    long long launched = 0;
+    bool pending = false;
+    cudaEvent_t ev;
+    CU(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    int rc = RBD_OK;
+    while (launched < cfg->d_max) {
+      cudaError_t e = cudaGraphLaunch(ctx->gexec, ctx->stream);
+      if (e != cudaSuccess) {
+        rc = set_err(RBD_ERR_CUDA, std::string("graph launch: ") + cudaGetErrorString(e));
+        break;
+      }
+      ctx->launches += ctx->graph_nodes;
+      launched += kGraphSteps;
+      if (pending) {
+        cudaEventSynchronize(ev);
+        if (*hdone) break;
+      }
+      cudaMemcpyAsync((void*)&ctx->h_state->done, &st->done, sizeof(int), cudaMemcpyDeviceToHost,
+                      ctx->stream);
+      cudaEventRecord(ev, ctx->stream);
+      pending = true;
     }
-    ctx->launches += ctx->graph_nodes;
-    launched += kGraphSteps;
-    if (pending) {
-      cudaEventSynchronize(ev);
-      if (*hdone) break;
-    }
-    cudaMemcpyAsync((void*)&ctx->h_state->done, &st->done, sizeof(int), cudaMemcpyDeviceToHost,
-                    ctx->stream);
-    cudaEventRecord(ev, ctx->stream);
-    pending = true;
+    cudaEventDestroy(ev);
+    if (rc != RBD_OK) return rc;
+    if (use_fused(cfg->d_max)) TRY(enqueue_fused_ext(ctx, L));  // last column's second pass
   }
-  cudaEventDestroy(ev);
-  if (rc != RBD_OK) return rc;
   CU(cudaEventRecord(ev2, ctx->stream));
   CU(cudaMemcpyAsync(ctx->h_state, st, sizeof(DevState), cudaMemcpyDeviceToHost, ctx->stream));
   CU(cudaStreamSynchronize(ctx->stream));

@@ -33,6 +33,8 @@ constexpr int kCoefTile = 2048;    // coefficients staged in smem per pass
 
 enum Gate : int { GATE_NONE = 0, GATE_LIVE = 1, GATE_REORTH = 2 };
 enum SweepMode : int { MODE_INIT = 0, MODE_DOT = 1 };
+// load flavour of the swept matrix: read-only path, streaming, or L2-coherent
+enum LoadKind : int { LOAD_NC = 0, LOAD_STREAM = 1, LOAD_CG = 2 };
 
 // Device-resident loop state. Every per-step kernel reads it, so one captured
 // CUDA graph of G steps is valid for any step index.
@@ -55,7 +57,9 @@ struct DevState {
   unsigned flags_nonzero;
   unsigned long long max_colsq_bits;  // max_j col_sq (as ordered bits, >= 0)
   int rank_owner;         // multi-GPU: rank owning jstar
-  int pad;
+  int pending;            // column d-1 of Y not yet materialised (fused path)
+  unsigned counter_b;     // last-CTA counter of k_ext_reduce
+  unsigned pad2;
 };
 
 struct Rec {            // max-loc record: value desc, index asc (workspace.cpp:109)
@@ -111,12 +115,15 @@ struct SweepArgs {
   int csel;               // 1: ncols = st->d (reorth pass over Y)
 };
 
-template <int VEC, int MODE, bool STREAM>
-__global__ void __launch_bounds__(kThreads, 2) k_sweep(SweepArgs a) {
-  if (gate_skip(a.st, a.gate)) return;
-  const long long m = a.m;
-  const long long ncols = a.csel ? a.st->d : a.ncols;
-  const double* __restrict__ v = a.vsel ? a.vbase + a.st->d * a.vstride : a.v;
+// Tile loop shared by the standalone sweep kernel and the persistent loop.
+template <int VEC, int MODE, int ALOAD, bool VCOH = false>
+__device__ __forceinline__ void sweep_tiles(const double* __restrict__ A, long long lda,
+                                            long long m, long long ncols,
+                                            const double* __restrict__ v,
+                                            double* __restrict__ partial, long long pstride,
+                                            long long tile_begin, long long tile_stride,
+                                            double (*red)[kCols], unsigned& nonfinite,
+                                            unsigned& nonzero) {
   const long long S = (m + kChunk - 1) / kChunk;
   const long long G = (ncols + kCols - 1) / kCols;
   const long long ntiles = S * G;
@@ -124,10 +131,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_sweep(SweepArgs a) {
   const int lane = tid & 31, warp = tid >> 5;
   constexpr int U = kChunk / (VEC * kThreads);  // element groups per thread per column
   constexpr int UB = (VEC == 2) ? 4 : 8;         // batch of groups loaded together
-  __shared__ double red[kWarps][kCols];
-  unsigned nonfinite = 0, nonzero = 0;
 
-  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  for (long long tile = tile_begin; tile < ntiles; tile += tile_stride) {
     const long long s = tile / G;
     const long long g = tile - s * G;
     const long long row0 = s * kChunk;
@@ -140,7 +145,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_sweep(SweepArgs a) {
 #pragma unroll
     for (int c = 0; c < kCols; ++c) {
       const long long cc = (col0 + c < ncols) ? col0 + c : col0;  // clamp (unused cols)
-      Ac[c] = a.A + cc * a.lda + row0;
+      Ac[c] = A + cc * lda + row0;
     }
     const double* vr = (MODE == MODE_DOT) ? v + row0 : nullptr;
 
@@ -153,10 +158,13 @@ __global__ void __launch_bounds__(kThreads, 2) k_sweep(SweepArgs a) {
 #pragma unroll
           for (int u = 0; u < UB; ++u) {
             const int e = (tid + (ub + u) * kThreads) * 2;
-            if constexpr (MODE == MODE_DOT) yv[u] = ld_keep2(vr + e);
+            if constexpr (MODE == MODE_DOT)
+              yv[u] = VCOH ? __ldcg(reinterpret_cast<const double2*>(vr + e)) : ld_keep2(vr + e);
 #pragma unroll
             for (int c = 0; c < kCols; ++c)
-              xv[u][c] = STREAM ? ld_stream2(Ac[c] + e) : ld_keep2(Ac[c] + e);
+              xv[u][c] = ALOAD == LOAD_STREAM ? ld_stream2(Ac[c] + e)
+                         : ALOAD == LOAD_CG   ? __ldcg(reinterpret_cast<const double2*>(Ac[c] + e))
+                                              : ld_keep2(Ac[c] + e);
           }
 #pragma unroll
           for (int u = 0; u < UB; ++u)
@@ -178,10 +186,12 @@ __global__ void __launch_bounds__(kThreads, 2) k_sweep(SweepArgs a) {
 #pragma unroll
           for (int u = 0; u < UB; ++u) {
             const int e = tid + (ub + u) * kThreads;
-            if constexpr (MODE == MODE_DOT) yv[u] = ld_keep1(vr + e);
+            if constexpr (MODE == MODE_DOT) yv[u] = VCOH ? __ldcg(vr + e) : ld_keep1(vr + e);
 #pragma unroll
             for (int c = 0; c < kCols; ++c)
-              xv[u][c] = STREAM ? ld_stream1(Ac[c] + e) : ld_keep1(Ac[c] + e);
+              xv[u][c] = ALOAD == LOAD_STREAM ? ld_stream1(Ac[c] + e)
+                         : ALOAD == LOAD_CG   ? __ldcg(Ac[c] + e)
+                                              : ld_keep1(Ac[c] + e);
           }
 #pragma unroll
           for (int u = 0; u < UB; ++u)
@@ -206,14 +216,14 @@ __global__ void __launch_bounds__(kThreads, 2) k_sweep(SweepArgs a) {
           const long long e = (long long)(tid + u * kThreads) * 2;
           double y0 = 0.0, y1 = 0.0;
           if constexpr (MODE == MODE_DOT) {
-            if (e < rows) y0 = vr[e];
-            if (e + 1 < rows) y1 = vr[e + 1];
+            if (e < rows) y0 = __ldcg(vr + e);
+            if (e + 1 < rows) y1 = __ldcg(vr + e + 1);
           }
 #pragma unroll
           for (int c = 0; c < kCols; ++c) {
             if (col0 + c >= ncols) continue;
-            const double x0 = (e < rows) ? Ac[c][e] : 0.0;
-            const double x1 = (e + 1 < rows) ? Ac[c][e + 1] : 0.0;
+            const double x0 = (e < rows) ? __ldcg(Ac[c] + e) : 0.0;
+            const double x1 = (e + 1 < rows) ? __ldcg(Ac[c] + e + 1) : 0.0;
             if constexpr (MODE == MODE_DOT) {
               acc[c] = fma(x0, y0, acc[c]);
               acc[c] = fma(x1, y1, acc[c]);
@@ -228,12 +238,12 @@ __global__ void __launch_bounds__(kThreads, 2) k_sweep(SweepArgs a) {
           const long long e = tid + (long long)u * kThreads;
           double y0 = 0.0;
           if constexpr (MODE == MODE_DOT) {
-            if (e < rows) y0 = vr[e];
+            if (e < rows) y0 = __ldcg(vr + e);
           }
 #pragma unroll
           for (int c = 0; c < kCols; ++c) {
             if (col0 + c >= ncols) continue;
-            const double x0 = (e < rows) ? Ac[c][e] : 0.0;
+            const double x0 = (e < rows) ? __ldcg(Ac[c] + e) : 0.0;
             if constexpr (MODE == MODE_DOT) {
               acc[c] = fma(x0, y0, acc[c]);
             } else {
@@ -260,10 +270,23 @@ __global__ void __launch_bounds__(kThreads, 2) k_sweep(SweepArgs a) {
       double sum = red[0][tid];
 #pragma unroll
       for (int w = 1; w < kWarps; ++w) sum += red[w][tid];
-      a.partial[s * a.pstride + col0 + tid] = sum;
+      partial[s * pstride + col0 + tid] = sum;
     }
     __syncthreads();
   }
+}
+
+template <int VEC, int MODE, bool STREAM>
+__global__ void __launch_bounds__(kThreads, 2) k_sweep(SweepArgs a) {
+  if (gate_skip(a.st, a.gate)) return;
+  const long long ncols = a.csel ? a.st->d : a.ncols;
+  const double* v = a.vsel ? a.vbase + a.st->d * a.vstride : a.v;
+  __shared__ double red[kWarps][kCols];
+  unsigned nonfinite = 0, nonzero = 0;
+  sweep_tiles<VEC, MODE, STREAM ? LOAD_STREAM : LOAD_NC>(a.A, a.lda, a.m, ncols, v, a.partial,
+                                                          a.pstride, blockIdx.x, gridDim.x, red,
+                                                          nonfinite, nonzero);
+  const int tid = threadIdx.x;
   if constexpr (MODE == MODE_INIT) {
     const int any_nf = __syncthreads_or(nonfinite);
     const int any_nz = __syncthreads_or(nonzero);
@@ -653,6 +676,361 @@ __global__ void k_error_sq(const double* T, long long n, long long d, long long 
   if (threadIdx.x == 0) {
     const double e2 = col_sq[j] - 2.0 * cross + quad;
     out[0] = e2 > 0.0 ? e2 : 0.0;
+  }
+}
+
+}  // namespace rbdk
+
+namespace rbdk {
+
+// ===========================================================================
+// Fused extension (decompose loop). Y is read from HBM once per step.
+//
+// Step k (k = st->d accepted columns; column k-1 may be "pending": its
+// second-pass correction not yet applied). For every 32-row block:
+//   phase 1 (one HBM read of Y[rows, 0:kb], kb = materialised columns):
+//     y_{k-1}  = (w1_{k-1} - Y p_{k-1}) / ||w_{k-1}||   -> Y[:, k-1]
+//     w1_k     = x_{j*} - Y[:, 0:k] c,   c = T[0:k, j*]  (CGS pass 1)
+//   phase 2 (re-read of the same block, L2 resident):
+//     p_k     += Y[rows, 0:k]' w1_k[rows]                (reorth coefficients)
+// k_ext_reduce then sums the CTA partials, applies decompose.cpp:28's
+// condition (second pass iff reorthogonalize or ||w1|| < 0.5 ||x||), sets
+// ||w_k||^2 = ||w1||^2 - ||p||^2 and performs the breakdown test (:29-30).
+// The sweep runs on the unnormalised w1_k and k_finalize_fused forms
+//   T[k, j] = (w1_k . x_j - p_k . T[0:k, j]) / ||w_k||  ( = y_k . x_j ).
+// ===========================================================================
+constexpr int kFRows = 32;        // rows per fused-extension block
+constexpr int kFMaxCoef = 4096;   // fused path handles d_max <= this
+
+struct FusedArgs {
+  double* Y;              // m x d_max column-major (ld m)
+  long long m;
+  const double* X;        // x = X + st->jlocal * ldx (if X != nullptr)
+  long long ldx;
+  const double* xsrc;     // otherwise x = xsrc
+  const double* c;        // T[0:k, j*]
+  const double* p;        // p_{k-1} (zeroed when the pass was skipped)
+  double* w;              // in: w1_{k-1}; out: w1_k
+  double* ppart;          // [gridDim.x][pstride]
+  long long pstride;
+  double* npart;          // [gridDim.x]
+  DevState* st;
+  long long dcap;         // coefficient capacity (= d_max) of the smem arrays
+};
+
+__global__ void __launch_bounds__(kThreads) k_ext_fused(FusedArgs a) {
+  DevState* st = a.st;
+  const int pending = st->pending;
+  const int live = !st->done;
+  if (!pending && !live) return;
+  const long long k = st->d;
+  const long long kb = pending ? k - 1 : k;  // columns already materialised
+  const long long m = a.m;
+  extern __shared__ double fsm[];
+  double* cs = fsm;                 // c[0:k]
+  double* ps = cs + a.dcap;         // p_{k-1}[0:kb]
+  double* pacc = ps + a.dcap;       // this CTA's p_k partial [0:k]
+  __shared__ double red_c[kWarps][kFRows];
+  __shared__ double red_p[kWarps][kFRows];
+  __shared__ double w1s[kFRows];
+  __shared__ double yns[kFRows];
+  __shared__ double smn[kWarps];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (long long l = tid; l < k; l += kThreads) {
+    cs[l] = live ? a.c[l] : 0.0;
+    pacc[l] = 0.0;
+  }
+  for (long long l = tid; l < kb; l += kThreads) ps[l] = pending ? a.p[l] : 0.0;
+  const double wprev_norm = st->wnorm;
+  const double* x = a.X ? a.X + st->jlocal * a.ldx : a.xsrc;
+  __syncthreads();
+
+  const long long nblk = (m + kFRows - 1) / kFRows;
+  const long long b0 = nblk * blockIdx.x / gridDim.x;
+  const long long b1 = nblk * (blockIdx.x + 1) / gridDim.x;
+  double nacc = 0.0;
+  for (long long b = b0; b < b1; ++b) {
+    const long long row0 = b * kFRows;
+    // ---- phase 1: lane = row, warp w takes l = w, w+8, ... ----
+    {
+      const long long i = row0 + lane;
+      const bool ok = i < m;
+      double acc_c = 0.0, acc_p = 0.0;
+      if (ok) {
+        const double* yp = a.Y + i + (long long)warp * m;
+        const long long stp = (long long)kWarps * m;
+        long long l = warp;
+        for (; l + 7 * kWarps < kb; l += 8 * kWarps) {
+          double yv[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) yv[q] = yp[q * stp];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            acc_c = fma(yv[q], cs[l + q * kWarps], acc_c);
+            acc_p = fma(yv[q], ps[l + q * kWarps], acc_p);
+          }
+          yp += 8 * stp;
+        }
+        for (; l < kb; l += kWarps) {
+          const double y0 = *yp;
+          acc_c = fma(y0, cs[l], acc_c);
+          acc_p = fma(y0, ps[l], acc_p);
+          yp += stp;
+        }
+      }
+      red_c[warp][lane] = acc_c;
+      red_p[warp][lane] = acc_p;
+      __syncthreads();
+      if (warp == 0) {
+        double sc = red_c[0][lane], sp = red_p[0][lane];
+#pragma unroll
+        for (int w = 1; w < kWarps; ++w) {
+          sc += red_c[w][lane];
+          sp += red_p[w][lane];
+        }
+        double yk1 = 0.0, w1 = 0.0;
+        if (ok) {
+          if (pending) {
+            yk1 = (a.w[i] - sp) / wprev_norm;        // second pass of column k-1
+            a.Y[i + (k - 1) * m] = yk1;
+            sc = fma(yk1, cs[k - 1], sc);
+          }
+          if (live) {
+            w1 = x[i] - sc;                          // first pass of column k
+            a.w[i] = w1;
+            nacc = fma(w1, w1, nacc);
+          }
+        }
+        w1s[lane] = w1;
+        yns[lane] = yk1;
+      }
+      __syncthreads();
+    }
+    if (!live) continue;
+    // ---- phase 2: p_k += Y[rows, 0:k]' w1 (lane = 8 columns x 4 row segments) ----
+    {
+      const int cq = lane >> 2, rs = lane & 3;
+      double wv[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) wv[q] = w1s[rs * 8 + q];
+      const long long ib = row0 + rs * 8;
+      const int nrow = (int)((m - ib) < 8 ? (m - ib) : 8);
+      // warp-uniform trip count: every lane reaches the shuffles
+      for (long long lb = warp * 8; lb < kb; lb += 64) {
+        const long long l = lb + cq;
+        double s = 0.0;
+        if (l < kb) {
+          const double* yp = a.Y + ib + l * m;
+          if (nrow == 8) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) s = fma(yp[q], wv[q], s);
+          } else {
+            for (int q = 0; q < nrow; ++q) s = fma(yp[q], wv[q], s);
+          }
+        }
+        s += __shfl_xor_sync(0xffffffffu, s, 1);
+        s += __shfl_xor_sync(0xffffffffu, s, 2);
+        if (rs == 0 && l < kb) pacc[l] += s;
+      }
+      if (pending && warp == 0) {   // the column materialised in phase 1
+        double s = yns[lane] * w1s[lane];
+        for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+        if (lane == 0) pacc[k - 1] += s;
+      }
+    }
+    __syncthreads();
+  }
+  // publish the CTA partials
+  if (live) {
+    for (long long l = tid; l < k; l += kThreads) a.ppart[blockIdx.x * a.pstride + l] = pacc[l];
+    const double s = block_sum_fixed<kThreads>(warp == 0 ? nacc : 0.0, smn);
+    if (tid == 0) a.npart[blockIdx.x] = s;
+  }
+}
+
+// Sum of the k_ext_fused partials, the reorth decision, ||w_k|| and the
+// breakdown test. Grid: ceil(k/32) CTAs of 256 threads (32 columns x 8 splits)
+// plus a last-CTA finish.
+struct ReduceArgs {
+  const double* ppart;
+  long long pstride;
+  int nparts;
+  const double* npart;
+  double* p;              // out: p_k (zeroed if the second pass is skipped)
+  DevState* st;
+  long long* selected;
+};
+
+__global__ void __launch_bounds__(kThreads) k_ext_reduce(ReduceArgs a) {
+  DevState* st = a.st;
+  __shared__ double sred[kWarps][32];
+  __shared__ double smn[kWarps];
+  __shared__ int is_last;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int live = !st->done;
+  const long long k = st->d;
+  if (live) {
+    const long long l = (long long)blockIdx.x * 32 + lane;
+    double s = 0.0;
+    if (l < k)
+      for (int b = warp; b < a.nparts; b += kWarps) s += a.ppart[(long long)b * a.pstride + l];
+    sred[warp][lane] = s;
+    __syncthreads();
+    if (warp == 0 && l < k) {
+      double t = sred[0][lane];
+#pragma unroll
+      for (int w = 1; w < kWarps; ++w) t += sred[w][lane];
+      a.p[l] = t;
+    }
+    __threadfence();
+  }
+  __syncthreads();
+  if (tid == 0) is_last = (atomicAdd(&st->counter_b, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  if (tid == 0) st->counter_b = 0u;
+  const int pending_was = st->pending;
+  if (!live) {
+    if (tid == 0 && pending_was) st->pending = 0;   // materialised by k_ext_fused
+    return;
+  }
+  double w1n2 = 0.0;
+  for (int b = tid; b < a.nparts; b += kThreads) w1n2 += a.npart[b];
+  w1n2 = block_sum_fixed<kThreads>(w1n2, smn);
+  double pn = 0.0;
+  for (long long l = tid; l < k; l += kThreads) {
+    const double v = __ldcg(&a.p[l]);
+    pn = fma(v, v, pn);
+  }
+  pn = block_sum_fixed<kThreads>(pn, smn);
+  const int reorth = (k > 0) && (st->cfg_reorth || sqrt(w1n2) < 0.5 * sqrt(st->xnorm2));
+  if (!reorth)
+    for (long long l = tid; l < k; l += kThreads) a.p[l] = 0.0;
+  if (tid == 0) {
+    st->pending = 0;
+    st->reorth = reorth;
+    st->w1n2 = w1n2;
+    double wn2 = reorth ? w1n2 - pn : w1n2;
+    wn2 = wn2 > 0.0 ? wn2 : 0.0;
+    const double norm = sqrt(wn2);
+    if (norm < st->breakdown_tol || norm == 0.0) {
+      st->done = 1;
+      st->breakdown = 1;
+    } else {
+      st->wnorm = norm;
+      if (a.selected) a.selected[k] = st->jstar;
+    }
+  }
+}
+
+// K3 for the fused path: combine sweep partials, apply the reorth correction
+// and the normalisation, update residuals, argmax, state.
+struct Finalize2Args {
+  const double* partial;
+  long long S;
+  long long n;
+  double* T;
+  const double* p;
+  double* r;
+  const double* col_sq;
+  DevState* st;
+  Rec* rec;
+  unsigned* counter;
+  double* history;
+  double* cbuf;
+  Rec* rec_out;          // multi-GPU: local record, no state update
+  long long col_offset;
+  int mode;              // 0 single GPU, 2 multi-GPU local
+};
+
+constexpr int kF2Cols = 32;   // columns per CTA
+__global__ void __launch_bounds__(kThreads) k_finalize_fused(Finalize2Args a) {
+  DevState* st = a.st;
+  if (st->done) return;
+  __shared__ double scorr[kWarps][kF2Cols];
+  __shared__ Rec smr[kWarps];
+  __shared__ int is_last;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const long long n = a.n;
+  const long long k = st->d;
+  const double norm = st->wnorm;
+  const int reorth = st->reorth;
+  double* Trow = a.T + k * n;
+  double bv = -1.0;
+  long long bj = 0x7fffffffffffffffLL;
+  const long long ngroups = (n + kF2Cols - 1) / kF2Cols;
+  for (long long g = blockIdx.x; g < ngroups; g += gridDim.x) {
+    const long long j = g * kF2Cols + lane;
+    const bool ok = j < n;
+    // correction p . T[0:k, j], l split over the 8 warps
+    double corr = 0.0;
+    if (ok && reorth) {
+      for (long long l = warp; l < k; l += kWarps) corr = fma(a.p[l], a.T[l * n + j], corr);
+    }
+    scorr[warp][lane] = corr;
+    // chunk partials (warp w sums chunks s = w, w+8, ... ; combined in order below)
+    __syncthreads();
+    if (warp == 0) {
+      double c = scorr[0][lane];
+#pragma unroll
+      for (int w = 1; w < kWarps; ++w) c += scorr[w][lane];
+      if (ok) {
+        double t = 0.0;
+        for (long long s = 0; s < a.S; ++s) t += a.partial[s * n + j];
+        t = (t - c) / norm;
+        Trow[j] = t;
+        const double sq = __dmul_rn(t, t);
+        double rj = __dsub_rn(a.r[j], sq);
+        rj = rj > 0.0 ? rj : 0.0;
+        a.r[j] = rj;
+        if (rec_better(rj, j, bv, bj)) {
+          bv = rj;
+          bj = j;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  __threadfence();
+  block_argmax<kThreads>(bv, bj, smr);
+  if (tid == 0) {
+    a.rec[blockIdx.x] = Rec{bv, bj};
+    __threadfence();
+    is_last = (atomicAdd(a.counter, 1u) == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  bv = -1.0;
+  bj = 0x7fffffffffffffffLL;
+  for (unsigned b = tid; b < gridDim.x; b += kThreads) {
+    const Rec rr{__ldcg(&a.rec[b].v), __ldcg(&a.rec[b].j)};
+    if (rec_better(rr.v, rr.j, bv, bj)) {
+      bv = rr.v;
+      bj = rr.j;
+    }
+  }
+  block_argmax<kThreads>(bv, bj, smr);
+  if (tid == 0) *a.counter = 0u;
+  if (a.mode == 2) {
+    if (tid == 0) a.rec_out[0] = Rec{bv, bj + a.col_offset};
+    return;
+  }
+  if (tid == 0) {
+    const double e_cur = sqrt(bv > 0.0 ? bv : 0.0);   // workspace.cpp:123
+    a.history[k] = e_cur;                              // decompose.cpp:99
+    st->e_cur = e_cur;
+    st->d = k + 1;                                     // :96
+    st->pending = 1;                                   // y_k awaits its second pass
+    st->jstar = bj;                                    // :101
+    st->jlocal = bj;
+    st->xnorm2 = a.col_sq[bj];
+    st->done = !((k + 1) < st->d_max && e_cur > st->eps_R) ? 1 : 0;  // :87
+  }
+  __syncthreads();
+  if (!st->done) {
+    for (long long l = tid; l <= k; l += kThreads) a.cbuf[l] = __ldcg(&a.T[l * n + bj]);
   }
 }
 

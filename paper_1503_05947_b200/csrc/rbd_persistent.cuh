@@ -1,0 +1,464 @@
+// rbd_persistent.cuh — the whole RBD greedy loop (decompose.cpp:87-102) as ONE
+// persistent cooperative kernel: one CTA pair per SM stays resident for all
+// steps; the phases of a step are separated by grid barriers instead of
+// kernel launches, and every CTA carries an identical copy of the (tiny) loop
+// state, so no host round trip or graph replay happens inside the loop.
+//
+// Step k (k accepted columns, column k-1 possibly "pending"):
+//   P1  extension pass over this CTA's rows (one HBM read of Y):
+//         y_{k-1} = (w1_{k-1} - Y p_{k-1}) / ||w_{k-1}||   -> Y[:, k-1]
+//         w1_k    = x_{j*} - Y c,   c = T[0:k, j*]           (+ ||w1_k||^2)
+//   --- barrier ---
+//   P2  one dynamically scheduled tile queue:
+//         Y'w1 tiles (reorth coefficients p_k; Y is still L2-hot) — the last
+//           one decides the second pass (decompose.cpp:28), ||w_k|| and the
+//           breakdown test (:29-30) and publishes them;
+//         X'w1 tiles (the fused sweep) — the last chunk of a 4-column group
+//           finalises T[k, j] = (w1_k . x_j - p_k . T[0:k, j]) / ||w_k||, the
+//           residuals (workspace.cpp:52-53) and a group record; the last group
+//           publishes the global argmax (workspace.cpp:107-113,123).
+//   --- barrier ---
+//       every CTA: stop test (decompose.cpp:87) on the published outcome
+#pragma once
+
+#include "rbd_device.cuh"
+
+namespace rbdk {
+
+struct PersistArgs {
+  const double* X;
+  long long ldx;
+  long long m;
+  long long n;
+  double* Y;
+  double* T;
+  double* w;
+  double* p;
+  double* ppart;      // [G][d_max]
+  double* npart;      // [G]
+  double* partial;    // [S][n]
+  double* r;
+  const double* col_sq;
+  Rec* rec;           // [G]
+  double* history;
+  long long* selected;
+  DevState* st;
+  unsigned* bar;      // [0] arrival count, [1] generation
+  long long d_max;
+  unsigned long long* phase_ns;  // optional [8] accumulated phase times (CTA 0)
+  struct StepCtl* ctl;           // queue / publish words
+};
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ long long ld_acquire_s64_(const long long* p) {
+  long long v;
+  asm volatile("ld.acquire.gpu.global.s64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void wait_step_ne(const long long* flag, long long bad) {
+  const unsigned long long t0 = globaltimer();
+  unsigned spins = 0;
+  while (ld_acquire_s64_(flag) == bad) {
+    __nanosleep(32);
+    if ((++spins & 0xfffu) == 0 && globaltimer() - t0 > 30000000000ull) __trap();
+  }
+}
+
+// Sense-reversing grid barrier (all CTAs co-resident: cooperative launch).
+// Traps after 30 s instead of hanging the device.
+__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned& gen) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned target = gen + 1;
+    if (atomicAdd(&bar[0], 1u) == gridDim.x - 1) {
+      bar[0] = 0u;
+      __threadfence();
+      atomicAdd(&bar[1], 1u);
+    } else {
+      const unsigned long long t0 = globaltimer();
+      unsigned spins = 0;
+      while (ld_acquire_u32(&bar[1]) != target) {
+        __nanosleep(64);
+        if ((++spins & 0xffffu) == 0 && globaltimer() - t0 > 30000000000ull) __trap();
+      }
+    }
+    __threadfence();
+    gen = target;
+  }
+  __syncthreads();
+}
+
+// Shared step bookkeeping (device memory, see PersistArgs::ctl).
+struct StepCtl {
+  unsigned long long tile_ctr;   // monotonic tile-claim counter (all steps, all calls)
+  // published by the decider (claimer of the last Y'w1 tile), tagged with step+1
+  long long p_step;
+  double norm;
+  int reorth;
+  int breakdown;
+  // published by the claimer of the last tile, tagged with step+1
+  long long r_step;
+  double e_cur;
+  long long jstar;
+};
+
+__device__ __forceinline__ long long ld_acquire_s64(const long long* p) {
+  long long v;
+  asm volatile("ld.acquire.gpu.global.s64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_s64(long long* p, long long v) {
+  asm volatile("st.release.gpu.global.s64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ double ld_relaxed_f64(const double* p) {
+  double v;
+  asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_f64(double* p, double v) {
+  asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+
+// Poll a value produced by an earlier-claimed tile (NaN = not yet written).
+__device__ __forceinline__ double poll_f64(const double* p) {
+  double v = ld_relaxed_f64(p);
+  if (v == v) return v;
+  const unsigned long long t0 = globaltimer();
+  unsigned spins = 0;
+  do {
+    __nanosleep(32);
+    v = ld_relaxed_f64(p);
+    if ((++spins & 0xfffu) == 0 && globaltimer() - t0 > 30000000000ull) __trap();
+  } while (v != v);
+  return v;
+}
+
+__device__ __forceinline__ void wait_step(const long long* flag, long long want) {
+  const unsigned long long t0 = globaltimer();
+  unsigned spins = 0;
+  while (ld_acquire_s64(flag) != want) {
+    __nanosleep(32);
+    if ((++spins & 0xfffu) == 0 && globaltimer() - t0 > 30000000000ull) __trap();
+  }
+}
+
+#define kNaN __longlong_as_double(-1LL)
+
+constexpr int kP3Groups = 4;   // column groups finalised together in P3
+
+template <int VEC>
+__global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
+  extern __shared__ double dsm[];
+  double* cs = dsm;                // c = T[0:k, j*]
+  double* ps = dsm + a.d_max;      // p_{k-1} (pending column)
+  __shared__ double red[kWarps][kCols];
+  __shared__ double red_c[kWarps][kFRows];
+  __shared__ double red_p[kWarps][kFRows];
+  __shared__ double smn[kWarps];
+  __shared__ Rec smr[kWarps];
+  __shared__ double fin_s[kThreads];
+  __shared__ double fin_c[kThreads];
+  __shared__ long long sh_tile;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const long long m = a.m, n = a.n;
+  const int G = gridDim.x, cta = blockIdx.x;
+  DevState* st = a.st;
+  StepCtl* ctl = a.ctl;
+  unsigned gen = 0;
+  if (tid == 0) gen = ld_acquire_u32(&a.bar[1]);
+  unsigned long long tile_base = ctl->tile_ctr;  // identical in every CTA (read before barrier 1)
+
+  // ---- loop state: identical in every CTA ----
+  long long k = st->d;
+  long long jstar = st->jstar;
+  int done = st->done;
+  int pending = 0, reorth_prev = 0, breakdown = 0;
+  double wnorm_prev = 1.0, e_cur = st->e_cur;
+  double xnorm2 = a.col_sq[jstar];
+  const double eps_R = st->eps_R, tol = st->breakdown_tol;
+  const int cfg_reorth = st->cfg_reorth;
+  const long long S = (m + kChunk - 1) / kChunk;
+  const long long nblk = (m + kFRows - 1) / kFRows;
+  const long long b0 = nblk * cta / G, b1 = nblk * (cta + 1) / G;
+  const long long ngx = (n + kCols - 1) / kCols;   // X column groups
+  const long long nx = ngx * S;                    // X tiles
+  unsigned dummy_nf = 0, dummy_nz = 0;
+  const bool timing = (a.phase_ns != nullptr) && cta == 0 && tid == 0;
+  unsigned long long tp = timing ? globaltimer() : 0ull;
+  auto mark = [&](int slot) {
+    if (timing) {
+      const unsigned long long t = globaltimer();
+      a.phase_ns[slot] += t - tp;
+      tp = t;
+    }
+  };
+
+  while (true) {
+    const int live = !done;
+    if (!live && !pending) break;
+    // =================== P1: w1 = x - Y c (and column k-1's second pass) ===========
+    const long long kb = pending ? k - 1 : k;
+    for (long long l = tid; l < k; l += kThreads) cs[l] = live ? __ldcg(&a.T[l * n + jstar]) : 0.0;
+    for (long long l = tid; l < kb; l += kThreads)
+      ps[l] = (pending && reorth_prev) ? __ldcg(&a.p[l]) : 0.0;
+    const double* x = a.X + jstar * a.ldx;
+    __syncthreads();
+    double nacc = 0.0;
+    for (long long b = b0; b < b1; ++b) {
+      const long long i = b * kFRows + lane;
+      const bool ok = i < m;
+      double acc_c = 0.0, acc_p = 0.0;
+      if (ok) {
+        const double* yp = a.Y + i + (long long)warp * m;
+        const long long stp = (long long)kWarps * m;
+        long long l = warp;
+        for (; l + 15 * kWarps < kb; l += 16 * kWarps) {   // 16 loads in flight per lane
+          double yv[16];
+#pragma unroll
+          for (int q = 0; q < 16; ++q) yv[q] = yp[q * stp];
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            acc_c = fma(yv[q], cs[l + q * kWarps], acc_c);
+            acc_p = fma(yv[q], ps[l + q * kWarps], acc_p);
+          }
+          yp += 16 * stp;
+        }
+        for (; l < kb; l += kWarps) {
+          const double y0 = *yp;
+          acc_c = fma(y0, cs[l], acc_c);
+          acc_p = fma(y0, ps[l], acc_p);
+          yp += stp;
+        }
+      }
+      red_c[warp][lane] = acc_c;
+      red_p[warp][lane] = acc_p;
+      __syncthreads();
+      if (warp == 0 && ok) {
+        double sc = red_c[0][lane], sp = red_p[0][lane];
+#pragma unroll
+        for (int w = 1; w < kWarps; ++w) {
+          sc += red_c[w][lane];
+          sp += red_p[w][lane];
+        }
+        if (pending) {
+          const double yk1 = (a.w[i] - sp) / wnorm_prev;   // second pass of column k-1
+          a.Y[i + (k - 1) * m] = yk1;
+          sc = fma(yk1, cs[k - 1], sc);
+        }
+        if (live) {
+          const double w1 = x[i] - sc;                     // first pass of column k
+          a.w[i] = w1;
+          nacc = fma(w1, w1, nacc);
+        }
+      }
+      __syncthreads();
+    }
+    pending = 0;
+    if (!live) continue;   // materialisation-only pass after the stop
+    {
+      const double sblk = block_sum_fixed<kThreads>(warp == 0 ? nacc : 0.0, smn);
+      if (tid == 0) a.npart[cta] = sblk;
+    }
+    mark(0);
+    grid_barrier(a.bar, gen);
+    mark(1);
+
+    // =================== P2: one dynamic queue of tiles ===================
+    //   [0, gy)       Y' w1 column groups, full height: p_k[4g..4g+3] (the
+    //                 reorth coefficients) summed over chunks in order by the
+    //                 same CTA — no cross-CTA reduction
+    //   [gy, gy+nx)   X' w1 tiles (the fused sweep), chunk partials
+    const long long gy = (k + kCols - 1) / kCols;
+    const long long total = gy + nx;
+    long long next = 0;
+    if (tid == 0) next = (long long)(atomicAdd(&ctl->tile_ctr, 1ull) - tile_base);
+    while (true) {
+      mark(9);
+      if (tid == 0) sh_tile = next;
+      __syncthreads();
+      const long long t = sh_tile;
+      mark(5);
+      if (t >= total) break;
+      if (tid == 0) next = (long long)(atomicAdd(&ctl->tile_ctr, 1ull) - tile_base);
+      if (t < gy) {
+        for (long long s = 0; s < S; ++s)
+          sweep_tiles<VEC, MODE_DOT, LOAD_CG, true>(a.Y, m, m, k, a.w, a.ppart, a.d_max,
+                                                     s * gy + t, 1LL << 40, red, dummy_nf,
+                                                     dummy_nz);
+        // the partials of this group were written by this CTA (CTA-visible)
+        if (tid < kCols && t * kCols + tid < k) {
+          const long long l = t * kCols + tid;
+          double v = 0.0;
+          for (long long s = 0; s < S; ++s) v += a.ppart[s * a.d_max + l];
+          a.p[l] = v;
+        }
+        mark(6);
+      } else {
+        const long long tx = t - gy;
+        const long long g = tx / S, s = tx - g * S;
+        sweep_tiles<VEC, MODE_DOT, LOAD_STREAM, true>(a.X, a.ldx, m, n, a.w, a.partial, n,
+                                                       s * ngx + g, 1LL << 40, red, dummy_nf,
+                                                       dummy_nz);
+        mark(7);
+      }
+    }
+    tile_base += (unsigned long long)(total + G);
+    mark(2);
+    grid_barrier(a.bar, gen);
+    mark(3);
+
+    // every CTA (redundantly, identical arithmetic): ||p||^2, ||w1||^2, the
+    // second-pass condition (decompose.cpp:28), ||w_k||, breakdown (:29-30)
+    double nrm;
+    int re;
+    {
+      double pn = 0.0;
+      for (long long l = tid; l < k; l += kThreads) {
+        const double pv = __ldcg(&a.p[l]);
+        pn = fma(pv, pv, pn);
+      }
+      pn = block_sum_fixed<kThreads>(pn, smn);
+      double w1n2 = 0.0;
+      for (int b = tid; b < G; b += kThreads) w1n2 += __ldcg(&a.npart[b]);
+      w1n2 = block_sum_fixed<kThreads>(w1n2, smn);
+      re = (k > 0) && (cfg_reorth || sqrt(w1n2) < 0.5 * sqrt(xnorm2));
+      double wn2 = re ? w1n2 - pn : w1n2;
+      wn2 = wn2 > 0.0 ? wn2 : 0.0;
+      nrm = sqrt(wn2);
+      if (nrm < tol || nrm == 0.0) {   // decompose.cpp:30 — keep the d we have
+        done = 1;
+        breakdown = 1;
+        continue;
+      }
+    }
+    mark(8);
+
+    // =================== P3: finalise T[k, :] and the residuals ===================
+    // Up to kP3Groups column groups of this CTA at once; thread t takes the
+    // correction terms l = t, t+256, ... and the chunk partials e = t, t+256,
+    // ... of every column, so all loads are issued before any reduction.
+    {
+      double bv = -1.0;
+      long long bj = 0x7fffffffffffffffLL;
+      for (long long g0 = cta; g0 < ngx; g0 += (long long)G * kP3Groups) {
+        double acc_s[kP3Groups * kCols], acc_c[kP3Groups * kCols];
+#pragma unroll
+        for (int e = 0; e < kP3Groups * kCols; ++e) acc_s[e] = acc_c[e] = 0.0;
+#pragma unroll
+        for (int gi = 0; gi < kP3Groups; ++gi) {
+          const long long g = g0 + (long long)gi * G;
+          if (g < ngx) {
+            const long long j0 = g * kCols;
+            for (long long ss = tid; ss < S; ss += kThreads)
+#pragma unroll
+              for (int c = 0; c < kCols; ++c)
+                if (j0 + c < n) acc_s[gi * kCols + c] += __ldcg(&a.partial[ss * n + j0 + c]);
+            if (re)
+              for (long long l = tid; l < k; l += kThreads) {
+                const double pl = __ldcg(&a.p[l]);
+#pragma unroll
+                for (int c = 0; c < kCols; ++c)
+                  if (j0 + c < n) acc_c[gi * kCols + c] = fma(pl, __ldcg(&a.T[l * n + j0 + c]), acc_c[gi * kCols + c]);
+              }
+          }
+        }
+        // fixed-order CTA reduction of the 2 x kP3Groups x 4 sums
+#pragma unroll
+        for (int e = 0; e < kP3Groups * kCols; ++e) {
+#pragma unroll
+          for (int off = 16; off > 0; off >>= 1) {
+            acc_s[e] += __shfl_xor_sync(0xffffffffu, acc_s[e], off);
+            acc_c[e] += __shfl_xor_sync(0xffffffffu, acc_c[e], off);
+          }
+        }
+        if (lane == 0) {
+#pragma unroll
+          for (int e = 0; e < kP3Groups * kCols; ++e) {
+            fin_s[warp * (kP3Groups * kCols) + e] = acc_s[e];
+            fin_c[warp * (kP3Groups * kCols) + e] = acc_c[e];
+          }
+        }
+        __syncthreads();
+        if (tid < kP3Groups * kCols) {
+          const int gi = tid / kCols, c = tid % kCols;
+          const long long jj = (g0 + (long long)gi * G) * kCols + c;
+          if (g0 + (long long)gi * G < ngx && jj < n) {
+            double ts = fin_s[tid], tc = fin_c[tid];
+#pragma unroll
+            for (int w2 = 1; w2 < kWarps; ++w2) {
+              ts += fin_s[w2 * (kP3Groups * kCols) + tid];
+              tc += fin_c[w2 * (kP3Groups * kCols) + tid];
+            }
+            const double tt = (ts - tc) / nrm;
+            a.T[k * n + jj] = tt;                                  // decompose.cpp:93
+            const double sq = __dmul_rn(tt, tt);
+            double rr = __dsub_rn(__ldcg(&a.r[jj]), sq);           // workspace.cpp:52-53
+            rr = rr > 0.0 ? rr : 0.0;
+            a.r[jj] = rr;
+            if (rec_better(rr, jj, bv, bj)) {
+              bv = rr;
+              bj = jj;
+            }
+          }
+        }
+        __syncthreads();
+      }
+      block_argmax<kThreads>(bv, bj, smr);
+      if (tid == 0) a.rec[cta] = Rec{bv, bj};
+    }
+    mark(9);
+    grid_barrier(a.bar, gen);
+    mark(3);
+
+    // every CTA: global argmax (workspace.cpp:107-113,123) and the stop test
+    {
+      double bv = -1.0;
+      long long bj = 0x7fffffffffffffffLL;
+      for (int b = tid; b < G; b += kThreads) {
+        const double v = __ldcg(&a.rec[b].v);
+        const long long jj = __ldcg(&a.rec[b].j);
+        if (rec_better(v, jj, bv, bj)) {
+          bv = v;
+          bj = jj;
+        }
+      }
+      block_argmax<kThreads>(bv, bj, smr);
+      e_cur = sqrt(bv > 0.0 ? bv : 0.0);
+      if (cta == 0 && tid == 0) {
+        a.selected[k] = jstar;         // decompose.cpp:94
+        a.history[k] = e_cur;          // :99
+      }
+      k += 1;                          // :96
+      pending = 1;
+      reorth_prev = re;
+      wnorm_prev = nrm;
+      jstar = bj;                      // :101
+      xnorm2 = a.col_sq[bj];
+      done = !(k < a.d_max && e_cur > eps_R) ? 1 : 0;   // :87
+    }
+    mark(4);
+  }
+  if (cta == 0 && tid == 0) {
+    st->d = k;
+    st->done = 1;
+    st->breakdown = breakdown;
+    st->e_cur = e_cur;
+    st->jstar = jstar;
+  }
+}
+
+}  // namespace rbdk
