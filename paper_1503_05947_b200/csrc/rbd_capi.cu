@@ -433,6 +433,8 @@ int launch_persistent(rbd_ctx_t ctx, const LoopBufs& L) {
   TRY(ensure(ctx->gcnt, sizeof(double) * (size_t)(L.d_max + 1)));   // p_k
   TRY(ensure(ctx->ygcnt, sizeof(Rec) * (size_t)grid));              // CTA records
   CU(cudaMemsetAsync(ctx->ctl.p, 0, sizeof(StepCtl), ctx->stream));
+  // chunk partials double as ready flags: NaN (all bytes 0xFF) = not written
+  CU(cudaMemsetAsync(ctx->partial.p, 0xFF, sizeof(double) * (size_t)S * L.n, ctx->stream));
   (void)ngx;
   TRY(ensure(ctx->nrm, sizeof(double) * std::max<long long>(gemv_grid(L.m), grid)));
   TRY(ensure(ctx->rec, sizeof(Rec) * (size_t)std::max(grid, ctx->nsm * 8)));
@@ -463,6 +465,14 @@ int launch_persistent(rbd_ctx_t ctx, const LoopBufs& L) {
     cudaMemsetAsync(ctx->scratch1.p, 0, 128, ctx->stream);
     a.phase_ns = ptr<unsigned long long>(ctx->scratch1);
   }
+  a.trace = nullptr;
+  DevBuf tracebuf;
+  if (const char* ts = getenv("RBD_TRACE_STEP")) {
+    TRY(ensure(tracebuf, sizeof(unsigned long long) * (size_t)grid * kTraceWords));
+    cudaMemsetAsync(tracebuf.p, 0, sizeof(unsigned long long) * (size_t)grid * kTraceWords, ctx->stream);
+    a.trace = ptr<unsigned long long>(tracebuf);
+    a.trace_step = atoll(ts);
+  }
   void* args[] = {&a};
   const size_t smem = persist_smem(L.d_max);
   cudaError_t e = vec == 2 ? cudaLaunchCooperativeKernel((void*)k_rbd_persistent<2>, grid, kThreads,
@@ -472,6 +482,20 @@ int launch_persistent(rbd_ctx_t ctx, const LoopBufs& L) {
   ctx->launches++;
   if (e != cudaSuccess)
     return set_err(RBD_ERR_CUDA, std::string("persistent launch: ") + cudaGetErrorString(e));
+  if (a.trace) {
+    std::vector<unsigned long long> h((size_t)grid * kTraceWords);
+    cudaMemcpyAsync(h.data(), a.trace, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost,
+                    ctx->stream);
+    cudaStreamSynchronize(ctx->stream);
+    const char* path = getenv("RBD_TRACE_FILE");
+    FILE* f = fopen(path ? path : "rbd_trace.bin", "wb");
+    if (f) {
+      fwrite(&grid, sizeof(int), 1, f);
+      fwrite(h.data(), sizeof(unsigned long long), h.size(), f);
+      fclose(f);
+    }
+    release(tracebuf);
+  }
   if (a.phase_ns) {
     unsigned long long h[10];
     cudaMemcpyAsync(h, a.phase_ns, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream);

@@ -137,21 +137,25 @@ __device__ __forceinline__ void sweep_tiles(const double* __restrict__ A, long l
     const long long g = tile - s * G;
     const long long row0 = s * kChunk;
     const long long col0 = g * kCols;
-    const bool full = (row0 + kChunk <= m) && (col0 + kCols <= ncols);
+    const long long rows = (m - row0 < kChunk) ? m - row0 : kChunk;
     double acc[kCols];
 #pragma unroll
     for (int c = 0; c < kCols; ++c) acc[c] = 0.0;
     const double* Ac[kCols];
 #pragma unroll
     for (int c = 0; c < kCols; ++c) {
-      const long long cc = (col0 + c < ncols) ? col0 + c : col0;  // clamp (unused cols)
+      const long long cc = (col0 + c < ncols) ? col0 + c : col0;  // clamp (result unused)
       Ac[c] = A + cc * lda + row0;
     }
     const double* vr = (MODE == MODE_DOT) ? v + row0 : nullptr;
-
-    if (full) {
+    // Batches of UB element groups; a batch lying entirely inside the matrix
+    // takes the vector path, the (at most one) straddling batch the
+    // predicated path. Both use the same per-thread fma order, out-of-range
+    // rows contribute +0, so the result is independent of the path taken.
+    constexpr int kBatchRows = UB * VEC * kThreads;
 #pragma unroll 1
-      for (int ub = 0; ub < U; ub += UB) {
+    for (int ub = 0; ub < U; ub += UB) {
+      if ((long long)(ub / UB + 1) * kBatchRows <= rows) {
         if constexpr (VEC == 2) {
           double2 yv[UB];
           double2 xv[UB][kCols];
@@ -206,50 +210,94 @@ __device__ __forceinline__ void sweep_tiles(const double* __restrict__ A, long l
               }
             }
         }
-      }
-    } else {
-      // Edge tile: identical arithmetic order, out-of-range rows contribute +0.
-      const long long rows = (m - row0 < kChunk) ? m - row0 : kChunk;
+      } else if ((long long)(ub / UB) * kBatchRows < rows) {
+        // straddling batch: groups wholly inside take vector loads, the
+        // rest predicated loads; identical order either way
 #pragma unroll 1
-      for (int u = 0; u < U; ++u) {
-        if constexpr (VEC == 2) {
-          const long long e = (long long)(tid + u * kThreads) * 2;
-          double y0 = 0.0, y1 = 0.0;
-          if constexpr (MODE == MODE_DOT) {
-            if (e < rows) y0 = __ldcg(vr + e);
-            if (e + 1 < rows) y1 = __ldcg(vr + e + 1);
-          }
+        for (int u = ub; u < ub + UB; ++u) {
+          if ((long long)(u + 1) * VEC * kThreads <= rows) {
+            const int e = (tid + u * kThreads) * VEC;
+            if constexpr (VEC == 2) {
+              double2 y2 = make_double2(0.0, 0.0);
+              if constexpr (MODE == MODE_DOT)
+                y2 = VCOH ? __ldcg(reinterpret_cast<const double2*>(vr + e)) : ld_keep2(vr + e);
+              double2 x2[kCols];
 #pragma unroll
-          for (int c = 0; c < kCols; ++c) {
-            if (col0 + c >= ncols) continue;
-            const double x0 = (e < rows) ? __ldcg(Ac[c] + e) : 0.0;
-            const double x1 = (e + 1 < rows) ? __ldcg(Ac[c] + e + 1) : 0.0;
-            if constexpr (MODE == MODE_DOT) {
-              acc[c] = fma(x0, y0, acc[c]);
-              acc[c] = fma(x1, y1, acc[c]);
+              for (int c = 0; c < kCols; ++c)
+                x2[c] = ALOAD == LOAD_STREAM ? ld_stream2(Ac[c] + e)
+                        : ALOAD == LOAD_CG   ? __ldcg(reinterpret_cast<const double2*>(Ac[c] + e))
+                                             : ld_keep2(Ac[c] + e);
+#pragma unroll
+              for (int c = 0; c < kCols; ++c) {
+                if constexpr (MODE == MODE_DOT) {
+                  acc[c] = fma(x2[c].x, y2.x, acc[c]);
+                  acc[c] = fma(x2[c].y, y2.y, acc[c]);
+                } else {
+                  acc[c] = fma(x2[c].x, x2[c].x, acc[c]);
+                  acc[c] = fma(x2[c].y, x2[c].y, acc[c]);
+                  nonfinite |= is_nonfinite(x2[c].x) | is_nonfinite(x2[c].y);
+                  nonzero |= (x2[c].x != 0.0) | (x2[c].y != 0.0);
+                }
+              }
             } else {
-              acc[c] = fma(x0, x0, acc[c]);
-              acc[c] = fma(x1, x1, acc[c]);
-              nonfinite |= is_nonfinite(x0) | is_nonfinite(x1);
-              nonzero |= (x0 != 0.0) | (x1 != 0.0);
+              double y1 = 0.0;
+              if constexpr (MODE == MODE_DOT) y1 = VCOH ? __ldcg(vr + e) : ld_keep1(vr + e);
+              double x1[kCols];
+#pragma unroll
+              for (int c = 0; c < kCols; ++c)
+                x1[c] = ALOAD == LOAD_STREAM ? ld_stream1(Ac[c] + e)
+                        : ALOAD == LOAD_CG   ? __ldcg(Ac[c] + e)
+                                             : ld_keep1(Ac[c] + e);
+#pragma unroll
+              for (int c = 0; c < kCols; ++c) {
+                if constexpr (MODE == MODE_DOT) {
+                  acc[c] = fma(x1[c], y1, acc[c]);
+                } else {
+                  acc[c] = fma(x1[c], x1[c], acc[c]);
+                  nonfinite |= is_nonfinite(x1[c]);
+                  nonzero |= (x1[c] != 0.0);
+                }
+              }
             }
+            continue;
           }
-        } else {
-          const long long e = tid + (long long)u * kThreads;
-          double y0 = 0.0;
-          if constexpr (MODE == MODE_DOT) {
-            if (e < rows) y0 = __ldcg(vr + e);
-          }
-#pragma unroll
-          for (int c = 0; c < kCols; ++c) {
-            if (col0 + c >= ncols) continue;
-            const double x0 = (e < rows) ? __ldcg(Ac[c] + e) : 0.0;
+          if constexpr (VEC == 2) {
+            const long long e = (long long)(tid + u * kThreads) * 2;
+            double y0 = 0.0, y1 = 0.0;
             if constexpr (MODE == MODE_DOT) {
-              acc[c] = fma(x0, y0, acc[c]);
-            } else {
-              acc[c] = fma(x0, x0, acc[c]);
-              nonfinite |= is_nonfinite(x0);
-              nonzero |= (x0 != 0.0);
+              if (e < rows) y0 = __ldcg(vr + e);
+              if (e + 1 < rows) y1 = __ldcg(vr + e + 1);
+            }
+#pragma unroll
+            for (int c = 0; c < kCols; ++c) {
+              const double x0 = (e < rows) ? __ldcg(Ac[c] + e) : 0.0;
+              const double x1 = (e + 1 < rows) ? __ldcg(Ac[c] + e + 1) : 0.0;
+              if constexpr (MODE == MODE_DOT) {
+                acc[c] = fma(x0, y0, acc[c]);
+                acc[c] = fma(x1, y1, acc[c]);
+              } else {
+                acc[c] = fma(x0, x0, acc[c]);
+                acc[c] = fma(x1, x1, acc[c]);
+                nonfinite |= is_nonfinite(x0) | is_nonfinite(x1);
+                nonzero |= (x0 != 0.0) | (x1 != 0.0);
+              }
+            }
+          } else {
+            const long long e = tid + (long long)u * kThreads;
+            double y0 = 0.0;
+            if constexpr (MODE == MODE_DOT) {
+              if (e < rows) y0 = __ldcg(vr + e);
+            }
+#pragma unroll
+            for (int c = 0; c < kCols; ++c) {
+              const double x0 = (e < rows) ? __ldcg(Ac[c] + e) : 0.0;
+              if constexpr (MODE == MODE_DOT) {
+                acc[c] = fma(x0, y0, acc[c]);
+              } else {
+                acc[c] = fma(x0, x0, acc[c]);
+                nonfinite |= is_nonfinite(x0);
+                nonzero |= (x0 != 0.0);
+              }
             }
           }
         }

@@ -46,6 +46,8 @@ struct PersistArgs {
   unsigned* bar;      // [0] arrival count, [1] generation
   long long d_max;
   unsigned long long* phase_ns;  // optional [8] accumulated phase times (CTA 0)
+  unsigned long long* trace;     // optional per-CTA timeline [G][kTraceWords] for steps
+  long long trace_step;          //   trace_step .. trace_step+1
   struct StepCtl* ctl;           // queue / publish words
 };
 
@@ -104,6 +106,8 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned& gen) {
 // Shared step bookkeeping (device memory, see PersistArgs::ctl).
 struct StepCtl {
   unsigned long long tile_ctr;   // monotonic tile-claim counter (all steps, all calls)
+  unsigned ydone;                // Y'w1 groups finished this step (reset by the decider)
+  unsigned pad;
   // published by the decider (claimer of the last Y'w1 tile), tagged with step+1
   long long p_step;
   double norm;
@@ -158,6 +162,7 @@ __device__ __forceinline__ void wait_step(const long long* flag, long long want)
 #define kNaN __longlong_as_double(-1LL)
 
 constexpr int kP3Groups = 4;   // column groups finalised together in P3
+constexpr int kTraceWords = 256;  // per CTA: [0] count, then (tag<<40 | time) words
 
 template <int VEC>
 __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
@@ -206,12 +211,25 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
       tp = t;
     }
   };
+  unsigned long long* trow = a.trace ? a.trace + (size_t)cta * kTraceWords : nullptr;
+  // tag: 1 P1 start, 2 P1 end, 3 bar1 out, 4 tile start (|tile<<8), 5 tile end,
+  //      6 P2 end, 7 bar2 out, 8 P3 end, 9 bar3 out, 10 step end
+  auto trace = [&](long long step, unsigned long long tag) {
+    if (trow && tid == 0 && step >= a.trace_step && step < a.trace_step + 2) {
+      const unsigned long long c = trow[0];
+      if (c + 1 < kTraceWords) {
+        trow[1 + c] = (tag << 40) | (globaltimer() & 0xFFFFFFFFFFull);
+        trow[0] = c + 1;
+      }
+    }
+  };
 
   while (true) {
     const int live = !done;
     if (!live && !pending) break;
     // =================== P1: w1 = x - Y c (and column k-1's second pass) ===========
     const long long kb = pending ? k - 1 : k;
+    trace(k, 1);
     for (long long l = tid; l < k; l += kThreads) cs[l] = live ? __ldcg(&a.T[l * n + jstar]) : 0.0;
     for (long long l = tid; l < kb; l += kThreads)
       ps[l] = (pending && reorth_prev) ? __ldcg(&a.p[l]) : 0.0;
@@ -274,16 +292,37 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
       if (tid == 0) a.npart[cta] = sblk;
     }
     mark(0);
+    trace(k, 2);
     grid_barrier(a.bar, gen);
+    trace(k, 3);
     mark(1);
 
     // =================== P2: one dynamic queue of tiles ===================
-    //   [0, gy)       Y' w1 column groups, full height: p_k[4g..4g+3] (the
-    //                 reorth coefficients) summed over chunks in order by the
-    //                 same CTA — no cross-CTA reduction
-    //   [gy, gy+nx)   X' w1 tiles (the fused sweep), chunk partials
+    //   [0, gy)       Y' w1 column groups, full height -> p_k[4g..4g+3] (the
+    //                 reorth coefficients) summed over chunks in order by one
+    //                 CTA; the last one to finish decides the second pass
+    //                 (decompose.cpp:28), ||w_k|| and breakdown (:29-30)
+    //   [gy, gy+nx)   X' w1 tiles (the fused sweep): chunks 0..S-2 group-major,
+    //                 then every group's last chunk. Its claimer finalises the
+    //                 group in-queue:
+    //                 T[k, j] = (w1.x_j - p.T[0:k, j]) / ||w_k||, residuals
+    //                 (workspace.cpp:52-53). Chunk partials double as ready
+    //                 flags (NaN = not written); siblings were claimed long
+    //                 before, so the poll practically never waits, and every
+    //                 wait targets an earlier-claimed tile (no deadlock).
     const long long gy = (k + kCols - 1) / kCols;
     const long long total = gy + nx;
+    double bv = -1.0;          // this CTA's best finalised residual (argmax record)
+    long long bj = 0x7fffffffffffffffLL;
+    if (gy == 0 && cta == 0 && tid == 0) {   // k == 0: nothing to orthogonalise against
+      double w1n2 = 0.0;
+      for (int b = 0; b < G; ++b) w1n2 += __ldcg(&a.npart[b]);
+      const double norm0 = sqrt(w1n2);
+      ctl->norm = norm0;
+      ctl->reorth = 0;
+      ctl->breakdown = (norm0 < tol || norm0 == 0.0) ? 1 : 0;
+      st_release_s64(&ctl->p_step, k + 1);
+    }
     long long next = 0;
     if (tid == 0) next = (long long)(atomicAdd(&ctl->tile_ctr, 1ull) - tile_base);
     while (true) {
@@ -293,6 +332,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
       const long long t = sh_tile;
       mark(5);
       if (t >= total) break;
+      trace(k, 4 | ((unsigned long long)t << 8));
       if (tid == 0) next = (long long)(atomicAdd(&ctl->tile_ctr, 1ull) - tile_base);
       if (t < gy) {
         for (long long s = 0; s < S; ++s)
@@ -306,138 +346,136 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
           for (long long s = 0; s < S; ++s) v += a.ppart[s * a.d_max + l];
           a.p[l] = v;
         }
+        __syncthreads();
+        if (tid == 0) {
+          __threadfence();
+          sh_tile = (atomicAdd(&ctl->ydone, 1u) == (unsigned)(gy - 1)) ? 1 : 0;
+          if (sh_tile) __threadfence();
+        }
+        __syncthreads();
+        if (sh_tile) {
+          // decider: ||p||^2, ||w1||^2, the second-pass condition, ||w||, breakdown
+          double pn = 0.0;
+          for (long long ll = tid; ll < k; ll += kThreads) {
+            const double pv = __ldcg(&a.p[ll]);
+            pn = fma(pv, pv, pn);
+          }
+          pn = block_sum_fixed<kThreads>(pn, smn);
+          double w1n2 = 0.0;
+          for (int b = tid; b < G; b += kThreads) w1n2 += __ldcg(&a.npart[b]);
+          w1n2 = block_sum_fixed<kThreads>(w1n2, smn);
+          if (tid == 0) {
+            ctl->ydone = 0u;
+            const int re = (cfg_reorth || sqrt(w1n2) < 0.5 * sqrt(xnorm2)) ? 1 : 0;  // :28
+            double wn2 = re ? w1n2 - pn : w1n2;
+            wn2 = wn2 > 0.0 ? wn2 : 0.0;
+            const double nrm = sqrt(wn2);
+            ctl->norm = nrm;
+            ctl->reorth = re;
+            ctl->breakdown = (nrm < tol || nrm == 0.0) ? 1 : 0;                     // :29-30
+            st_release_s64(&ctl->p_step, k + 1);
+          }
+        }
         mark(6);
+        trace(k, 5);
       } else {
+        // X tile order: chunks 0..S-2 group-major (contiguous column runs),
+        // then the last chunk of every group (these finalise their group)
         const long long tx = t - gy;
-        const long long g = tx / S, s = tx - g * S;
+        const long long head = ngx * (S - 1);
+        long long s, g;
+        if (tx < head) {
+          g = tx / (S - 1);
+          s = tx - g * (S - 1);
+        } else {
+          s = S - 1;
+          g = tx - head;
+        }
         sweep_tiles<VEC, MODE_DOT, LOAD_STREAM, true>(a.X, a.ldx, m, n, a.w, a.partial, n,
                                                        s * ngx + g, 1LL << 40, red, dummy_nf,
                                                        dummy_nz);
         mark(7);
+        if (s == S - 1) {
+          // ---- finalise columns 4g..4g+3 (warps 0..3, one column each) ----
+          if (tid == 0) wait_step(&ctl->p_step, k + 1);
+          __syncthreads();
+          const int re = __ldcg(&ctl->reorth);
+          const int bd = __ldcg(&ctl->breakdown);
+          const double nrm = __ldcg(&ctl->norm);
+          const long long j = g * kCols + warp;
+          if (warp < kCols && j < n) {
+            double sp = 0.0, corr = 0.0;
+            for (long long ss = lane; ss < S; ss += 32) {
+              sp += poll_f64(&a.partial[ss * n + j]);
+              st_relaxed_f64(&a.partial[ss * n + j], kNaN);
+            }
+            if (re && !bd) {
+              for (long long l0 = 0; l0 < k; l0 += 512) {
+                double tv[16], pv[16];
+#pragma unroll
+                for (int q = 0; q < 16; ++q) {
+                  const long long l = l0 + lane + 32 * q;
+                  tv[q] = (l < k) ? __ldcg(&a.T[l * n + j]) : 0.0;
+                  pv[q] = (l < k) ? __ldcg(&a.p[l]) : 0.0;
+                }
+#pragma unroll
+                for (int q = 0; q < 16; ++q) corr = fma(pv[q], tv[q], corr);
+              }
+            }
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+              sp += __shfl_xor_sync(0xffffffffu, sp, off);
+              corr += __shfl_xor_sync(0xffffffffu, corr, off);
+            }
+            if (lane == 0 && !bd) {
+              const double tt = (sp - corr) / nrm;
+              a.T[k * n + j] = tt;                                   // decompose.cpp:93
+              const double sq = __dmul_rn(tt, tt);
+              double rr = __dsub_rn(__ldcg(&a.r[j]), sq);            // workspace.cpp:52-53
+              rr = rr > 0.0 ? rr : 0.0;
+              a.r[j] = rr;
+              if (rec_better(rr, j, bv, bj)) {
+                bv = rr;
+                bj = j;
+              }
+            }
+          }
+        }
+        trace(k, 5);
       }
     }
+    block_argmax<kThreads>(bv, bj, smr);
+    if (tid == 0) a.rec[cta] = Rec{bv, bj};
     tile_base += (unsigned long long)(total + G);
     mark(2);
+    trace(k, 6);
     grid_barrier(a.bar, gen);
+    trace(k, 7);
     mark(3);
 
-    // every CTA (redundantly, identical arithmetic): ||p||^2, ||w1||^2, the
-    // second-pass condition (decompose.cpp:28), ||w_k||, breakdown (:29-30)
-    double nrm;
-    int re;
+    // every CTA: the published decision, the global argmax over the CTA
+    // records (workspace.cpp:107-113,123) and the stop test (decompose.cpp:87)
     {
-      double pn = 0.0;
-      for (long long l = tid; l < k; l += kThreads) {
-        const double pv = __ldcg(&a.p[l]);
-        pn = fma(pv, pv, pn);
-      }
-      pn = block_sum_fixed<kThreads>(pn, smn);
-      double w1n2 = 0.0;
-      for (int b = tid; b < G; b += kThreads) w1n2 += __ldcg(&a.npart[b]);
-      w1n2 = block_sum_fixed<kThreads>(w1n2, smn);
-      re = (k > 0) && (cfg_reorth || sqrt(w1n2) < 0.5 * sqrt(xnorm2));
-      double wn2 = re ? w1n2 - pn : w1n2;
-      wn2 = wn2 > 0.0 ? wn2 : 0.0;
-      nrm = sqrt(wn2);
-      if (nrm < tol || nrm == 0.0) {   // decompose.cpp:30 — keep the d we have
+      const int bd = __ldcg(&ctl->breakdown);
+      if (bd) {                        // decompose.cpp:90 — keep the d we have
         done = 1;
         breakdown = 1;
         continue;
       }
-    }
-    mark(8);
-
-    // =================== P3: finalise T[k, :] and the residuals ===================
-    // Up to kP3Groups column groups of this CTA at once; thread t takes the
-    // correction terms l = t, t+256, ... and the chunk partials e = t, t+256,
-    // ... of every column, so all loads are issued before any reduction.
-    {
-      double bv = -1.0;
-      long long bj = 0x7fffffffffffffffLL;
-      for (long long g0 = cta; g0 < ngx; g0 += (long long)G * kP3Groups) {
-        double acc_s[kP3Groups * kCols], acc_c[kP3Groups * kCols];
-#pragma unroll
-        for (int e = 0; e < kP3Groups * kCols; ++e) acc_s[e] = acc_c[e] = 0.0;
-#pragma unroll
-        for (int gi = 0; gi < kP3Groups; ++gi) {
-          const long long g = g0 + (long long)gi * G;
-          if (g < ngx) {
-            const long long j0 = g * kCols;
-            for (long long ss = tid; ss < S; ss += kThreads)
-#pragma unroll
-              for (int c = 0; c < kCols; ++c)
-                if (j0 + c < n) acc_s[gi * kCols + c] += __ldcg(&a.partial[ss * n + j0 + c]);
-            if (re)
-              for (long long l = tid; l < k; l += kThreads) {
-                const double pl = __ldcg(&a.p[l]);
-#pragma unroll
-                for (int c = 0; c < kCols; ++c)
-                  if (j0 + c < n) acc_c[gi * kCols + c] = fma(pl, __ldcg(&a.T[l * n + j0 + c]), acc_c[gi * kCols + c]);
-              }
-          }
-        }
-        // fixed-order CTA reduction of the 2 x kP3Groups x 4 sums
-#pragma unroll
-        for (int e = 0; e < kP3Groups * kCols; ++e) {
-#pragma unroll
-          for (int off = 16; off > 0; off >>= 1) {
-            acc_s[e] += __shfl_xor_sync(0xffffffffu, acc_s[e], off);
-            acc_c[e] += __shfl_xor_sync(0xffffffffu, acc_c[e], off);
-          }
-        }
-        if (lane == 0) {
-#pragma unroll
-          for (int e = 0; e < kP3Groups * kCols; ++e) {
-            fin_s[warp * (kP3Groups * kCols) + e] = acc_s[e];
-            fin_c[warp * (kP3Groups * kCols) + e] = acc_c[e];
-          }
-        }
-        __syncthreads();
-        if (tid < kP3Groups * kCols) {
-          const int gi = tid / kCols, c = tid % kCols;
-          const long long jj = (g0 + (long long)gi * G) * kCols + c;
-          if (g0 + (long long)gi * G < ngx && jj < n) {
-            double ts = fin_s[tid], tc = fin_c[tid];
-#pragma unroll
-            for (int w2 = 1; w2 < kWarps; ++w2) {
-              ts += fin_s[w2 * (kP3Groups * kCols) + tid];
-              tc += fin_c[w2 * (kP3Groups * kCols) + tid];
-            }
-            const double tt = (ts - tc) / nrm;
-            a.T[k * n + jj] = tt;                                  // decompose.cpp:93
-            const double sq = __dmul_rn(tt, tt);
-            double rr = __dsub_rn(__ldcg(&a.r[jj]), sq);           // workspace.cpp:52-53
-            rr = rr > 0.0 ? rr : 0.0;
-            a.r[jj] = rr;
-            if (rec_better(rr, jj, bv, bj)) {
-              bv = rr;
-              bj = jj;
-            }
-          }
-        }
-        __syncthreads();
-      }
-      block_argmax<kThreads>(bv, bj, smr);
-      if (tid == 0) a.rec[cta] = Rec{bv, bj};
-    }
-    mark(9);
-    grid_barrier(a.bar, gen);
-    mark(3);
-
-    // every CTA: global argmax (workspace.cpp:107-113,123) and the stop test
-    {
-      double bv = -1.0;
-      long long bj = 0x7fffffffffffffffLL;
+      const double nrm = __ldcg(&ctl->norm);
+      const int re = __ldcg(&ctl->reorth);
+      double gv = -1.0;
+      long long gj = 0x7fffffffffffffffLL;
       for (int b = tid; b < G; b += kThreads) {
         const double v = __ldcg(&a.rec[b].v);
         const long long jj = __ldcg(&a.rec[b].j);
-        if (rec_better(v, jj, bv, bj)) {
-          bv = v;
-          bj = jj;
+        if (rec_better(v, jj, gv, gj)) {
+          gv = v;
+          gj = jj;
         }
       }
-      block_argmax<kThreads>(bv, bj, smr);
-      e_cur = sqrt(bv > 0.0 ? bv : 0.0);
+      block_argmax<kThreads>(gv, gj, smr);
+      e_cur = sqrt(gv > 0.0 ? gv : 0.0);
       if (cta == 0 && tid == 0) {
         a.selected[k] = jstar;         // decompose.cpp:94
         a.history[k] = e_cur;          // :99
@@ -446,10 +484,11 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
       pending = 1;
       reorth_prev = re;
       wnorm_prev = nrm;
-      jstar = bj;                      // :101
-      xnorm2 = a.col_sq[bj];
+      jstar = gj;                      // :101
+      xnorm2 = a.col_sq[gj];
       done = !(k < a.d_max && e_cur > eps_R) ? 1 : 0;   // :87
     }
+    trace(k - 1, 10);
     mark(4);
   }
   if (cta == 0 && tid == 0) {
