@@ -47,6 +47,17 @@ def _col_major_torch(x):
     return xc, m
 
 
+def _host_outputs(m: int, n: int, cap: int):
+    """Y (m x cap, column-major) and T (cap x n) host buffers; page-locked when
+    torch is available so the device-to-host copies run at full PCIe rate."""
+    if torch is not None and torch.cuda.is_available() and m * cap + cap * n >= (1 << 20):
+        Yt = torch.empty((cap, max(m, 1)), dtype=torch.float64, pin_memory=True)
+        Tt = torch.empty((cap, max(n, 1)), dtype=torch.float64, pin_memory=True)
+        return Yt.numpy().T, Tt.numpy()
+    return (np.zeros((m, cap), dtype=np.float64, order="F"),
+            np.zeros((cap, n), dtype=np.float64))
+
+
 def make_config(d_max: int, eps_r: float = 0.0, start_column: int = 0,
                 reorthogonalize: bool = False, breakdown_tol: float = -1.0,
                 start_seed: Optional[int] = None, diag=None, sparse=None) -> Config:
@@ -150,8 +161,7 @@ def decompose(x, d_max: int, eps_r: float = 0.0, diag=None, sparse=None, start_c
         raise InvalidArgument("decompose: X must be a 2-D matrix")
     m, n = xa.shape
     cap = max(1, min(int(d_max), n)) if n > 0 else 1
-    Y = np.zeros((m, cap), dtype=np.float64, order="F")
-    T = np.zeros((cap, n), dtype=np.float64)
+    Y, T = _host_outputs(m, n, cap)
     sel = np.zeros(cap, dtype=np.int64)
     hist = np.zeros(cap, dtype=np.float64)
     check(lib.rbd_decompose_host(ctx.handle, _dp(xa), m, n, max(m, 1), C.byref(cfg), _dp(Y),
