@@ -163,6 +163,18 @@ int rbd_decompose_sharded(rbd_ctx_t ctx, const double* dX_local, int64_t m, int6
                           const rbd_config_t* cfg, double* dY, double* dT_local,
                           int64_t* h_selected, double* h_history, rbd_result_t* result);
 
+/* Single-device emulation of the sharded loop: nranks column shards (shard r
+ * holds n_locals[r] consecutive global columns) stepped in lockstep in this
+ * process, with the payload allgather done by device copies. Same kernels and
+ * protocol as rbd_decompose_sharded; used to test cross-shard bitwise identity
+ * on one GPU. dY_ranks[r]: m x d_max per rank (replicated Y); dT_ranks[r]:
+ * d_max x n_locals[r] row-major. */
+int rbd_decompose_sharded_virtual(rbd_ctx_t ctx, int nranks, const double* const* dX_shards,
+                                  const int64_t* n_locals, int64_t m, int64_t ldx,
+                                  const rbd_config_t* cfg, double* const* dY_ranks,
+                                  double* const* dT_ranks, int64_t* h_selected, double* h_history,
+                                  rbd_result_t* result);
+
 #ifdef __cplusplus
 }
 #endif

@@ -138,6 +138,8 @@ _SIGS = {
     "rbd_ctx_init_comm": (C.c_int, [_P, C.c_int, C.c_int, C.c_char_p]),
     "rbd_decompose_sharded": (C.c_int, [_P, _P, _I64, _I64, _I64, _I64, _I64, C.POINTER(Config),
                                         _P, _P, _P, _P, C.POINTER(Result)]),
+    "rbd_decompose_sharded_virtual": (C.c_int, [_P, C.c_int, _P, _P, _I64, _I64, C.POINTER(Config),
+                                                _P, _P, _P, _P, C.POINTER(Result)]),
 }
 
 EXPORTED = tuple(_SIGS)

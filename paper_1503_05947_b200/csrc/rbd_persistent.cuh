@@ -48,6 +48,11 @@ struct PersistArgs {
   unsigned long long* phase_ns;  // optional [8] accumulated phase times (CTA 0)
   unsigned long long* trace;     // optional per-CTA timeline [G][kTraceWords] for steps
   long long trace_step;          //   trace_step .. trace_step+1
+  // sharded mode (one step per launch; see rbd_capi.cu's sharded driver)
+  const double* recv;            // gathered payloads [nranks][pay_stride]
+  double* send;                  // this rank's payload
+  long long pay_stride;          // doubles per payload
+  long long col_offset;          // global index of local column 0
   struct StepCtl* ctl;           // queue / publish words
 };
 
@@ -161,10 +166,19 @@ __device__ __forceinline__ void wait_step(const long long* flag, long long want)
 
 #define kNaN __longlong_as_double(-1LL)
 
+__device__ __forceinline__ bool live_at_exit(int done, int breakdown) {
+  return !done && !breakdown;
+}
+
 constexpr int kP3Groups = 4;   // column groups finalised together in P3
 constexpr int kTraceWords = 256;  // per CTA: [0] count, then (tag<<40 | time) words
 
-template <int VEC>
+// Payload of a rank in sharded mode (doubles): [0] best residual, [1] global
+// column index (bits), [2] col_sq of that column, [3] pad, [4, 4+m) the
+// column x_j, [4+m, 4+m+k+1) the column T[0:k+1, j].
+constexpr int kPayHead = 4;
+
+template <int VEC, bool SHARD>
 __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
   extern __shared__ double dsm[];
   double* cs = dsm;                // c = T[0:k, j*]
@@ -174,8 +188,6 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
   __shared__ double red_p[kWarps][kFRows];
   __shared__ double smn[kWarps];
   __shared__ Rec smr[kWarps];
-  __shared__ double fin_s[kThreads];
-  __shared__ double fin_c[kThreads];
   __shared__ long long sh_tile;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -187,13 +199,23 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
   if (tid == 0) gen = ld_acquire_u32(&a.bar[1]);
   unsigned long long tile_base = ctl->tile_ctr;  // identical in every CTA (read before barrier 1)
 
-  // ---- loop state: identical in every CTA ----
+  // ---- loop state: identical in every CTA (and, sharded, on every rank) ----
   long long k = st->d;
   long long jstar = st->jstar;
   int done = st->done;
   int pending = 0, reorth_prev = 0, breakdown = 0;
   double wnorm_prev = 1.0, e_cur = st->e_cur;
-  double xnorm2 = a.col_sq[jstar];
+  double xnorm2 = 0.0;
+  const double* pay = nullptr;   // sharded: the winner's payload
+  if constexpr (SHARD) {
+    pending = st->pending;
+    reorth_prev = st->reorth;
+    wnorm_prev = st->wnorm;
+    xnorm2 = st->xnorm2;
+    pay = a.recv + (long long)st->rank_owner * a.pay_stride;
+  } else {
+    xnorm2 = a.col_sq[jstar];
+  }
   const double eps_R = st->eps_R, tol = st->breakdown_tol;
   const int cfg_reorth = st->cfg_reorth;
   const long long S = (m + kChunk - 1) / kChunk;
@@ -230,10 +252,11 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
     // =================== P1: w1 = x - Y c (and column k-1's second pass) ===========
     const long long kb = pending ? k - 1 : k;
     trace(k, 1);
-    for (long long l = tid; l < k; l += kThreads) cs[l] = live ? __ldcg(&a.T[l * n + jstar]) : 0.0;
+    for (long long l = tid; l < k; l += kThreads)
+      cs[l] = !live ? 0.0 : SHARD ? __ldcg(&pay[kPayHead + m + l]) : __ldcg(&a.T[l * n + jstar]);
     for (long long l = tid; l < kb; l += kThreads)
       ps[l] = (pending && reorth_prev) ? __ldcg(&a.p[l]) : 0.0;
-    const double* x = a.X + jstar * a.ldx;
+    const double* x = SHARD ? pay + kPayHead : a.X + jstar * a.ldx;
     __syncthreads();
     double nacc = 0.0;
     for (long long b = b0; b < b1; ++b) {
@@ -460,6 +483,14 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
       if (bd) {                        // decompose.cpp:90 — keep the d we have
         done = 1;
         breakdown = 1;
+        if constexpr (SHARD) {
+          if (cta == 0 && tid == 0) {
+            st->breakdown = 1;
+            st->done = 1;
+            st->pending = 0;
+          }
+          break;
+        }
         continue;
       }
       const double nrm = __ldcg(&ctl->norm);
@@ -475,28 +506,114 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
         }
       }
       block_argmax<kThreads>(gv, gj, smr);
-      e_cur = sqrt(gv > 0.0 ? gv : 0.0);
-      if (cta == 0 && tid == 0) {
-        a.selected[k] = jstar;         // decompose.cpp:94
-        a.history[k] = e_cur;          // :99
+      if constexpr (SHARD) {
+        // pack this rank's candidate: record, x_{gj}, T[0:k+1, gj]; the select
+        // kernel picks the winner after the allgather
+        const bool have = gj != 0x7fffffffffffffffLL;
+        if (cta == 0 && tid == 0) {
+          a.send[0] = have ? gv : -2.0;
+          a.send[1] = __longlong_as_double(have ? a.col_offset + gj : -1LL);
+          a.send[2] = have ? a.col_sq[gj] : 0.0;
+          a.send[3] = 0.0;
+          st->reorth = re;
+          st->wnorm = nrm;
+          st->pending = 0;
+        }
+        if (have) {
+          const double* xs = a.X + gj * a.ldx;
+          for (long long i = (long long)cta * kThreads + tid; i < m; i += (long long)G * kThreads)
+            a.send[kPayHead + i] = xs[i];
+          for (long long l = (long long)cta * kThreads + tid; l <= k; l += (long long)G * kThreads)
+            a.send[kPayHead + m + l] = __ldcg(&a.T[l * n + gj]);
+        }
+        break;
+      } else {
+        e_cur = sqrt(gv > 0.0 ? gv : 0.0);
+        if (cta == 0 && tid == 0) {
+          a.selected[k] = jstar;         // decompose.cpp:94
+          a.history[k] = e_cur;          // :99
+        }
+        k += 1;                          // :96
+        pending = 1;
+        reorth_prev = re;
+        wnorm_prev = nrm;
+        jstar = gj;                      // :101
+        xnorm2 = a.col_sq[gj];
+        done = !(k < a.d_max && e_cur > eps_R) ? 1 : 0;   // :87
       }
-      k += 1;                          // :96
-      pending = 1;
-      reorth_prev = re;
-      wnorm_prev = nrm;
-      jstar = gj;                      // :101
-      xnorm2 = a.col_sq[gj];
-      done = !(k < a.d_max && e_cur > eps_R) ? 1 : 0;   // :87
     }
     trace(k - 1, 10);
     mark(4);
   }
-  if (cta == 0 && tid == 0) {
-    st->d = k;
-    st->done = 1;
-    st->breakdown = breakdown;
-    st->e_cur = e_cur;
-    st->jstar = jstar;
+  if constexpr (SHARD) {
+    if (cta == 0 && tid == 0 && !live_at_exit(done, breakdown)) st->pending = 0;
+  } else {
+    if (cta == 0 && tid == 0) {
+      st->d = k;
+      st->done = 1;
+      st->breakdown = breakdown;
+      st->e_cur = e_cur;
+      st->jstar = jstar;
+    }
+  }
+}
+
+// Sharded mode: winner selection after the payload allgather (every rank runs
+// it on identical data, so every rank takes the same decision).
+__global__ void k_shard_select(DevState* st, const double* recv, long long pay_stride, int nranks,
+                               double* history, long long* selected) {
+  if (threadIdx.x != 0 || st->done) return;
+  double bv = -1.0;
+  long long bj = 0x7fffffffffffffffLL;
+  int br = -1;
+  for (int r = 0; r < nranks; ++r) {
+    const double* h = recv + (long long)r * pay_stride;
+    const long long j = __double_as_longlong(h[1]);
+    if (j < 0) continue;
+    if (rec_better(h[0], j, bv, bj)) {
+      bv = h[0];
+      bj = j;
+      br = r;
+    }
+  }
+  const long long k = st->d;
+  const double e_cur = sqrt(bv > 0.0 ? bv : 0.0);      // workspace.cpp:123
+  history[k] = e_cur;                                   // decompose.cpp:99
+  selected[k] = st->jstar;                              // :94
+  st->e_cur = e_cur;
+  st->d = k + 1;                                        // :96
+  st->pending = 1;
+  st->jstar = bj;                                       // :101
+  st->rank_owner = br;
+  st->xnorm2 = recv[(long long)br * pay_stride + 2];
+  st->done = !((k + 1) < st->d_max && e_cur > st->eps_R) ? 1 : 0;  // :87
+}
+
+// Sharded mode, before step 0: the owner of the start column publishes it.
+__global__ void k_shard_seed_pack(const double* X, long long ldx, long long m, long long jlocal,
+                                  long long col_offset, const double* col_sq, double* send) {
+  const long long i0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i0 == 0) {
+    send[0] = 0.0;
+    send[1] = __longlong_as_double(jlocal >= 0 ? col_offset + jlocal : -1LL);
+    send[2] = jlocal >= 0 ? col_sq[jlocal] : 0.0;
+    send[3] = 0.0;
+  }
+  if (jlocal < 0) return;
+  for (long long i = i0; i < m; i += (long long)gridDim.x * blockDim.x)
+    send[kPayHead + i] = X[jlocal * ldx + i];
+}
+
+__global__ void k_shard_seed_select(DevState* st, const double* recv, long long pay_stride,
+                                    int nranks) {
+  if (threadIdx.x != 0) return;
+  for (int r = 0; r < nranks; ++r) {
+    const double* h = recv + (long long)r * pay_stride;
+    if (__double_as_longlong(h[1]) >= 0) {
+      st->rank_owner = r;
+      st->xnorm2 = h[2];
+      return;
+    }
   }
 }
 

@@ -1,0 +1,83 @@
+"""Sharded (multi-GPU) path on one B200: the same kernels and payload protocol
+with R column shards stepped in lockstep in one process. Results must be
+bit-identical to the single-GPU loop for any R (per-column
+sums depend on m only; the allgather moves bits, never adds them)."""
+import numpy as np
+import pytest
+
+import oracle
+import paper_1503_05947_b200 as rbd
+from paper_1503_05947_b200 import configs, distributed
+
+pytestmark = pytest.mark.gpu
+
+
+def dev(a, cuda):
+    import torch
+    return torch.as_tensor(np.asfortranarray(a).T.copy(), device=cuda).t()
+
+
+def single(X, d_max, eps=0.0, **kw):
+    g = rbd.decompose(X, d_max=d_max, eps_r=eps, **kw)
+    return g.Y.cpu().numpy(), g.T.cpu().numpy(), g.d, g.selected, g.residual_history
+
+
+def check_same(ref, Ys, T, d, sel, hist):
+    Yr, Tr, dr, selr, histr = ref
+    assert d == dr and sel == selr and hist == histr
+    for Y in Ys:
+        assert np.array_equal(Y.cpu().numpy(), Yr)
+    assert np.array_equal(T.cpu().numpy(), Tr)
+
+
+@pytest.mark.parametrize("R", [1, 2, 3, 4, 8])
+def test_c0_bitwise_across_shards(cuda, R):
+    X = dev(configs.c0_matrix(), cuda)
+    ref = single(X, 64, 1e-6)
+    check_same(ref, *distributed.decompose_virtual(X, R, 64, 1e-6)[:5])
+
+
+@pytest.mark.parametrize("R", [2, 5])
+def test_multichunk_rows_bitwise(cuda, R):
+    X = dev(oracle.random_matrix(9000, 210, 4), cuda)
+    ref = single(X, 40)
+    check_same(ref, *distributed.decompose_virtual(X, R, 40)[:5])
+
+
+def test_uneven_shards_and_start_in_last(cuda):
+    X = dev(oracle.random_matrix(700, 200, 5), cuda)
+    ref = single(X, 30, start_column=199)
+    out = distributed.decompose_virtual(X, 3, 30, n_locals=[1, 100, 99], start_column=199)
+    check_same(ref, *out[:5])
+    assert out[3][0] == 199
+
+
+def test_breakdown_and_oracle_parity(cuda):
+    x = oracle.random_low_rank(40, 30, 5, 210)
+    X = dev(x, cuda)
+    Ys, T, d, sel, hist, _ = distributed.decompose_virtual(X, 4, 30)
+    assert d == 5
+    r = oracle.decompose(x, 30)
+    assert sel == r.selected
+    assert np.abs(Ys[0].cpu().numpy() - r.Y).max() < 1e-10
+
+
+def test_ties_across_shards_smallest_global_index(cuda):
+    # identical columns in different shards: the smallest global index must win
+    x = oracle.random_matrix(64, 12, 6)
+    x[:, 9] = x[:, 2] * 3.0
+    x[:, 5] = x[:, 2] * 3.0
+    X = dev(x, cuda)
+    ref = single(X, 6)
+    check_same(ref, *distributed.decompose_virtual(X, 3, 6)[:5])
+
+
+def test_sharded_gating(cuda):
+    with pytest.raises(rbd.DegenerateInput):
+        distributed.decompose_virtual(dev(np.zeros((8, 6)), cuda), 2, 3)
+    x = oracle.random_matrix(8, 6, 1)
+    x[2, 4] = np.nan
+    with pytest.raises(rbd.InvalidArgument):
+        distributed.decompose_virtual(dev(x, cuda), 2, 3)
+    with pytest.raises(rbd.InvalidArgument):
+        distributed.decompose_virtual(dev(oracle.random_matrix(8, 6, 1), cuda), 2, 7)
