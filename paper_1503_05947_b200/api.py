@@ -240,6 +240,8 @@ def project_batch(Y, Xn, with_error: bool = True, ctx: Optional[Context] = None)
         N = Xc.shape[1]
         Tn = torch.empty((N, d), dtype=torch.float64, device=Y.device).t()
         err = torch.empty(N, dtype=torch.float64, device=Y.device) if with_error else None
+        ldt = Tn.stride(1)
+        assert ldt == d
         torch.cuda.current_stream(Y.device).synchronize()
         check(lib.rbd_project_batch(ctx.handle, C.c_void_p(Yc.data_ptr()), m, d, ldy,
                                     C.c_void_p(Xc.data_ptr()), N, ldx, C.c_void_p(Tn.data_ptr()),

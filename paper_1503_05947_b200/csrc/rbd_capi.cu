@@ -1099,7 +1099,9 @@ int rbd_project_batch(rbd_ctx_t ctx, const double* dY, int64_t m, int64_t d, int
   if (N == 0) return RBD_OK;
   CU(cudaSetDevice(ctx->device));
   long long nl = 0;
-  int rc = rbdk::launch_project_f64(dY, m, d, ldy, dXn, N, ldx, dTn, d_err, ctx->stream, &nl);
+  if (d_err) TRY(ensure(ctx->scratch1, sizeof(double) * (size_t)std::max<int64_t>(N, 32)));
+  int rc = rbdk::launch_project_f64(dY, m, d, ldy, dXn, N, ldx, dTn, d_err, ctx->stream, &nl,
+                                    d_err ? ptr<double>(ctx->scratch1) : nullptr);
   ctx->launches += nl;
   if (rc != 0) return set_err(RBD_ERR_CUDA, std::string("project kernel: ") + cudaGetErrorString((cudaError_t)rc));
   return RBD_OK;

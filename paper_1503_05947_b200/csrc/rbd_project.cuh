@@ -9,6 +9,8 @@
 
 #include <cuda_runtime.h>
 
+#include "rbd_project_dmma.cuh"
+
 namespace rbdk {
 
 constexpr int kPjBM = 64;   // rows of T_new (basis index k) per CTA
@@ -103,7 +105,30 @@ __global__ void k_reconstruct(const double* __restrict__ Y, long long m, long lo
 
 inline int launch_project_f64(const double* Y, long long m, long long d, long long ldy,
                               const double* Xn, long long N, long long ldx, double* Tn,
-                              double* err, cudaStream_t s, long long* nlaunch) {
+                              double* err, cudaStream_t s, long long* nlaunch,
+                              double* xnorm_scratch = nullptr) {
+  const bool dmma_ok = (ldy % 2 == 0) && (ldx % 2 == 0) &&
+                       ((reinterpret_cast<uintptr_t>(Y) | reinterpret_cast<uintptr_t>(Xn)) & 15) == 0;
+  *nlaunch = 0;
+  if (dmma_ok) {
+    constexpr int BM = 64, BN = 64, WM = 2, WN = 2;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_project_dmma<BM, BN, WM, WN>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dm_smem_bytes<BM, BN>());
+      attr = true;
+    }
+    double* xn = err ? xnorm_scratch : nullptr;
+    dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((d + BM - 1) / BM));
+    k_project_dmma<BM, BN, WM, WN><<<grid, WM * WN * 32, dm_smem_bytes<BM, BN>(), s>>>(
+        Y, m, d, ldy, Xn, N, ldx, Tn, xn);
+    *nlaunch += 1;
+    if (err) {
+      k_project_err_fused<<<(unsigned)((N + 7) / 8), 256, 0, s>>>(xn, Tn, d, N, err);
+      *nlaunch += 1;
+    }
+    return (int)cudaGetLastError();
+  }
   dim3 grid((unsigned)((N + kPjBN - 1) / kPjBN), (unsigned)((d + kPjBM - 1) / kPjBM));
   k_project_f64<<<grid, 256, 0, s>>>(Y, m, d, ldy, Xn, N, ldx, Tn);
   *nlaunch = 1;

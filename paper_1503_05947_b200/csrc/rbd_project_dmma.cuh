@@ -1,0 +1,175 @@
+// rbd_project_dmma.cuh — out-of-sample compression T_new = Y' X_new on the
+// FP64 tensor cores (DMMA: mma.sync.aligned.m16n8k4.row.col.f64), the one
+// dense contraction of the path (BASELINE north_star).
+//
+// CTA tile BM (basis rows l) x BN (new columns j), K = rows i of Y / X_new in
+// steps of 16 through a 3-stage cp.async pipeline. Both operands are staged
+// K-contiguous exactly as they sit in global memory (Y and X_new are
+// column-major) in XOR-swizzled 16-double rows (no padding). 64 x 64 tiles,
+// 2 x 2 warps of 32 x 32, fragments loaded per k4 sub-step so a thread needs
+// < 128 registers and four CTAs (16 warps) share an SM: the DMMA issue latency
+// is hidden by warps.
+// CTAs of the first l-tile also accumulate ||x_j||^2 from the staged X_new
+// tiles (no second pass over X_new for the error indicator).
+#pragma once
+
+#include <cuda_runtime.h>
+
+namespace rbdk {
+
+constexpr int kDmBK = 16;           // i per stage (row of 16 doubles, no padding)
+constexpr int kDmStages = 3;
+
+template <int BM, int BN>
+constexpr size_t dm_smem_bytes() {
+  return sizeof(double) * (size_t)kDmStages * (BM + BN) * kDmBK;
+}
+
+// XOR swizzle of the 16-double rows: element (row, k) lives at
+// row*16 + (k ^ (4*(row & 3))). Keeps 16-byte chunks intact (cp.async) and
+// makes the m16n8k4 fragment loads (row g / g+8, k = kk + t) conflict free.
+__device__ __forceinline__ int dm_swz(int row, int k) { return row * kDmBK + (k ^ ((row & 3) << 2)); }
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+__device__ __forceinline__ void dmma_16x8x4(double (&c)[4], double a0, double a1, double b0) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, "
+      "{%0,%1,%2,%3};\n"
+      : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+      : "d"(a0), "d"(a1), "d"(b0));
+}
+
+// One stage of a K-contiguous operand: ROWS tile rows (columns of Y or X_new),
+// 16 consecutive i each (8 chunks of 16 B). `full` = no bounds checks needed.
+template <int ROWS, int NTHREADS>
+__device__ __forceinline__ void dm_load_tile(double* s, const double* __restrict__ g, long long ld,
+                                             long long r0, long long rmax, long long i0,
+                                             long long m, bool full) {
+  static_assert((ROWS * 8) % NTHREADS == 0, "loader split");
+#pragma unroll
+  for (int q = 0; q < ROWS * 8 / NTHREADS; ++q) {
+    const int c = threadIdx.x + q * NTHREADS;
+    const int row = c >> 3, ch = c & 7;
+    const long long r = r0 + row;
+    const long long i = i0 + ch * 2;
+    int bytes = 16;
+    if (!full) bytes = (r < rmax && i < m) ? ((i + 1 < m) ? 16 : 8) : 0;
+    const double* src = (bytes > 0) ? g + r * ld + i : g;
+    cp_async16(s + dm_swz(row, ch * 2), src, bytes);
+  }
+}
+
+template <int BM, int BN, int WARPS_M, int WARPS_N>
+__global__ void __launch_bounds__(WARPS_M * WARPS_N * 32, 4)
+    k_project_dmma(const double* __restrict__ Y, long long m, long long d, long long ldy,
+                   const double* __restrict__ Xn, long long N, long long ldx,
+                   double* __restrict__ Tn, double* __restrict__ xnorm2) {
+  constexpr int NTHREADS = WARPS_M * WARPS_N * 32;
+  constexpr int WM = BM / WARPS_M, WN = BN / WARPS_N;   // warp tile
+  constexpr int MT = WM / 16, NT = WN / 8;               // mma tiles per warp
+  extern __shared__ __align__(16) double dm_smem[];
+  double* As = dm_smem;                                  // [stages][BM][16] swizzled
+  double* Bs = dm_smem + kDmStages * BM * kDmBK;         // [stages][BN][16] swizzled
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp / WARPS_N, wn = warp % WARPS_N;
+  const int g = lane >> 2, t = lane & 3;
+  const long long l0 = (long long)blockIdx.y * BM;
+  const long long j0 = (long long)blockIdx.x * BN;
+  const bool do_norm = (xnorm2 != nullptr) && blockIdx.y == 0;
+  const bool fullA = (l0 + BM <= d), fullB = (j0 + BN <= N);
+  double acc[MT][NT][4];
+#pragma unroll
+  for (int a = 0; a < MT; ++a)
+#pragma unroll
+    for (int b = 0; b < NT; ++b)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[a][b][e] = 0.0;
+  double xn = 0.0;   // ||x_j||^2: thread tid < BN owns column j0 + tid
+  const long long nk = (m + kDmBK - 1) / kDmBK;
+  auto load_stage = [&](int st, long long kt) {
+    const long long i0 = kt * kDmBK;
+    const bool kfull = i0 + kDmBK <= m;
+    dm_load_tile<BM, NTHREADS>(As + st * BM * kDmBK, Y, ldy, l0, d, i0, m, fullA && kfull);
+    dm_load_tile<BN, NTHREADS>(Bs + st * BN * kDmBK, Xn, ldx, j0, N, i0, m, fullB && kfull);
+  };
+#pragma unroll
+  for (int st = 0; st < kDmStages - 1; ++st) {
+    if (st < nk) load_stage(st, st);
+    cp_async_commit();
+  }
+  // swizzled fragment offsets: every fragment row has (row & 3) == (g & 3),
+  // so (row, 4q + t) sits at row*16 + 4*(q ^ (g & 3)) + t
+  const int baseA = (wm * WM + g) * kDmBK, baseB = (wn * WN + g) * kDmBK;
+  int koff[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) koff[q] = 4 * (q ^ (g & 3)) + t;
+  for (long long kt = 0; kt < nk; ++kt) {
+    cp_async_wait<kDmStages - 2>();
+    __syncthreads();
+    {
+      const long long kn = kt + kDmStages - 1;
+      if (kn < nk) load_stage((int)(kn % kDmStages), kn);
+      cp_async_commit();
+    }
+    const int sc = (int)(kt % kDmStages);
+    const double* A = As + sc * BM * kDmBK;
+    const double* B = Bs + sc * BN * kDmBK;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      double af[MT][2], bf[NT];
+#pragma unroll
+      for (int a = 0; a < MT; ++a) {
+        af[a][0] = A[baseA + (a * 16) * kDmBK + koff[q]];
+        af[a][1] = A[baseA + (a * 16 + 8) * kDmBK + koff[q]];
+      }
+#pragma unroll
+      for (int b = 0; b < NT; ++b) bf[b] = B[baseB + (b * 8) * kDmBK + koff[q]];
+#pragma unroll
+      for (int a = 0; a < MT; ++a)
+#pragma unroll
+        for (int b = 0; b < NT; ++b) dmma_16x8x4(acc[a][b], af[a][0], af[a][1], bf[b]);
+    }
+    if (do_norm && tid < BN) {
+      const double* xr = B + tid * kDmBK;
+#pragma unroll
+      for (int q = 0; q < kDmBK; ++q) xn = fma(xr[q], xr[q], xn);
+    }
+  }
+  cp_async_wait<0>();
+  // epilogue: T_new is d x N column-major (ld d)
+#pragma unroll
+  for (int a = 0; a < MT; ++a)
+#pragma unroll
+    for (int b = 0; b < NT; ++b)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const long long l = l0 + wm * WM + a * 16 + g + (e >= 2 ? 8 : 0);
+        const long long j = j0 + wn * WN + b * 8 + t * 2 + (e & 1);
+        if (l < d && j < N) Tn[l + j * d] = acc[a][b][e];
+      }
+  if (do_norm && tid < BN && j0 + tid < N) xnorm2[j0 + tid] = xn;
+}
+
+// err_j = max(||x_j||^2 - ||t_j||^2, 0) from the fused ||x||^2 (one warp per column).
+__global__ void k_project_err_fused(const double* __restrict__ xnorm2, const double* __restrict__ Tn,
+                                    long long d, long long N, double* __restrict__ err) {
+  const long long j = (long long)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  if (j >= N) return;
+  double tt = 0.0;
+  for (long long k = lane; k < d; k += 32) tt = fma(Tn[k + j * d], Tn[k + j * d], tt);
+  for (int off = 16; off > 0; off >>= 1) tt += __shfl_xor_sync(0xffffffffu, tt, off);
+  if (lane == 0) {
+    const double e = xnorm2[j] - tt;
+    err[j] = e > 0.0 ? e : 0.0;
+  }
+}
+
+}  // namespace rbdk
