@@ -36,6 +36,7 @@ def parse():
     p.add_argument("--cpu-seconds", type=float, default=15.0)
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--d-max", type=int, default=None, help="override d_max (quick runs)")
     return p.parse_args()
 
 
@@ -344,10 +345,103 @@ def run_b200(args):
         dist.destroy_process_group()
 
 
+def run_sharded(args):
+    """C3: X sharded by contiguous column blocks over the ranks (NCCL payload
+    allgather inside the library); weak per-GPU data, strong on the job."""
+    import torch
+    rank, world, local = dist_env()
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    import paper_1503_05947_b200 as rbd
+    from paper_1503_05947_b200 import configs, distributed as rd
+    w = configs.WORKLOADS[args.workload]
+    key = w.name.split("-")[0]
+    rank_r = {"C2": 1024, "C3": 2048, "C4": 512}.get(key, 64)
+    plan = rd.plan_shards(w.n, world)
+    o, nl = plan.offsets[rank], plan.n_locals[rank]
+    X = configs.low_rank_shard_torch(w.m, w.n, rank_r, configs.spectrum(key, rank_r),
+                                     {"C2": 1e-8, "C3": 1e-10, "C4": 1e-6}.get(key, 1e-6), w.seed,
+                                     o, nl, device=dev)
+    torch.cuda.synchronize(dev)
+    d_max = args.d_max or w.d_max
+    ctx = rbd.Context(local)
+    if world > 1:
+        uid = rd.exchange_unique_id(rank)
+    else:
+        import ctypes as C
+        buf = C.create_string_buffer(128)
+        from paper_1503_05947_b200._lib import check, load_library
+        check(load_library().rbd_comm_unique_id(buf))
+        uid = bytes(buf.raw)
+    rd.init_comm(ctx, rank, world, uid)
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    for _ in range(max(args.warmup, 0)):
+        r = rd.decompose_sharded(X, plan, rank, d_max, 0.0, ctx=ctx)
+    clocks = ClockSampler(local)
+    barrier()
+    torch.cuda.synchronize(dev)
+    clocks.start()
+    stream = torch.cuda.ExternalStream(ctx.stream, device=dev)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    launches0 = ctx.launches
+    e0.record(stream)
+    ds = []
+    for _ in range(args.steps):
+        r = rd.decompose_sharded(X, plan, rank, d_max, 0.0, ctx=ctx)
+        ds.append(r.d)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    barrier()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    t_max = ms
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_max = float(t.item())
+    total = w.m * w.n * 8 * sum(ds)
+    value = total / (t_max / 1e3) / 1e9
+    if rank == 0:
+        peak, src = peak_hbm()
+        per_gpu = value / world
+        line = {
+            "metric": "rbd_effective_hbm_gbs", "value": value, "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": w.name, "m": w.m, "n": w.n, "d_max": d_max,
+                       "d_reached": int(np.mean(ds)), "parallelism": f"colshard{world}",
+                       "shard_cols": list(plan.n_locals), "describe": w.describe},
+            "roofline": {"bound": "hbm", "achieved": per_gpu, "peak": peak, "unit": "GB/s",
+                         "frac": per_gpu / peak, "traffic": None,
+                         "kernel": "k_rbd_persistent<2,true> per step + payload allgather",
+                         "note": "per-GPU X bytes x steps / time", "peak_source": src},
+            "cpu_baseline": None, "e2e": None, "gpu_launches": ctx.launches - launches0,
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+    elif args.workload.startswith(("C2", "C3")):
+        run_sharded(args)
     else:
         run_b200(args)
 

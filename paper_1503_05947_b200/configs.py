@@ -133,3 +133,30 @@ def spectrum(name: str, rank: int):
 
 def eps_for(w: Workload, max_col_norm: float) -> float:
     return w.eps_abs if w.eps_rel == 0.0 else w.eps_rel * max_col_norm
+
+
+def low_rank_shard_torch(m: int, n: int, rank: int, s, noise_var: float, seed: int,
+                         col_offset: int, n_local: int, device="cuda", block: int = 1024):
+    """Columns [col_offset, col_offset + n_local) of the same X as
+    low_rank_matrix_torch-style generation, identical for any sharding:
+    U, V from one generator (seed), noise per 1024-column block from a
+    generator keyed by (seed, block)."""
+    import torch
+
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    U = torch.linalg.qr(torch.randn(m, rank, dtype=torch.float64, device=device, generator=g))[0]
+    V = torch.linalg.qr(torch.randn(n, rank, dtype=torch.float64, device=device, generator=g))[0]
+    sv = torch.as_tensor(np.asarray(s, dtype=np.float64), device=device)
+    Xt = torch.empty((n_local, m), dtype=torch.float64, device=device)
+    sigma = float(np.sqrt(noise_var))
+    gn = torch.Generator(device=device)
+    for b0 in range((col_offset // block) * block, col_offset + n_local, block):
+        lo, hi = max(b0, col_offset), min(b0 + block, col_offset + n_local)
+        gn.manual_seed(seed * 1000003 + b0 // block)
+        noise = torch.randn((min(block, n - b0), m), dtype=torch.float64, device=device, generator=gn)
+        blk = (V[lo:hi] * sv) @ U.t()
+        blk += sigma * noise[lo - b0:hi - b0]
+        Xt[lo - col_offset:hi - col_offset] = blk
+    del U, V
+    return Xt.t()

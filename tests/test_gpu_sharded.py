@@ -81,3 +81,21 @@ def test_sharded_gating(cuda):
         distributed.decompose_virtual(dev(x, cuda), 2, 3)
     with pytest.raises(rbd.InvalidArgument):
         distributed.decompose_virtual(dev(oracle.random_matrix(8, 6, 1), cuda), 2, 7)
+
+
+def test_nccl_world1_matches_single_gpu(cuda):
+    """The real NCCL exchange (communicator of size 1) gives the single-GPU bits."""
+    import ctypes as C
+    from paper_1503_05947_b200._lib import check, load_library
+    X = dev(oracle.random_matrix(5000, 300, 8), cuda)
+    ref = single(X, 50)
+    ctx = rbd.Context(0)
+    buf = C.create_string_buffer(128)
+    check(load_library().rbd_comm_unique_id(buf))
+    distributed.init_comm(ctx, 0, 1, bytes(buf.raw))
+    plan = distributed.plan_shards(300, 1)
+    r = distributed.decompose_sharded(X, plan, 0, 50, ctx=ctx)
+    assert r.d == ref[2] and r.selected == ref[3] and r.residual_history == ref[4]
+    assert np.array_equal(r.Y.cpu().numpy(), ref[0])
+    assert np.array_equal(r.T_local.cpu().numpy(), ref[1])
+    ctx.close()
