@@ -1,0 +1,142 @@
+// rbd/decompose.hpp — drop-in for proj/include/rbd/decompose.hpp:13-79 on B200:
+// same names, fields, defaults and error types; the work runs on the GPU
+// through the C ABI (include/rbd_cuda.h). Link with librbd_b200.so.
+#ifndef RBD_B200_DECOMPOSE_HPP
+#define RBD_B200_DECOMPOSE_HPP
+
+#include <cstdint>
+#include <optional>
+#include <vector>
+
+#include "rbd/errors.hpp"
+#include "rbd/types.hpp"
+#include "rbd/weight.hpp"
+#include "rbd_cuda.h"
+
+namespace rbd {
+
+struct StartSpec {                                   // decompose.hpp:14-23
+  enum class Kind { fixed_column, seeded_random };
+  static StartSpec column(Index i) { return {Kind::fixed_column, i, 0}; }
+  static StartSpec seeded(std::uint64_t s) { return {Kind::seeded_random, 0, s}; }
+  Kind kind = Kind::fixed_column;
+  Index column_index = 0;
+  std::uint64_t seed = 0;
+};
+
+struct RbdConfig {                                   // decompose.hpp:25-36
+  Index d_max = 1;
+  double eps_R = 0.0;
+  StartSpec start{};
+  WeightSpec weight{};
+  bool reorthogonalize = false;
+  double breakdown_tol = -1.0;
+};
+
+struct RbdModel {                                    // decompose.hpp:39-46
+  Matrix Y;                                          // m x d
+  Matrix T;                                          // d x n
+  std::vector<Index> selected;
+  std::vector<double> residual_history;
+  Index d = 0;
+  WeightSpec weight{};
+};
+
+struct MgsResult {                                   // decompose.hpp:48-51
+  Vector xi;
+  double residual_norm;
+};
+
+namespace detail {
+// One context per host thread (rbd_cuda.h threading contract).
+inline rbd_ctx_t context() {
+  struct Holder {
+    rbd_ctx_t c = nullptr;
+    ~Holder() {
+      if (c) rbd_ctx_destroy(c);
+    }
+  };
+  thread_local Holder h;
+  if (!h.c) check(rbd_ctx_create(0, &h.c));
+  return h.c;
+}
+}  // namespace detail
+
+inline std::optional<MgsResult> mgs_project(const VectorRef& v, const MatrixRef& basis,
+                                            double breakdown_tol, bool reorthogonalize = false) {
+  if (basis.cols() > 0 && basis.rows() != v.size())
+    throw DimensionMismatch("mgs_project: vector length != basis row count");
+  Vector xi(v.size());
+  double norm = 0.0;
+  int ok = 0;
+  detail::check(rbd_mgs_project_host(detail::context(), v.data(), v.size(), basis.data(),
+                                     basis.cols(), basis.rows(), breakdown_tol,
+                                     reorthogonalize ? 1 : 0, xi.data(), &norm, &ok));
+  if (!ok) return std::nullopt;
+  return MgsResult{std::move(xi), norm};
+}
+
+inline RbdModel decompose(const Matrix& x, const RbdConfig& cfg) {
+  rbd_config_t c;
+  rbd_config_default(&c);
+  c.d_max = cfg.d_max;
+  c.eps_R = cfg.eps_R;
+  c.start_kind = cfg.start.kind == StartSpec::Kind::seeded_random ? RBD_START_SEEDED_RANDOM
+                                                                  : RBD_START_FIXED_COLUMN;
+  c.start_column = cfg.start.column_index;
+  c.start_seed = cfg.start.seed;
+  c.reorthogonalize = cfg.reorthogonalize ? 1 : 0;
+  c.breakdown_tol = cfg.breakdown_tol;
+  c.weight_kind = static_cast<int32_t>(cfg.weight.kind());
+  c.weight_dim = cfg.weight.dim();
+  const Index m = x.rows(), n = x.cols();
+  const Index cap = std::max<Index>(1, std::min<Index>(cfg.d_max, std::max<Index>(n, 1)));
+  std::vector<double> Yb(static_cast<size_t>(std::max<Index>(m, 1) * cap));
+  std::vector<double> Tb(static_cast<size_t>(cap * std::max<Index>(n, 1)));
+  std::vector<int64_t> sel(static_cast<size_t>(cap));
+  std::vector<double> hist(static_cast<size_t>(cap));
+  rbd_result_t r{};
+  detail::check(rbd_decompose_host(detail::context(), x.data(), m, n, std::max<Index>(m, 1), &c,
+                                   Yb.data(), Tb.data(), sel.data(), hist.data(), &r));
+  RbdModel model;
+  model.d = r.d;
+  model.weight = cfg.weight;
+  model.Y = Matrix(m, r.d);
+  for (Index j = 0; j < r.d; ++j)
+    for (Index i = 0; i < m; ++i) model.Y(i, j) = Yb[static_cast<size_t>(i + j * m)];
+  model.T = Matrix(r.d, n);   // device T is row-major (T[k*n + j])
+  for (Index k = 0; k < r.d; ++k)
+    for (Index j = 0; j < n; ++j) model.T(k, j) = Tb[static_cast<size_t>(k * n + j)];
+  model.selected.assign(sel.begin(), sel.begin() + r.d);
+  model.residual_history.assign(hist.begin(), hist.begin() + r.d);
+  return model;
+}
+
+inline Vector project(const RbdModel& model, const VectorRef& v) {     // decompose.cpp:113-117
+  if (v.size() != model.Y.rows()) throw DimensionMismatch("project: vector length != m");
+  Vector c(model.d);
+  if (model.d == 0) return c;
+  detail::check(rbd_project_host(detail::context(), model.Y.data(), model.Y.rows(), model.d,
+                                 v.data(), 1, c.data(), nullptr));
+  return c;
+}
+
+inline Vector reconstruct(const RbdModel& model, const VectorRef& c) { // decompose.cpp:119-123
+  if (c.size() != model.d) throw DimensionMismatch("reconstruct: coefficient length != d");
+  Vector v(model.Y.rows());
+  detail::check(rbd_reconstruct_host(detail::context(), model.Y.data(), model.Y.rows(), model.d,
+                                     c.data(), v.data()));
+  return v;
+}
+
+inline Matrix compress_matrix(const RbdModel& model) {                 // decompose.cpp:125
+  Matrix out(model.Y.rows(), model.T.cols());
+  if (model.d == 0 || model.T.cols() == 0) return out;
+  detail::check(rbd_compress_host(detail::context(), model.Y.data(), model.Y.rows(), model.d,
+                                  model.T.data(), model.T.cols(), out.data()));
+  return out;
+}
+
+}  // namespace rbd
+
+#endif

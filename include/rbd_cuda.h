@@ -3,7 +3,7 @@
  * This is the drop-in boundary under the reference's C++ API
  * (proj/include/rbd/decompose.hpp:61-77, workspace.hpp:34-54). Every entry
  * point takes plain pointers and sizes; no torch or Eigen types cross it.
- * The C++ mirror of the reference API (include/rbd/*.hpp) and the Python
+ * The C++ mirror of the reference API (include/rbd/<name>.hpp) and the Python
  * package (paper_1503_05947_b200) are thin layers over these functions.
  *
  * Layouts (all fp64):
@@ -129,6 +129,15 @@ int rbd_ws_error_sq(rbd_ws_t ws, int64_t j, const double* h_c, int64_t clen, dou
 int64_t rbd_ws_d(rbd_ws_t ws);
 int rbd_ws_read(rbd_ws_t ws, double* h_col_sq, double* h_residual_sq, double* h_yax /* d x n row-major */);
 
+/* Host-buffer variants used by the C++ mirror (include/rbd/<name>.hpp). */
+int rbd_mgs_project_host(rbd_ctx_t ctx, const double* hv, int64_t m, const double* hB, int64_t k,
+                         int64_t ldb, double breakdown_tol, int reorthogonalize, double* hxi,
+                         double* norm, int* ok);
+/* Workspace over a device copy of host X (owned by the workspace). */
+int rbd_ws_init_host(rbd_ctx_t ctx, const double* hX, int64_t m, int64_t n, int64_t ldx,
+                     int64_t cap, rbd_ws_t* out);
+int rbd_ws_extend_host(rbd_ws_t ws, const double* hxi);
+
 /* Out-of-sample compression (decompose.cpp:113-117, batched) plus the
  * identity error indicator err_j = max(||x_j||^2 - ||t_j||^2, 0) (Eq. 3,
  * workspace.cpp:88-97). dY m x d (ld ldy), dXn m x N (ld ldx);
@@ -138,6 +147,12 @@ int rbd_project_batch(rbd_ctx_t ctx, const double* dY, int64_t m, int64_t d, int
 /* rbd::reconstruct (decompose.cpp:119-123): dv = Y c (dc length d). */
 int rbd_reconstruct(rbd_ctx_t ctx, const double* dY, int64_t m, int64_t d, int64_t ldy,
                     const double* dc, double* dv);
+/* rbd::compress_matrix (decompose.cpp:125): V = Y C, C d x N column-major
+ * (ld d), V m x N column-major (ld m). */
+int rbd_reconstruct_batch(rbd_ctx_t ctx, const double* dY, int64_t m, int64_t d, int64_t ldy,
+                          const double* dC, int64_t N, double* dV);
+int rbd_compress_host(rbd_ctx_t ctx, const double* hY, int64_t m, int64_t d, const double* hC,
+                      int64_t N, double* hV);
 /* Host-buffer variants (upload, kernel, download inside the call). */
 int rbd_project_host(rbd_ctx_t ctx, const double* hY, int64_t m, int64_t d, const double* hXn,
                      int64_t N, double* hTn, double* h_err);

@@ -138,6 +138,12 @@ _SIGS = {
     "rbd_ctx_init_comm": (C.c_int, [_P, C.c_int, C.c_int, C.c_char_p]),
     "rbd_decompose_sharded": (C.c_int, [_P, _P, _I64, _I64, _I64, _I64, _I64, C.POINTER(Config),
                                         _P, _P, _P, _P, C.POINTER(Result)]),
+    "rbd_mgs_project_host": (C.c_int, [_P, _P, _I64, _P, _I64, _I64, _D, C.c_int, _P, _DP,
+                                       C.POINTER(C.c_int)]),
+    "rbd_ws_init_host": (C.c_int, [_P, _P, _I64, _I64, _I64, _I64, C.POINTER(_P)]),
+    "rbd_ws_extend_host": (C.c_int, [_P, _P]),
+    "rbd_reconstruct_batch": (C.c_int, [_P, _P, _I64, _I64, _I64, _P, _I64, _P]),
+    "rbd_compress_host": (C.c_int, [_P, _P, _I64, _I64, _P, _I64, _P]),
     "rbd_decompose_sharded_virtual": (C.c_int, [_P, C.c_int, _P, _P, _I64, _I64, C.POINTER(Config),
                                                 _P, _P, _P, _P, C.POINTER(Result)]),
 }

@@ -131,6 +131,7 @@ struct rbd_ws_s {
   const double* X;
   long long m, n, ldx, cap, d;
   DevBuf T, colsq, resid, partial, rec, counter, out, tmp;
+  DevBuf Xown;   // host-entry workspaces own a device copy of X
 };
 
 namespace {
@@ -994,7 +995,8 @@ int rbd_ws_init(rbd_ctx_t ctx, const double* dX, int64_t m, int64_t n, int64_t l
 
 int rbd_ws_destroy(rbd_ws_t ws) {
   if (!ws) return RBD_OK;
-  DevBuf* bl[] = {&ws->T, &ws->colsq, &ws->resid, &ws->partial, &ws->rec, &ws->counter, &ws->out, &ws->tmp};
+  DevBuf* bl[] = {&ws->T,       &ws->colsq, &ws->resid, &ws->partial, &ws->rec,
+                  &ws->counter, &ws->out,   &ws->tmp,   &ws->Xown};
   for (DevBuf* b : bl) release(*b);
   delete ws;
   return RBD_OK;
@@ -1566,6 +1568,125 @@ int rbd_decompose_sharded_virtual(rbd_ctx_t ctx, int nranks, const double* const
   int rc = sharded_decompose(R, ex, sh, m, ldx, off, cfg, h_selected, h_history, result);
   for (auto c : R) ctx->launches += c->launches;
   return rc;
+}
+
+}  // extern "C"
+
+extern "C" {
+
+int rbd_mgs_project_host(rbd_ctx_t ctx, const double* hv, int64_t m, const double* hB, int64_t k,
+                         int64_t ldb, double breakdown_tol, int reorthogonalize, double* hxi,
+                         double* norm, int* ok) {
+  if (!ctx) return set_err(RBD_ERR_INVALID_ARGUMENT, "null context");
+  if (m < 1) return set_err(RBD_ERR_DIMENSION_MISMATCH, "mgs_project: vector length != basis row count");
+  if (k > 0 && ldb < m) return set_err(RBD_ERR_DIMENSION_MISMATCH, "mgs_project: vector length != basis row count");
+  CU(cudaSetDevice(ctx->device));
+  DevBuf bv, bB, bx;
+  auto fin = [&](int rc) {
+    release(bv);
+    release(bB);
+    release(bx);
+    return rc;
+  };
+  int rc;
+  if ((rc = ensure(bv, sizeof(double) * m)) || (rc = ensure(bx, sizeof(double) * m)) ||
+      (rc = ensure(bB, sizeof(double) * m * std::max<int64_t>(k, 1))))
+    return fin(rc);
+  if (cudaMemcpyAsync(bv.p, hv, sizeof(double) * m, cudaMemcpyHostToDevice, ctx->stream) ||
+      (k > 0 && cudaMemcpy2DAsync(bB.p, sizeof(double) * m, hB, sizeof(double) * ldb,
+                                  sizeof(double) * m, k, cudaMemcpyHostToDevice, ctx->stream)))
+    return fin(set_err(RBD_ERR_CUDA, "mgs_project_host: H2D failed"));
+  int okv = 0;
+  double nv = 0.0;
+  rc = rbd_mgs_project(ctx, ptr<double>(bv), m, ptr<double>(bB), k, m, breakdown_tol,
+                       reorthogonalize, ptr<double>(bx), &nv, &okv);
+  if (rc) return fin(rc);
+  if (okv && hxi && cudaMemcpy(hxi, bx.p, sizeof(double) * m, cudaMemcpyDeviceToHost))
+    return fin(set_err(RBD_ERR_CUDA, "mgs_project_host: D2H failed"));
+  if (ok) *ok = okv;
+  if (norm) *norm = nv;
+  return fin(RBD_OK);
+}
+
+int rbd_ws_init_host(rbd_ctx_t ctx, const double* hX, int64_t m, int64_t n, int64_t ldx,
+                     int64_t cap, rbd_ws_t* out) {
+  if (!ctx || !out) return set_err(RBD_ERR_INVALID_ARGUMENT, "null argument");
+  if (m < 1 || n < 1) return set_err(RBD_ERR_INVALID_ARGUMENT, "workspace_init: empty matrix");
+  if (ldx < m) return set_err(RBD_ERR_DIMENSION_MISMATCH, "workspace_init: ldx < m");
+  CU(cudaSetDevice(ctx->device));
+  DevBuf xb;
+  TRY(ensure(xb, sizeof(double) * m * n));
+  if (cudaMemcpy2D(xb.p, sizeof(double) * m, hX, sizeof(double) * ldx, sizeof(double) * m, n,
+                   cudaMemcpyHostToDevice) != cudaSuccess) {
+    release(xb);
+    return set_err(RBD_ERR_CUDA, "workspace_init: H2D failed");
+  }
+  rbd_ws_t ws = nullptr;
+  int rc = rbd_ws_init(ctx, ptr<double>(xb), m, n, m, cap, &ws);
+  if (rc) {
+    release(xb);
+    return rc;
+  }
+  ws->Xown = xb;
+  *out = ws;
+  return RBD_OK;
+}
+
+int rbd_ws_extend_host(rbd_ws_t ws, const double* hxi) {
+  if (!ws) return set_err(RBD_ERR_INVALID_ARGUMENT, "null workspace");
+  DevBuf b;
+  TRY(ensure(b, sizeof(double) * ws->m));
+  if (cudaMemcpy(b.p, hxi, sizeof(double) * ws->m, cudaMemcpyHostToDevice) != cudaSuccess) {
+    release(b);
+    return set_err(RBD_ERR_CUDA, "workspace_extend: H2D failed");
+  }
+  int rc = rbd_ws_extend(ws, ptr<double>(b));
+  release(b);
+  return rc;
+}
+
+int rbd_reconstruct_batch(rbd_ctx_t ctx, const double* dY, int64_t m, int64_t d, int64_t ldy,
+                          const double* dC, int64_t N, double* dV) {
+  if (!ctx) return set_err(RBD_ERR_INVALID_ARGUMENT, "null context");
+  if (ldy < m || m < 1 || N < 0) return set_err(RBD_ERR_DIMENSION_MISMATCH, "compress: bad sizes");
+  if (N == 0) return RBD_OK;
+  CU(cudaSetDevice(ctx->device));
+  const long long gx = std::min<long long>(cdiv(m, 256), 1024);
+  for (long long j0 = 0; j0 < N; j0 += 65535) {
+    const long long nb = std::min<long long>(65535, N - j0);
+    k_reconstruct_batch<<<dim3((unsigned)gx, (unsigned)nb), 256, 0, ctx->stream>>>(
+        dY, m, d, ldy, dC + j0 * d, nb, dV + j0 * m);
+    ctx->launches++;
+  }
+  CU(cudaGetLastError());
+  return RBD_OK;
+}
+
+int rbd_compress_host(rbd_ctx_t ctx, const double* hY, int64_t m, int64_t d, const double* hC,
+                      int64_t N, double* hV) {
+  if (!ctx) return set_err(RBD_ERR_INVALID_ARGUMENT, "null context");
+  if (m < 1 || d < 1 || N < 1) return set_err(RBD_ERR_DIMENSION_MISMATCH, "compress: bad sizes");
+  CU(cudaSetDevice(ctx->device));
+  DevBuf bY, bC, bV;
+  auto fin = [&](int rc) {
+    release(bY);
+    release(bC);
+    release(bV);
+    return rc;
+  };
+  int rc;
+  if ((rc = ensure(bY, sizeof(double) * m * d)) || (rc = ensure(bC, sizeof(double) * d * N)) ||
+      (rc = ensure(bV, sizeof(double) * m * N)))
+    return fin(rc);
+  if (cudaMemcpyAsync(bY.p, hY, sizeof(double) * m * d, cudaMemcpyHostToDevice, ctx->stream) ||
+      cudaMemcpyAsync(bC.p, hC, sizeof(double) * d * N, cudaMemcpyHostToDevice, ctx->stream))
+    return fin(set_err(RBD_ERR_CUDA, "compress_host: H2D failed"));
+  rc = rbd_reconstruct_batch(ctx, ptr<double>(bY), m, d, m, ptr<double>(bC), N, ptr<double>(bV));
+  if (rc) return fin(rc);
+  if (cudaMemcpyAsync(hV, bV.p, sizeof(double) * m * N, cudaMemcpyDeviceToHost, ctx->stream) ||
+      cudaStreamSynchronize(ctx->stream))
+    return fin(set_err(RBD_ERR_CUDA, "compress_host: D2H failed"));
+  return fin(RBD_OK);
 }
 
 }  // extern "C"

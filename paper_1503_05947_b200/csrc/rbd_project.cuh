@@ -139,6 +139,20 @@ inline int launch_project_f64(const double* Y, long long m, long long d, long lo
   return (int)cudaGetLastError();
 }
 
+// V = Y C (decompose.cpp:119-125): thread per row i, one column j per grid.y.
+__global__ void k_reconstruct_batch(const double* __restrict__ Y, long long m, long long d,
+                                    long long ldy, const double* __restrict__ C, long long N,
+                                    double* __restrict__ V) {
+  const long long j = blockIdx.y;
+  const double* c = C + j * d;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m;
+       i += (long long)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (long long k = 0; k < d; ++k) s = fma(Y[i + k * ldy], c[k], s);
+    V[i + j * m] = s;
+  }
+}
+
 inline int launch_reconstruct_f64(const double* Y, long long m, long long d, long long ldy,
                                   const double* c, double* v, cudaStream_t s, long long* nlaunch) {
   const long long g = (m + 255) / 256;
