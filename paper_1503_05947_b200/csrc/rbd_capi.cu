@@ -436,6 +436,7 @@ int launch_persistent(rbd_ctx_t ctx, const LoopBufs& L) {
   TRY(ensure(ctx->gcnt, sizeof(double) * (size_t)(L.d_max + 1)));   // p_k
   TRY(ensure(ctx->ygcnt, sizeof(Rec) * (size_t)grid));              // CTA records
   CU(cudaMemsetAsync(ctx->ctl.p, 0, sizeof(StepCtl), ctx->stream));
+  CU(cudaMemsetAsync(ctx->bar.p, 0, 64, ctx->stream));
   // chunk partials double as ready flags: NaN (all bytes 0xFF) = not written
   CU(cudaMemsetAsync(ctx->partial.p, 0xFF, sizeof(double) * (size_t)S * L.n, ctx->stream));
   (void)ngx;
@@ -1384,6 +1385,7 @@ int sharded_decompose(std::vector<rbd_ctx_t>& R, Exchange& ex, std::vector<Shard
     DevState* st = ptr<DevState>(c->state);
     CU(cudaMemsetAsync(st, 0, sizeof(DevState), c->stream));
     CU(cudaMemsetAsync(c->ctl.p, 0, sizeof(StepCtl), c->stream));
+    CU(cudaMemsetAsync(c->bar.p, 0, 64, c->stream));
     CU(cudaMemsetAsync(c->partial.p, 0xFF, sizeof(double) * (size_t)cdiv(m, kChunk) * nloc, c->stream));
     if (sh[r].n_local > 0)
       TRY(enqueue_init(c, sh[r].X, m, sh[r].n_local, ldx, ptr<double>(c->partial),

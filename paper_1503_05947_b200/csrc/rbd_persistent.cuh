@@ -83,27 +83,23 @@ __device__ __forceinline__ void wait_step_ne(const long long* flag, long long ba
   }
 }
 
-// Sense-reversing grid barrier (all CTAs co-resident: cooperative launch).
-// Traps after 30 s instead of hanging the device.
+// Grid barrier (all CTAs co-resident: cooperative launch): one monotonic
+// arrival counter, release-add on arrival, acquire-poll until it reaches the
+// next multiple of gridDim.x. The counter is zeroed before every decompose
+// and every launch of one decompose uses the same grid, so barrier b of the
+// call completes at b * gridDim.x. Traps after 30 s instead of hanging.
 __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned& gen) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence();
-    const unsigned target = gen + 1;
-    if (atomicAdd(&bar[0], 1u) == gridDim.x - 1) {
-      bar[0] = 0u;
-      __threadfence();
-      atomicAdd(&bar[1], 1u);
-    } else {
-      const unsigned long long t0 = globaltimer();
-      unsigned spins = 0;
-      while (ld_acquire_u32(&bar[1]) != target) {
-        __nanosleep(64);
-        if ((++spins & 0xffffu) == 0 && globaltimer() - t0 > 30000000000ull) __trap();
-      }
+    unsigned old;
+    asm volatile("atom.add.release.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(bar) : "memory");
+    const unsigned goal = (old / gridDim.x + 1) * gridDim.x;
+    const unsigned long long t0 = globaltimer();
+    unsigned spins = 0;
+    while ((int)(ld_acquire_u32(bar) - goal) < 0) {
+      if ((++spins & 0xffffu) == 0 && globaltimer() - t0 > 30000000000ull) __trap();
     }
-    __threadfence();
-    gen = target;
+    gen = goal;
   }
   __syncthreads();
 }
@@ -184,8 +180,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
   double* cs = dsm;                // c = T[0:k, j*]
   double* ps = dsm + a.d_max;      // p_{k-1} (pending column)
   __shared__ double red[kWarps][kCols];
-  __shared__ double red_c[kWarps][kFRows];
-  __shared__ double red_p[kWarps][kFRows];
+  constexpr int kPRows = 32 * VEC;  // rows per P1 block
+  __shared__ double red_c[kWarps][kPRows];
+  __shared__ double red_p[kWarps][kPRows];
   __shared__ double smn[kWarps];
   __shared__ Rec smr[kWarps];
   __shared__ long long sh_tile;
@@ -219,7 +216,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
   const double eps_R = st->eps_R, tol = st->breakdown_tol;
   const int cfg_reorth = st->cfg_reorth;
   const long long S = (m + kChunk - 1) / kChunk;
-  const long long nblk = (m + kFRows - 1) / kFRows;
+  const long long nblk = (m + kPRows - 1) / kPRows;
   const long long b0 = nblk * cta / G, b1 = nblk * (cta + 1) / G;
   const long long ngx = (n + kCols - 1) / kCols;   // X column groups
   const long long nx = ngx * S;                    // X tiles
@@ -260,50 +257,82 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
     __syncthreads();
     double nacc = 0.0;
     for (long long b = b0; b < b1; ++b) {
-      const long long i = b * kFRows + lane;
-      const bool ok = i < m;
-      double acc_c = 0.0, acc_p = 0.0;
-      if (ok) {
-        const double* yp = a.Y + i + (long long)warp * m;
+      // lane owns rows i0 .. i0+VEC-1 (a 16-byte pair when VEC == 2)
+      const long long i0 = b * kPRows + (long long)VEC * lane;
+      double acc_c[VEC], acc_p[VEC];
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) acc_c[v] = acc_p[v] = 0.0;
+      if (i0 + VEC <= m) {
+        const double* yp = a.Y + i0 + (long long)warp * m;
         const long long stp = (long long)kWarps * m;
         long long l = warp;
         for (; l + 15 * kWarps < kb; l += 16 * kWarps) {   // 16 loads in flight per lane
-          double yv[16];
-#pragma unroll
-          for (int q = 0; q < 16; ++q) yv[q] = yp[q * stp];
+          double yv[16][VEC];
 #pragma unroll
           for (int q = 0; q < 16; ++q) {
-            acc_c = fma(yv[q], cs[l + q * kWarps], acc_c);
-            acc_p = fma(yv[q], ps[l + q * kWarps], acc_p);
+            if constexpr (VEC == 2) {
+              const double2 t2 = *reinterpret_cast<const double2*>(yp + q * stp);
+              yv[q][0] = t2.x;
+              yv[q][VEC - 1] = t2.y;
+            } else {
+              yv[q][0] = yp[q * stp];
+            }
           }
+#pragma unroll
+          for (int q = 0; q < 16; ++q)
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) {
+              acc_c[v] = fma(yv[q][v], cs[l + q * kWarps], acc_c[v]);
+              acc_p[v] = fma(yv[q][v], ps[l + q * kWarps], acc_p[v]);
+            }
           yp += 16 * stp;
         }
         for (; l < kb; l += kWarps) {
-          const double y0 = *yp;
-          acc_c = fma(y0, cs[l], acc_c);
-          acc_p = fma(y0, ps[l], acc_p);
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) {
+            acc_c[v] = fma(yp[v], cs[l], acc_c[v]);
+            acc_p[v] = fma(yp[v], ps[l], acc_p[v]);
+          }
           yp += stp;
         }
+      } else {
+        for (int v = 0; v < VEC; ++v) {
+          if (i0 + v >= m) break;
+          const double* yp = a.Y + i0 + v + (long long)warp * m;
+          for (long long l = warp; l < kb; l += kWarps) {
+            acc_c[v] = fma(*yp, cs[l], acc_c[v]);
+            acc_p[v] = fma(*yp, ps[l], acc_p[v]);
+            yp += (long long)kWarps * m;
+          }
+        }
       }
-      red_c[warp][lane] = acc_c;
-      red_p[warp][lane] = acc_p;
-      __syncthreads();
-      if (warp == 0 && ok) {
-        double sc = red_c[0][lane], sp = red_p[0][lane];
 #pragma unroll
-        for (int w = 1; w < kWarps; ++w) {
-          sc += red_c[w][lane];
-          sp += red_p[w][lane];
-        }
-        if (pending) {
-          const double yk1 = (a.w[i] - sp) / wnorm_prev;   // second pass of column k-1
-          a.Y[i + (k - 1) * m] = yk1;
-          sc = fma(yk1, cs[k - 1], sc);
-        }
-        if (live) {
-          const double w1 = x[i] - sc;                     // first pass of column k
-          a.w[i] = w1;
-          nacc = fma(w1, w1, nacc);
+      for (int v = 0; v < VEC; ++v) {
+        red_c[warp][VEC * lane + v] = acc_c[v];
+        red_p[warp][VEC * lane + v] = acc_p[v];
+      }
+      __syncthreads();
+      if (warp == 0) {
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) {
+          const long long i = i0 + v;
+          if (i >= m) break;
+          double sc = red_c[0][VEC * lane + v], sp = red_p[0][VEC * lane + v];
+#pragma unroll
+          for (int w = 1; w < kWarps; ++w) {
+            sc += red_c[w][VEC * lane + v];
+            sp += red_p[w][VEC * lane + v];
+          }
+          if (pending) {
+            const double yk1 = (a.w[i] - sp) / wnorm_prev;   // second pass of column k-1
+            a.Y[i + (k - 1) * m] = yk1;
+            sc = fma(yk1, cs[k - 1], sc);
+          }
+          if (live) {
+            const double w1 = x[i] - sc;                     // first pass of column k
+            a.w[i] = w1;
+            nacc = fma(w1, w1, nacc);
+          }
         }
       }
       __syncthreads();
@@ -346,6 +375,53 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
       ctl->breakdown = (norm0 < tol || norm0 == 0.0) ? 1 : 0;
       st_release_s64(&ctl->p_step, k + 1);
     }
+    long long pend_g = -1;
+    auto finalize_group = [&](const long long g) {
+          // ---- finalise columns 4g..4g+3 (warps 0..3, one column each) ----
+            if (tid == 0) wait_step(&ctl->p_step, k + 1);
+            __syncthreads();
+            const int re = __ldcg(&ctl->reorth);
+            const int bd = __ldcg(&ctl->breakdown);
+            const double nrm = __ldcg(&ctl->norm);
+            const long long j = g * kCols + warp;
+            if (warp < kCols && j < n) {
+              double sp = 0.0, corr = 0.0;
+              for (long long ss = lane; ss < S; ss += 32) {
+                sp += poll_f64(&a.partial[ss * n + j]);
+                st_relaxed_f64(&a.partial[ss * n + j], kNaN);
+              }
+              if (re && !bd) {
+                for (long long l0 = 0; l0 < k; l0 += 512) {
+                  double tv[16], pv[16];
+  #pragma unroll
+                  for (int q = 0; q < 16; ++q) {
+                    const long long l = l0 + lane + 32 * q;
+                    tv[q] = (l < k) ? __ldcg(&a.T[l * n + j]) : 0.0;
+                    pv[q] = (l < k) ? __ldcg(&a.p[l]) : 0.0;
+                  }
+  #pragma unroll
+                  for (int q = 0; q < 16; ++q) corr = fma(pv[q], tv[q], corr);
+                }
+              }
+  #pragma unroll
+              for (int off = 16; off > 0; off >>= 1) {
+                sp += __shfl_xor_sync(0xffffffffu, sp, off);
+                corr += __shfl_xor_sync(0xffffffffu, corr, off);
+              }
+              if (lane == 0 && !bd) {
+                const double tt = (sp - corr) / nrm;
+                a.T[k * n + j] = tt;                                   // decompose.cpp:93
+                const double sq = __dmul_rn(tt, tt);
+                double rr = __dsub_rn(__ldcg(&a.r[j]), sq);            // workspace.cpp:52-53
+                rr = rr > 0.0 ? rr : 0.0;
+                a.r[j] = rr;
+                if (rec_better(rr, j, bv, bj)) {
+                  bv = rr;
+                  bj = j;
+                }
+              }
+            }
+    };
     long long next = 0;
     if (tid == 0) next = (long long)(atomicAdd(&ctl->tile_ctr, 1ull) - tile_base);
     while (true) {
@@ -402,70 +478,27 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
         mark(6);
         trace(k, 5);
       } else {
-        // X tile order: chunks 0..S-2 group-major (contiguous column runs),
-        // then the last chunk of every group (these finalise their group)
+        // X tiles group-major (contiguous column runs per group); the claimer of
+        // a group's last chunk finalises it after its NEXT tile (deferred), so
+        // the siblings are long done and finalisation never piles up at the
+        // end of the queue
         const long long tx = t - gy;
-        const long long head = ngx * (S - 1);
-        long long s, g;
-        if (tx < head) {
-          g = tx / (S - 1);
-          s = tx - g * (S - 1);
-        } else {
-          s = S - 1;
-          g = tx - head;
-        }
+        const long long g = tx / S, s = tx - g * S;
         sweep_tiles<VEC, MODE_DOT, LOAD_STREAM, true>(a.X, a.ldx, m, n, a.w, a.partial, n,
                                                        s * ngx + g, 1LL << 40, red, dummy_nf,
                                                        dummy_nz);
         mark(7);
-        if (s == S - 1) {
-          // ---- finalise columns 4g..4g+3 (warps 0..3, one column each) ----
-          if (tid == 0) wait_step(&ctl->p_step, k + 1);
-          __syncthreads();
-          const int re = __ldcg(&ctl->reorth);
-          const int bd = __ldcg(&ctl->breakdown);
-          const double nrm = __ldcg(&ctl->norm);
-          const long long j = g * kCols + warp;
-          if (warp < kCols && j < n) {
-            double sp = 0.0, corr = 0.0;
-            for (long long ss = lane; ss < S; ss += 32) {
-              sp += poll_f64(&a.partial[ss * n + j]);
-              st_relaxed_f64(&a.partial[ss * n + j], kNaN);
-            }
-            if (re && !bd) {
-              for (long long l0 = 0; l0 < k; l0 += 512) {
-                double tv[16], pv[16];
-#pragma unroll
-                for (int q = 0; q < 16; ++q) {
-                  const long long l = l0 + lane + 32 * q;
-                  tv[q] = (l < k) ? __ldcg(&a.T[l * n + j]) : 0.0;
-                  pv[q] = (l < k) ? __ldcg(&a.p[l]) : 0.0;
-                }
-#pragma unroll
-                for (int q = 0; q < 16; ++q) corr = fma(pv[q], tv[q], corr);
-              }
-            }
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) {
-              sp += __shfl_xor_sync(0xffffffffu, sp, off);
-              corr += __shfl_xor_sync(0xffffffffu, corr, off);
-            }
-            if (lane == 0 && !bd) {
-              const double tt = (sp - corr) / nrm;
-              a.T[k * n + j] = tt;                                   // decompose.cpp:93
-              const double sq = __dmul_rn(tt, tt);
-              double rr = __dsub_rn(__ldcg(&a.r[j]), sq);            // workspace.cpp:52-53
-              rr = rr > 0.0 ? rr : 0.0;
-              a.r[j] = rr;
-              if (rec_better(rr, j, bv, bj)) {
-                bv = rr;
-                bj = j;
-              }
-            }
-          }
+        if (pend_g >= 0) {
+          finalize_group(pend_g);
+          pend_g = -1;
         }
+        if (s == S - 1) pend_g = g;
         trace(k, 5);
       }
+    }
+    if (pend_g >= 0) {
+      finalize_group(pend_g);
+      pend_g = -1;
     }
     block_argmax<kThreads>(bv, bj, smr);
     if (tid == 0) a.rec[cta] = Rec{bv, bj};
