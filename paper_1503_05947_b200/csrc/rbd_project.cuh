@@ -119,7 +119,7 @@ inline int launch_project_f64(const double* Y, long long m, long long d, long lo
       attr = true;
     }
     double* xn = err ? xnorm_scratch : nullptr;
-    dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((d + BM - 1) / BM));
+    dim3 grid((unsigned)((d + BM - 1) / BM), (unsigned)((N + BN - 1) / BN));
     k_project_dmma<BM, BN, WM, WN><<<grid, WM * WN * 32, dm_smem_bytes<BM, BN>(), s>>>(
         Y, m, d, ldy, Xn, N, ldx, Tn, xn);
     *nlaunch += 1;

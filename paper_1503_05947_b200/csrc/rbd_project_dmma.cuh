@@ -80,9 +80,11 @@ __global__ void __launch_bounds__(WARPS_M * WARPS_N * 32, 4)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp / WARPS_N, wn = warp % WARPS_N;
   const int g = lane >> 2, t = lane & 3;
-  const long long l0 = (long long)blockIdx.y * BM;
-  const long long j0 = (long long)blockIdx.x * BN;
-  const bool do_norm = (xnorm2 != nullptr) && blockIdx.y == 0;
+  // blockIdx.x = l-tile (fastest): the d/BM CTAs sharing an X_new tile run
+  // together, so X_new streams from DRAM once and is re-read from L2
+  const long long l0 = (long long)blockIdx.x * BM;
+  const long long j0 = (long long)blockIdx.y * BN;
+  const bool do_norm = (xnorm2 != nullptr) && blockIdx.x == 0;
   const bool fullA = (l0 + BM <= d), fullB = (j0 + BN <= N);
   double acc[MT][NT][4];
 #pragma unroll
