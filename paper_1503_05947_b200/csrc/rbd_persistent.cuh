@@ -216,8 +216,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
   const double eps_R = st->eps_R, tol = st->breakdown_tol;
   const int cfg_reorth = st->cfg_reorth;
   const long long S = (m + kChunk - 1) / kChunk;
-  const long long nblk = (m + kPRows - 1) / kPRows;
-  const long long b0 = nblk * cta / G, b1 = nblk * (cta + 1) / G;
+  // P1 row range of this CTA: an even split of the rows (kept even so 16-byte
+  // row pairs never straddle two CTAs), processed in kPRows-row blocks
+  const long long r_lo = ((m * cta / G) + 1) & ~1LL;
+  const long long r_hi = (cta + 1 == G) ? m : (((m * (cta + 1) / G) + 1) & ~1LL);
   const long long ngx = (n + kCols - 1) / kCols;   // X column groups
   const long long nx = ngx * S;                    // X tiles
   unsigned dummy_nf = 0, dummy_nz = 0;
@@ -256,13 +258,14 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
     const double* x = SHARD ? pay + kPayHead : a.X + jstar * a.ldx;
     __syncthreads();
     double nacc = 0.0;
-    for (long long b = b0; b < b1; ++b) {
+    for (long long rb = r_lo; rb < r_hi; rb += kPRows) {
       // lane owns rows i0 .. i0+VEC-1 (a 16-byte pair when VEC == 2)
-      const long long i0 = b * kPRows + (long long)VEC * lane;
+      const long long i0 = rb + (long long)VEC * lane;
+      const long long iend = (rb + kPRows < r_hi) ? rb + kPRows : r_hi;   // rows of this block
       double acc_c[VEC], acc_p[VEC];
 #pragma unroll
       for (int v = 0; v < VEC; ++v) acc_c[v] = acc_p[v] = 0.0;
-      if (i0 + VEC <= m) {
+      if (i0 + VEC <= iend) {
         const double* yp = a.Y + i0 + (long long)warp * m;
         const long long stp = (long long)kWarps * m;
         long long l = warp;
@@ -297,7 +300,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
         }
       } else {
         for (int v = 0; v < VEC; ++v) {
-          if (i0 + v >= m) break;
+          if (i0 + v >= iend) break;
           const double* yp = a.Y + i0 + v + (long long)warp * m;
           for (long long l = warp; l < kb; l += kWarps) {
             acc_c[v] = fma(*yp, cs[l], acc_c[v]);
@@ -316,7 +319,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
 #pragma unroll
         for (int v = 0; v < VEC; ++v) {
           const long long i = i0 + v;
-          if (i >= m) break;
+          if (i >= iend) break;
           double sc = red_c[0][VEC * lane + v], sp = red_p[0][VEC * lane + v];
 #pragma unroll
           for (int w = 1; w < kWarps; ++w) {
