@@ -100,6 +100,42 @@ def test_c1_parity_first_steps_and_full_properties(cuda):
     assert len(set(g.selected)) == g.d
 
 
+@pytest.mark.slow
+def test_c1_full_parity_all_steps(cuda):
+    """C1 at full size, all 400 greedy steps against the threaded oracle."""
+    import os
+    w = configs.C1
+    Xd = configs.c1_matrix(n=w.n, seed=w.seed, device=cuda)
+    X = np.asfortranarray(Xd.cpu().numpy())
+    eps = configs.eps_for(w, float(np.sqrt((X * X).sum(0)).max()))
+    g = rbd.decompose(Xd, d_max=w.d_max, eps_r=eps)
+    r = oracle.decompose(X, w.d_max, eps, nthreads=os.cpu_count() or 1)
+    assert compare(g, r, X) == r.d == g.d == w.d_max
+
+
+@pytest.mark.slow
+def test_c2_prefix_parity(cuda):
+    """C2 (34 GB) at full size: the first 8 greedy steps against the oracle."""
+    import os
+    import torch
+    w = configs.C2
+    Xd = configs.low_rank_matrix_torch(w.m, w.n, 1024, configs.spectrum("C2", 1024), 1e-8,
+                                       w.seed, device=cuda)
+    g = rbd.decompose(Xd, d_max=8)
+    Xh = torch.empty((w.n, w.m), dtype=torch.float64, pin_memory=True)
+    Xh.copy_(Xd.t())
+    del Xd
+    X = Xh.numpy().T
+    r = oracle.decompose(X, 8, nthreads=os.cpu_count() or 1)
+
+    class P:
+        pass
+    gp = P()
+    gp.Y, gp.T, gp.d = g.Y.cpu().numpy(), g.T.cpu().numpy(), g.d
+    gp.selected, gp.residual_history = g.selected, g.residual_history
+    assert compare(gp, r, X) == 8
+
+
 def test_determinism_bitwise(cuda):
     X = configs.c0_matrix()
     a = basic(X, 64, 1e-6)
