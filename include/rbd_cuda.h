@@ -144,6 +144,13 @@ int rbd_ws_extend_host(rbd_ws_t ws, const double* hxi);
  * dTn d x N column-major (ld d), d_err length N (may be NULL). */
 int rbd_project_batch(rbd_ctx_t ctx, const double* dY, int64_t m, int64_t d, int64_t ldy,
                       const double* dXn, int64_t N, int64_t ldx, double* dTn, double* d_err);
+/* fp32 mode of the out-of-sample compression (BASELINE north_star, 1e-4
+ * parity): Y and X_new in fp32, T_new = Y'X_new on the tcgen05 tensor cores
+ * (kind::tf32, 3xTF32 split, TMEM accumulators, TMA operand staging); the
+ * error indicator is accumulated in fp64. dTn: d x N column-major fp32.
+ * ldy/ldx must be multiples of 4 and the bases 16-byte aligned (TMA). */
+int rbd_project_batch_f32(rbd_ctx_t ctx, const float* dY, int64_t m, int64_t d, int64_t ldy,
+                          const float* dXn, int64_t N, int64_t ldx, float* dTn, double* d_err);
 /* rbd::reconstruct (decompose.cpp:119-123): dv = Y c (dc length d). */
 int rbd_reconstruct(rbd_ctx_t ctx, const double* dY, int64_t m, int64_t d, int64_t ldy,
                     const double* dc, double* dv);

@@ -8,11 +8,11 @@ from ._lib import (CudaError, DegenerateInput, DimensionMismatch, IncompatibleWe
                    IndexOutOfRange, InvalidArgument, NoConvergence, NotPositive, RbdError,
                    Context, default_context, load_library)
 from .api import (Model, Workspace, decompose, make_config, mgs_project, project, project_batch,
-                  reconstruct)
+                  project_batch_f32, reconstruct)
 
 __all__ = [
     "RbdError", "InvalidArgument", "IncompatibleWeight", "DegenerateInput", "IndexOutOfRange",
     "DimensionMismatch", "NotPositive", "NoConvergence", "CudaError", "Context",
     "default_context", "load_library", "Model", "Workspace", "decompose", "make_config",
-    "mgs_project", "project", "project_batch", "reconstruct",
+    "mgs_project", "project", "project_batch", "project_batch_f32", "reconstruct",
 ]

@@ -131,6 +131,7 @@ _SIGS = {
     "rbd_ws_read": (C.c_int, [_P, _P, _P, _P]),
     "rbd_project_batch": (C.c_int, [_P, _P, _I64, _I64, _I64, _P, _I64, _I64, _P, _P]),
     "rbd_reconstruct": (C.c_int, [_P, _P, _I64, _I64, _I64, _P, _P]),
+    "rbd_project_batch_f32": (C.c_int, [_P, _P, _I64, _I64, _I64, _P, _I64, _I64, _P, _P]),
     "rbd_project_host": (C.c_int, [_P, _P, _I64, _I64, _P, _I64, _P, _P]),
     "rbd_reconstruct_host": (C.c_int, [_P, _P, _I64, _I64, _P, _P]),
     "rbd_time_sweep": (C.c_int, [_P, _P, _I64, _I64, _I64, _P, C.c_int, _DP]),

@@ -262,6 +262,40 @@ def project_batch(Y, Xn, with_error: bool = True, ctx: Optional[Context] = None)
     return Tn, (err if with_error else None)
 
 
+def project_batch_f32(Y, Xn, with_error: bool = True, ctx: Optional[Context] = None):
+    """fp32 mode of the out-of-sample compression: Y, X_new as float32 CUDA
+    tensors (column-major views, leading dimensions multiple of 4); T_new on the
+    tcgen05 tensor cores (3xTF32), error indicator accumulated in fp64."""
+    lib = load_library()
+    if not (_is_torch_cuda(Y) and _is_torch_cuda(Xn)):
+        raise InvalidArgument("project_batch_f32: pass torch CUDA tensors")
+    ctx = ctx or default_context(Y.device.index or 0)
+
+    def colmajor32(a):
+        a = a.to(torch.float32)
+        m_ = a.shape[0]
+        if a.stride(0) == 1 and a.stride(1) >= m_ and a.stride(1) % 4 == 0:
+            return a, a.stride(1)
+        ld = (m_ + 3) // 4 * 4
+        buf = torch.zeros((a.shape[1], ld), dtype=torch.float32, device=a.device)
+        buf[:, :m_] = a.t()
+        return buf.t()[:m_], ld
+    Yc, ldy = colmajor32(Y)
+    Xc, ldx = colmajor32(Xn)
+    m, d = Yc.shape
+    if Xc.shape[0] != m:
+        raise DimensionMismatch("project: vector length != m")
+    N = Xc.shape[1]
+    Tn = torch.empty((N, d), dtype=torch.float32, device=Y.device).t()
+    err = torch.empty(N, dtype=torch.float64, device=Y.device) if with_error else None
+    torch.cuda.current_stream(Y.device).synchronize()
+    check(lib.rbd_project_batch_f32(ctx.handle, C.c_void_p(Yc.data_ptr()), m, d, ldy,
+                                    C.c_void_p(Xc.data_ptr()), N, ldx, C.c_void_p(Tn.data_ptr()),
+                                    C.c_void_p(err.data_ptr()) if err is not None else None))
+    ctx.synchronize()
+    return Tn, err
+
+
 def mgs_project(v, basis, breakdown_tol: float, reorthogonalize: bool = False,
                 ctx: Optional[Context] = None):
     """rbd::mgs_project (decompose.cpp:12-33) on device tensors.

@@ -17,6 +17,9 @@
 #include "rbd_device.cuh"
 #include "rbd_project.cuh"
 #include "rbd_persistent.cuh"
+#include "rbd_project_tc.cuh"
+
+#include <cudaTypedefs.h>
 
 using namespace rbdk;
 
@@ -1689,6 +1692,80 @@ int rbd_compress_host(rbd_ctx_t ctx, const double* hY, int64_t m, int64_t d, con
       cudaStreamSynchronize(ctx->stream))
     return fin(set_err(RBD_ERR_CUDA, "compress_host: D2H failed"));
   return fin(RBD_OK);
+}
+
+}  // extern "C"
+
+// ===========================================================================
+// fp32 out-of-sample compression on tcgen05 (K6)
+// ===========================================================================
+namespace {
+
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return (PFN_cuTensorMapEncodeTiled_v12000) nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }();
+  return fn;
+}
+
+// 2-D fp32 column-major operand (rows = contiguous dim of length `inner`,
+// `outer` columns, leading dimension ld), box 32 x 128, 128-byte swizzle.
+int make_map_f32(CUtensorMap* map, const float* base, long long inner, long long outer, long long ld) {
+  auto enc = tensor_map_encoder();
+  if (!enc) return set_err(RBD_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * sizeof(float)};
+  cuuint32_t box[2] = {(cuuint32_t)kTcBK, (cuuint32_t)kTcBM};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_err(RBD_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  return RBD_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int rbd_project_batch_f32(rbd_ctx_t ctx, const float* dY, int64_t m, int64_t d, int64_t ldy,
+                          const float* dXn, int64_t N, int64_t ldx, float* dTn, double* d_err) {
+  if (!ctx) return set_err(RBD_ERR_INVALID_ARGUMENT, "null context");
+  if (m < 1 || d < 1 || N < 0) return set_err(RBD_ERR_DIMENSION_MISMATCH, "project: bad sizes");
+  if (ldy < m || ldx < m) return set_err(RBD_ERR_DIMENSION_MISMATCH, "project: vector length != m");
+  if (N == 0) return RBD_OK;
+  if ((ldy % 4) || (ldx % 4) || !aligned16(dY) || !aligned16(dXn))
+    return set_err(RBD_ERR_INVALID_ARGUMENT,
+                   "project f32: leading dimensions must be multiples of 4 floats and bases 16-byte aligned (TMA)");
+  CU(cudaSetDevice(ctx->device));
+  CUtensorMap mY, mX;
+  TRY(make_map_f32(&mY, dY, m, d, ldy));
+  TRY(make_map_f32(&mX, dXn, m, N, ldx));
+  static bool attr = false;
+  if (!attr) {
+    CU(cudaFuncSetAttribute(k_project_tf32x3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTcSmem));
+    attr = true;
+  }
+  double* xn = nullptr;
+  if (d_err) {
+    TRY(ensure(ctx->scratch1, sizeof(double) * (size_t)std::max<int64_t>(N, 32)));
+    xn = ptr<double>(ctx->scratch1);
+  }
+  dim3 grid((unsigned)cdiv(d, kTcBM), (unsigned)cdiv(N, kTcBN));
+  k_project_tf32x3<<<grid, kTcThreads, kTcSmem, ctx->stream>>>(mY, mX, m, d, N, dTn, xn);
+  ctx->launches++;
+  CU(cudaGetLastError());
+  if (d_err) {
+    k_project_err_f32<<<(unsigned)cdiv(N, 8), 256, 0, ctx->stream>>>(xn, dTn, d, N, d_err);
+    ctx->launches++;
+    CU(cudaGetLastError());
+  }
+  return RBD_OK;
 }
 
 }  // extern "C"

@@ -57,6 +57,31 @@ def main():
     torch.cuda.synchronize()
     ms2 = e0.elapsed_time(e1) / nb
     print(f"[ours, T only] {ms2:.2f} ms/batch -> {flops / ms2 / 1e9:.2f} TFLOP/s")
+    # fp32 mode: tcgen05 kind::tf32 with the 3xTF32 split
+    Y32 = Y.to(torch.float32).t().contiguous().t()
+    b32 = [Xn.to(torch.float32).t().contiguous().t() for Xn in batches]
+    rbd.project_batch_f32(Y32, b32[0], ctx=ctx)
+    torch.cuda.synchronize()
+    e0.record(st)
+    for Xn in b32:
+        T32, err32 = rbd.project_batch_f32(Y32, Xn, ctx=ctx)
+    e1.record(st)
+    torch.cuda.synchronize()
+    ms3 = e0.elapsed_time(e1) / nb
+    print(f"[ours fp32 tcgen05 3xTF32] {ms3:.2f} ms/batch -> {flops / ms3 / 1e9:.2f} TFLOP/s "
+          f"(fp32-equivalent; 3 tf32 MMAs per product)")
+    Yt32 = Y32.t().contiguous()
+    torch.backends.cuda.matmul.allow_tf32 = False
+    e0.record()
+    for Xn in b32:
+        Tc32 = torch.matmul(Yt32, Xn)
+    e1.record()
+    torch.cuda.synchronize()
+    ms4 = e0.elapsed_time(e1) / nb
+    print(f"[cuBLAS SGEMM fp32] {ms4:.2f} ms/batch -> {flops / ms4 / 1e9:.2f} TFLOP/s")
+    ref32 = Y32.double().t() @ b32[-1].double()
+    sc32 = (b32[-1].double() ** 2).sum(0).sqrt()
+    print(f"[check fp32] max|dT|/||x|| = {float(((T32.double() - ref32).abs() / sc32).max()):.2e}")
     # cuBLAS DGEMM (context / ceiling)
     Yt = Y.t().contiguous()
     torch.matmul(Yt, batches[0])
