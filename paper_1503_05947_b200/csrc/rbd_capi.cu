@@ -341,7 +341,10 @@ int fused_grid(rbd_ctx_t ctx, long long m) {
 }
 
 size_t fused_smem(long long dcap) { return sizeof(double) * 3 * (size_t)std::max<long long>(dcap, 1); }
-size_t persist_smem(long long dcap) { return sizeof(double) * 2 * (size_t)std::max<long long>(dcap, 1); }
+// c and p vectors, each zero-padded by one P1 batch (16 loads x kWarps columns)
+size_t persist_smem(long long dcap) {
+  return sizeof(double) * 2 * ((size_t)std::max<long long>(dcap, 1) + 16 * kWarps);
+}
 
 // Materialise a pending column / clear the pending flag (used after the loop).
 int enqueue_fused_ext(rbd_ctx_t ctx, const LoopBufs& L) {

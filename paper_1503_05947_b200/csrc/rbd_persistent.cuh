@@ -177,8 +177,9 @@ constexpr int kPayHead = 4;
 template <int VEC, bool SHARD>
 __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
   extern __shared__ double dsm[];
-  double* cs = dsm;                // c = T[0:k, j*]
-  double* ps = dsm + a.d_max;      // p_{k-1} (pending column)
+  constexpr int kPBatch = 16 * kWarps;   // columns per P1 batch (16 loads in flight per lane)
+  double* cs = dsm;                        // c = T[0:k, j*], zero-padded to a batch multiple
+  double* ps = dsm + a.d_max + kPBatch;    // p_{k-1} (pending column), zero-padded
   __shared__ double red[kWarps][kCols];
   constexpr int kPRows = 32 * VEC;  // rows per P1 block
   __shared__ double red_c[kWarps][kPRows];
@@ -186,6 +187,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
   __shared__ double smn[kWarps];
   __shared__ Rec smr[kWarps];
   __shared__ long long sh_tile;
+  __shared__ int sh_ok;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const long long m = a.m, n = a.n;
@@ -251,10 +253,13 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
     // =================== P1: w1 = x - Y c (and column k-1's second pass) ===========
     const long long kb = pending ? k - 1 : k;
     trace(k, 1);
-    for (long long l = tid; l < k; l += kThreads)
-      cs[l] = !live ? 0.0 : SHARD ? __ldcg(&pay[kPayHead + m + l]) : __ldcg(&a.T[l * n + jstar]);
-    for (long long l = tid; l < kb; l += kThreads)
-      ps[l] = (pending && reorth_prev) ? __ldcg(&a.p[l]) : 0.0;
+    const long long kpad = (k + kPBatch - 1) / kPBatch * kPBatch;
+    for (long long l = tid; l < kpad; l += kThreads) {
+      cs[l] = (!live || l >= k) ? 0.0
+              : SHARD           ? __ldcg(&pay[kPayHead + m + l])
+                                : __ldcg(&a.T[l * n + jstar]);
+      ps[l] = (pending && reorth_prev && l < kb) ? __ldcg(&a.p[l]) : 0.0;
+    }
     const double* x = SHARD ? pay + kPayHead : a.X + jstar * a.ldx;
     __syncthreads();
     double nacc = 0.0;
@@ -265,48 +270,40 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
       double acc_c[VEC], acc_p[VEC];
 #pragma unroll
       for (int v = 0; v < VEC; ++v) acc_c[v] = acc_p[v] = 0.0;
-      if (i0 + VEC <= iend) {
+      // rows this lane owns in the block (VEC, fewer at an odd tail, or none);
+      // every lane keeps 16 predicated loads in flight per batch, including the
+      // last partial batch (a serial remainder costs one L2 round trip per column)
+      const long long nv_ = iend - i0;
+      const int nv = nv_ >= VEC ? VEC : (nv_ > 0 ? (int)nv_ : 0);
+      if (nv > 0) {
         const double* yp = a.Y + i0 + (long long)warp * m;
         const long long stp = (long long)kWarps * m;
-        long long l = warp;
-        for (; l + 15 * kWarps < kb; l += 16 * kWarps) {   // 16 loads in flight per lane
+        for (long long l = warp; l < kb; l += 16 * kWarps) {
           double yv[16][VEC];
 #pragma unroll
           for (int q = 0; q < 16; ++q) {
+            const bool ok = l + q * kWarps < kb;
             if constexpr (VEC == 2) {
-              const double2 t2 = *reinterpret_cast<const double2*>(yp + q * stp);
-              yv[q][0] = t2.x;
-              yv[q][VEC - 1] = t2.y;
+              if (ok && nv == 2) {
+                const double2 t2 = __ldcg(reinterpret_cast<const double2*>(yp + q * stp));
+                yv[q][0] = t2.x;
+                yv[q][VEC - 1] = t2.y;
+              } else {
+                yv[q][0] = ok ? __ldcg(yp + q * stp) : 0.0;
+                yv[q][VEC - 1] = 0.0;
+              }
             } else {
-              yv[q][0] = yp[q * stp];
+              yv[q][0] = ok ? __ldcg(yp + q * stp) : 0.0;
             }
           }
 #pragma unroll
           for (int q = 0; q < 16; ++q)
 #pragma unroll
             for (int v = 0; v < VEC; ++v) {
-              acc_c[v] = fma(yv[q][v], cs[l + q * kWarps], acc_c[v]);
+              acc_c[v] = fma(yv[q][v], cs[l + q * kWarps], acc_c[v]);   // zero past kb
               acc_p[v] = fma(yv[q][v], ps[l + q * kWarps], acc_p[v]);
             }
           yp += 16 * stp;
-        }
-        for (; l < kb; l += kWarps) {
-#pragma unroll
-          for (int v = 0; v < VEC; ++v) {
-            acc_c[v] = fma(yp[v], cs[l], acc_c[v]);
-            acc_p[v] = fma(yp[v], ps[l], acc_p[v]);
-          }
-          yp += stp;
-        }
-      } else {
-        for (int v = 0; v < VEC; ++v) {
-          if (i0 + v >= iend) break;
-          const double* yp = a.Y + i0 + v + (long long)warp * m;
-          for (long long l = warp; l < kb; l += kWarps) {
-            acc_c[v] = fma(*yp, cs[l], acc_c[v]);
-            acc_p[v] = fma(*yp, ps[l], acc_p[v]);
-            yp += (long long)kWarps * m;
-          }
         }
       }
 #pragma unroll
@@ -378,52 +375,99 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
       ctl->breakdown = (norm0 < tol || norm0 == 0.0) ? 1 : 0;
       st_release_s64(&ctl->p_step, k + 1);
     }
-    long long pend_g = -1;
-    auto finalize_group = [&](const long long g) {
-          // ---- finalise columns 4g..4g+3 (warps 0..3, one column each) ----
-            if (tid == 0) wait_step(&ctl->p_step, k + 1);
-            __syncthreads();
-            const int re = __ldcg(&ctl->reorth);
-            const int bd = __ldcg(&ctl->breakdown);
-            const double nrm = __ldcg(&ctl->norm);
-            const long long j = g * kCols + warp;
-            if (warp < kCols && j < n) {
-              double sp = 0.0, corr = 0.0;
-              for (long long ss = lane; ss < S; ss += 32) {
-                sp += poll_f64(&a.partial[ss * n + j]);
-                st_relaxed_f64(&a.partial[ss * n + j], kNaN);
-              }
-              if (re && !bd) {
-                for (long long l0 = 0; l0 < k; l0 += 512) {
-                  double tv[16], pv[16];
-  #pragma unroll
-                  for (int q = 0; q < 16; ++q) {
-                    const long long l = l0 + lane + 32 * q;
-                    tv[q] = (l < k) ? __ldcg(&a.T[l * n + j]) : 0.0;
-                    pv[q] = (l < k) ? __ldcg(&a.p[l]) : 0.0;
-                  }
-  #pragma unroll
-                  for (int q = 0; q < 16; ++q) corr = fma(pv[q], tv[q], corr);
-                }
-              }
-  #pragma unroll
-              for (int off = 16; off > 0; off >>= 1) {
-                sp += __shfl_xor_sync(0xffffffffu, sp, off);
-                corr += __shfl_xor_sync(0xffffffffu, corr, off);
-              }
-              if (lane == 0 && !bd) {
-                const double tt = (sp - corr) / nrm;
-                a.T[k * n + j] = tt;                                   // decompose.cpp:93
-                const double sq = __dmul_rn(tt, tt);
-                double rr = __dsub_rn(__ldcg(&a.r[j]), sq);            // workspace.cpp:52-53
-                rr = rr > 0.0 ? rr : 0.0;
-                a.r[j] = rr;
-                if (rec_better(rr, j, bv, bj)) {
-                  bv = rr;
-                  bj = j;
-                }
-              }
+    // Groups whose last chunk this CTA swept and that are not finalised yet
+    // (FIFO, uniform across the CTA). Finalisation is attempted after the next
+    // tile without waiting; it blocks only when the FIFO is full or the queue
+    // is exhausted. Every wait targets an earlier-claimed tile (a sibling
+    // chunk, or the Y'w1 groups that precede all X tiles): no cycles.
+    constexpr int kPend = 4;
+    long long pend[kPend] = {-1, -1, -1, -1};
+    int npend = 0;
+    // the step's published decision, read once per CTA
+    bool p_ready = false;
+    int re_s = 0, bd_s = 0;
+    double nrm_s = 1.0;
+    auto ensure_p = [&](const bool block) -> bool {
+      if (p_ready) return true;
+      if (tid == 0) {
+        int ok = ld_acquire_s64(&ctl->p_step) == k + 1;
+        if (!ok && block) {
+          wait_step(&ctl->p_step, k + 1);
+          ok = 1;
+        }
+        sh_ok = ok;
+      }
+      __syncthreads();
+      if (!sh_ok) return false;
+      re_s = __ldcg(&ctl->reorth);
+      bd_s = __ldcg(&ctl->breakdown);
+      nrm_s = __ldcg(&ctl->norm);
+      p_ready = true;
+      return true;
+    };
+    // Finalise up to two groups at once (warps 0-3: pend[0], warps 4-7:
+    // pend[1]; one column per warp): all loads of the pass are issued together.
+    // Groups whose chunk partials are not all written yet (a NaN sum) are kept
+    // unless block. Returns the number of groups retired from the FIFO front.
+    auto finalize_pass = [&](const bool block) {
+      if (!ensure_p(block)) return;
+      const int q = warp >> 2;
+      const long long g = q < npend ? pend[q] : -1;
+      const long long j = g * kCols + (warp & 3);
+      const bool mine = g >= 0 && j < n;
+      double sp = 0.0, corr = 0.0, rj = 0.0;
+      if (mine) {   // a chunk partial not written yet is NaN, and so is the sum
+        for (long long ss = lane; ss < S; ss += 32) sp += ld_relaxed_f64(&a.partial[ss * n + j]);
+        if (lane == 0) rj = __ldcg(&a.r[j]);
+        if (re_s && !bd_s) {
+          for (long long l0 = 0; l0 < k; l0 += 512) {
+            double tv[16], pv[16];
+#pragma unroll
+            for (int u = 0; u < 16; ++u) {
+              const long long l = l0 + lane + 32 * u;
+              tv[u] = (l < k) ? __ldcg(&a.T[l * n + j]) : 0.0;
+              pv[u] = (l < k) ? __ldcg(&a.p[l]) : 0.0;
             }
+#pragma unroll
+            for (int u = 0; u < 16; ++u) corr = fma(pv[u], tv[u], corr);
+          }
+        }
+      }
+      const bool nr0 = __syncthreads_or(mine && q == 0 && sp != sp);
+      const bool nr1 = __syncthreads_or(mine && q == 1 && sp != sp);
+      bool commit = mine && !(q == 0 ? nr0 : nr1);
+      if (block && mine && !commit) {
+        sp = 0.0;
+        for (long long ss = lane; ss < S; ss += 32) sp += poll_f64(&a.partial[ss * n + j]);
+        commit = true;
+      }
+      if (commit) {
+        for (long long ss = lane; ss < S; ss += 32) st_relaxed_f64(&a.partial[ss * n + j], kNaN);
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+          sp += __shfl_xor_sync(0xffffffffu, sp, off);
+          corr += __shfl_xor_sync(0xffffffffu, corr, off);
+        }
+        if (lane == 0 && !bd_s) {
+          const double tt = (sp - corr) / nrm_s;
+          a.T[k * n + j] = tt;                                   // decompose.cpp:93
+          const double sq = __dmul_rn(tt, tt);
+          double rr = __dsub_rn(rj, sq);                         // workspace.cpp:52-53
+          rr = rr > 0.0 ? rr : 0.0;
+          a.r[j] = rr;
+          if (rec_better(rr, j, bv, bj)) {
+            bv = rr;
+            bj = j;
+          }
+        }
+      }
+      // retire committed groups (uniform: nr0/nr1 are CTA-wide)
+      const bool ok0 = npend > 0 && (block || !nr0);
+      const bool ok1 = npend > 1 && (block || !nr1);
+      int w = 0;
+      for (int i = 0; i < npend; ++i)
+        if (!((i == 0 && ok0) || (i == 1 && ok1))) pend[w++] = pend[i];
+      npend = w;
     };
     long long next = 0;
     if (tid == 0) next = (long long)(atomicAdd(&ctl->tile_ctr, 1ull) - tile_base);
@@ -491,18 +535,15 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
                                                        s * ngx + g, 1LL << 40, red, dummy_nf,
                                                        dummy_nz);
         mark(7);
-        if (pend_g >= 0) {
-          finalize_group(pend_g);
-          pend_g = -1;
+        if (npend > 0) finalize_pass(false);
+        if (s == S - 1) {
+          if (npend == kPend) finalize_pass(true);   // full: retire the two oldest
+          pend[npend++] = g;
         }
-        if (s == S - 1) pend_g = g;
         trace(k, 5);
       }
     }
-    if (pend_g >= 0) {
-      finalize_group(pend_g);
-      pend_g = -1;
-    }
+    while (npend > 0) finalize_pass(true);
     block_argmax<kThreads>(bv, bj, smr);
     if (tid == 0) a.rec[cta] = Rec{bv, bj};
     tile_base += (unsigned long long)(total + G);
