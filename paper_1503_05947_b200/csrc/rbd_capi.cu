@@ -121,7 +121,8 @@ struct rbd_ctx_s {
   int persist_occ2 = 0, persist_occ1 = 0;  // co-resident CTAs/SM of the persistent kernel
   int path = 0;                            // 0 persistent, 1 graph of per-phase kernels
   DevBuf bar;                              // grid-barrier words
-  DevBuf ctl, gcnt, ygcnt;                 // persistent loop: ctl words, p, CTA records
+  DevBuf ctl, gcnt, ygcnt;                 // persistent loop: ctl words, p (x2), CTA records
+  DevBuf rdy;                              // persistent loop: P1 readiness counters
   DevBuf send, recv;                       // sharded mode: payload exchange buffers
   // multi-GPU
   void* comm = nullptr;                    // ncclComm_t (dlopen'ed NCCL)
@@ -439,9 +440,11 @@ int launch_persistent(rbd_ctx_t ctx, const LoopBufs& L) {
   const long long ngx = cdiv(L.n, kCols);
   TRY(ensure(ctx->ppart, sizeof(double) * (size_t)std::max<long long>(grid, S) * L.d_max));
   TRY(ensure(ctx->ctl, sizeof(StepCtl)));
-  TRY(ensure(ctx->gcnt, sizeof(double) * (size_t)(L.d_max + 1)));   // p_k
-  TRY(ensure(ctx->ygcnt, sizeof(Rec) * (size_t)grid));              // CTA records
+  TRY(ensure(ctx->gcnt, sizeof(double) * 2 * (size_t)(L.d_max + 1)));   // p_k, by step parity
+  TRY(ensure(ctx->ygcnt, sizeof(Rec) * (size_t)grid));                  // CTA records
+  TRY(ensure(ctx->rdy, sizeof(unsigned long long) * (size_t)(S + 1)));
   CU(cudaMemsetAsync(ctx->ctl.p, 0, sizeof(StepCtl), ctx->stream));
+  CU(cudaMemsetAsync(ctx->rdy.p, 0, sizeof(unsigned long long) * (size_t)(S + 1), ctx->stream));
   CU(cudaMemsetAsync(ctx->bar.p, 0, 64, ctx->stream));
   // chunk partials double as ready flags: NaN (all bytes 0xFF) = not written
   CU(cudaMemsetAsync(ctx->partial.p, 0xFF, sizeof(double) * (size_t)S * L.n, ctx->stream));
@@ -469,6 +472,7 @@ int launch_persistent(rbd_ctx_t ctx, const LoopBufs& L) {
   a.bar = ptr<unsigned>(ctx->bar);
   a.d_max = L.d_max;
   a.ctl = ptr<StepCtl>(ctx->ctl);
+  a.rdy = ptr<unsigned long long>(ctx->rdy);
   a.phase_ns = nullptr;
   if (getenv("RBD_PHASE_TIMING")) {
     TRY(ensure(ctx->scratch1, 256));
@@ -697,7 +701,7 @@ int rbd_ctx_destroy(rbd_ctx_t ctx) {
                   &ctx->resid,   &ctx->w,    &ctx->c,       &ctx->p,     &ctx->nrm,
                   &ctx->hist,    &ctx->sel,  &ctx->out_rec, &ctx->scratch1,
                   &ctx->hX,      &ctx->hY,   &ctx->hT,      &ctx->ppart, &ctx->bar,
-                  &ctx->ctl,     &ctx->gcnt, &ctx->ygcnt,   &ctx->send,  &ctx->recv};
+                  &ctx->ctl,     &ctx->gcnt, &ctx->ygcnt,   &ctx->rdy,   &ctx->send,  &ctx->recv};
   for (DevBuf* b : bl) release(*b);
   if (ctx->h_state) cudaFreeHost(ctx->h_state);
   if (ctx->h_rec) cudaFreeHost(ctx->h_rec);
@@ -1346,6 +1350,7 @@ int shard_step_launch(rbd_ctx_t c, const Shard& sh, long long m, long long ldx, 
   a.bar = ptr<unsigned>(c->bar);
   a.d_max = d_max;
   a.ctl = ptr<StepCtl>(c->ctl);
+  a.rdy = ptr<unsigned long long>(c->rdy);
   a.recv = ptr<double>(c->recv);
   a.send = ptr<double>(c->send);
   a.pay_stride = pay_stride;
@@ -1383,7 +1388,8 @@ int sharded_decompose(std::vector<rbd_ctx_t>& R, Exchange& ex, std::vector<Shard
     TRY(ensure(c->send, sizeof(double) * pay_stride));
     TRY(ensure(c->recv, sizeof(double) * pay_stride * ex.world()));
     TRY(ensure(c->ctl, sizeof(StepCtl)));
-    TRY(ensure(c->gcnt, sizeof(double) * (size_t)(d_cap + 1)));
+    TRY(ensure(c->gcnt, sizeof(double) * 2 * (size_t)(d_cap + 1)));
+    TRY(ensure(c->rdy, sizeof(unsigned long long) * (size_t)(cdiv(m, kChunk) + 1)));
     const int grid = persistent_grid(c, vec, d_cap);
     TRY(ensure(c->ppart, sizeof(double) * (size_t)std::max<long long>(grid, cdiv(m, kChunk)) * d_cap));
     TRY(ensure(c->nrm, sizeof(double) * std::max<long long>(gemv_grid(m), grid)));
@@ -1391,6 +1397,8 @@ int sharded_decompose(std::vector<rbd_ctx_t>& R, Exchange& ex, std::vector<Shard
     DevState* st = ptr<DevState>(c->state);
     CU(cudaMemsetAsync(st, 0, sizeof(DevState), c->stream));
     CU(cudaMemsetAsync(c->ctl.p, 0, sizeof(StepCtl), c->stream));
+    CU(cudaMemsetAsync(c->rdy.p, 0, sizeof(unsigned long long) * (size_t)(cdiv(m, kChunk) + 1),
+                       c->stream));
     CU(cudaMemsetAsync(c->bar.p, 0, 64, c->stream));
     CU(cudaMemsetAsync(c->partial.p, 0xFF, sizeof(double) * (size_t)cdiv(m, kChunk) * nloc, c->stream));
     if (sh[r].n_local > 0)

@@ -116,7 +116,10 @@ struct SweepArgs {
 };
 
 // Tile loop shared by the standalone sweep kernel and the persistent loop.
-template <int VEC, int MODE, int ALOAD, bool VCOH = false>
+// KC = columns per tile. A column's chunk sum depends only on the row layout
+// (thread -> rows, fma order, reduction tree), never on KC or on how loads are
+// batched, so tiles of different widths give bit-identical partials.
+template <int VEC, int MODE, int ALOAD, bool VCOH = false, int KC = kCols>
 __device__ __forceinline__ void sweep_tiles(const double* __restrict__ A, long long lda,
                                             long long m, long long ncols,
                                             const double* __restrict__ v,
@@ -125,25 +128,28 @@ __device__ __forceinline__ void sweep_tiles(const double* __restrict__ A, long l
                                             double (*red)[kCols], unsigned& nonfinite,
                                             unsigned& nonzero) {
   const long long S = (m + kChunk - 1) / kChunk;
-  const long long G = (ncols + kCols - 1) / kCols;
+  const long long G = (ncols + KC - 1) / KC;
   const long long ntiles = S * G;
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   constexpr int U = kChunk / (VEC * kThreads);  // element groups per thread per column
-  constexpr int UB = (VEC == 2) ? 4 : 8;         // batch of groups loaded together
+  // batch of element groups loaded together: 16 (VEC 2) / 32 (VEC 1) column
+  // loads in flight per thread, capped at the whole chunk
+  constexpr int UB0 = ((VEC == 2) ? 4 : 8) * (kCols / KC);
+  constexpr int UB = UB0 < U ? UB0 : U;
 
   for (long long tile = tile_begin; tile < ntiles; tile += tile_stride) {
     const long long s = tile / G;
     const long long g = tile - s * G;
     const long long row0 = s * kChunk;
-    const long long col0 = g * kCols;
+    const long long col0 = g * KC;
     const long long rows = (m - row0 < kChunk) ? m - row0 : kChunk;
-    double acc[kCols];
+    double acc[KC];
 #pragma unroll
-    for (int c = 0; c < kCols; ++c) acc[c] = 0.0;
-    const double* Ac[kCols];
+    for (int c = 0; c < KC; ++c) acc[c] = 0.0;
+    const double* Ac[KC];
 #pragma unroll
-    for (int c = 0; c < kCols; ++c) {
+    for (int c = 0; c < KC; ++c) {
       const long long cc = (col0 + c < ncols) ? col0 + c : col0;  // clamp (result unused)
       Ac[c] = A + cc * lda + row0;
     }
@@ -158,14 +164,14 @@ __device__ __forceinline__ void sweep_tiles(const double* __restrict__ A, long l
       if ((long long)(ub / UB + 1) * kBatchRows <= rows) {
         if constexpr (VEC == 2) {
           double2 yv[UB];
-          double2 xv[UB][kCols];
+          double2 xv[UB][KC];
 #pragma unroll
           for (int u = 0; u < UB; ++u) {
             const int e = (tid + (ub + u) * kThreads) * 2;
             if constexpr (MODE == MODE_DOT)
               yv[u] = VCOH ? __ldcg(reinterpret_cast<const double2*>(vr + e)) : ld_keep2(vr + e);
 #pragma unroll
-            for (int c = 0; c < kCols; ++c)
+            for (int c = 0; c < KC; ++c)
               xv[u][c] = ALOAD == LOAD_STREAM ? ld_stream2(Ac[c] + e)
                          : ALOAD == LOAD_CG   ? __ldcg(reinterpret_cast<const double2*>(Ac[c] + e))
                                               : ld_keep2(Ac[c] + e);
@@ -173,7 +179,7 @@ __device__ __forceinline__ void sweep_tiles(const double* __restrict__ A, long l
 #pragma unroll
           for (int u = 0; u < UB; ++u)
 #pragma unroll
-            for (int c = 0; c < kCols; ++c) {
+            for (int c = 0; c < KC; ++c) {
               if constexpr (MODE == MODE_DOT) {
                 acc[c] = fma(xv[u][c].x, yv[u].x, acc[c]);
                 acc[c] = fma(xv[u][c].y, yv[u].y, acc[c]);
@@ -186,13 +192,13 @@ __device__ __forceinline__ void sweep_tiles(const double* __restrict__ A, long l
             }
         } else {
           double yv[UB];
-          double xv[UB][kCols];
+          double xv[UB][KC];
 #pragma unroll
           for (int u = 0; u < UB; ++u) {
             const int e = tid + (ub + u) * kThreads;
             if constexpr (MODE == MODE_DOT) yv[u] = VCOH ? __ldcg(vr + e) : ld_keep1(vr + e);
 #pragma unroll
-            for (int c = 0; c < kCols; ++c)
+            for (int c = 0; c < KC; ++c)
               xv[u][c] = ALOAD == LOAD_STREAM ? ld_stream1(Ac[c] + e)
                          : ALOAD == LOAD_CG   ? __ldcg(Ac[c] + e)
                                               : ld_keep1(Ac[c] + e);
@@ -200,7 +206,7 @@ __device__ __forceinline__ void sweep_tiles(const double* __restrict__ A, long l
 #pragma unroll
           for (int u = 0; u < UB; ++u)
 #pragma unroll
-            for (int c = 0; c < kCols; ++c) {
+            for (int c = 0; c < KC; ++c) {
               if constexpr (MODE == MODE_DOT) {
                 acc[c] = fma(xv[u][c], yv[u], acc[c]);
               } else {
@@ -221,14 +227,14 @@ __device__ __forceinline__ void sweep_tiles(const double* __restrict__ A, long l
               double2 y2 = make_double2(0.0, 0.0);
               if constexpr (MODE == MODE_DOT)
                 y2 = VCOH ? __ldcg(reinterpret_cast<const double2*>(vr + e)) : ld_keep2(vr + e);
-              double2 x2[kCols];
+              double2 x2[KC];
 #pragma unroll
-              for (int c = 0; c < kCols; ++c)
+              for (int c = 0; c < KC; ++c)
                 x2[c] = ALOAD == LOAD_STREAM ? ld_stream2(Ac[c] + e)
                         : ALOAD == LOAD_CG   ? __ldcg(reinterpret_cast<const double2*>(Ac[c] + e))
                                              : ld_keep2(Ac[c] + e);
 #pragma unroll
-              for (int c = 0; c < kCols; ++c) {
+              for (int c = 0; c < KC; ++c) {
                 if constexpr (MODE == MODE_DOT) {
                   acc[c] = fma(x2[c].x, y2.x, acc[c]);
                   acc[c] = fma(x2[c].y, y2.y, acc[c]);
@@ -242,14 +248,14 @@ __device__ __forceinline__ void sweep_tiles(const double* __restrict__ A, long l
             } else {
               double y1 = 0.0;
               if constexpr (MODE == MODE_DOT) y1 = VCOH ? __ldcg(vr + e) : ld_keep1(vr + e);
-              double x1[kCols];
+              double x1[KC];
 #pragma unroll
-              for (int c = 0; c < kCols; ++c)
+              for (int c = 0; c < KC; ++c)
                 x1[c] = ALOAD == LOAD_STREAM ? ld_stream1(Ac[c] + e)
                         : ALOAD == LOAD_CG   ? __ldcg(Ac[c] + e)
                                              : ld_keep1(Ac[c] + e);
 #pragma unroll
-              for (int c = 0; c < kCols; ++c) {
+              for (int c = 0; c < KC; ++c) {
                 if constexpr (MODE == MODE_DOT) {
                   acc[c] = fma(x1[c], y1, acc[c]);
                 } else {
@@ -269,7 +275,7 @@ __device__ __forceinline__ void sweep_tiles(const double* __restrict__ A, long l
               if (e + 1 < rows) y1 = __ldcg(vr + e + 1);
             }
 #pragma unroll
-            for (int c = 0; c < kCols; ++c) {
+            for (int c = 0; c < KC; ++c) {
               const double x0 = (e < rows) ? __ldcg(Ac[c] + e) : 0.0;
               const double x1 = (e + 1 < rows) ? __ldcg(Ac[c] + e + 1) : 0.0;
               if constexpr (MODE == MODE_DOT) {
@@ -289,7 +295,7 @@ __device__ __forceinline__ void sweep_tiles(const double* __restrict__ A, long l
               if (e < rows) y0 = __ldcg(vr + e);
             }
 #pragma unroll
-            for (int c = 0; c < kCols; ++c) {
+            for (int c = 0; c < KC; ++c) {
               const double x0 = (e < rows) ? __ldcg(Ac[c] + e) : 0.0;
               if constexpr (MODE == MODE_DOT) {
                 acc[c] = fma(x0, y0, acc[c]);
@@ -305,16 +311,16 @@ __device__ __forceinline__ void sweep_tiles(const double* __restrict__ A, long l
     }
     // CTA reduction in a fixed order: xor-butterfly in the warp, then warps 0..7.
 #pragma unroll
-    for (int c = 0; c < kCols; ++c) {
+    for (int c = 0; c < KC; ++c) {
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], off);
     }
     if (lane == 0) {
 #pragma unroll
-      for (int c = 0; c < kCols; ++c) red[warp][c] = acc[c];
+      for (int c = 0; c < KC; ++c) red[warp][c] = acc[c];
     }
     __syncthreads();
-    if (tid < kCols && col0 + tid < ncols) {
+    if (tid < KC && col0 + tid < ncols) {
       double sum = red[0][tid];
 #pragma unroll
       for (int w = 1; w < kWarps; ++w) sum += red[w][tid];

@@ -8,7 +8,9 @@
 //   P1  extension pass over this CTA's rows (one HBM read of Y):
 //         y_{k-1} = (w1_{k-1} - Y p_{k-1}) / ||w_{k-1}||   -> Y[:, k-1]
 //         w1_k    = x_{j*} - Y c,   c = T[0:k, j*]           (+ ||w1_k||^2)
-//   --- barrier ---
+//   --- no barrier: each CTA publishes the rows it finished (per 4096-row
+//       chunk, release-add); an X tile of chunk s starts once chunk s is
+//       complete, the Y'w1 tiles once every CTA is through P1 ---
 //   P2  one dynamically scheduled tile queue:
 //         Y'w1 tiles (reorth coefficients p_k; Y is still L2-hot) — the last
 //           one decides the second pass (decompose.cpp:28), ||w_k|| and the
@@ -54,7 +56,18 @@ struct PersistArgs {
   long long pay_stride;          // doubles per payload
   long long col_offset;          // global index of local column 0
   struct StepCtl* ctl;           // queue / publish words
+  unsigned long long* rdy;       // [0] CTAs through P1, [1 + s] rows of chunk s written by P1
+                                 // (monotonic within a decompose, zeroed with ctl)
 };
+
+__device__ __forceinline__ void red_release_add_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
 
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
   unsigned v;
@@ -106,7 +119,7 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned& gen) {
 
 // Shared step bookkeeping (device memory, see PersistArgs::ctl).
 struct StepCtl {
-  unsigned long long tile_ctr;   // monotonic tile-claim counter (all steps, all calls)
+  unsigned long long tile_ctr;   // tile-claim counter: 0 at kernel entry, then monotonic
   unsigned ydone;                // Y'w1 groups finished this step (reset by the decider)
   unsigned pad;
   // published by the decider (claimer of the last Y'w1 tile), tagged with step+1
@@ -196,10 +209,15 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
   StepCtl* ctl = a.ctl;
   unsigned gen = 0;
   if (tid == 0) gen = ld_acquire_u32(&a.bar[1]);
-  unsigned long long tile_base = ctl->tile_ctr;  // identical in every CTA (read before barrier 1)
+  // the claim counter is 0 at entry (ctl is zeroed before a single-GPU launch;
+  // in sharded mode CTA 0 rezeroes it after the step's last barrier), and
+  // advances by exactly total + G per step
+  unsigned long long tile_base = 0;
 
   // ---- loop state: identical in every CTA (and, sharded, on every rank) ----
   long long k = st->d;
+  // P1 publications are counted from the k the counters were zeroed at
+  const long long k_base = SHARD ? 0 : k;
   long long jstar = st->jstar;
   int done = st->done;
   int pending = 0, reorth_prev = 0, breakdown = 0;
@@ -218,6 +236,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
   const double eps_R = st->eps_R, tol = st->breakdown_tol;
   const int cfg_reorth = st->cfg_reorth;
   const long long S = (m + kChunk - 1) / kChunk;
+  // p_k by step parity: a CTA still in P1 of step k reads p_{k-1} while
+  // faster CTAs already write p_k
+  auto pbuf = [&](long long kk) { return a.p + (kk & 1) * (a.d_max + 1); };
   // P1 row range of this CTA: an even split of the rows (kept even so 16-byte
   // row pairs never straddle two CTAs), processed in kPRows-row blocks
   const long long r_lo = ((m * cta / G) + 1) & ~1LL;
@@ -258,7 +279,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
       cs[l] = (!live || l >= k) ? 0.0
               : SHARD           ? __ldcg(&pay[kPayHead + m + l])
                                 : __ldcg(&a.T[l * n + jstar]);
-      ps[l] = (pending && reorth_prev && l < kb) ? __ldcg(&a.p[l]) : 0.0;
+      ps[l] = (pending && reorth_prev && l < kb) ? __ldcg(&pbuf(k - 1)[l]) : 0.0;
     }
     const double* x = SHARD ? pay + kPayHead : a.X + jstar * a.ldx;
     __syncthreads();
@@ -341,11 +362,48 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
     if (!live) continue;   // materialisation-only pass after the stop
     {
       const double sblk = block_sum_fixed<kThreads>(warp == 0 ? nacc : 0.0, smn);
-      if (tid == 0) a.npart[cta] = sblk;
+      // block_sum_fixed ends with __syncthreads: every P1 write of this CTA
+      // (w1 rows, Y column k-1 rows) precedes the release-adds below
+      if (tid == 0) {
+        a.npart[cta] = sblk;
+        if (r_lo < r_hi)
+          for (long long sc = r_lo / kChunk; sc * kChunk < r_hi; ++sc) {
+            const long long lo = sc * kChunk > r_lo ? sc * kChunk : r_lo;
+            const long long hi = (sc + 1) * kChunk < r_hi ? (sc + 1) * kChunk : r_hi;
+            red_release_add_u64(&a.rdy[1 + sc], (unsigned long long)(hi - lo));
+          }
+        red_release_add_u64(&a.rdy[0], 1ull);
+      }
     }
+    const unsigned long long ord = (unsigned long long)(k - k_base + 1);   // P1s published so far
+    bool all_rdy = false;   // (tid 0) every CTA is through this step's P1
+    auto wait_ge = [&](const unsigned long long* c, unsigned long long want) {
+      if (ld_acquire_u64(c) >= want) return;
+      const unsigned long long t0 = globaltimer();
+      unsigned spins = 0;
+      do {
+        __nanosleep(32);
+        if ((++spins & 0xfffu) == 0 && globaltimer() - t0 > 30000000000ull) __trap();
+      } while (ld_acquire_u64(c) < want);
+    };
+    // (tid 0, before publishing tile t to the CTA) the P1 rows tile t reads
+    auto wait_inputs = [&](long long t, long long gy_, long long total_) {
+      if (t >= total_ || all_rdy) return;
+      if (ld_acquire_u64(&a.rdy[0]) >= (unsigned long long)G * ord) {
+        all_rdy = true;
+        return;
+      }
+      if (t < gy_) {
+        wait_ge(&a.rdy[0], (unsigned long long)G * ord);
+        all_rdy = true;
+      } else {
+        const long long sc = (t - gy_) % S;
+        const long long rows = (m - sc * kChunk < kChunk) ? m - sc * kChunk : kChunk;
+        wait_ge(&a.rdy[1 + sc], (unsigned long long)rows * ord);
+      }
+    };
     mark(0);
     trace(k, 2);
-    grid_barrier(a.bar, gen);
     trace(k, 3);
     mark(1);
 
@@ -367,6 +425,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
     double bv = -1.0;          // this CTA's best finalised residual (argmax record)
     long long bj = 0x7fffffffffffffffLL;
     if (gy == 0 && cta == 0 && tid == 0) {   // k == 0: nothing to orthogonalise against
+      wait_ge(&a.rdy[0], (unsigned long long)G * ord);
       double w1n2 = 0.0;
       for (int b = 0; b < G; ++b) w1n2 += __ldcg(&a.npart[b]);
       const double norm0 = sqrt(w1n2);
@@ -426,7 +485,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
             for (int u = 0; u < 16; ++u) {
               const long long l = l0 + lane + 32 * u;
               tv[u] = (l < k) ? __ldcg(&a.T[l * n + j]) : 0.0;
-              pv[u] = (l < k) ? __ldcg(&a.p[l]) : 0.0;
+              pv[u] = (l < k) ? __ldcg(&pbuf(k)[l]) : 0.0;
             }
 #pragma unroll
             for (int u = 0; u < 16; ++u) corr = fma(pv[u], tv[u], corr);
@@ -473,7 +532,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
     if (tid == 0) next = (long long)(atomicAdd(&ctl->tile_ctr, 1ull) - tile_base);
     while (true) {
       mark(9);
-      if (tid == 0) sh_tile = next;
+      if (tid == 0) {
+        wait_inputs(next, gy, total);   // acquire by tid 0, published by the barrier below
+        sh_tile = next;
+      }
       __syncthreads();
       const long long t = sh_tile;
       mark(5);
@@ -490,7 +552,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
           const long long l = t * kCols + tid;
           double v = 0.0;
           for (long long s = 0; s < S; ++s) v += a.ppart[s * a.d_max + l];
-          a.p[l] = v;
+          pbuf(k)[l] = v;
         }
         __syncthreads();
         if (tid == 0) {
@@ -503,7 +565,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
           // decider: ||p||^2, ||w1||^2, the second-pass condition, ||w||, breakdown
           double pn = 0.0;
           for (long long ll = tid; ll < k; ll += kThreads) {
-            const double pv = __ldcg(&a.p[ll]);
+            const double pv = __ldcg(&pbuf(k)[ll]);
             pn = fma(pv, pv, pn);
           }
           pn = block_sum_fixed<kThreads>(pn, smn);
@@ -552,6 +614,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
     grid_barrier(a.bar, gen);
     trace(k, 7);
     mark(3);
+    if constexpr (SHARD) {   // every claim of this launch is done: rezero for the next launch
+      if (cta == 0 && tid == 0) ctl->tile_ctr = 0ull;
+    }
 
     // every CTA: the published decision, the global argmax over the CTA
     // records (workspace.cpp:107-113,123) and the stop test (decompose.cpp:87)
