@@ -23,6 +23,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "build", "liborc.so")
 
 ORC_OK = 0
+ORC_INCOMPATIBLE_WEIGHT = 2
 ERRORS = {1: "InvalidArgument", 2: "IncompatibleWeight", 3: "DegenerateInput",
           4: "IndexOutOfRange", 5: "DimensionMismatch"}
 
@@ -73,6 +74,16 @@ def lib():
         L.orc_acceptance3_count.restype = I64
         L.orc_seeded_start.argtypes = [C.c_uint64, I64]
         L.orc_seeded_start.restype = I64
+        L.orc_decompose_diag.argtypes = [P, I64, I64, I64, P, I64, I64, D, I, I64, C.c_uint64, I,
+                                         D, I64, P, P, P, P, P]
+        L.orc_decompose_diag.restype = I
+        L.orc_ws_init_diag.argtypes = [P, I64, I64, I64, P, I64]
+        L.orc_ws_init_diag.restype = P
+        L.orc_ws_scan_T.argtypes = [P, P, P, P]
+        L.orc_ws_scan_T.restype = I
+        L.orc_ws_yay.argtypes = [P, P]
+        L.orc_ws_yay.restype = I
+        L.orc_random_positive.argtypes = [I64, C.c_uint64, P]
         _lib = L
     return _lib
 
@@ -93,8 +104,8 @@ class OracleModel:
 def decompose(x, d_max: int, eps_r: float = 0.0, start_column: int = 0,
               start_seed: Optional[int] = None, reorthogonalize: bool = False,
               breakdown_tol: float = -1.0, nthreads: int = 1,
-              max_steps: Optional[int] = None) -> OracleModel:
-    """rbd::decompose restated (decompose.cpp:53-111)."""
+              max_steps: Optional[int] = None, diag=None) -> OracleModel:
+    """rbd::decompose restated (decompose.cpp:53-111); diag = WeightSpec::diagonal."""
     xa = np.asfortranarray(np.asarray(x, dtype=np.float64))
     m, n = xa.shape if xa.ndim == 2 else (0, 0)
     cap = max(1, min(int(d_max), max(n, 1)))
@@ -103,11 +114,20 @@ def decompose(x, d_max: int, eps_r: float = 0.0, start_column: int = 0,
     sel = np.zeros(cap, dtype=np.int64)
     hist = np.zeros(cap)
     d = C.c_int64(0)
-    rc = lib().orc_decompose_steps(
-        _p(xa), m, n, max(m, 1), int(d_max), float(eps_r), 1 if start_seed is not None else 0,
-        int(start_column), int(start_seed or 0) & 0xFFFFFFFFFFFFFFFF, 1 if reorthogonalize else 0,
-        float(breakdown_tol), int(nthreads), int(max_steps if max_steps is not None else 2**62),
-        _p(Y), _p(T), _p(sel), _p(hist), C.byref(d))
+    steps = int(max_steps if max_steps is not None else 2**62)
+    seed = int(start_seed or 0) & 0xFFFFFFFFFFFFFFFF
+    kind = 1 if start_seed is not None else 0
+    if diag is not None:
+        dg = np.ascontiguousarray(np.asarray(diag, dtype=np.float64).reshape(-1))
+        rc = lib().orc_decompose_diag(
+            _p(xa), m, n, max(m, 1), _p(dg) if dg.size else None, dg.size, int(d_max),
+            float(eps_r), kind, int(start_column), seed, 1 if reorthogonalize else 0,
+            float(breakdown_tol), steps, _p(Y), _p(T), _p(sel), _p(hist), C.byref(d))
+    else:
+        rc = lib().orc_decompose_steps(
+            _p(xa), m, n, max(m, 1), int(d_max), float(eps_r), kind, int(start_column), seed,
+            1 if reorthogonalize else 0, float(breakdown_tol), int(nthreads), steps,
+            _p(Y), _p(T), _p(sel), _p(hist), C.byref(d))
     if rc != ORC_OK:
         raise OracleError(rc, lib().orc_last_error().decode())
     k = d.value
@@ -133,12 +153,20 @@ def mgs_project(v, basis, breakdown_tol: float, reorthogonalize: bool = False):
 
 
 class Workspace:
-    """ErrorWorkspace, identity weight (workspace.cpp:9-125)."""
+    """ErrorWorkspace, identity or diagonal weight (workspace.cpp:9-125)."""
 
-    def __init__(self, x):
+    def __init__(self, x, diag=None):
         self.x = np.asfortranarray(np.asarray(x, dtype=np.float64))
         self.m, self.n = self.x.shape
-        self.h = lib().orc_ws_init(_p(self.x), self.m, self.n, self.m)
+        self.h = None
+        if diag is None:
+            self.h = lib().orc_ws_init(_p(self.x), self.m, self.n, self.m)
+        else:
+            self.diag = np.ascontiguousarray(np.asarray(diag, dtype=np.float64).reshape(-1))
+            self.h = lib().orc_ws_init_diag(_p(self.x), self.m, self.n, self.m, _p(self.diag),
+                                            self.diag.size)
+            if not self.h:
+                raise OracleError(ORC_INCOMPATIBLE_WEIGHT, lib().orc_last_error().decode())
 
     def __del__(self):
         if getattr(self, "h", None):
@@ -177,6 +205,20 @@ class Workspace:
             raise OracleError(rc, lib().orc_last_error().decode())
         return out.value
 
+    def scan_T(self, T):
+        """residual_scan(ws, T) for any weight (T is d x n)."""
+        Ta = np.ascontiguousarray(np.asarray(T, dtype=np.float64))
+        e = C.c_double()
+        j = C.c_int64()
+        lib().orc_ws_scan_T(self.h, _p(Ta), C.byref(e), C.byref(j))
+        return e.value, j.value
+
+    def yay(self):
+        d = self.d
+        out = np.zeros((d, d))
+        lib().orc_ws_yay(self.h, _p(out))
+        return out
+
     def scan(self):
         e = C.c_double()
         j = C.c_int64()
@@ -193,6 +235,13 @@ def project_batch(Y, Xn, nthreads: int = 1):
     err = np.zeros(N)
     lib().orc_project_batch(_p(Ya), m, d, _p(Xa), N, m, int(nthreads), _p(Tn), _p(err))
     return Tn, err
+
+
+def random_positive(n, seed):
+    """testutil::random_positive (helpers.hpp:28-34), bit-identical draws."""
+    out = np.zeros(n)
+    lib().orc_random_positive(int(n), int(seed) & 0xFFFFFFFFFFFFFFFF, _p(out))
+    return out
 
 
 def random_matrix(m, n, seed):

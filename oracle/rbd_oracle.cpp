@@ -187,32 +187,76 @@ int orc_decompose(const double* X, int64_t m, int64_t n, int64_t ldx, int64_t d_
                              selected, history, d_out);
 }
 
-// ---- ErrorWorkspace, identity path ----
+// ---- ErrorWorkspace: identity and diagonal paths ----
 struct orc_ws_s {
   const double* X;
   int64_t m, n, ldx, d;
   std::vector<double> col_sq, residual_sq;
   std::vector<std::vector<double>> yax_rows;
+  // diagonal weight (workspace.hpp:18-30): diag, yay = Y'AY (row-major d x d,
+  // grown per step), a_basis = A*Y (column k = A xi_k)
+  std::vector<double> diag;
+  std::vector<std::vector<double>> yay;
+  std::vector<std::vector<double>> a_basis;
 };
 
 orc_ws_t orc_ws_init(const double* X, int64_t m, int64_t n, int64_t ldx) {
-  auto* ws = new orc_ws_s{X, m, n, ldx, 0, {}, {}, {}};
+  auto* ws = new orc_ws_s{X, m, n, ldx, 0, {}, {}, {}, {}, {}, {}};
   ws->col_sq.resize(n);
   for (int64_t j = 0; j < n; ++j) ws->col_sq[j] = std::max(sqnorm(X + j * ldx, m), 0.0);  // :22,37
   ws->residual_sq = ws->col_sq;                                                           // :38
   return ws;
 }
+
+orc_ws_t orc_ws_init_diag(const double* X, int64_t m, int64_t n, int64_t ldx, const double* diag,
+                          int64_t diag_len) {
+  if (diag_len != m) {  // workspace.cpp:12-13 (compatible_with, weight.cpp:71-74)
+    fail(ORC_INCOMPATIBLE_WEIGHT, "weight dimension does not match matrix rows");
+    return nullptr;
+  }
+  auto* ws = new orc_ws_s{X, m, n, ldx, 0, {}, {}, {}, {}, {}, {}};
+  ws->diag.assign(diag, diag + m);
+  ws->col_sq.resize(n);
+  for (int64_t j = 0; j < n; ++j) {  // workspace.cpp:24-29: sum_i x_ij^2 a_i, clamp :37
+    const double* x = X + j * ldx;
+    double s = 0.0;
+    for (int64_t i = 0; i < m; ++i) s += (x[i] * x[i]) * diag[i];
+    ws->col_sq[j] = std::max(s, 0.0);
+  }
+  ws->residual_sq = ws->col_sq;  // :38
+  return ws;
+}
 void orc_ws_free(orc_ws_t ws) { delete ws; }
 
-int orc_ws_extend(orc_ws_t ws, const double* xi) {  // workspace.cpp:50-60
-  std::vector<double> row(ws->n);
-  gemv_t(ws->X, ws->m, ws->n, ws->ldx, xi, row.data(), 1);
-  for (int64_t j = 0; j < ws->n; ++j) {
-    ws->residual_sq[j] -= row[j] * row[j];
-    ws->residual_sq[j] = std::max(ws->residual_sq[j], 0.0);
+int orc_ws_extend(orc_ws_t ws, const double* xi) {
+  if (ws->diag.empty()) {  // identity, workspace.cpp:50-60
+    std::vector<double> row(ws->n);
+    gemv_t(ws->X, ws->m, ws->n, ws->ldx, xi, row.data(), 1);
+    for (int64_t j = 0; j < ws->n; ++j) {
+      ws->residual_sq[j] -= row[j] * row[j];
+      ws->residual_sq[j] = std::max(ws->residual_sq[j], 0.0);
+    }
+    ws->yax_rows.push_back(std::move(row));
+    ws->d += 1;
+    return ORC_OK;
   }
+  // diagonal, workspace.cpp:61-79
+  const int64_t m = ws->m, d = ws->d;
+  std::vector<double> axi(m);
+  for (int64_t i = 0; i < m; ++i) axi[i] = ws->diag[i] * xi[i];  // :64 apply (weight.cpp:83)
+  std::vector<double> row(ws->n);
+  gemv_t(ws->X, m, ws->n, ws->ldx, axi.data(), row.data(), 1);   // :66 X' axi
   ws->yax_rows.push_back(std::move(row));
-  ws->d += 1;
+  for (auto& r : ws->yay) r.resize(d + 1, 0.0);                  // :68 conservativeResize
+  ws->yay.emplace_back(d + 1, 0.0);
+  for (int64_t k = 0; k < d; ++k) {                              // :69-74
+    const double v = dot8(xi, ws->a_basis[k].data(), m);
+    ws->yay[d][k] = v;
+    ws->yay[k][d] = v;
+  }
+  ws->yay[d][d] = dot8(axi.data(), xi, m);                       // :75
+  ws->a_basis.push_back(std::move(axi));                         // :76-77
+  ws->d = d + 1;                                                 // :81
   return ORC_OK;
 }
 int64_t orc_ws_d(orc_ws_t ws) { return ws->d; }
@@ -231,9 +275,118 @@ int orc_ws_error_sq(orc_ws_t ws, int64_t j, const double* c, int64_t clen, doubl
   double cross = 0.0;
   for (int64_t k = 0; k < ws->d; ++k) cross += c[k] * ws->yax_rows[k][j];
   double quad = 0.0;
-  for (int64_t k = 0; k < ws->d; ++k) quad += c[k] * c[k];
+  if (ws->diag.empty()) {
+    for (int64_t k = 0; k < ws->d; ++k) quad += c[k] * c[k];  // :91 Y'AY = I
+  } else {
+    for (int64_t k = 0; k < ws->d; ++k) {                     // :93 c.dot(yay * c)
+      double yc = 0.0;
+      for (int64_t l = 0; l < ws->d; ++l) yc += ws->yay[k][l] * c[l];
+      quad += c[k] * yc;
+    }
+  }
   const double e2 = ws->col_sq[j] - 2.0 * cross + quad;
   *out = e2 > 0.0 ? e2 : 0.0;
+  return ORC_OK;
+}
+
+// residual_scan, general weight (workspace.cpp:114-122): error_sq of every
+// column with c = T[:, j] (T row-major d x n).
+int orc_ws_scan_T(orc_ws_t ws, const double* T, double* e_cur, int64_t* argmax) {
+  double best = -1.0;
+  int64_t arg = 0;
+  std::vector<double> c(ws->d);
+  for (int64_t j = 0; j < ws->n; ++j) {
+    for (int64_t k = 0; k < ws->d; ++k) c[k] = T[k * ws->n + j];
+    double e2;
+    orc_ws_error_sq(ws, j, c.data(), ws->d, &e2);
+    if (e2 > best) {
+      best = e2;
+      arg = j;
+    }
+  }
+  *e_cur = std::sqrt(best > 0.0 ? best : 0.0);  // :123
+  *argmax = arg;
+  return ORC_OK;
+}
+
+int orc_ws_yay(orc_ws_t ws, double* out) {  // row-major d x d (zero-sized for identity)
+  for (int64_t k = 0; k < (int64_t)ws->yay.size(); ++k)
+    std::copy(ws->yay[k].begin(), ws->yay[k].end(), out + k * ws->d);
+  return ORC_OK;
+}
+
+// rbd::decompose with a diagonal weight (decompose.cpp:53-111 with
+// WeightSpec::diagonal, weight.cpp:11-21): Y and T stay Euclidean (mgs_project
+// and T = xi'X are weight-free); the weight enters workspace_init/extend and
+// the error_sq scan.
+int orc_decompose_diag(const double* X, int64_t m, int64_t n, int64_t ldx, const double* diag,
+                       int64_t diag_len, int64_t d_max, double eps_R, int start_kind,
+                       int64_t start_column, uint64_t start_seed, int reorthogonalize,
+                       double cfg_breakdown_tol, int64_t max_steps, double* Y, double* T,
+                       int64_t* selected, double* history, int64_t* d_out) {
+  // WeightSpec::diagonal (weight.cpp:11-17), constructed before decompose runs
+  if (diag_len == 0) return fail(ORC_INVALID_ARGUMENT, "diagonal weight must be non-empty");
+  for (int64_t i = 0; i < diag_len; ++i)
+    if (!(diag[i] > 0.0) || !std::isfinite(diag[i]))
+      return fail(ORC_INVALID_ARGUMENT, "diagonal weight entries must be strictly positive and finite");
+  // validation, decompose.cpp:56-64 (same order)
+  if (m < 1 || n < 1) return fail(ORC_INVALID_ARGUMENT, "decompose: matrix must be non-empty");
+  for (int64_t j = 0; j < n; ++j)
+    for (int64_t i = 0; i < m; ++i)
+      if (!std::isfinite(X[i + j * ldx]))
+        return fail(ORC_INVALID_ARGUMENT, "decompose: matrix has non-finite entries");
+  if (d_max < 1 || d_max > n)
+    return fail(ORC_INVALID_ARGUMENT, "decompose: d_max must satisfy 1 <= d_max <= n");
+  if (!(eps_R >= 0.0)) return fail(ORC_INVALID_ARGUMENT, "decompose: eps_R must be >= 0");
+  if (diag_len != m) return fail(ORC_INCOMPATIBLE_WEIGHT, "decompose: weight dimension != m");
+  bool all_zero = true;
+  for (int64_t j = 0; j < n && all_zero; ++j)
+    for (int64_t i = 0; i < m; ++i)
+      if (X[i + j * ldx] != 0.0) {
+        all_zero = false;
+        break;
+      }
+  if (all_zero) return fail(ORC_DEGENERATE_INPUT, "decompose: zero matrix, no basis can be built");
+  double max_col_norm = 0.0;  // :70-74 (Euclidean column norms)
+  for (int64_t j = 0; j < n; ++j)
+    max_col_norm = std::max(max_col_norm, std::sqrt(sqnorm(X + j * ldx, m)));
+  const double noise_floor =
+      max_col_norm * std::sqrt(static_cast<double>(m)) * std::numeric_limits<double>::epsilon() * 16.0;
+  const double breakdown_tol =
+      std::max(cfg_breakdown_tol < 0.0 ? eps_R : cfg_breakdown_tol, noise_floor);
+  orc_ws_t ws = orc_ws_init_diag(X, m, n, ldx, diag, diag_len);  // :81
+  int64_t i;
+  if (start_kind == 0) {
+    if (start_column < 0 || start_column >= n) {
+      orc_ws_free(ws);
+      return fail(ORC_INDEX_OUT_OF_RANGE, "start column index out of range");
+    }
+    i = start_column;
+  } else {
+    i = orc_seeded_start(start_seed, n);
+  }
+  int64_t d = 0;
+  double e_cur = std::numeric_limits<double>::infinity();
+  std::vector<double> xi(m), row(n);
+  while (d < d_max && e_cur > eps_R && d < max_steps) {  // :87
+    double nrm;
+    if (!orc_mgs_project(X + i * ldx, m, Y, d, m, breakdown_tol, reorthogonalize, xi.data(), &nrm))
+      break;                                              // :90
+    std::memcpy(Y + d * m, xi.data(), sizeof(double) * m);  // :92
+    gemv_t(X, m, n, ldx, xi.data(), row.data(), 1);       // :93
+    std::memcpy(T + d * n, row.data(), sizeof(double) * n);
+    selected[d] = i;                                      // :94
+    orc_ws_extend(ws, xi.data());                         // :95
+    ++d;                                                  // :96
+    int64_t arg;
+    orc_ws_scan_T(ws, T, &e_cur, &arg);                   // :98 (T.topRows(d))
+    history[d - 1] = e_cur;                               // :99
+    i = arg;                                              // :101
+  }
+  orc_ws_free(ws);
+  if (d == 0)
+    return fail(ORC_DEGENERATE_INPUT, "decompose: start column is numerically zero, no basis built");
+  *d_out = d;
   return ORC_OK;
 }
 
@@ -286,6 +439,13 @@ void orc_random_matrix(int64_t m, int64_t n, uint64_t seed, double* out) {
   std::normal_distribution<double> gauss;
   for (int64_t j = 0; j < n; ++j)
     for (int64_t i = 0; i < m; ++i) out[i + j * m] = gauss(rng);
+}
+
+void orc_random_positive(int64_t n, uint64_t seed, double* out) {
+  // helpers.hpp:28-34: U[0.5, 3.0) draws
+  std::mt19937_64 rng(seed);
+  std::uniform_real_distribution<double> u(0.5, 3.0);
+  for (int64_t i = 0; i < n; ++i) out[i] = u(rng);
 }
 
 void orc_random_low_rank(int64_t m, int64_t n, int64_t r, uint64_t seed, double* out) {

@@ -1,7 +1,7 @@
 /* TEST INFRASTRUCTURE ONLY — NOT PART OF THE PRODUCT.
  *
- * CPU restatement ("oracle") of the reference RBD greedy loop, identity-weight
- * path, written with plain loops (no Eigen: Eigen 3.4 is absent from this image,
+ * CPU restatement ("oracle") of the reference RBD greedy loop (identity and
+ * diagonal weights), written with plain loops (no Eigen: Eigen 3.4 is absent from this image,
  * so /root/reference cannot be compiled — see DESIGN.md §Oracle).
  *
  * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
@@ -58,14 +58,31 @@ int orc_decompose_steps(const double* X, int64_t m, int64_t n, int64_t ldx, int6
                         int nthreads, int64_t max_steps, double* Y, double* T,
                         int64_t* selected, double* history, int64_t* d_out);
 
+/* rbd::decompose with WeightSpec::diagonal(diag) (decompose.cpp:53-111,
+ * weight.cpp:11-21, workspace.cpp:24-29,61-99,114-122). Single-threaded;
+ * Y/T/selected/history as orc_decompose. */
+int orc_decompose_diag(const double* X, int64_t m, int64_t n, int64_t ldx, const double* diag,
+                       int64_t diag_len, int64_t d_max, double eps_R, int start_kind,
+                       int64_t start_column, uint64_t start_seed, int reorthogonalize,
+                       double breakdown_tol, int64_t max_steps, double* Y, double* T,
+                       int64_t* selected, double* history, int64_t* d_out);
+
 /* rbd::mgs_project (decompose.cpp:12-33). Returns 1 with xi/norm filled, 0 on
  * breakdown (std::nullopt), negative on DimensionMismatch. */
 int orc_mgs_project(const double* v, int64_t m, const double* basis, int64_t k, int64_t ldb,
                     double breakdown_tol, int reorthogonalize, double* xi, double* norm);
 
-/* ErrorWorkspace identity path (workspace.cpp:9-60, 84-125). */
+/* ErrorWorkspace identity path (workspace.cpp:9-60, 84-125) and diagonal path
+ * (workspace.cpp:24-29, 61-79, 84-99, 114-122). */
 typedef struct orc_ws_s* orc_ws_t;
 orc_ws_t orc_ws_init(const double* X, int64_t m, int64_t n, int64_t ldx);
+/* NULL (ORC_INCOMPATIBLE_WEIGHT in orc_last_error) when diag_len != m. */
+orc_ws_t orc_ws_init_diag(const double* X, int64_t m, int64_t n, int64_t ldx, const double* diag,
+                          int64_t diag_len);
+/* residual_scan with T (row-major d x n), any weight (workspace.cpp:101-125). */
+int orc_ws_scan_T(orc_ws_t ws, const double* T, double* e_cur, int64_t* argmax);
+/* Y'AY (row-major d x d), diagonal workspaces only. */
+int orc_ws_yay(orc_ws_t ws, double* out);
 void orc_ws_free(orc_ws_t ws);
 int orc_ws_extend(orc_ws_t ws, const double* xi);
 int64_t orc_ws_d(orc_ws_t ws);
@@ -83,6 +100,7 @@ void orc_project_batch(const double* Y, int64_t m, int64_t d, const double* Xn, 
 
 /* Fixture generators restating the reference's test helpers. */
 void orc_random_matrix(int64_t m, int64_t n, uint64_t seed, double* out);      /* helpers.hpp:14-21 */
+void orc_random_positive(int64_t n, uint64_t seed, double* out);        /* helpers.hpp:28-34 */
 void orc_random_low_rank(int64_t m, int64_t n, int64_t r, uint64_t seed, double* out); /* :23-26 */
 int orc_gen_grid_matrix(int fid, int64_t n_points, double* out); /* datasets.cpp:30-65 */
 int64_t orc_acceptance3_count(void);  /* acceptance.cpp:185-231 column-evaluation count */
