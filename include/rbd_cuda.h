@@ -62,7 +62,7 @@ typedef struct {
   int64_t start_column;     /* fixed start column (default 0)                      */
   uint64_t start_seed;      /* seed for RBD_START_SEEDED_RANDOM                    */
   double breakdown_tol;     /* < 0: use eps_R (reference default -1.0)             */
-  int32_t weight_kind;      /* rbd_weight_kind; only IDENTITY runs on this path    */
+  int32_t weight_kind;      /* rbd_weight_kind; DIAGONAL via rbd_decompose_diag_*  */
   int64_t weight_dim;       /* dimension of a non-identity weight (compat check)   */
 } rbd_config_t;
 
@@ -109,6 +109,23 @@ int rbd_decompose_device(rbd_ctx_t ctx, const double* dX, int64_t m, int64_t n, 
 int rbd_decompose_host(rbd_ctx_t ctx, const double* hX, int64_t m, int64_t n, int64_t ldx,
                        const rbd_config_t* cfg, double* hY, double* hT, int64_t* h_selected,
                        double* h_history, rbd_result_t* result);
+
+/* rbd::decompose with cfg.weight = WeightSpec::diagonal(diag) (
+ * reference decompose.cpp:53-111, weight.cpp:11-21, workspace.cpp:24-29,61-99,
+ * 114-122). Y and T are Euclidean as in the reference; the weight steers the
+ * greedy selection through the A-norm residual. diag: diag_len positive finite
+ * doubles (device memory for _device, host memory for _host); InvalidArgument
+ * for an empty/non-positive/non-finite diagonal (weight.cpp:11-17),
+ * IncompatibleWeight when diag_len != m (decompose.cpp:61-62). cfg->weight_kind
+ * and weight_dim are taken from the call. */
+int rbd_decompose_diag_device(rbd_ctx_t ctx, const double* dX, int64_t m, int64_t n, int64_t ldx,
+                              const rbd_config_t* cfg, const double* d_diag, int64_t diag_len,
+                              double* dY, double* dT, int64_t* h_selected, double* h_history,
+                              rbd_result_t* result);
+int rbd_decompose_diag_host(rbd_ctx_t ctx, const double* hX, int64_t m, int64_t n, int64_t ldx,
+                            const rbd_config_t* cfg, const double* h_diag, int64_t diag_len,
+                            double* hY, double* hT, int64_t* h_selected, double* h_history,
+                            rbd_result_t* result);
 
 /* rbd::mgs_project (decompose.cpp:12-33) on device vectors: orthonormalise dv
  * against the k orthonormal columns of dB (ld ldb). On success *ok = 1 and

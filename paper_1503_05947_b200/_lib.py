@@ -120,6 +120,10 @@ _SIGS = {
                                        C.POINTER(Result)]),
     "rbd_decompose_host": (C.c_int, [_P, _P, _I64, _I64, _I64, C.POINTER(Config), _P, _P, _P, _P,
                                      C.POINTER(Result)]),
+    "rbd_decompose_diag_device": (C.c_int, [_P, _P, _I64, _I64, _I64, C.POINTER(Config), _P, _I64,
+                                            _P, _P, _P, _P, C.POINTER(Result)]),
+    "rbd_decompose_diag_host": (C.c_int, [_P, _P, _I64, _I64, _I64, C.POINTER(Config), _P, _I64,
+                                          _P, _P, _P, _P, C.POINTER(Result)]),
     "rbd_mgs_project": (C.c_int, [_P, _P, _I64, _P, _I64, _I64, _D, C.c_int, _P, _DP,
                                   C.POINTER(C.c_int)]),
     "rbd_ws_init": (C.c_int, [_P, _P, _I64, _I64, _I64, _I64, C.POINTER(_P)]),

@@ -76,7 +76,7 @@ def make_config(d_max: int, eps_r: float = 0.0, start_column: int = 0,
         cfg.start_column = int(start_column)
     if diag is not None:
         cfg.weight_kind = 1
-        cfg.weight_dim = int(np.asarray(diag).shape[0])
+        cfg.weight_dim = int(diag.shape[0]) if hasattr(diag, "shape") else len(diag)
     elif sparse is not None:
         cfg.weight_kind = 2
         cfg.weight_dim = int(sparse.shape[0])
@@ -149,10 +149,19 @@ def decompose(x, d_max: int, eps_r: float = 0.0, diag=None, sparse=None, start_c
         sel = np.zeros(cap, dtype=np.int64)
         hist = np.zeros(cap, dtype=np.float64)
         torch.cuda.current_stream(x.device).synchronize()
-        check(lib.rbd_decompose_device(ctx.handle, C.c_void_p(xc.data_ptr()), m, n, ldx,
-                                       C.byref(cfg), C.c_void_p(Y.data_ptr()),
-                                       C.c_void_p(T.data_ptr()), _dp(sel), _dp(hist),
-                                       C.byref(res)))
+        if diag is not None:   # WeightSpec::diagonal
+            dg = torch.as_tensor(diag, dtype=torch.float64, device=x.device).reshape(-1).contiguous()
+            torch.cuda.current_stream(x.device).synchronize()
+            check(lib.rbd_decompose_diag_device(
+                ctx.handle, C.c_void_p(xc.data_ptr()), m, n, ldx, C.byref(cfg),
+                C.c_void_p(dg.data_ptr()) if dg.numel() else None, dg.numel(),
+                C.c_void_p(Y.data_ptr()), C.c_void_p(T.data_ptr()), _dp(sel), _dp(hist),
+                C.byref(res)))
+        else:
+            check(lib.rbd_decompose_device(ctx.handle, C.c_void_p(xc.data_ptr()), m, n, ldx,
+                                           C.byref(cfg), C.c_void_p(Y.data_ptr()),
+                                           C.c_void_p(T.data_ptr()), _dp(sel), _dp(hist),
+                                           C.byref(res)))
         d = res.d
         return Model(Y, T, d, sel[:d], hist[:d], res, ctx)
     ctx = ctx or default_context(0)
@@ -164,8 +173,14 @@ def decompose(x, d_max: int, eps_r: float = 0.0, diag=None, sparse=None, start_c
     Y, T = _host_outputs(m, n, cap)
     sel = np.zeros(cap, dtype=np.int64)
     hist = np.zeros(cap, dtype=np.float64)
-    check(lib.rbd_decompose_host(ctx.handle, _dp(xa), m, n, max(m, 1), C.byref(cfg), _dp(Y),
-                                 _dp(T), _dp(sel), _dp(hist), C.byref(res)))
+    if diag is not None:   # WeightSpec::diagonal
+        dg = np.ascontiguousarray(np.asarray(diag, dtype=np.float64).reshape(-1))
+        check(lib.rbd_decompose_diag_host(ctx.handle, _dp(xa), m, n, max(m, 1), C.byref(cfg),
+                                          _dp(dg) if dg.size else None, dg.size, _dp(Y), _dp(T),
+                                          _dp(sel), _dp(hist), C.byref(res)))
+    else:
+        check(lib.rbd_decompose_host(ctx.handle, _dp(xa), m, n, max(m, 1), C.byref(cfg),
+                                     _dp(Y), _dp(T), _dp(sel), _dp(hist), C.byref(res)))
     d = res.d
     return Model(Y, T, d, sel[:d], hist[:d], res, ctx)
 

@@ -18,6 +18,7 @@
 #include "rbd_project.cuh"
 #include "rbd_persistent.cuh"
 #include "rbd_project_tc.cuh"
+#include "rbd_weighted.cuh"
 
 #include <cudaTypedefs.h>
 
@@ -123,6 +124,9 @@ struct rbd_ctx_s {
   DevBuf bar;                              // grid-barrier words
   DevBuf ctl, gcnt, ygcnt;                 // persistent loop: ctl words, p (x2), CTA records
   DevBuf rdy;                              // persistent loop: P1 readiness counters
+  // diagonal-weight loop (rbd_weighted.cuh): a o xi, xi'A xi partials, YAX row
+  // partials, YAY row, YAX (d_max x n), cross, quad, col_sq_A, host-entry diag
+  DevBuf wd_axi, wd_yy, wd_part2, wd_yrow, wd_yax, wd_cross, wd_quad, wd_colsq, wd_diag;
   DevBuf send, recv;                       // sharded mode: payload exchange buffers
   // multi-GPU
   void* comm = nullptr;                    // ncclComm_t (dlopen'ed NCCL)
@@ -282,6 +286,10 @@ struct LoopBufs {
 };
 
 // One greedy step: extension (K4) + fused sweep (K2) + finalize/argmax (K3).
+int diag_vec_grid(rbd_ctx_t ctx, long long m) {
+  return (int)std::max<long long>(1, std::min<long long>(cdiv(m, kThreads), (long long)ctx->nsm * 2));
+}
+
 int enqueue_step(rbd_ctx_t ctx, const LoopBufs& L) {
   DevState* st = ptr<DevState>(ctx->state);
   ExtBufs b{};
@@ -330,6 +338,91 @@ int enqueue_step(rbd_ctx_t ctx, const LoopBufs& L) {
   f.cbuf = ptr<double>(ctx->c);
   f.mode = 0;
   k_finalize<<<finalize_grid(ctx, L.n), kThreads, 0, ctx->stream>>>(f);
+  ctx->launches++;
+  CU(cudaGetLastError());
+  return RBD_OK;
+}
+
+// One greedy step with a diagonal weight (rbd_weighted.cuh): extension (K4,
+// Euclidean, unchanged), a o xi, the YAY row over Y, one X pass for the T and
+// YAX rows, and the weighted finalize/argmax.
+int enqueue_step_diag(rbd_ctx_t ctx, const LoopBufs& L, const double* diag) {
+  DevState* st = ptr<DevState>(ctx->state);
+  ExtBufs b{};
+  b.B = L.Y;
+  b.m = L.m;
+  b.dcap = L.d_max;
+  b.X = L.X;
+  b.ldx = L.ldx;
+  b.c = ptr<double>(ctx->c);
+  b.w = ptr<double>(ctx->w);
+  b.p = ptr<double>(ctx->p);
+  b.nrm = ptr<double>(ctx->nrm);
+  b.partial = ptr<double>(ctx->partial);
+  b.ybase = L.Y;
+  b.use_d = 1;
+  b.selected = ptr<long long>(ctx->sel);
+  b.st = st;
+  TRY(enqueue_extension(ctx, b));
+  const int gv = diag_vec_grid(ctx, L.m);
+  k_diag_vec<<<gv, kThreads, 0, ctx->stream>>>(L.Y, L.m, diag, ptr<double>(ctx->wd_axi),
+                                               ptr<double>(ctx->wd_yy), st);
+  ctx->launches++;
+  // YAY[d, 0:d] = Y' (a o xi): chunked dots over the first st->d columns of Y
+  const int vy = (L.m % 2 == 0 && aligned16(L.Y) && aligned16(ctx->wd_axi.p)) ? 2 : 1;
+  SweepArgs s{};
+  s.A = L.Y;
+  s.lda = L.m;
+  s.m = L.m;
+  s.ncols = L.d_max;
+  s.v = ptr<double>(ctx->wd_axi);
+  s.partial = ptr<double>(ctx->ppart);
+  s.pstride = L.d_max;
+  s.st = st;
+  s.gate = GATE_LIVE;
+  s.csel = 1;
+  TRY(launch_sweep(ctx, s, vy, MODE_DOT, false, L.d_max));
+  k_coef_combine<<<(unsigned)std::max<long long>(1, cdiv(L.d_max, 256)), 256, 0, ctx->stream>>>(
+      ptr<double>(ctx->ppart), cdiv(L.m, kChunk), L.d_max, ptr<double>(ctx->wd_yrow), st, GATE_LIVE);
+  ctx->launches++;
+  // T and YAX rows in one X pass
+  const int vx = (L.ldx % 2 == 0 && L.m % 2 == 0 && aligned16(L.X) && aligned16(L.Y) &&
+                  aligned16(ctx->wd_axi.p)) ? 2 : 1;
+  const long long ntiles = cdiv(L.m, kChunk) * cdiv(L.n, kCols);
+  const int gx = (int)std::max<long long>(1, std::min<long long>(ntiles, (long long)ctx->nsm * 2));
+  if (vx == 2)
+    k_sweep_diag<2><<<gx, kThreads, 0, ctx->stream>>>(L.X, L.ldx, L.m, L.n, L.Y,
+                                                      ptr<double>(ctx->wd_axi),
+                                                      ptr<double>(ctx->partial),
+                                                      ptr<double>(ctx->wd_part2), st);
+  else
+    k_sweep_diag<1><<<gx, kThreads, 0, ctx->stream>>>(L.X, L.ldx, L.m, L.n, L.Y,
+                                                      ptr<double>(ctx->wd_axi),
+                                                      ptr<double>(ctx->partial),
+                                                      ptr<double>(ctx->wd_part2), st);
+  ctx->launches++;
+  FinalizeDiagArgs f{};
+  f.f.partial = ptr<double>(ctx->partial);
+  f.f.S = cdiv(L.m, kChunk);
+  f.f.n = L.n;
+  f.f.T = L.T;
+  f.f.r = ptr<double>(ctx->resid);
+  f.f.col_sq = ptr<double>(ctx->colsq);
+  f.f.st = st;
+  f.f.rec = ptr<Rec>(ctx->rec);
+  f.f.counter = ptr<unsigned>(ctx->counter);
+  f.f.history = ptr<double>(ctx->hist);
+  f.f.cbuf = ptr<double>(ctx->c);
+  f.f.mode = 0;
+  f.partial2 = ptr<double>(ctx->wd_part2);
+  f.YAX = ptr<double>(ctx->wd_yax);
+  f.yrow = ptr<double>(ctx->wd_yrow);
+  f.yy_part = ptr<double>(ctx->wd_yy);
+  f.yy_np = gv;
+  f.cross = ptr<double>(ctx->wd_cross);
+  f.quad = ptr<double>(ctx->wd_quad);
+  f.colsq_a = ptr<double>(ctx->wd_colsq);
+  k_finalize_diag<<<finalize_grid(ctx, L.n), kThreads, 0, ctx->stream>>>(f);
   ctx->launches++;
   CU(cudaGetLastError());
   return RBD_OK;
@@ -588,7 +681,8 @@ int get_step_graph(rbd_ctx_t ctx, const LoopBufs& L) {
 
 // Validation shared by the single- and multi-GPU entries: reference order of
 // decompose.cpp:56-64 after the K1 flags are known.
-int validate_after_init(const rbd_config_t* cfg, long long m, long long n, const DevState& hs) {
+int validate_after_init(const rbd_config_t* cfg, long long m, long long n, const DevState& hs,
+                        bool diag_supplied = false) {
   if (hs.flags_nonfinite)
     return set_err(RBD_ERR_INVALID_ARGUMENT, "decompose: matrix has non-finite entries");
   if (cfg->d_max < 1 || cfg->d_max > n)
@@ -597,9 +691,12 @@ int validate_after_init(const rbd_config_t* cfg, long long m, long long n, const
   if (cfg->weight_kind != RBD_WEIGHT_IDENTITY) {
     if (cfg->weight_dim != 0 && cfg->weight_dim != m)
       return set_err(RBD_ERR_INCOMPATIBLE_WEIGHT, "decompose: weight dimension != m");
-    return set_err(RBD_ERR_INVALID_ARGUMENT,
-                   "decompose: only the identity weight runs on the B200 path (diagonal/SPD "
-                   "weights are out of scope, SURVEY.md §8(f1))");
+    if (!(cfg->weight_kind == RBD_WEIGHT_DIAGONAL && diag_supplied))
+      return set_err(RBD_ERR_INVALID_ARGUMENT,
+                     cfg->weight_kind == RBD_WEIGHT_DIAGONAL
+                         ? "decompose: a diagonal weight runs through rbd_decompose_diag_*"
+                         : "decompose: sparse SPD weights are out of scope on the B200 path "
+                           "(SURVEY.md §8(f1))");
   }
   if (!hs.flags_nonzero)
     return set_err(RBD_ERR_DEGENERATE_INPUT, "decompose: zero matrix, no basis can be built");
@@ -701,6 +798,8 @@ int rbd_ctx_destroy(rbd_ctx_t ctx) {
                   &ctx->resid,   &ctx->w,    &ctx->c,       &ctx->p,     &ctx->nrm,
                   &ctx->hist,    &ctx->sel,  &ctx->out_rec, &ctx->scratch1,
                   &ctx->hX,      &ctx->hY,   &ctx->hT,      &ctx->ppart, &ctx->bar,
+                  &ctx->wd_axi,  &ctx->wd_yy, &ctx->wd_part2, &ctx->wd_yrow, &ctx->wd_yax,
+                  &ctx->wd_cross, &ctx->wd_quad, &ctx->wd_colsq, &ctx->wd_diag,
                   &ctx->ctl,     &ctx->gcnt, &ctx->ygcnt,   &ctx->rdy,   &ctx->send,  &ctx->recv};
   for (DevBuf* b : bl) release(*b);
   if (ctx->h_state) cudaFreeHost(ctx->h_state);
@@ -726,9 +825,13 @@ int rbd_ctx_synchronize(rbd_ctx_t ctx) {
 
 void* rbd_ctx_stream(rbd_ctx_t ctx) { return ctx ? (void*)ctx->stream : nullptr; }
 
-int rbd_decompose_device(rbd_ctx_t ctx, const double* dX, int64_t m, int64_t n, int64_t ldx,
-                         const rbd_config_t* cfg, double* dY, double* dT, int64_t* h_selected,
-                         double* h_history, rbd_result_t* result) {
+namespace {
+// Single-GPU decompose; diag == nullptr: identity weight (persistent loop),
+// else the diagonal-weight loop of rbd_weighted.cuh (diag: m device doubles,
+// already validated as a WeightSpec::diagonal).
+int decompose_device_impl(rbd_ctx_t ctx, const double* dX, int64_t m, int64_t n, int64_t ldx,
+                          const rbd_config_t* cfg, const double* diag, double* dY, double* dT,
+                          int64_t* h_selected, double* h_history, rbd_result_t* result) {
   if (!ctx || !cfg) return set_err(RBD_ERR_INVALID_ARGUMENT, "decompose: null context/config");
   if (m < 1 || n < 1) return set_err(RBD_ERR_INVALID_ARGUMENT, "decompose: matrix must be non-empty");
   if (ldx < m) return set_err(RBD_ERR_DIMENSION_MISMATCH, "decompose: ldx < m");
@@ -755,6 +858,12 @@ int rbd_decompose_device(rbd_ctx_t ctx, const double* dX, int64_t m, int64_t n, 
   CU(cudaEventRecord(ev0, ctx->stream));
   TRY(enqueue_init(ctx, dX, m, n, ldx, ptr<double>(ctx->partial), ptr<double>(ctx->colsq),
                    ptr<double>(ctx->resid), st));
+  if (diag) {   // workspace_init, diagonal kind (workspace.cpp:24-29)
+    TRY(ensure(ctx->wd_colsq, sizeof(double) * n));
+    const int g = (int)std::max<long long>(1, std::min<long long>(n, (long long)ctx->nsm * 8));
+    k_colsq_diag<<<g, kThreads, 0, ctx->stream>>>(dX, ldx, m, n, diag, ptr<double>(ctx->wd_colsq));
+    ctx->launches++;
+  }
   CU(cudaEventRecord(ev1, ctx->stream));
   CU(cudaMemsetAsync(ctx->counter.p, 0, 64, ctx->stream));
   CU(cudaMemcpyAsync(ctx->h_state, st, sizeof(DevState), cudaMemcpyDeviceToHost, ctx->stream));
@@ -766,7 +875,7 @@ int rbd_decompose_device(rbd_ctx_t ctx, const double* dX, int64_t m, int64_t n, 
     cudaEventElapsedTime(&t, ev0, ev1);
     init_ms = t;
   }
-  TRY(validate_after_init(cfg, m, n, hs));
+  TRY(validate_after_init(cfg, m, n, hs, diag != nullptr));
   double max_colsq;
   {
     unsigned long long b = hs.max_colsq_bits;
@@ -792,7 +901,44 @@ int rbd_decompose_device(rbd_ctx_t ctx, const double* dX, int64_t m, int64_t n, 
   CU(cudaMemcpyAsync(st, ctx->h_state, sizeof(DevState), cudaMemcpyHostToDevice, ctx->stream));
 
   LoopBufs L{dX, m, n, ldx, cfg->d_max, dY, dT};
-  if (ctx->path == 0 && use_fused(cfg->d_max)) {
+  if (diag) {
+    const long long S = cdiv(m, kChunk);
+    TRY(ensure(ctx->wd_axi, sizeof(double) * m));
+    TRY(ensure(ctx->wd_yy, sizeof(double) * diag_vec_grid(ctx, m)));
+    TRY(ensure(ctx->wd_part2, sizeof(double) * S * n));
+    TRY(ensure(ctx->wd_yrow, sizeof(double) * d_cap));
+    TRY(ensure(ctx->wd_yax, sizeof(double) * d_cap * n));
+    TRY(ensure(ctx->wd_cross, sizeof(double) * n));
+    TRY(ensure(ctx->wd_quad, sizeof(double) * n));
+    TRY(ensure(ctx->ppart, sizeof(double) * S * d_cap));
+    CU(cudaMemsetAsync(ctx->wd_cross.p, 0, sizeof(double) * n, ctx->stream));
+    CU(cudaMemsetAsync(ctx->wd_quad.p, 0, sizeof(double) * n, ctx->stream));
+    CU(cudaEventRecord(ev1, ctx->stream));
+    // host-driven steps; the done flag is polled every kDiagPoll steps, one
+    // batch behind, so the device never waits for the host
+    constexpr long long kDiagPoll = 8;
+    volatile int* hdone = &ctx->h_state->done;
+    bool pending = false;
+    cudaEvent_t ev;
+    CU(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    int rc = RBD_OK;
+    for (long long step = 0; step < cfg->d_max && rc == RBD_OK; ++step) {
+      rc = enqueue_step_diag(ctx, L, diag);
+      if (rc != RBD_OK) break;
+      if ((step + 1) % kDiagPoll == 0) {
+        if (pending) {
+          cudaEventSynchronize(ev);
+          if (*hdone) break;
+        }
+        cudaMemcpyAsync((void*)&ctx->h_state->done, &st->done, sizeof(int), cudaMemcpyDeviceToHost,
+                        ctx->stream);
+        cudaEventRecord(ev, ctx->stream);
+        pending = true;
+      }
+    }
+    cudaEventDestroy(ev);
+    if (rc != RBD_OK) return rc;
+  } else if (ctx->path == 0 && use_fused(cfg->d_max)) {
     CU(cudaEventRecord(ev1, ctx->stream));
     TRY(launch_persistent(ctx, L));
   } else {
@@ -854,9 +1000,54 @@ int rbd_decompose_device(rbd_ctx_t ctx, const double* dX, int64_t m, int64_t n, 
   return RBD_OK;
 }
 
-int rbd_decompose_host(rbd_ctx_t ctx, const double* hX, int64_t m, int64_t n, int64_t ldx,
-                       const rbd_config_t* cfg, double* hY, double* hT, int64_t* h_selected,
-                       double* h_history, rbd_result_t* result) {
+// WeightSpec::diagonal validation (weight.cpp:11-17) on host values.
+int check_diagonal(const double* h, int64_t len) {
+  if (len <= 0) return set_err(RBD_ERR_INVALID_ARGUMENT, "diagonal weight must be non-empty");
+  for (int64_t i = 0; i < len; ++i)
+    if (!(h[i] > 0.0) || !std::isfinite(h[i]))
+      return set_err(RBD_ERR_INVALID_ARGUMENT,
+                     "diagonal weight entries must be strictly positive and finite");
+  return RBD_OK;
+}
+}  // namespace
+
+int rbd_decompose_device(rbd_ctx_t ctx, const double* dX, int64_t m, int64_t n, int64_t ldx,
+                         const rbd_config_t* cfg, double* dY, double* dT, int64_t* h_selected,
+                         double* h_history, rbd_result_t* result) {
+  return decompose_device_impl(ctx, dX, m, n, ldx, cfg, nullptr, dY, dT, h_selected, h_history,
+                               result);
+}
+
+int rbd_decompose_diag_device(rbd_ctx_t ctx, const double* dX, int64_t m, int64_t n, int64_t ldx,
+                              const rbd_config_t* cfg, const double* d_diag, int64_t diag_len,
+                              double* dY, double* dT, int64_t* h_selected, double* h_history,
+                              rbd_result_t* result) {
+  if (!ctx || !cfg) return set_err(RBD_ERR_INVALID_ARGUMENT, "decompose: null context/config");
+  if (diag_len > 0 && !d_diag) return set_err(RBD_ERR_INVALID_ARGUMENT, "decompose: null diagonal");
+  CU(cudaSetDevice(ctx->device));
+  std::vector<double> h((size_t)std::max<int64_t>(diag_len, 0));
+  if (diag_len > 0) {   // on the context stream: d_diag may have been uploaded there
+    CU(cudaMemcpyAsync(h.data(), d_diag, sizeof(double) * diag_len, cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+  }
+  TRY(check_diagonal(h.data(), diag_len));
+  rbd_config_t c = *cfg;
+  c.weight_kind = RBD_WEIGHT_DIAGONAL;
+  c.weight_dim = diag_len;
+  if (diag_len != m) {   // decompose.cpp:61-62 order: checked after init, before the zero test
+    return decompose_device_impl(ctx, dX, m, n, ldx, &c, nullptr, dY, dT, h_selected, h_history,
+                                 result);
+  }
+  return decompose_device_impl(ctx, dX, m, n, ldx, &c, d_diag, dY, dT, h_selected, h_history,
+                               result);
+}
+
+namespace {
+int decompose_host_impl(rbd_ctx_t ctx, const double* hX, int64_t m, int64_t n, int64_t ldx,
+                        const rbd_config_t* cfg, const double* h_diag, int64_t diag_len,
+                        double* hY, double* hT, int64_t* h_selected, double* h_history,
+                        rbd_result_t* result) {
   if (!ctx || !cfg) return set_err(RBD_ERR_INVALID_ARGUMENT, "decompose: null context/config");
   if (m < 1 || n < 1) return set_err(RBD_ERR_INVALID_ARGUMENT, "decompose: matrix must be non-empty");
   if (ldx < m) return set_err(RBD_ERR_DIMENSION_MISMATCH, "decompose: ldx < m");
@@ -873,7 +1064,17 @@ int rbd_decompose_host(rbd_ctx_t ctx, const double* hX, int64_t m, int64_t n, in
                                     sizeof(double) * m, n, cudaMemcpyHostToDevice, ctx->stream);
   if (e != cudaSuccess) return set_err(RBD_ERR_CUDA, std::string("H2D X: ") + cudaGetErrorString(e));
   rbd_result_t r{};
-  int rc = rbd_decompose_device(ctx, dX, m, n, ldd, cfg, dY, dT, h_selected, h_history, &r);
+  int rc;
+  if (h_diag || diag_len != 0) {
+    TRY(check_diagonal(h_diag, diag_len));
+    TRY(ensure(ctx->wd_diag, sizeof(double) * diag_len));
+    CU(cudaMemcpyAsync(ctx->wd_diag.p, h_diag, sizeof(double) * diag_len, cudaMemcpyHostToDevice,
+                       ctx->stream));
+    rc = rbd_decompose_diag_device(ctx, dX, m, n, ldd, cfg, ptr<double>(ctx->wd_diag), diag_len,
+                                   dY, dT, h_selected, h_history, &r);
+  } else {
+    rc = rbd_decompose_device(ctx, dX, m, n, ldd, cfg, dY, dT, h_selected, h_history, &r);
+  }
   // dY was allocated with d_cap columns; the device call writes at most d_cap
   if (rc == RBD_OK) {
     if (hY) e = cudaMemcpyAsync(hY, dY, sizeof(double) * m * r.d, cudaMemcpyDeviceToHost, ctx->stream);
@@ -884,6 +1085,25 @@ int rbd_decompose_host(rbd_ctx_t ctx, const double* hX, int64_t m, int64_t n, in
     if (result) *result = r;
   }
   return rc;
+}
+
+}  // namespace
+
+int rbd_decompose_host(rbd_ctx_t ctx, const double* hX, int64_t m, int64_t n, int64_t ldx,
+                       const rbd_config_t* cfg, double* hY, double* hT, int64_t* h_selected,
+                       double* h_history, rbd_result_t* result) {
+  return decompose_host_impl(ctx, hX, m, n, ldx, cfg, nullptr, 0, hY, hT, h_selected, h_history,
+                             result);
+}
+
+int rbd_decompose_diag_host(rbd_ctx_t ctx, const double* hX, int64_t m, int64_t n, int64_t ldx,
+                            const rbd_config_t* cfg, const double* h_diag, int64_t diag_len,
+                            double* hY, double* hT, int64_t* h_selected, double* h_history,
+                            rbd_result_t* result) {
+  if (!h_diag && diag_len > 0) return set_err(RBD_ERR_INVALID_ARGUMENT, "decompose: null diagonal");
+  if (diag_len <= 0) return set_err(RBD_ERR_INVALID_ARGUMENT, "diagonal weight must be non-empty");
+  return decompose_host_impl(ctx, hX, m, n, ldx, cfg, h_diag, diag_len, hY, hT, h_selected,
+                             h_history, result);
 }
 
 int rbd_mgs_project(rbd_ctx_t ctx, const double* dv, int64_t m, const double* dB, int64_t k,
@@ -1410,7 +1630,8 @@ int sharded_decompose(std::vector<rbd_ctx_t>& R, Exchange& ex, std::vector<Shard
     CU(cudaStreamSynchronize(c->stream));
     double head[4] = {(double)c->h_state->flags_nonfinite, (double)c->h_state->flags_nonzero, 0.0, 0.0};
     std::memcpy(&head[2], &c->h_state->max_colsq_bits, sizeof(double));
-    CU(cudaMemcpy(c->send.p, head, sizeof(head), cudaMemcpyHostToDevice));
+    CU(cudaMemcpyAsync(c->send.p, head, sizeof(head), cudaMemcpyHostToDevice, c->stream));
+    CU(cudaStreamSynchronize(c->stream));   // head is a stack buffer
   }
   TRY(ex.allgather(R, 4));
   std::vector<double> all(4 * (size_t)ex.world());
@@ -1652,7 +1873,10 @@ int rbd_ws_extend_host(rbd_ws_t ws, const double* hxi) {
   if (!ws) return set_err(RBD_ERR_INVALID_ARGUMENT, "null workspace");
   DevBuf b;
   TRY(ensure(b, sizeof(double) * ws->m));
-  if (cudaMemcpy(b.p, hxi, sizeof(double) * ws->m, cudaMemcpyHostToDevice) != cudaSuccess) {
+  // on the workspace's stream (a pageable-source cudaMemcpy may return before its
+  // DMA lands, and the context stream does not wait for the legacy stream)
+  if (cudaMemcpyAsync(b.p, hxi, sizeof(double) * ws->m, cudaMemcpyHostToDevice,
+                      ws->ctx->stream) != cudaSuccess) {
     release(b);
     return set_err(RBD_ERR_CUDA, "workspace_extend: H2D failed");
   }

@@ -463,6 +463,9 @@ __device__ void finalize_state(const FinalizeArgs& a, double best, long long arg
   st->done = !((k + 1) < st->d_max && e_cur > st->eps_R) ? 1 : 0;  // :87
 }
 
+__device__ __forceinline__ void finalize_reduce_tail(const FinalizeArgs& a, long long k, double bv,
+                                                     long long bj, Rec* smr, int* is_last_s);
+
 __global__ void __launch_bounds__(kThreads) k_finalize(FinalizeArgs a) {
   if (a.mode != 1 && a.st->done) return;
   __shared__ Rec smr[kWarps];
@@ -487,6 +490,15 @@ __global__ void __launch_bounds__(kThreads) k_finalize(FinalizeArgs a) {
     }
   }
   if (a.mode == 1) return;
+  finalize_reduce_tail(a, k, bv, bj, smr, &is_last);
+}
+
+// Shared tail of K3 (mode 0/2): the CTA record, the last CTA's global argmax,
+// then (mode 0) the state update and the next step's coefficients.
+__device__ __forceinline__ void finalize_reduce_tail(const FinalizeArgs& a, long long k, double bv,
+                                                     long long bj, Rec* smr, int* is_last_s) {
+  int& is_last = *is_last_s;
+  const long long n = a.n;
   __threadfence();  // publish this CTA's T/r writes before the done-counter
   block_argmax<kThreads>(bv, bj, smr);
   if (threadIdx.x == 0) {

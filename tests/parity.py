@@ -15,6 +15,10 @@
             running residual bookkeeping col_sq - sum t^2 cancels, so the error
             scales with col_sq, not with e_k^2; cf. acceptance.cpp:223,
             test_workspace.cpp:91)
+* diagonal weight: selection follows the A-norm residual
+  e2_j = ||x_j - Y T_j||_A^2, so near ties and the history bound use those
+  residuals (computed directly from the oracle's Y and T) and max col_sq_A;
+  kappa_k stays Euclidean (the orthogonalisation is Euclidean).
 """
 from __future__ import annotations
 
@@ -32,6 +36,17 @@ def running_residuals(X: np.ndarray, T: np.ndarray):
     return col_sq, out
 
 
+def weighted_residuals(X: np.ndarray, Y: np.ndarray, T: np.ndarray, diag: np.ndarray):
+    """Oracle-side A-norm residuals after each step (workspace.cpp:84-99 evaluated
+    directly: ||x_j - Y_k T_k[:, j]||_A^2)."""
+    col_sq = np.einsum("ij,i,ij->j", X, diag, X)
+    out = []
+    for k in range(T.shape[0]):
+        R = X - Y[:, : k + 1] @ T[: k + 1]
+        out.append(np.maximum(np.einsum("ij,i,ij->j", R, diag, R), 0.0))
+    return col_sq, out
+
+
 def top2_gap(r: np.ndarray) -> float:
     if r.size < 2:
         return np.inf
@@ -39,20 +54,25 @@ def top2_gap(r: np.ndarray) -> float:
     return float(abs(a[1] - a[0]))
 
 
-def compare(gpu, ref, X, tol: float = 1e-10, tau: float = 1e-12, require_same_d: bool = True):
+def compare(gpu, ref, X, tol: float = 1e-10, tau: float = 1e-12, require_same_d: bool = True,
+            diag=None):
     """Returns the number of steps compared; raises AssertionError on mismatch."""
     X = np.asarray(X, dtype=np.float64)
     gY = np.asarray(gpu.Y.cpu() if hasattr(gpu.Y, "cpu") else gpu.Y)
     gT = np.asarray(gpu.T.cpu() if hasattr(gpu.T, "cpu") else gpu.T)
     col_sq, rsteps = running_residuals(X, ref.T)
-    max_colsq = float(col_sq.max())
     colnorm = np.sqrt(col_sq)
+    if diag is None:
+        sel_sq, ssteps = col_sq, rsteps
+    else:
+        sel_sq, ssteps = weighted_residuals(X, ref.Y, ref.T, np.asarray(diag, dtype=np.float64))
+    max_colsq = float(sel_sq.max())
     d_cmp = min(gpu.d, ref.d)
     upto = d_cmp
     for k in range(d_cmp):
         if gpu.selected[k] != ref.selected[k]:
             assert k > 0, f"start column differs: {gpu.selected[0]} vs {ref.selected[0]}"
-            gap = top2_gap(rsteps[k - 1])
+            gap = top2_gap(ssteps[k - 1])
             assert gap <= tau * max_colsq, (
                 f"selected diverges at step {k}: gpu {gpu.selected[k]} ref {ref.selected[k]}, "
                 f"top-two gap {gap:.3e} > {tau * max_colsq:.3e}")
