@@ -422,7 +422,9 @@ int enqueue_step_diag(rbd_ctx_t ctx, const LoopBufs& L, const double* diag) {
   f.cross = ptr<double>(ctx->wd_cross);
   f.quad = ptr<double>(ctx->wd_quad);
   f.colsq_a = ptr<double>(ctx->wd_colsq);
-  k_finalize_diag<<<finalize_grid(ctx, L.n), kThreads, 0, ctx->stream>>>(f);
+  const int gf = (int)std::max<long long>(
+      1, std::min<long long>(cdiv(L.n, kFdCols), (long long)ctx->nsm * 4));
+  k_finalize_diag<<<gf, kThreads, 0, ctx->stream>>>(f);
   ctx->launches++;
   CU(cudaGetLastError());
   return RBD_OK;

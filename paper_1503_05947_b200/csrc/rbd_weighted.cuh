@@ -59,9 +59,114 @@ __global__ void __launch_bounds__(kThreads) k_diag_vec(const double* __restrict_
   if (threadIdx.x == 0) yy_part[blockIdx.x] = acc;
 }
 
-// One X pass for both new rows: partial[s][j] = xi . x_j over chunk s (T row,
-// decompose.cpp:93) and partial2[s][j] = (A xi) . x_j (YAX row, workspace.cpp:66).
-// The tile is swept twice back to back; the second sweep reads it from L2.
+// Two dot products per column in one pass over a (chunk, 4-column) tile:
+//   partial[s][j] = v . x_j,  partial2[s][j] = v2 . x_j  over the rows of chunk s.
+// Same thread -> row layout, per-thread fma order (groups ascending, .x then
+// .y) and reduction tree as sweep_tiles<VEC, MODE_DOT>, so `partial` is
+// bit-identical to the identity sweep's; out-of-range rows load 0.
+template <int VEC>
+__device__ __forceinline__ void sweep_tile_dot2(const double* __restrict__ A, long long lda,
+                                                long long m, long long ncols,
+                                                const double* __restrict__ v,
+                                                const double* __restrict__ v2,
+                                                double* __restrict__ partial,
+                                                double* __restrict__ partial2, long long pstride,
+                                                long long tile, double (*red)[2 * kCols]) {
+  const long long G = (ncols + kCols - 1) / kCols;
+  const long long s = tile / G;
+  const long long g = tile - s * G;
+  const long long row0 = s * kChunk;
+  const long long col0 = g * kCols;
+  const long long rows = (m - row0 < kChunk) ? m - row0 : kChunk;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int U = kChunk / (VEC * kThreads);
+  constexpr int UB = 2;
+  double acc[kCols], acc2[kCols];
+  const double* Ac[kCols];
+#pragma unroll
+  for (int c = 0; c < kCols; ++c) {
+    acc[c] = acc2[c] = 0.0;
+    const long long cc = (col0 + c < ncols) ? col0 + c : col0;   // clamp (result unused)
+    Ac[c] = A + cc * lda + row0;
+  }
+  const double* vr = v + row0;
+  const double* wr = v2 + row0;
+#pragma unroll 1
+  for (int ub = 0; ub < U; ub += UB) {
+    if ((long long)ub * VEC * kThreads >= rows) break;
+    double xv[UB][kCols][VEC], yv[UB][VEC], zv[UB][VEC];
+#pragma unroll
+    for (int u = 0; u < UB; ++u) {
+      const long long e = (long long)(tid + (ub + u) * kThreads) * VEC;
+      if (e + VEC <= rows) {
+        if constexpr (VEC == 2) {
+          const double2 y2 = ld_keep2(vr + e), z2 = ld_keep2(wr + e);
+          yv[u][0] = y2.x;
+          yv[u][VEC - 1] = y2.y;
+          zv[u][0] = z2.x;
+          zv[u][VEC - 1] = z2.y;
+#pragma unroll
+          for (int c = 0; c < kCols; ++c) {
+            const double2 x2 = ld_stream2(Ac[c] + e);
+            xv[u][c][0] = x2.x;
+            xv[u][c][VEC - 1] = x2.y;
+          }
+        } else {
+          yv[u][0] = ld_keep1(vr + e);
+          zv[u][0] = ld_keep1(wr + e);
+#pragma unroll
+          for (int c = 0; c < kCols; ++c) xv[u][c][0] = ld_stream1(Ac[c] + e);
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < VEC; ++q) {
+          const bool in = e + q < rows;
+          yv[u][q] = in ? __ldg(vr + e + q) : 0.0;
+          zv[u][q] = in ? __ldg(wr + e + q) : 0.0;
+#pragma unroll
+          for (int c = 0; c < kCols; ++c) xv[u][c][q] = in ? __ldcs(Ac[c] + e + q) : 0.0;
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < UB; ++u)
+#pragma unroll
+      for (int c = 0; c < kCols; ++c)
+#pragma unroll
+        for (int q = 0; q < VEC; ++q) {
+          acc[c] = fma(xv[u][c][q], yv[u][q], acc[c]);
+          acc2[c] = fma(xv[u][c][q], zv[u][q], acc2[c]);
+        }
+  }
+#pragma unroll
+  for (int c = 0; c < kCols; ++c)
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], off);
+      acc2[c] += __shfl_xor_sync(0xffffffffu, acc2[c], off);
+    }
+  if (lane == 0) {
+#pragma unroll
+    for (int c = 0; c < kCols; ++c) {
+      red[warp][c] = acc[c];
+      red[warp][kCols + c] = acc2[c];
+    }
+  }
+  __syncthreads();
+  if (tid < 2 * kCols) {
+    const int c = tid % kCols;
+    if (col0 + c < ncols) {
+      double sum = red[0][tid];
+#pragma unroll
+      for (int w = 1; w < kWarps; ++w) sum += red[w][tid];
+      (tid < kCols ? partial : partial2)[s * pstride + col0 + c] = sum;
+    }
+  }
+  __syncthreads();
+}
+
+// One X pass for both new rows: T row partials (xi . x_j, decompose.cpp:93) and
+// YAX row partials ((A xi) . x_j, workspace.cpp:66).
 template <int VEC>
 __global__ void __launch_bounds__(kThreads, 2) k_sweep_diag(const double* __restrict__ X,
                                                             long long ldx, long long m, long long n,
@@ -71,14 +176,11 @@ __global__ void __launch_bounds__(kThreads, 2) k_sweep_diag(const double* __rest
                                                             double* __restrict__ partial2,
                                                             const DevState* st) {
   if (st->done) return;
-  __shared__ double red[kWarps][kCols];
-  unsigned nf = 0, nz = 0;
+  __shared__ double red[kWarps][2 * kCols];
   const double* xi = Y + st->d * m;
   const long long ntiles = ((m + kChunk - 1) / kChunk) * ((n + kCols - 1) / kCols);
-  for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    sweep_tiles<VEC, MODE_DOT, LOAD_NC>(X, ldx, m, n, xi, partial, n, t, 1LL << 40, red, nf, nz);
-    sweep_tiles<VEC, MODE_DOT, LOAD_NC>(X, ldx, m, n, axi, partial2, n, t, 1LL << 40, red, nf, nz);
-  }
+  for (long long t = blockIdx.x; t < ntiles; t += gridDim.x)
+    sweep_tile_dot2<VEC>(X, ldx, m, n, xi, axi, partial, partial2, n, t, red);
 }
 
 struct FinalizeDiagArgs {
@@ -96,44 +198,70 @@ struct FinalizeDiagArgs {
 // K3 with a diagonal weight: new T and YAX rows, the carried cross/quad sums,
 // e2_j = max(col_sq_A - 2 cross + quad, 0) (workspace.cpp:88-97), the argmax
 // with smallest-index ties (workspace.cpp:114-122) and the stop test.
+// CTA = 32 columns; g_j = YAY[d,0:d] . T[0:d,j] is split over the 8 warps
+// (l = warp, warp+8, ...; coalesced T rows) and combined in warp order.
+constexpr int kFdCols = 32;
 __global__ void __launch_bounds__(kThreads) k_finalize_diag(FinalizeDiagArgs a) {
   const FinalizeArgs& f = a.f;
   if (f.st->done) return;
   __shared__ Rec smr[kWarps];
   __shared__ int is_last;
   __shared__ double yydd_s;
+  __shared__ double gpart[kWarps][kFdCols];
   const long long n = f.n;
   const long long k = f.st->d;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) {
     double s = 0.0;
     for (int b = 0; b < a.yy_np; ++b) s += a.yy_part[b];
     yydd_s = s;
   }
-  __syncthreads();
-  const double yydd = yydd_s;
   double bv = -1.0;  // workspace.cpp:105
   long long bj = 0x7fffffffffffffffLL;
-  for (long long j = blockIdx.x * (long long)kThreads + threadIdx.x; j < n;
-       j += (long long)gridDim.x * kThreads) {
-    double t = 0.0, ya = 0.0;
-    for (long long s = 0; s < f.S; ++s) {
-      t += f.partial[s * n + j];
-      ya += a.partial2[s * n + j];
+  const long long nb = (n + kFdCols - 1) / kFdCols;
+  for (long long blk = blockIdx.x; blk < nb; blk += gridDim.x) {
+    const long long j = blk * kFdCols + lane;
+    const bool col = j < n;
+    double gp = 0.0;
+    if (col) {
+      long long l = warp;
+      for (; l + 3 * kWarps < k; l += 4 * kWarps) {   // 4 loads in flight per lane
+        const double t0 = __ldcg(&f.T[l * n + j]), t1 = __ldcg(&f.T[(l + kWarps) * n + j]);
+        const double t2 = __ldcg(&f.T[(l + 2 * kWarps) * n + j]);
+        const double t3 = __ldcg(&f.T[(l + 3 * kWarps) * n + j]);
+        gp = fma(a.yrow[l], t0, gp);
+        gp = fma(a.yrow[l + kWarps], t1, gp);
+        gp = fma(a.yrow[l + 2 * kWarps], t2, gp);
+        gp = fma(a.yrow[l + 3 * kWarps], t3, gp);
+      }
+      for (; l < k; l += kWarps) gp = fma(a.yrow[l], __ldcg(&f.T[l * n + j]), gp);
     }
-    f.T[k * n + j] = t;
-    a.YAX[k * n + j] = ya;
-    double g = 0.0;
-    for (long long l = 0; l < k; ++l) g = fma(a.yrow[l], f.T[l * n + j], g);
-    const double cr = a.cross[j] + t * ya;
-    const double qd = a.quad[j] + (2.0 * t * g + yydd * t * t);
-    a.cross[j] = cr;
-    a.quad[j] = qd;
-    double e2 = a.colsq_a[j] - 2.0 * cr + qd;
-    e2 = e2 > 0.0 ? e2 : 0.0;
-    if (rec_better(e2, j, bv, bj)) {
-      bv = e2;
-      bj = j;
+    gpart[warp][lane] = gp;
+    __syncthreads();
+    if (warp == 0 && col) {
+      double g = gpart[0][lane];
+#pragma unroll
+      for (int w = 1; w < kWarps; ++w) g += gpart[w][lane];
+      double t = 0.0, ya = 0.0;
+      for (long long s = 0; s < f.S; ++s) {
+        t += f.partial[s * n + j];
+        ya += a.partial2[s * n + j];
+      }
+      f.T[k * n + j] = t;
+      a.YAX[k * n + j] = ya;
+      const double yydd = yydd_s;
+      const double cr = a.cross[j] + t * ya;
+      const double qd = a.quad[j] + (2.0 * t * g + yydd * t * t);
+      a.cross[j] = cr;
+      a.quad[j] = qd;
+      double e2 = a.colsq_a[j] - 2.0 * cr + qd;
+      e2 = e2 > 0.0 ? e2 : 0.0;
+      if (rec_better(e2, j, bv, bj)) {
+        bv = e2;
+        bj = j;
+      }
     }
+    __syncthreads();
   }
   finalize_reduce_tail(f, k, bv, bj, smr, &is_last);
 }
