@@ -96,8 +96,15 @@ inline RbdModel decompose(const Matrix& x, const RbdConfig& cfg) {
   std::vector<int64_t> sel(static_cast<size_t>(cap));
   std::vector<double> hist(static_cast<size_t>(cap));
   rbd_result_t r{};
-  detail::check(rbd_decompose_host(detail::context(), x.data(), m, n, std::max<Index>(m, 1), &c,
-                                   Yb.data(), Tb.data(), sel.data(), hist.data(), &r));
+  if (cfg.weight.kind() == WeightKind::diagonal) {
+    const Vector& dg = cfg.weight.diagonal_values();
+    detail::check(rbd_decompose_diag_host(detail::context(), x.data(), m, n,
+                                          std::max<Index>(m, 1), &c, dg.data(), dg.size(),
+                                          Yb.data(), Tb.data(), sel.data(), hist.data(), &r));
+  } else {
+    detail::check(rbd_decompose_host(detail::context(), x.data(), m, n, std::max<Index>(m, 1),
+                                     &c, Yb.data(), Tb.data(), sel.data(), hist.data(), &r));
+  }
   RbdModel model;
   model.d = r.d;
   model.weight = cfg.weight;

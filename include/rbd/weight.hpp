@@ -23,14 +23,26 @@ class WeightSpec {
     w.diag_ = std::move(d);
     return w;
   }
+  // marker for a model whose sparse SPD weight lives outside the model file
+  // (weight.hpp:26-28); carries the kind only
+  static WeightSpec sparse_external() {
+    WeightSpec w;
+    w.kind_ = WeightKind::sparse_spd;
+    w.external_ = true;
+    return w;
+  }
   WeightKind kind() const { return kind_; }
-  Index dim() const { return kind_ == WeightKind::identity ? 0 : diag_.size(); }
-  bool compatible_with(Index m) const { return kind_ == WeightKind::identity || dim() == m; }
+  Index dim() const { return kind_ == WeightKind::diagonal ? diag_.size() : 0; }
+  bool compatible_with(Index m) const {
+    return kind_ == WeightKind::identity || external_ || dim() == m;
+  }
+  bool evaluable() const { return !external_; }
   const Vector& diagonal_values() const { return diag_; }
 
  private:
   WeightKind kind_ = WeightKind::identity;
   Vector diag_;
+  bool external_ = false;
 };
 
 }  // namespace rbd

@@ -45,6 +45,9 @@ typedef enum {
   RBD_ERR_DIMENSION_MISMATCH = 5, /* rbd::DimensionMismatch errors.hpp:15-18 */
   RBD_ERR_NOT_POSITIVE = 6,       /* rbd::NotPositive       errors.hpp:33-36 */
   RBD_ERR_NO_CONVERGENCE = 7,     /* rbd::NoConvergence     errors.hpp:45-48 */
+  RBD_ERR_UNSUPPORTED_FORMAT = 8, /* rbd::UnsupportedFormat errors.hpp:54-57 */
+  RBD_ERR_IO = 9,                 /* rbd::IoError           errors.hpp:59-62 */
+  RBD_ERR_PARSE = 10,             /* rbd::ParseError        errors.hpp:64-77 ("path:line: what") */
   RBD_ERR_CUDA = 100,             /* CUDA runtime failure (maps to rbd::Error) */
   RBD_ERR_NCCL = 101,             /* NCCL failure (maps to rbd::Error) */
   RBD_ERR_OUT_OF_MEMORY = 102     /* device allocation failure (maps to rbd::Error) */
@@ -213,6 +216,26 @@ int rbd_decompose_sharded_virtual(rbd_ctx_t ctx, int nranks, const double* const
                                   const rbd_config_t* cfg, double* const* dY_ranks,
                                   double* const* dT_ranks, int64_t* h_selected, double* h_history,
                                   rbd_result_t* result);
+
+/* ---- RBD1 model container (io.cpp:527-622, io.hpp:51-64) ----
+ * Layout (little-endian): "RBD1" | u64 m, n, d | u8 weight tag | f64 Y (m x d,
+ * column-major) | f64 T (d x n, row-major) | f64 eps_R | f64 history[d] |
+ * (tag 1) f64 diag[m]; 29-byte header. Y and T may be device or host pointers
+ * (device data streams through pinned double buffers on the context stream;
+ * ctx may be NULL for host-only use). history (and diag on write) are host
+ * arrays; diag may also be device memory. Writes are atomic (path + ".tmp",
+ * then rename, io.cpp:60-73). Errors: IoError (cannot open / write / rename),
+ * ParseError "path:0: what" (bad magic, implausible dimensions, unknown tag,
+ * size mismatch, truncation), DimensionMismatch for inconsistent shapes. */
+int rbd_model_write(rbd_ctx_t ctx, const char* path, int64_t m, int64_t n, int64_t d,
+                    const double* Y, int64_t ldy, const double* T, double eps_r,
+                    const double* h_history, int weight_kind, const double* h_diag);
+/* Validates the header and the file size (io.cpp:577-596) and returns the shape. */
+int rbd_model_read_header(const char* path, int64_t* m, int64_t* n, int64_t* d, int* weight_kind);
+/* Reads a validated file into Y (ld ldy >= m), T (d x n row-major), eps_r,
+ * h_history[d] and (tag 1) h_diag[m]. */
+int rbd_model_read(rbd_ctx_t ctx, const char* path, double* Y, int64_t ldy, double* T,
+                   double* eps_r, double* h_history, double* h_diag);
 
 #ifdef __cplusplus
 }

@@ -274,3 +274,47 @@ def acceptance3_count() -> int:
 
 def seeded_start(seed: int, n: int) -> int:
     return int(lib().orc_seeded_start(int(seed) & 0xFFFFFFFFFFFFFFFF, int(n)))
+
+
+# ---- RBD1 model container, restated (proj/src/io.cpp:527-622, io.hpp:51-64) ----
+
+def model_bytes(Y, T, eps_r, history, tag=0, diag=None) -> bytes:
+    """write_model's byte stream (io.cpp:533-570): "RBD1", u64 m/n/d, u8 tag,
+    Y column-major, T row-major, eps_R, history, (tag 1) diag; little-endian."""
+    import struct
+    Y = np.asarray(Y, dtype=np.float64)
+    T = np.asarray(T, dtype=np.float64)
+    m, d = Y.shape
+    n = T.shape[1]
+    assert T.shape[0] == d, "write_model: inconsistent model shapes"     # io.cpp:537-538
+    out = [b"RBD1", struct.pack("<QQQB", m, n, d, tag),                    # :556-560
+           np.asarray(Y, dtype="<f8").tobytes(order="F"),                   # :561-562
+           np.asarray(T, dtype="<f8").tobytes(order="C"),                   # :563-564
+           struct.pack("<d", float(eps_r)),                                 # :565
+           np.asarray(history, dtype="<f8").tobytes()]                      # :566-567
+    if tag == 1:
+        out.append(np.asarray(diag, dtype="<f8").tobytes())                # :568-569
+    return b"".join(out)
+
+
+def parse_model(data: bytes):
+    """read_model (io.cpp:574-622): returns (Y, T, eps_r, history, tag, diag) or
+    raises ValueError with the reference's ParseError text."""
+    import struct
+    if len(data) < 29 or data[:4] != b"RBD1":
+        raise ValueError("not a model file (bad magic)")                    # :580-581
+    m, n, d, tag = struct.unpack_from("<QQQB", data, 4)
+    if m < 1 or n < 1 or d < 1 or d > n:
+        raise ValueError("implausible model dimensions")                    # :587-588
+    if tag > 2:
+        raise ValueError("unknown weight tag")                              # :590
+    expected = 29 + 8 * (m * d + d * n + 1 + d) + (8 * m if tag == 1 else 0)
+    if len(data) != expected:
+        raise ValueError("model file size does not match header")           # :592-596
+    f = np.frombuffer(data, dtype="<f8", offset=29)
+    Y = f[: m * d].reshape((m, d), order="F")
+    T = f[m * d: m * d + d * n].reshape((d, n))
+    eps_r = float(f[m * d + d * n])
+    hist = f[m * d + d * n + 1: m * d + d * n + 1 + d]
+    diag = f[m * d + d * n + 1 + d:] if tag == 1 else None
+    return Y, T, eps_r, hist, tag, diag

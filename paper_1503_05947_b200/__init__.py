@@ -5,14 +5,16 @@ A drop-in for the hot path of the reference (arXiv 1503.05947, proj/): the
 hand-written sm_100a CUDA kernels behind the C ABI ``include/rbd_cuda.h``.
 """
 from ._lib import (CudaError, DegenerateInput, DimensionMismatch, IncompatibleWeight,
-                   IndexOutOfRange, InvalidArgument, NoConvergence, NotPositive, RbdError,
-                   Context, default_context, load_library)
-from .api import (Model, Workspace, decompose, make_config, mgs_project, project, project_batch,
-                  project_batch_f32, reconstruct)
+                   IndexOutOfRange, InvalidArgument, IoError, NoConvergence, NotPositive,
+                   ParseError, RbdError, UnsupportedFormat, Context, default_context,
+                   load_library)
+from .api import (Model, Workspace, decompose, load, make_config, mgs_project, project,
+                  project_batch, project_batch_f32, reconstruct, save)
 
 __all__ = [
     "RbdError", "InvalidArgument", "IncompatibleWeight", "DegenerateInput", "IndexOutOfRange",
-    "DimensionMismatch", "NotPositive", "NoConvergence", "CudaError", "Context",
-    "default_context", "load_library", "Model", "Workspace", "decompose", "make_config",
-    "mgs_project", "project", "project_batch", "project_batch_f32", "reconstruct",
+    "DimensionMismatch", "NotPositive", "NoConvergence", "UnsupportedFormat", "IoError",
+    "ParseError", "CudaError", "Context", "default_context", "load_library", "Model",
+    "Workspace", "decompose", "load", "make_config", "mgs_project", "project", "project_batch",
+    "project_batch_f32", "reconstruct", "save",
 ]

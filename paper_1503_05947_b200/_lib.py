@@ -20,6 +20,9 @@ RBD_ERR_INDEX_OUT_OF_RANGE = 4
 RBD_ERR_DIMENSION_MISMATCH = 5
 RBD_ERR_NOT_POSITIVE = 6
 RBD_ERR_NO_CONVERGENCE = 7
+RBD_ERR_UNSUPPORTED_FORMAT = 8
+RBD_ERR_IO = 9
+RBD_ERR_PARSE = 10
 RBD_ERR_CUDA = 100
 RBD_ERR_NCCL = 101
 RBD_ERR_OUT_OF_MEMORY = 102
@@ -57,6 +60,18 @@ class NoConvergence(RbdError):
     pass
 
 
+class UnsupportedFormat(RbdError):
+    pass
+
+
+class IoError(RbdError):
+    pass
+
+
+class ParseError(RbdError):
+    """errors.hpp:64-77; the message is "path:line: what"."""
+
+
 class CudaError(RbdError):
     pass
 
@@ -69,6 +84,9 @@ _ERRORS = {
     RBD_ERR_DIMENSION_MISMATCH: DimensionMismatch,
     RBD_ERR_NOT_POSITIVE: NotPositive,
     RBD_ERR_NO_CONVERGENCE: NoConvergence,
+    RBD_ERR_UNSUPPORTED_FORMAT: UnsupportedFormat,
+    RBD_ERR_IO: IoError,
+    RBD_ERR_PARSE: ParseError,
 }
 
 
@@ -120,6 +138,11 @@ _SIGS = {
                                        C.POINTER(Result)]),
     "rbd_decompose_host": (C.c_int, [_P, _P, _I64, _I64, _I64, C.POINTER(Config), _P, _P, _P, _P,
                                      C.POINTER(Result)]),
+    "rbd_model_write": (C.c_int, [_P, C.c_char_p, _I64, _I64, _I64, _P, _I64, _P, C.c_double, _P,
+                                  C.c_int, _P]),
+    "rbd_model_read_header": (C.c_int, [C.c_char_p, C.POINTER(_I64), C.POINTER(_I64),
+                                        C.POINTER(_I64), C.POINTER(C.c_int)]),
+    "rbd_model_read": (C.c_int, [_P, C.c_char_p, _P, _I64, _P, C.POINTER(C.c_double), _P, _P]),
     "rbd_decompose_diag_device": (C.c_int, [_P, _P, _I64, _I64, _I64, C.POINTER(Config), _P, _I64,
                                             _P, _P, _P, _P, C.POINTER(Result)]),
     "rbd_decompose_diag_host": (C.c_int, [_P, _P, _I64, _I64, _I64, C.POINTER(Config), _P, _I64,

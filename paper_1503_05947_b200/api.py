@@ -9,6 +9,7 @@ through the device-resident entry points. There is no CPU compute path.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from typing import Optional
 
 import numpy as np
@@ -90,7 +91,8 @@ class Model:
     device calls); ``selected`` and ``residual_history`` are Python lists.
     """
 
-    def __init__(self, Y, T, d, selected, residual_history, result: Result, ctx: Context):
+    def __init__(self, Y, T, d, selected, residual_history, result: Result, ctx: Context,
+                 weight_kind: int = 0, diag=None):
         self._Y = Y
         self._T = T
         self.d = int(d)
@@ -98,6 +100,12 @@ class Model:
         self.residual_history = list(float(h) for h in residual_history)
         self.result = result
         self._ctx = ctx
+        # RbdModel::weight (decompose.hpp:45): 0 identity, 1 diagonal (values in
+        # `diag`, host numpy), 2 sparse SPD held externally (loaded models only)
+        self.weight_kind = int(weight_kind)
+        self.diag = None if diag is None else np.ascontiguousarray(
+            diag.detach().cpu().numpy() if hasattr(diag, "detach") else np.asarray(diag),
+            dtype=np.float64).reshape(-1)
 
     @property
     def Y(self):
@@ -118,6 +126,11 @@ class Model:
     def reconstruct(self, c):
         """Y c (decompose.cpp:119-123)."""
         return reconstruct(self, c)
+
+    def save(self, path, eps_r: float = 0.0):
+        """Model.save (bindings.cpp:63-67) -> write_model (io.cpp:533-570): the RBD1
+        container, written atomically; device-resident Y/T stream from HBM."""
+        return save(self, path, eps_r)
 
     def compress(self):
         """Y T (decompose.cpp:125)."""
@@ -163,7 +176,7 @@ def decompose(x, d_max: int, eps_r: float = 0.0, diag=None, sparse=None, start_c
                                            C.c_void_p(T.data_ptr()), _dp(sel), _dp(hist),
                                            C.byref(res)))
         d = res.d
-        return Model(Y, T, d, sel[:d], hist[:d], res, ctx)
+        return Model(Y, T, d, sel[:d], hist[:d], res, ctx, 1 if diag is not None else 0, diag)
     ctx = ctx or default_context(0)
     xa = _col_major_np(x)
     if xa.ndim != 2:
@@ -182,7 +195,70 @@ def decompose(x, d_max: int, eps_r: float = 0.0, diag=None, sparse=None, start_c
         check(lib.rbd_decompose_host(ctx.handle, _dp(xa), m, n, max(m, 1), C.byref(cfg),
                                      _dp(Y), _dp(T), _dp(sel), _dp(hist), C.byref(res)))
     d = res.d
-    return Model(Y, T, d, sel[:d], hist[:d], res, ctx)
+    return Model(Y, T, d, sel[:d], hist[:d], res, ctx, 1 if diag is not None else 0, diag)
+
+
+def _ptr(a):
+    return C.c_void_p(a.data_ptr()) if hasattr(a, "data_ptr") else _dp(a)
+
+
+def save(model: Model, path, eps_r: float = 0.0):
+    """write_model (io.cpp:533-570) through rbd_model_write."""
+    lib = load_library()
+    Y, T = model.Y, model.T
+    if _is_torch_cuda(Y):
+        Yc = Y if Y.stride(0) == 1 else Y.t().contiguous().t()
+        Tc = T.contiguous()
+        ldy = Yc.stride(1) if Yc.dim() == 2 and Yc.shape[1] > 1 else Yc.shape[0]
+        torch.cuda.current_stream(Y.device).synchronize()
+    else:
+        Yc = np.asfortranarray(Y)
+        Tc = np.ascontiguousarray(T)
+        ldy = Yc.shape[0]
+    m, d = Yc.shape
+    n = Tc.shape[1]
+    hist = np.ascontiguousarray(np.asarray(model.residual_history, dtype=np.float64))
+    if d != model.d or Tc.shape[0] != model.d or hist.shape[0] != model.d:   # io.cpp:537-538
+        raise DimensionMismatch("write_model: inconsistent model shapes")
+    if model.weight_kind == 1 and (model.diag is None or model.diag.shape[0] != m):
+        raise DimensionMismatch("write_model: diagonal weight length != m")
+    diag = model.diag if model.weight_kind == 1 else None
+    ctx = model._ctx
+    check(lib.rbd_model_write(ctx.handle if ctx is not None else None, os.fsencode(str(path)), m,
+                              n, d, _ptr(Yc), ldy, _ptr(Tc), float(eps_r), _dp(hist),
+                              model.weight_kind, _dp(diag) if diag is not None else None))
+
+
+def load(path, device=None, ctx: Optional[Context] = None):
+    """rbd.load (bindings.cpp:80-85) -> read_model (io.cpp:574-622): returns
+    (Model, eps_r). device=None: numpy Y/T; a CUDA device: Y/T are torch tensors
+    filled straight from the file through pinned staging buffers. `selected` is
+    not part of the container (io.hpp:56) and comes back empty."""
+    lib = load_library()
+    p = os.fsencode(str(path))
+    m, n, d = C.c_int64(), C.c_int64(), C.c_int64()
+    kind = C.c_int()
+    check(lib.rbd_model_read_header(p, C.byref(m), C.byref(n), C.byref(d), C.byref(kind)))
+    m, n, d, kind = m.value, n.value, d.value, kind.value
+    hist = np.zeros(d)
+    diag = np.zeros(m) if kind == 1 else None
+    eps = C.c_double()
+    if device is not None:
+        dev = torch.device(device)
+        ctx = ctx or default_context(dev.index or 0)
+        Y = torch.empty((d, m), dtype=torch.float64, device=dev).t()
+        T = torch.empty((d, n), dtype=torch.float64, device=dev)
+        torch.cuda.current_stream(dev).synchronize()
+        ldy = m
+    else:
+        Y = np.zeros((m, d), order="F")
+        T = np.zeros((d, n))
+        ldy = m
+    check(lib.rbd_model_read(ctx.handle if ctx is not None else None, p, _ptr(Y), ldy, _ptr(T),
+                             C.byref(eps), _dp(hist), _dp(diag) if diag is not None else None))
+    res = Result()
+    res.d = d
+    return Model(Y, T, d, [], hist, res, ctx, kind, diag), eps.value
 
 
 def project(model: Model, v):

@@ -14,6 +14,7 @@
 #include <vector>
 
 #include "rbd_cuda.h"
+#include "rbd_internal.h"
 #include "rbd_device.cuh"
 #include "rbd_project.cuh"
 #include "rbd_persistent.cuh"
@@ -734,6 +735,11 @@ double breakdown_tolerance(const rbd_config_t* cfg, long long m, double max_cols
 extern "C" {
 
 const char* rbd_last_error(void) { return g_err.c_str(); }
+
+// for the library's other translation units (csrc/rbd_internal.h)
+__attribute__((visibility("hidden"))) int rbd_internal_set_error(int code, const char* msg) {
+  return set_err(code, msg);
+}
 int rbd_abi_version(void) { return RBD_ABI_VERSION; }
 
 void rbd_config_default(rbd_config_t* cfg) {

@@ -1,13 +1,20 @@
 // Port of the reference's hot-path C++ tests (proj/tests/test_decompose.cpp,
-// proj/tests/test_workspace.cpp identity cases) onto the B200 C++ mirror
+// proj/tests/test_workspace.cpp identity cases, the diagonal-weight cases of
+// test_decompose.cpp:88-126,208-229 and the container cases of
+// test_io.cpp:273-345) onto the B200 C++ mirror
 // (include/rbd/*.hpp). Same fixtures (helpers.hpp:14-26 draws), same
 // assertions and tolerances. Exit code = number of failed checks.
 #include <cmath>
+#include <cstdint>
+#include <filesystem>
+#include <fstream>
+#include <string>
 #include <cstdio>
 #include <limits>
 #include <random>
 
 #include "rbd/decompose.hpp"
+#include "rbd/io.hpp"
 #include "rbd/workspace.hpp"
 
 using namespace rbd;
@@ -67,6 +74,23 @@ static double max_abs_diff(const Matrix& a, const Matrix& b) {
 }
 static double orthonormality_defect(const Matrix& y) {
   return max_abs_diff(matmul(transpose(y), y), Matrix::Identity(y.cols(), y.cols()));
+}
+// helpers.hpp:28-34
+static Vector random_positive(Index n, std::uint64_t seed) {
+  std::mt19937_64 rng(seed);
+  std::uniform_real_distribution<double> u(0.5, 3.0);
+  Vector v(n);
+  for (Index i = 0; i < n; ++i) v[i] = u(rng);
+  return v;
+}
+static double a_norm_sq(const Matrix& x, Index j, const RbdModel& model, const Vector& a) {
+  double s = 0.0;
+  for (Index i = 0; i < x.rows(); ++i) {
+    double r = x(i, j);
+    for (Index k = 0; k < model.d; ++k) r -= model.Y(i, k) * model.T(k, j);
+    s += a[i] * r * r;
+  }
+  return std::max(s, 0.0);
 }
 static RbdConfig basic(Index d_max, double eps = 0.0) {
   RbdConfig c;
@@ -245,6 +269,86 @@ int main() {
     CHECK(std::abs(scan.e_cur - std::sqrt(best)) <= 1e-7 * std::sqrt(best));
     CHECK_THROWS_AS(error_sq(ws, -1, Vector::Zero(3)), IndexOutOfRange);
     CHECK_THROWS_AS(error_sq(ws, 0, Vector::Zero(2)), DimensionMismatch);
+  }
+  // test_decompose.cpp:113-126: the history equals the directly computed A-norm errors
+  {
+    const Matrix x = random_matrix(20, 15, 260);
+    RbdConfig cfg = basic(8);
+    const Vector a = random_positive(20, 261);
+    cfg.weight = WeightSpec::diagonal(a);
+    const RbdModel model = decompose(x, cfg);
+    double worst = 0.0;
+    for (Index j = 0; j < 15; ++j) worst = std::max(worst, std::sqrt(a_norm_sq(x, j, model, a)));
+    CHECK(std::abs(model.residual_history.back() - worst) <= 1e-7 * worst);
+    RbdConfig wrong = basic(2);                     // test_decompose.cpp:196-198
+    Vector ones9(9);
+    for (Index i = 0; i < 9; ++i) ones9[i] = 1.0;
+    wrong.weight = WeightSpec::diagonal(ones9);
+    CHECK_THROWS_AS(decompose(random_matrix(10, 6, 310), wrong), IncompatibleWeight);
+  }
+  // test_decompose.cpp:208-229: a diagonal weight steers the greedy selection
+  {
+    Matrix x(4, 3);
+    x(0, 0) = 1.0;
+    x(1, 1) = 2.0;
+    x(2, 2) = 0.5;
+    RbdConfig plain = basic(2);
+    plain.start = StartSpec::column(2);
+    CHECK(decompose(x, plain).selected[1] == 1);
+    RbdConfig weighted = plain;
+    weighted.weight = WeightSpec::diagonal(Vector{100.0, 1.0, 1.0, 1.0});
+    CHECK(decompose(x, weighted).selected[1] == 0);
+  }
+  // test_io.cpp:273-332: container round trip, size, corruption, missing file
+  {
+    namespace fs = std::filesystem;
+    const fs::path dir = fs::temp_directory_path() / "rbd_b200_cpp_io";
+    fs::create_directories(dir);
+    const fs::path p = dir / "model.rbd";
+    const Matrix x = random_matrix(12, 9, 1040);
+    const WeightSpec kinds[] = {WeightSpec::identity(),
+                                WeightSpec::diagonal(random_positive(12, 1041))};
+    for (const WeightSpec& w : kinds) {
+      RbdConfig cfg = basic(5, 1e-9);
+      cfg.weight = w;
+      const RbdModel model = decompose(x, cfg);
+      write_model(model, cfg.eps_R, p);
+      const LoadedModel back = read_model(p);
+      CHECK(max_abs_diff(back.model.Y, model.Y) == 0.0);
+      CHECK(max_abs_diff(back.model.T, model.T) == 0.0);
+      CHECK(back.model.d == model.d);
+      CHECK(back.model.residual_history == model.residual_history);
+      CHECK(back.eps_r == cfg.eps_R);
+      CHECK(back.model.weight.kind() == w.kind());
+      size_t expect = 29 + 8 * static_cast<size_t>(12 * model.d + model.d * 9 + 1 + model.d);
+      if (w.kind() == WeightKind::diagonal) {
+        expect += 8 * 12;
+        bool same = true;
+        for (Index i = 0; i < 12; ++i)
+          same = same && back.model.weight.diagonal_values()[i] == w.diagonal_values()[i];
+        CHECK(same);
+      }
+      CHECK(fs::file_size(p) == expect);
+    }
+    std::string raw;
+    {
+      std::ifstream in(p, std::ios::binary);
+      raw.assign(std::istreambuf_iterator<char>(in), std::istreambuf_iterator<char>());
+    }
+    auto put = [&](const std::string& bytes) {
+      std::ofstream out(p, std::ios::binary | std::ios::trunc);
+      out.write(bytes.data(), static_cast<std::streamsize>(bytes.size()));
+    };
+    put("XXXX" + raw.substr(4));
+    CHECK_THROWS_AS(read_model(p), ParseError);
+    put(raw.substr(0, raw.size() - 8));
+    CHECK_THROWS_AS(read_model(p), ParseError);
+    std::string bad_tag = raw;
+    bad_tag[28] = 9;
+    put(bad_tag);
+    CHECK_THROWS_AS(read_model(p), ParseError);
+    CHECK_THROWS_AS(read_model(dir / "nope.rbd"), IoError);
+    fs::remove_all(dir);
   }
   std::printf("%d checks, %d failed\n", g_checks, g_fail);
   return g_fail;
