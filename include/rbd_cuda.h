@@ -217,6 +217,24 @@ int rbd_decompose_sharded_virtual(rbd_ctx_t ctx, int nranks, const double* const
                                   double* const* dT_ranks, int64_t* h_selected, double* h_history,
                                   rbd_result_t* result);
 
+/* ---- Batched Classifier::predict (classify.cpp:22-34) ----
+ * For every query column v_q of dQ (m x Q, ld ldq): c_q = Y'v_q (K5), then the
+ * training column j minimising ||T[:,j] - c_q||^2 (difference form, summed in
+ * coordinate order; smallest j on ties, classify.cpp:24-32). dT is the d x
+ * n_train decompose T, row-major (T[k*n_train + j]). d_best[Q] (int64) and
+ * optional d_dist[Q] are device outputs; the label lookup stays with the caller
+ * (Classifier::labels). */
+int rbd_classify_batch(rbd_ctx_t ctx, const double* dY, int64_t m, int64_t d, int64_t ldy,
+                       const double* dT, int64_t n_train, const double* dQ, int64_t Q,
+                       int64_t ldq, int64_t* d_best, double* d_dist);
+/* Same with host buffers (Y m x d col-major ld m, T row-major, Q m x Q ld m). */
+int rbd_classify_host(rbd_ctx_t ctx, const double* hY, int64_t m, int64_t d, const double* hT,
+                      int64_t n_train, const double* hQ, int64_t Q, int64_t* h_best,
+                      double* h_dist);
+/* The nearest-column step alone, for query coordinates dC (d x Q, ld ldc). */
+int rbd_nearest_columns(rbd_ctx_t ctx, const double* dC, int64_t d, int64_t Q, int64_t ldc,
+                        const double* dT, int64_t n_train, int64_t* d_best, double* d_dist);
+
 /* ---- RBD1 model container (io.cpp:527-622, io.hpp:51-64) ----
  * Layout (little-endian): "RBD1" | u64 m, n, d | u8 weight tag | f64 Y (m x d,
  * column-major) | f64 T (d x n, row-major) | f64 eps_R | f64 history[d] |

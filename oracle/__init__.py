@@ -84,6 +84,9 @@ def lib():
         L.orc_ws_yay.argtypes = [P, P]
         L.orc_ws_yay.restype = I
         L.orc_random_positive.argtypes = [I64, C.c_uint64, P]
+        L.orc_predict_batch.argtypes = [P, I64, I64, P, I64, P, I64, I, P, P]
+        L.orc_gen_labeled_blobs.argtypes = [I, I, I, D, C.c_uint64, P, P]
+        L.orc_gen_labeled_blobs.restype = I
         _lib = L
     return _lib
 
@@ -318,3 +321,34 @@ def parse_model(data: bytes):
     hist = f[m * d + d * n + 1: m * d + d * n + 1 + d]
     diag = f[m * d + d * n + 1 + d:] if tag == 1 else None
     return Y, T, eps_r, hist, tag, diag
+
+
+# ---- Classifier (classify.cpp:11-48), restated ----
+
+def predict_batch(Y, T, Qm, nthreads: int = 1):
+    """Best training column and squared distance per query (classify.cpp:22-34)."""
+    Ya = np.asfortranarray(np.asarray(Y, dtype=np.float64))
+    Ta = np.ascontiguousarray(np.asarray(T, dtype=np.float64))
+    Qa = np.asfortranarray(np.asarray(Qm, dtype=np.float64))
+    if Qa.ndim == 1:
+        Qa = Qa.reshape(-1, 1, order="F")
+    m, d = Ya.shape
+    n_tr = Ta.shape[1]
+    nq = Qa.shape[1]
+    best = np.zeros(nq, dtype=np.int64)
+    dist = np.zeros(nq)
+    lib().orc_predict_batch(_p(Ya), m, d, _p(Ta), n_tr, _p(Qa), nq, int(nthreads), _p(best),
+                            _p(dist))
+    return best, dist
+
+
+def gen_labeled_blobs(n_classes, per_class, dim, spread, seed):
+    """datasets.cpp:67-97 (samples dim x n, integer labels), bit-identical draws."""
+    n = n_classes * per_class
+    samples = np.zeros((dim, n), order="F")
+    labels = np.zeros(n, dtype=np.int32)
+    rc = lib().orc_gen_labeled_blobs(int(n_classes), int(per_class), int(dim), float(spread),
+                                     int(seed) & 0xFFFFFFFFFFFFFFFF, _p(samples), _p(labels))
+    if rc != ORC_OK:
+        raise OracleError(rc, lib().orc_last_error().decode())
+    return samples, labels

@@ -432,6 +432,69 @@ void orc_project_batch(const double* Y, int64_t m, int64_t d, const double* Xn, 
   (void)nthreads;
 }
 
+// ---- Classifier::predict, batched (classify.cpp:22-34) ----
+// c = Y'v (decompose.cpp:113-117), then the training column with the smallest
+// (T[:,j] - c).squaredNorm(), strict '<' so the earliest column wins ties.
+void orc_predict_batch(const double* Y, int64_t m, int64_t d, const double* T, int64_t n_tr,
+                       const double* Qm, int64_t nq, int nthreads, int64_t* best_out,
+                       double* dist_out) {
+#ifdef _OPENMP
+#pragma omp parallel for num_threads(nthreads) schedule(static) if (nthreads > 1)
+#endif
+  for (int64_t q = 0; q < nq; ++q) {
+    std::vector<double> c(d);
+    for (int64_t k = 0; k < d; ++k) c[k] = dot8(Y + k * m, Qm + q * m, m);   // :23
+    auto dist = [&](int64_t j) {                                                // :25,27
+      double s = 0.0;
+      for (int64_t k = 0; k < d; ++k) {
+        const double df = T[k * n_tr + j] - c[k];
+        s += df * df;
+      }
+      return s;
+    };
+    int64_t best = 0;
+    double best_dist = dist(0);
+    for (int64_t j = 1; j < n_tr; ++j) {                                        // :26-32
+      const double dj = dist(j);
+      if (dj < best_dist) {
+        best_dist = dj;
+        best = j;
+      }
+    }
+    best_out[q] = best;
+    if (dist_out) dist_out[q] = best_dist;
+  }
+  (void)nthreads;
+}
+
+// gen_labeled_blobs (datasets.cpp:67-97): unit-norm Gaussian class centres plus
+// spread * N(0,1) per sample, classes in order; samples dim x (n_classes*per_class).
+int orc_gen_labeled_blobs(int n_classes, int per_class, int dim, double spread, uint64_t seed,
+                          double* samples, int* labels) {
+  if (n_classes < 1 || per_class < 1 || dim < 1) return fail(ORC_INVALID_ARGUMENT, "blob counts must be >= 1");
+  if (!(spread >= 0.0)) return fail(ORC_INVALID_ARGUMENT, "spread must be >= 0");
+  std::mt19937_64 rng(seed);
+  std::normal_distribution<double> gauss(0.0, 1.0);
+  std::vector<double> centers(static_cast<size_t>(dim) * n_classes);
+  for (int c = 0; c < n_classes; ++c) {
+    std::vector<double> g(dim);
+    for (int i = 0; i < dim; ++i) g[i] = gauss(rng);
+    double nrm = 0.0;   // Eigen norm(): sqrt of the squared norm
+    for (int i = 0; i < dim; ++i) nrm += g[i] * g[i];
+    nrm = std::sqrt(nrm);
+    for (int i = 0; i < dim; ++i)
+      centers[i + static_cast<size_t>(c) * dim] = nrm > 0.0 ? g[i] / nrm : (i == 0 ? 1.0 : 0.0);
+  }
+  int64_t col = 0;
+  for (int c = 0; c < n_classes; ++c)
+    for (int k = 0; k < per_class; ++k, ++col) {
+      for (int i = 0; i < dim; ++i)
+        samples[i + col * dim] = centers[i + static_cast<size_t>(c) * dim] + spread * gauss(rng);
+      labels[col] = c;
+    }
+  return ORC_OK;
+}
+
 // ---- fixtures ----
 void orc_random_matrix(int64_t m, int64_t n, uint64_t seed, double* out) {
   // helpers.hpp:14-21 / acceptance.cpp:56-63: column-major fill

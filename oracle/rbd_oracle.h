@@ -98,6 +98,15 @@ void orc_reconstruct(const double* Y, int64_t m, int64_t d, const double* c, dou
 void orc_project_batch(const double* Y, int64_t m, int64_t d, const double* Xn, int64_t N,
                        int64_t ldx, int nthreads, double* Tn, double* err);
 
+/* Batched Classifier::predict (classify.cpp:22-34): Y m x d (ld m), T d x n_tr
+ * row-major, queries m x nq (ld m); best column and its squared distance. */
+void orc_predict_batch(const double* Y, int64_t m, int64_t d, const double* T, int64_t n_tr,
+                       const double* Qm, int64_t nq, int nthreads, int64_t* best_out,
+                       double* dist_out);
+/* gen_labeled_blobs (datasets.cpp:67-97), bit-identical draws. */
+int orc_gen_labeled_blobs(int n_classes, int per_class, int dim, double spread, uint64_t seed,
+                          double* samples, int* labels);
+
 /* Fixture generators restating the reference's test helpers. */
 void orc_random_matrix(int64_t m, int64_t n, uint64_t seed, double* out);      /* helpers.hpp:14-21 */
 void orc_random_positive(int64_t n, uint64_t seed, double* out);        /* helpers.hpp:28-34 */

@@ -261,6 +261,95 @@ def load(path, device=None, ctx: Optional[Context] = None):
     return Model(Y, T, d, [], hist, res, ctx, kind, diag), eps.value
 
 
+class Classifier:
+    """rbd::Classifier (classify.hpp:14-21): nearest-neighbour recognition in reduced
+    coordinates. ``train_coords`` is ``model.T`` (d x n_train); ``labels`` has one
+    entry per training column. Predictions run batched on the GPU
+    (rbd_classify_batch: K5 projection + the fused nearest-column kernel)."""
+
+    def __init__(self, model: Model, labels):
+        self.model = model
+        self.labels = list(labels)
+        self._dev = None
+
+    @property
+    def train_coords(self):
+        return self.model.T
+
+    def _device_model(self):
+        if self._dev is None:
+            Y, T = self.model.Y, self.model.T
+            if _is_torch_cuda(Y):
+                Yd = Y if Y.stride(0) == 1 else Y.t().contiguous().t()
+                Td = T.contiguous()
+            else:
+                m, d = Y.shape
+                Yd = torch.empty((d, m), dtype=torch.float64, device="cuda").t()
+                Yd.copy_(torch.from_numpy(np.asfortranarray(Y)))
+                Td = torch.from_numpy(np.ascontiguousarray(T)).cuda()
+            torch.cuda.current_stream(Yd.device).synchronize()
+            self._dev = (Yd, Td)
+        return self._dev
+
+    def predict_indices(self, queries):
+        """Best training column per query column (classify.cpp:22-32, batched)."""
+        lib = load_library()
+        Yd, Td = self._device_model()
+        m, d = Yd.shape
+        if _is_torch_cuda(queries):
+            Qd = queries.reshape(m, -1) if queries.dim() == 1 else queries
+            if Qd.dim() != 2 or Qd.shape[0] != m:
+                raise DimensionMismatch("project: vector length != m")
+            Qd = Qd if Qd.stride(0) == 1 else Qd.t().contiguous().t()
+        else:
+            qa = np.asarray(queries, dtype=np.float64)
+            qa = qa.reshape(-1, 1) if qa.ndim == 1 else qa
+            if qa.shape[0] != m:
+                raise DimensionMismatch("project: vector length != m")
+            Qd = torch.empty((qa.shape[1], m), dtype=torch.float64, device=Yd.device).t()
+            Qd.copy_(torch.from_numpy(np.asfortranarray(qa)))
+        nq = Qd.shape[1]
+        best = torch.empty(nq, dtype=torch.int64, device=Yd.device)
+        ctx = self.model._ctx or default_context(Yd.device.index or 0)
+        torch.cuda.current_stream(Yd.device).synchronize()
+        ldq = Qd.stride(1) if nq > 1 else m
+        check(lib.rbd_classify_batch(ctx.handle, C.c_void_p(Yd.data_ptr()), m, d, Yd.stride(1)
+                                     if d > 1 else m, C.c_void_p(Td.data_ptr()), Td.shape[1],
+                                     C.c_void_p(Qd.data_ptr()), nq, ldq,
+                                     C.c_void_p(best.data_ptr()), None))
+        ctx.synchronize()
+        return best.cpu().numpy()
+
+    def predict(self, v):
+        """Classifier::predict (classify.cpp:22-34): the label of the nearest column."""
+        return self.labels[int(self.predict_indices(v)[0])]
+
+    def predict_batch(self, queries):
+        return [self.labels[int(j)] for j in self.predict_indices(queries)]
+
+    def evaluate(self, test, labels):
+        """Fraction of misclassified test columns (classify.cpp:36-48)."""
+        ncols = test.shape[1]
+        if len(labels) != ncols:
+            raise DimensionMismatch("evaluate: one label per test column required")
+        if test.shape[0] != self.model.Y.shape[0]:
+            raise DimensionMismatch("evaluate: test dimension != training dimension")
+        pred = self.predict_batch(test)
+        wrong = sum(1 for p_, t_ in zip(pred, labels) if p_ != t_)
+        return wrong / ncols
+
+
+def fit(train, labels, d_max: int, eps_r: float = 0.0, diag=None, sparse=None,
+        start_column: int = 0, reorthogonalize: bool = False, ctx: Optional[Context] = None):
+    """rbd.fit (bindings.cpp:165-178) -> rbd::fit (classify.cpp:11-20)."""
+    labels = list(labels)
+    if len(labels) != train.shape[1]:
+        raise DimensionMismatch("fit: one label per training column required")
+    model = decompose(train, d_max, eps_r, diag=diag, sparse=sparse, start_column=start_column,
+                      reorthogonalize=reorthogonalize, ctx=ctx)
+    return Classifier(model, labels)
+
+
 def project(model: Model, v):
     """rbd::project (decompose.cpp:113-117): c = Y'v; DimensionMismatch if len(v) != m."""
     lib = load_library()

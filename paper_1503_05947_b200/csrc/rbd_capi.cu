@@ -20,6 +20,7 @@
 #include "rbd_persistent.cuh"
 #include "rbd_project_tc.cuh"
 #include "rbd_weighted.cuh"
+#include "rbd_classify.cuh"
 
 #include <cudaTypedefs.h>
 
@@ -128,6 +129,7 @@ struct rbd_ctx_s {
   // diagonal-weight loop (rbd_weighted.cuh): a o xi, xi'A xi partials, YAX row
   // partials, YAY row, YAX (d_max x n), cross, quad, col_sq_A, host-entry diag
   DevBuf wd_axi, wd_yy, wd_part2, wd_yrow, wd_yax, wd_cross, wd_quad, wd_colsq, wd_diag;
+  DevBuf nn_part, nn_coords;               // classify: split minima, query coordinates
   DevBuf send, recv;                       // sharded mode: payload exchange buffers
   // multi-GPU
   void* comm = nullptr;                    // ncclComm_t (dlopen'ed NCCL)
@@ -808,6 +810,7 @@ int rbd_ctx_destroy(rbd_ctx_t ctx) {
                   &ctx->hX,      &ctx->hY,   &ctx->hT,      &ctx->ppart, &ctx->bar,
                   &ctx->wd_axi,  &ctx->wd_yy, &ctx->wd_part2, &ctx->wd_yrow, &ctx->wd_yax,
                   &ctx->wd_cross, &ctx->wd_quad, &ctx->wd_colsq, &ctx->wd_diag,
+                  &ctx->nn_part, &ctx->nn_coords,
                   &ctx->ctl,     &ctx->gcnt, &ctx->ygcnt,   &ctx->rdy,   &ctx->send,  &ctx->recv};
   for (DevBuf* b : bl) release(*b);
   if (ctx->h_state) cudaFreeHost(ctx->h_state);
@@ -1346,6 +1349,90 @@ int rbd_project_batch(rbd_ctx_t ctx, const double* dY, int64_t m, int64_t d, int
   ctx->launches += nl;
   if (rc != 0) return set_err(RBD_ERR_CUDA, std::string("project kernel: ") + cudaGetErrorString((cudaError_t)rc));
   return RBD_OK;
+}
+
+int rbd_nearest_columns(rbd_ctx_t ctx, const double* dC, int64_t d, int64_t Q, int64_t ldc,
+                        const double* dT, int64_t n_train, int64_t* d_best, double* d_dist) {
+  if (!ctx) return set_err(RBD_ERR_INVALID_ARGUMENT, "null context");
+  if (d < 1 || n_train < 1 || Q < 0 || ldc < d)
+    return set_err(RBD_ERR_DIMENSION_MISMATCH, "nearest: bad sizes");
+  if (Q == 0) return RBD_OK;
+  if (!dC || !dT || !d_best) return set_err(RBD_ERR_INVALID_ARGUMENT, "nearest: null buffer");
+  CU(cudaSetDevice(ctx->device));
+  const long long gx = cdiv(Q, kNnTile);
+  const long long tiles = cdiv(n_train, kNnTile);
+  // split the training columns so the grid covers ~4 CTAs per SM
+  long long nsplit = std::max<long long>(1, std::min<long long>(tiles, cdiv(4LL * ctx->nsm, gx)));
+  const long long per = cdiv(tiles, nsplit) * kNnTile;
+  nsplit = cdiv(n_train, per);
+  if (gx > 0x7fffffffLL || nsplit > 65535)
+    return set_err(RBD_ERR_INVALID_ARGUMENT, "nearest: problem too large for one launch");
+  TRY(ensure(ctx->nn_part, sizeof(NnRec) * (size_t)nsplit * (size_t)Q));
+  k_nearest<<<dim3((unsigned)gx, (unsigned)nsplit), kThreads, 0, ctx->stream>>>(
+      dC, ldc, dT, n_train, d, Q, per, ptr<NnRec>(ctx->nn_part));
+  const int gr = (int)std::max<long long>(1, std::min<long long>(cdiv(Q, 256), (long long)ctx->nsm * 4));
+  k_nearest_reduce<<<gr, 256, 0, ctx->stream>>>(ptr<NnRec>(ctx->nn_part), Q, (int)nsplit,
+                                                reinterpret_cast<long long*>(d_best),
+                                                d_dist);
+  ctx->launches += 2;
+  CU(cudaGetLastError());
+  return RBD_OK;
+}
+
+int rbd_classify_batch(rbd_ctx_t ctx, const double* dY, int64_t m, int64_t d, int64_t ldy,
+                       const double* dT, int64_t n_train, const double* dQ, int64_t Q,
+                       int64_t ldq, int64_t* d_best, double* d_dist) {
+  if (!ctx) return set_err(RBD_ERR_INVALID_ARGUMENT, "null context");
+  if (m < 1 || d < 1 || n_train < 1 || Q < 0)
+    return set_err(RBD_ERR_DIMENSION_MISMATCH, "classify: bad sizes");
+  if (ldy < m || ldq < m)
+    return set_err(RBD_ERR_DIMENSION_MISMATCH, "classify: test dimension != training dimension");
+  if (Q == 0) return RBD_OK;
+  CU(cudaSetDevice(ctx->device));
+  TRY(ensure(ctx->nn_coords, sizeof(double) * (size_t)d * (size_t)Q));
+  double* C = ptr<double>(ctx->nn_coords);
+  TRY(rbd_project_batch(ctx, dY, m, d, ldy, dQ, Q, ldq, C, nullptr));   // c = Y'v (K5)
+  return rbd_nearest_columns(ctx, C, d, Q, d, dT, n_train, d_best, d_dist);
+}
+
+int rbd_classify_host(rbd_ctx_t ctx, const double* hY, int64_t m, int64_t d, const double* hT,
+                      int64_t n_train, const double* hQ, int64_t Q, int64_t* h_best,
+                      double* h_dist) {
+  if (!ctx) return set_err(RBD_ERR_INVALID_ARGUMENT, "null context");
+  if (m < 1 || d < 1 || n_train < 1 || Q < 0)
+    return set_err(RBD_ERR_DIMENSION_MISMATCH, "classify: bad sizes");
+  if (Q == 0) return RBD_OK;
+  CU(cudaSetDevice(ctx->device));
+  DevBuf bY, bT, bQ, bB, bD;
+  auto fin = [&](int rc) {
+    release(bY);
+    release(bT);
+    release(bQ);
+    release(bB);
+    release(bD);
+    return rc;
+  };
+  const long long ldm = (m % 2 == 0) ? m : m + 1;   // 16-byte aligned columns for K5
+  int rc;
+  if ((rc = ensure(bY, sizeof(double) * ldm * d)) || (rc = ensure(bT, sizeof(double) * d * n_train)) ||
+      (rc = ensure(bQ, sizeof(double) * ldm * Q)) || (rc = ensure(bB, sizeof(int64_t) * Q)) ||
+      (rc = ensure(bD, sizeof(double) * Q)))
+    return fin(rc);
+  if (cudaMemcpy2DAsync(bY.p, sizeof(double) * ldm, hY, sizeof(double) * m, sizeof(double) * m, d,
+                        cudaMemcpyHostToDevice, ctx->stream) ||
+      cudaMemcpyAsync(bT.p, hT, sizeof(double) * d * n_train, cudaMemcpyHostToDevice, ctx->stream) ||
+      cudaMemcpy2DAsync(bQ.p, sizeof(double) * ldm, hQ, sizeof(double) * m, sizeof(double) * m, Q,
+                        cudaMemcpyHostToDevice, ctx->stream))
+    return fin(set_err(RBD_ERR_CUDA, "classify_host: H2D failed"));
+  rc = rbd_classify_batch(ctx, ptr<double>(bY), m, d, ldm, ptr<double>(bT), n_train, ptr<double>(bQ),
+                          Q, ldm, ptr<int64_t>(bB), ptr<double>(bD));
+  if (rc) return fin(rc);
+  if (cudaMemcpyAsync(h_best, bB.p, sizeof(int64_t) * Q, cudaMemcpyDeviceToHost, ctx->stream) ||
+      (h_dist && cudaMemcpyAsync(h_dist, bD.p, sizeof(double) * Q, cudaMemcpyDeviceToHost,
+                                 ctx->stream)) ||
+      cudaStreamSynchronize(ctx->stream))
+    return fin(set_err(RBD_ERR_CUDA, "classify_host: D2H failed"));
+  return fin(RBD_OK);
 }
 
 int rbd_reconstruct(rbd_ctx_t ctx, const double* dY, int64_t m, int64_t d, int64_t ldy,
