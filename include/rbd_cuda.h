@@ -174,6 +174,11 @@ int rbd_project_batch_f32(rbd_ctx_t ctx, const float* dY, int64_t m, int64_t d, 
 /* rbd::reconstruct (decompose.cpp:119-123): dv = Y c (dc length d). */
 int rbd_reconstruct(rbd_ctx_t ctx, const double* dY, int64_t m, int64_t d, int64_t ldy,
                     const double* dc, double* dv);
+/* compress_matrix (decompose.cpp:125) on device: V (m x n, column-major, ld ldv)
+ * = Y (m x d, ld ldy) T, with T the d x n decompose T in the library's
+ * row-major layout (T[k*ldt + j]); FP64 tensor cores (DMMA). */
+int rbd_compress_device(rbd_ctx_t ctx, const double* dY, int64_t m, int64_t d, int64_t ldy,
+                        const double* dT, int64_t n, int64_t ldt, double* dV, int64_t ldv);
 /* rbd::compress_matrix (decompose.cpp:125): V = Y C, C d x N column-major
  * (ld d), V m x N column-major (ld m). */
 int rbd_reconstruct_batch(rbd_ctx_t ctx, const double* dY, int64_t m, int64_t d, int64_t ldy,

@@ -133,10 +133,30 @@ class Model:
         return save(self, path, eps_r)
 
     def compress(self):
-        """Y T (decompose.cpp:125)."""
+        """compress_matrix: Y T (decompose.cpp:125) on the FP64 tensor cores
+        (rbd_compress_device / rbd_compress_host)."""
+        lib = load_library()
+        Y, T = self.Y, self.T
+        m, d = Y.shape
+        n = T.shape[1]
         if self.on_device:
-            return self.Y @ self.T
-        return self.Y @ self.T
+            Yc = Y if Y.stride(0) == 1 else Y.t().contiguous().t()
+            Tc = T.contiguous()
+            V = torch.empty((n, m), dtype=torch.float64, device=Y.device).t()
+            ctx = self._ctx or default_context(Y.device.index or 0)
+            torch.cuda.current_stream(Y.device).synchronize()
+            check(lib.rbd_compress_device(ctx.handle, C.c_void_p(Yc.data_ptr()), m, d,
+                                          Yc.stride(1) if d > 1 else m,
+                                          C.c_void_p(Tc.data_ptr()), n, n,
+                                          C.c_void_p(V.data_ptr()), m))
+            ctx.synchronize()
+            return V
+        ctx = self._ctx or default_context(0)
+        Yh = np.asfortranarray(Y)
+        Ch = np.asfortranarray(T)        # d x n column-major coefficients
+        V = np.zeros((m, n), order="F")
+        check(lib.rbd_compress_host(ctx.handle, _dp(Yh), m, d, _dp(Ch), n, _dp(V)))
+        return V
 
 
 def decompose(x, d_max: int, eps_r: float = 0.0, diag=None, sparse=None, start_column: int = 0,

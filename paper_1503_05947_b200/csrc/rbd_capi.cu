@@ -21,6 +21,7 @@
 #include "rbd_project_tc.cuh"
 #include "rbd_weighted.cuh"
 #include "rbd_classify.cuh"
+#include "rbd_compress_dmma.cuh"
 
 #include <cudaTypedefs.h>
 
@@ -1986,6 +1987,11 @@ int rbd_reconstruct_batch(rbd_ctx_t ctx, const double* dY, int64_t m, int64_t d,
   if (ldy < m || m < 1 || N < 0) return set_err(RBD_ERR_DIMENSION_MISMATCH, "compress: bad sizes");
   if (N == 0) return RBD_OK;
   CU(cudaSetDevice(ctx->device));
+  if (d >= 1 && launch_compress_dmma<true>(dY, m, d, ldy, dC, N, d, dV, m, ctx->stream)) {
+    ctx->launches += cdiv(cdiv(N, 64), 65535);
+    CU(cudaGetLastError());
+    return RBD_OK;
+  }
   const long long gx = std::min<long long>(cdiv(m, 256), 1024);
   for (long long j0 = 0; j0 < N; j0 += 65535) {
     const long long nb = std::min<long long>(65535, N - j0);
@@ -1995,6 +2001,35 @@ int rbd_reconstruct_batch(rbd_ctx_t ctx, const double* dY, int64_t m, int64_t d,
   }
   CU(cudaGetLastError());
   return RBD_OK;
+}
+
+int rbd_compress_device(rbd_ctx_t ctx, const double* dY, int64_t m, int64_t d, int64_t ldy,
+                        const double* dT, int64_t n, int64_t ldt, double* dV, int64_t ldv) {
+  if (!ctx) return set_err(RBD_ERR_INVALID_ARGUMENT, "null context");
+  if (m < 1 || d < 1 || n < 0 || ldy < m || ldt < n || ldv < m)
+    return set_err(RBD_ERR_DIMENSION_MISMATCH, "compress: bad sizes");
+  if (n == 0) return RBD_OK;
+  CU(cudaSetDevice(ctx->device));
+  if (launch_compress_dmma<false>(dY, m, d, ldy, dT, n, ldt, dV, ldv, ctx->stream)) {
+    ctx->launches += cdiv(cdiv(n, 64), 65535);
+    CU(cudaGetLastError());
+    return RBD_OK;
+  }
+  // unaligned operands: transpose T into column-major coefficients, SIMT path
+  DevBuf c;
+  TRY(ensure(c, sizeof(double) * (size_t)d * (size_t)n));
+  for (int64_t k = 0; k < d; ++k)   // row k of T -> element k of every column
+    CU(cudaMemcpy2DAsync(ptr<double>(c) + k, sizeof(double) * d, dT + k * ldt, sizeof(double),
+                         sizeof(double), n, cudaMemcpyDeviceToDevice, ctx->stream));
+  int rc = RBD_OK;
+  if (ldv == m) {
+    rc = rbd_reconstruct_batch(ctx, dY, m, d, ldy, ptr<double>(c), n, dV);
+  } else {
+    rc = set_err(RBD_ERR_INVALID_ARGUMENT, "compress: unaligned operands need ldv == m");
+  }
+  cudaStreamSynchronize(ctx->stream);
+  release(c);
+  return rc;
 }
 
 int rbd_compress_host(rbd_ctx_t ctx, const double* hY, int64_t m, int64_t d, const double* hC,
