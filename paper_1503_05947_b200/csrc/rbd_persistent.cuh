@@ -288,6 +288,15 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
       // lane owns rows i0 .. i0+VEC-1 (a 16-byte pair when VEC == 2)
       const long long i0 = rb + (long long)VEC * lane;
       const long long iend = (rb + kPRows < r_hi) ? rb + kPRows : r_hi;   // rows of this block
+      // warp 0 finishes the block's rows: their x and w1_{k-1} loads go out
+      // now and land while the block's Y batches stream
+      double xpre[VEC], wpre[VEC];
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) {
+        const bool in = warp == 0 && i0 + v < iend;
+        xpre[v] = (in && live) ? __ldcg(&x[i0 + v]) : 0.0;
+        wpre[v] = (in && pending) ? __ldcg(&a.w[i0 + v]) : 0.0;
+      }
       double acc_c[VEC], acc_p[VEC];
 #pragma unroll
       for (int v = 0; v < VEC; ++v) acc_c[v] = acc_p[v] = 0.0;
@@ -345,12 +354,12 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
             sp += red_p[w][VEC * lane + v];
           }
           if (pending) {
-            const double yk1 = (a.w[i] - sp) / wnorm_prev;   // second pass of column k-1
+            const double yk1 = (wpre[v] - sp) / wnorm_prev;  // second pass of column k-1
             a.Y[i + (k - 1) * m] = yk1;
             sc = fma(yk1, cs[k - 1], sc);
           }
           if (live) {
-            const double w1 = x[i] - sc;                     // first pass of column k
+            const double w1 = xpre[v] - sc;                  // first pass of column k
             a.w[i] = w1;
             nacc = fma(w1, w1, nacc);
           }
