@@ -388,3 +388,16 @@ def test_acceptance4_invariants(cuda):                    # :242-297
         brute = y @ np.linalg.solve(y.T @ y, y.T @ x)
         assert np.abs(brute - m.Y @ m.T).max() < 1e-10
         compare(m, oracle.decompose(x, d_max, 1e-6), x)
+
+
+def test_host_entry_pinned_outputs_stream_y_from_the_loop(cuda):
+    # large enough for page-locked host outputs (api._host_outputs): the
+    # persistent loop writes Y into them directly; must equal the device entry
+    rng = np.random.default_rng(21)
+    x = np.asfortranarray(rng.standard_normal((8192, 300)))
+    h = rbd.decompose(x, d_max=150)
+    import torch
+    dv = rbd.decompose(torch.from_numpy(x).cuda(), d_max=150)
+    assert h.selected == dv.selected
+    np.testing.assert_array_equal(h.Y, dv.Y.cpu().numpy())
+    np.testing.assert_array_equal(h.T, dv.T.cpu().numpy())
