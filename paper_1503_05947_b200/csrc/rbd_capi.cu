@@ -131,6 +131,7 @@ struct rbd_ctx_s {
   // partials, YAY row, YAX (d_max x n), cross, quad, col_sq_A, host-entry diag
   DevBuf wd_axi, wd_yy, wd_part2, wd_yrow, wd_yax, wd_cross, wd_quad, wd_colsq, wd_diag;
   DevBuf nn_part, nn_coords;               // classify: split minima, query coordinates
+  DevBuf pj_ws;                            // K5 split-K partial slices
   DevBuf send, recv;                       // sharded mode: payload exchange buffers
   // multi-GPU
   void* comm = nullptr;                    // ncclComm_t (dlopen'ed NCCL)
@@ -811,7 +812,7 @@ int rbd_ctx_destroy(rbd_ctx_t ctx) {
                   &ctx->hX,      &ctx->hY,   &ctx->hT,      &ctx->ppart, &ctx->bar,
                   &ctx->wd_axi,  &ctx->wd_yy, &ctx->wd_part2, &ctx->wd_yrow, &ctx->wd_yax,
                   &ctx->wd_cross, &ctx->wd_quad, &ctx->wd_colsq, &ctx->wd_diag,
-                  &ctx->nn_part, &ctx->nn_coords,
+                  &ctx->nn_part, &ctx->nn_coords, &ctx->pj_ws,
                   &ctx->ctl,     &ctx->gcnt, &ctx->ygcnt,   &ctx->rdy,   &ctx->send,  &ctx->recv};
   for (DevBuf* b : bl) release(*b);
   if (ctx->h_state) cudaFreeHost(ctx->h_state);
@@ -1345,8 +1346,13 @@ int rbd_project_batch(rbd_ctx_t ctx, const double* dY, int64_t m, int64_t d, int
   CU(cudaSetDevice(ctx->device));
   long long nl = 0;
   if (d_err) TRY(ensure(ctx->scratch1, sizeof(double) * (size_t)std::max<int64_t>(N, 32)));
+  // split the K = m reduction when the DMMA grid would leave a partial last wave
+  int sk = rbdk::project_splitk(m, d, N, ctx->nsm);
+  if (sk > 1 && ensure(ctx->pj_ws, sizeof(double) * (size_t)(sk - 1) * (size_t)(d * N + N)) != RBD_OK)
+    sk = 1;
   int rc = rbdk::launch_project_f64(dY, m, d, ldy, dXn, N, ldx, dTn, d_err, ctx->stream, &nl,
-                                    d_err ? ptr<double>(ctx->scratch1) : nullptr);
+                                    d_err ? ptr<double>(ctx->scratch1) : nullptr, sk,
+                                    sk > 1 ? ptr<double>(ctx->pj_ws) : nullptr);
   ctx->launches += nl;
   if (rc != 0) return set_err(RBD_ERR_CUDA, std::string("project kernel: ") + cudaGetErrorString((cudaError_t)rc));
   return RBD_OK;

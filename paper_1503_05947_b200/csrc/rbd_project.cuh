@@ -103,10 +103,25 @@ __global__ void k_reconstruct(const double* __restrict__ Y, long long m, long lo
   }
 }
 
+// Split-K factor for the DMMA grid: the smallest of 1..4 whose last wave is
+// >= 97% full (4 CTAs per SM), keeping >= 1024 rows per split.
+inline int project_splitk(long long m, long long d, long long N, int nsm) {
+  const long long ctas = ((d + 63) / 64) * ((N + 63) / 64);
+  const long long slots = 4LL * nsm;
+  for (int s = 1; s <= 4; ++s) {
+    if (s > 1 && m / s < 1024) break;
+    const long long c = ctas * s;
+    const long long waves = (c + slots - 1) / slots;
+    if ((double)c / (double)(waves * slots) >= 0.97) return s;
+  }
+  return 1;
+}
+
 inline int launch_project_f64(const double* Y, long long m, long long d, long long ldy,
                               const double* Xn, long long N, long long ldx, double* Tn,
                               double* err, cudaStream_t s, long long* nlaunch,
-                              double* xnorm_scratch = nullptr) {
+                              double* xnorm_scratch = nullptr, int splitk = 1,
+                              double* splitk_ws = nullptr) {
   const bool dmma_ok = (ldy % 2 == 0) && (ldx % 2 == 0) &&
                        ((reinterpret_cast<uintptr_t>(Y) | reinterpret_cast<uintptr_t>(Xn)) & 15) == 0;
   *nlaunch = 0;
@@ -119,10 +134,19 @@ inline int launch_project_f64(const double* Y, long long m, long long d, long lo
       attr = true;
     }
     double* xn = err ? xnorm_scratch : nullptr;
-    dim3 grid((unsigned)((d + BM - 1) / BM), (unsigned)((N + BN - 1) / BN));
+    const int sk = (splitk > 1 && splitk_ws) ? splitk : 1;
+    // workspace layout: (sk-1) T slices of d*N, then (sk-1) ||x||^2 slices of N
+    double* Tws = splitk_ws;
+    double* xws = splitk_ws ? splitk_ws + (long long)(sk - 1) * d * N : nullptr;
+    const long long kc = ((m + sk - 1) / sk + 15) / 16 * 16;
+    dim3 grid((unsigned)((d + BM - 1) / BM), (unsigned)((N + BN - 1) / BN), (unsigned)sk);
     k_project_dmma<BM, BN, WM, WN><<<grid, WM * WN * 32, dm_smem_bytes<BM, BN>(), s>>>(
-        Y, m, d, ldy, Xn, N, ldx, Tn, xn);
+        Y, m, d, ldy, Xn, N, ldx, Tn, xn, kc, Tws, xws);
     *nlaunch += 1;
+    if (sk > 1) {
+      k_splitk_sum<<<1184, 256, 0, s>>>(Tn, Tws, d * N, sk - 1, xn, xws, N);
+      *nlaunch += 1;
+    }
     if (err) {
       k_project_err_fused<<<(unsigned)((N + 7) / 8), 256, 0, s>>>(xn, Tn, d, N, err);
       *nlaunch += 1;

@@ -70,7 +70,21 @@ template <int BM, int BN, int WARPS_M, int WARPS_N>
 __global__ void __launch_bounds__(WARPS_M * WARPS_N * 32, 4)
     k_project_dmma(const double* __restrict__ Y, long long m, long long d, long long ldy,
                    const double* __restrict__ Xn, long long N, long long ldx,
-                   double* __restrict__ Tn, double* __restrict__ xnorm2) {
+                   double* __restrict__ Tn, double* __restrict__ xnorm2, long long kc,
+                   double* __restrict__ Tws, double* __restrict__ xws) {
+  // split-K: blockIdx.z takes rows [z*kc, min(m, (z+1)*kc)) of Y / X_new (kc a
+  // multiple of 16); split 0 writes Tn / xnorm2, split z > 0 its workspace slice
+  {
+    const long long z = blockIdx.z;
+    const long long kb = z * kc, ke = (kb + kc < m) ? kb + kc : m;
+    if (z > 0) {
+      Tn = Tws + (z - 1) * d * N;
+      if (xnorm2) xnorm2 = xws + (z - 1) * N;
+    }
+    Y += kb;
+    Xn += kb;
+    m = ke - kb;
+  }
   constexpr int NTHREADS = WARPS_M * WARPS_N * 32;
   constexpr int WM = BM / WARPS_M, WN = BN / WARPS_N;   // warp tile
   constexpr int MT = WM / 16, NT = WN / 8;               // mma tiles per warp
@@ -157,6 +171,23 @@ __global__ void __launch_bounds__(WARPS_M * WARPS_N * 32, 4)
         if (l < d && j < N) Tn[l + j * d] = acc[a][b][e];
       }
   if (do_norm && tid < BN && j0 + tid < N) xnorm2[j0 + tid] = xn;
+}
+
+// Split-K combine: Tn += workspace slices (and ||x||^2), splits in order.
+__global__ void k_splitk_sum(double* __restrict__ Tn, const double* __restrict__ Tws,
+                             long long dN, int nws, double* __restrict__ xn,
+                             const double* __restrict__ xws, long long N) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < dN;
+       e += (long long)gridDim.x * blockDim.x) {
+    double v = Tn[e];
+    for (int z = 0; z < nws; ++z) v += Tws[(long long)z * dN + e];
+    Tn[e] = v;
+    if (xn && e < N) {
+      double x = xn[e];
+      for (int z = 0; z < nws; ++z) x += xws[(long long)z * N + e];
+      xn[e] = x;
+    }
+  }
 }
 
 // err_j = max(||x_j||^2 - ||t_j||^2, 0) from the fused ||x||^2 (one warp per column).
