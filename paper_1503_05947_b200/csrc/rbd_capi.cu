@@ -115,6 +115,14 @@ struct rbd_ctx_s {
   DevBuf hX, hY, hT;  // cached device copies for the host entry
   DevBuf ppart;       // fused-extension partials
   DevState* h_state = nullptr;  // pinned
+  // host entry with a page-locked Y: the loop posts its progress to a mapped
+  // word and finished Y columns are copied out on a second stream meanwhile
+  long long* h_progress = nullptr;
+  long long* d_progress = nullptr;
+  cudaStream_t copy_stream = nullptr;
+  double* ystream_dst = nullptr;   // host Y (ld m) to stream into, or null
+  double* tstream_dst = nullptr;   // host T (row-major, n per row), or null
+  long long ystream_copied = 0;    // Y columns / T rows already copied (or in flight)
   Rec* h_rec = nullptr;         // pinned
   cudaGraphExec_t gexec = nullptr;
   GraphKey gkey;
@@ -573,6 +581,8 @@ int launch_persistent(rbd_ctx_t ctx, const LoopBufs& L) {
   a.d_max = L.d_max;
   a.ctl = ptr<StepCtl>(ctx->ctl);
   a.rdy = ptr<unsigned long long>(ctx->rdy);
+  a.progress = (ctx->ystream_dst && ctx->d_progress) ? ctx->d_progress : nullptr;
+  if (a.progress) *(volatile long long*)ctx->h_progress = 0;
   a.phase_ns = nullptr;
   if (getenv("RBD_PHASE_TIMING")) {
     TRY(ensure(ctx->scratch1, 256));
@@ -775,6 +785,16 @@ int rbd_ctx_create(int device, rbd_ctx_t* out) {
   ctx->stream = ctx->own_stream;
   cudaMallocHost(&ctx->h_state, sizeof(DevState));
   cudaMallocHost(&ctx->h_rec, sizeof(Rec) * 4);
+  if (cudaHostAlloc(&ctx->h_progress, sizeof(long long), cudaHostAllocMapped) == cudaSuccess) {
+    if (cudaHostGetDevicePointer(reinterpret_cast<void**>(&ctx->d_progress), ctx->h_progress, 0) !=
+        cudaSuccess) {
+      cudaGetLastError();
+      ctx->d_progress = nullptr;
+    }
+  } else {
+    cudaGetLastError();
+    ctx->h_progress = nullptr;
+  }
   int o = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_sweep<2, MODE_DOT, true>, kThreads, 0) ==
           cudaSuccess && o > 0)
@@ -816,6 +836,8 @@ int rbd_ctx_destroy(rbd_ctx_t ctx) {
                   &ctx->ctl,     &ctx->gcnt, &ctx->ygcnt,   &ctx->rdy,   &ctx->send,  &ctx->recv};
   for (DevBuf* b : bl) release(*b);
   if (ctx->h_state) cudaFreeHost(ctx->h_state);
+  if (ctx->h_progress) cudaFreeHost(ctx->h_progress);
+  if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
   if (ctx->h_rec) cudaFreeHost(ctx->h_rec);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   rbd_comm_release(ctx);
@@ -987,6 +1009,27 @@ int decompose_device_impl(rbd_ctx_t ctx, const double* dX, int64_t m, int64_t n,
     if (use_fused(cfg->d_max)) TRY(enqueue_fused_ext(ctx, L));  // last column's second pass
   }
   CU(cudaEventRecord(ev2, ctx->stream));
+  ctx->ystream_copied = 0;
+  if (ctx->ystream_dst && ctx->d_progress && ctx->path == 0 && use_fused(cfg->d_max) && !diag) {
+    // stream finished Y columns to the host while the loop runs (copy engine,
+    // second stream), 16 columns or more per copy
+    if (!ctx->copy_stream) CU(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+    long long copied = 0;
+    while (cudaEventQuery(ev2) == cudaErrorNotReady) {
+      const long long done_cols = *(volatile long long*)ctx->h_progress;
+      if (done_cols - copied >= 16) {   // Y columns and T rows [copied, done_cols)
+        CU(cudaMemcpyAsync(ctx->ystream_dst + copied * m, dY + copied * m,
+                           sizeof(double) * (size_t)((done_cols - copied) * m),
+                           cudaMemcpyDeviceToHost, ctx->copy_stream));
+        if (ctx->tstream_dst)
+          CU(cudaMemcpyAsync(ctx->tstream_dst + copied * n, dT + copied * n,
+                             sizeof(double) * (size_t)((done_cols - copied) * n),
+                             cudaMemcpyDeviceToHost, ctx->copy_stream));
+        copied = done_cols;
+      }
+    }
+    ctx->ystream_copied = copied;
+  }
   CU(cudaMemcpyAsync(ctx->h_state, st, sizeof(DevState), cudaMemcpyDeviceToHost, ctx->stream));
   CU(cudaStreamSynchronize(ctx->stream));
   hs = *ctx->h_state;
@@ -1078,6 +1121,7 @@ int decompose_host_impl(rbd_ctx_t ctx, const double* hX, int64_t m, int64_t n, i
   if (e != cudaSuccess) return set_err(RBD_ERR_CUDA, std::string("H2D X: ") + cudaGetErrorString(e));
   rbd_result_t r{};
   int rc;
+  bool t_streamed = false;
   if (h_diag || diag_len != 0) {
     TRY(check_diagonal(h_diag, diag_len));
     TRY(ensure(ctx->wd_diag, sizeof(double) * diag_len));
@@ -1086,13 +1130,39 @@ int decompose_host_impl(rbd_ctx_t ctx, const double* hX, int64_t m, int64_t n, i
     rc = rbd_decompose_diag_device(ctx, dX, m, n, ldd, cfg, ptr<double>(ctx->wd_diag), diag_len,
                                    dY, dT, h_selected, h_history, &r);
   } else {
+    ctx->ystream_dst = nullptr;
+    ctx->tstream_dst = nullptr;
+    if (hY) {   // page-locked Y: columns (and T rows) stream out while the loop runs
+      cudaPointerAttributes pa{};
+      if (cudaPointerGetAttributes(&pa, hY) == cudaSuccess && pa.type == cudaMemoryTypeHost) {
+        ctx->ystream_dst = hY;
+        if (hT && cudaPointerGetAttributes(&pa, hT) == cudaSuccess &&
+            pa.type == cudaMemoryTypeHost)
+          ctx->tstream_dst = hT;
+        else
+          cudaGetLastError();
+      } else {
+        cudaGetLastError();
+      }
+    }
     rc = rbd_decompose_device(ctx, dX, m, n, ldd, cfg, dY, dT, h_selected, h_history, &r);
+    t_streamed = ctx->tstream_dst != nullptr;
+    ctx->ystream_dst = nullptr;
+    ctx->tstream_dst = nullptr;
   }
+  const long long y_done = (rc == RBD_OK) ? std::min<long long>(ctx->ystream_copied, r.d) : 0;
+  const long long t_done = t_streamed ? y_done : 0;
+  ctx->ystream_copied = 0;
   // dY was allocated with d_cap columns; the device call writes at most d_cap
   if (rc == RBD_OK) {
-    if (hY) e = cudaMemcpyAsync(hY, dY, sizeof(double) * m * r.d, cudaMemcpyDeviceToHost, ctx->stream);
-    if (e == cudaSuccess && hT)
-      e = cudaMemcpyAsync(hT, dT, sizeof(double) * r.d * n, cudaMemcpyDeviceToHost, ctx->stream);
+    if (hY && r.d > y_done)
+      e = cudaMemcpyAsync(hY + y_done * m, dY + y_done * m, sizeof(double) * m * (r.d - y_done),
+                          cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess && y_done > 0 && ctx->copy_stream)
+      e = cudaStreamSynchronize(ctx->copy_stream);   // the streamed columns
+    if (e == cudaSuccess && hT && r.d > t_done)
+      e = cudaMemcpyAsync(hT + t_done * n, dT + t_done * n, sizeof(double) * (r.d - t_done) * n,
+                          cudaMemcpyDeviceToHost, ctx->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
     if (e != cudaSuccess) rc = set_err(RBD_ERR_CUDA, std::string("D2H model: ") + cudaGetErrorString(e));
     if (result) *result = r;

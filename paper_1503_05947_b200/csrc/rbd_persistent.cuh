@@ -58,6 +58,7 @@ struct PersistArgs {
   struct StepCtl* ctl;           // queue / publish words
   unsigned long long* rdy;       // [0] CTAs through P1, [1 + s] rows of chunk s written by P1
                                  // (monotonic within a decompose, zeroed with ctl)
+  long long* progress;           // optional mapped host word: Y columns [0, value) are final
 };
 
 __device__ __forceinline__ void red_release_add_u64(unsigned long long* p, unsigned long long v) {
@@ -623,6 +624,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
     grid_barrier(a.bar, gen);
     trace(k, 7);
     mark(3);
+    // columns [0, k) of Y (column k-1 materialised in this step's P1) are
+    // written at GPU scope: a copy engine may fetch them while the loop runs
+    if (a.progress && cta == 0 && tid == 0) *(volatile long long*)a.progress = k;
     if constexpr (SHARD) {   // every claim of this launch is done: rezero for the next launch
       if (cta == 0 && tid == 0) ctl->tile_ctr = 0ull;
     }
