@@ -182,16 +182,23 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       for (int kb = 0; kb < nk; ++kb) {
         const int s = kb % kTcStages;
         const uint32_t ph = (kb / kTcStages) & 1;
+        // hi x hi needs only the TMA data; the two lo products wait for the
+        // converters (they run while the first four MMAs execute)
         mbar_wait(&full[s], ph);
-        mbar_wait(&conv[s], ph);
         asm volatile("tcgen05.fence::after_thread_sync;");
 #pragma unroll
         for (int kk = 0; kk < kTcBK / 8; ++kk) {   // K = 8 tf32 = 32 bytes per MMA
           const uint32_t off = kk * 32;
+          umma_tf32(tmem, umma_desc_sw128(stageA(s), off), umma_desc_sw128(stageB(s), off), idesc,
+                    (kb | kk) ? 1u : 0u);
+        }
+        mbar_wait(&conv[s], ph);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll
+        for (int kk = 0; kk < kTcBK / 8; ++kk) {
+          const uint32_t off = kk * 32;
           const uint64_t ah = umma_desc_sw128(stageA(s), off), al = umma_desc_sw128(stageAlo(s), off);
           const uint64_t bh = umma_desc_sw128(stageB(s), off), bl = umma_desc_sw128(stageBlo(s), off);
-          const uint32_t acc0 = (kb | kk) ? 1u : 0u;
-          umma_tf32(tmem, ah, bh, idesc, acc0);
           umma_tf32(tmem, ah, bl, idesc, 1u);
           umma_tf32(tmem, al, bh, idesc, 1u);
         }
@@ -202,7 +209,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   } else {
     // ---------------- converters (warps 2-5): lo tiles, ||x_j||^2 (fp64) ----------------
     const int r = threadIdx.x - 64;   // 0..127: row r of the A tile and of the B tile
-    double xn = 0.0;
+    double xn0 = 0.0, xn1 = 0.0, xn2 = 0.0, xn3 = 0.0;   // four chains (fixed combination)
     for (int kb = 0; kb < nk; ++kb) {
       const int s = kb % kTcStages;
       const uint32_t ph = (kb / kTcStages) & 1;
@@ -220,14 +227,15 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         alo[c] = make_float4(tf32_lo(a.x), tf32_lo(a.y), tf32_lo(a.z), tf32_lo(a.w));
         const float4 b = br[c];
         blo[c] = make_float4(tf32_lo(b.x), tf32_lo(b.y), tf32_lo(b.z), tf32_lo(b.w));
-        xn = fma((double)b.x, (double)b.x, xn);
-        xn = fma((double)b.y, (double)b.y, xn);
-        xn = fma((double)b.z, (double)b.z, xn);
-        xn = fma((double)b.w, (double)b.w, xn);
+        xn0 = fma((double)b.x, (double)b.x, xn0);
+        xn1 = fma((double)b.y, (double)b.y, xn1);
+        xn2 = fma((double)b.z, (double)b.z, xn2);
+        xn3 = fma((double)b.w, (double)b.w, xn3);
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic -> async proxy
       mbar_arrive(&conv[s]);
     }
+    const double xn = (xn0 + xn1) + (xn2 + xn3);
     if (xnorm2 != nullptr && blockIdx.x == 0 && j0 + r < N) xnorm2[j0 + r] = xn;
     // ---------------- epilogue: TMEM -> registers -> T_new ----------------
     mbar_wait(tmem_full, 0);
