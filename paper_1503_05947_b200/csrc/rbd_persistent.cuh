@@ -191,13 +191,18 @@ constexpr int kPayHead = 4;
 template <int VEC, bool SHARD>
 __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
   extern __shared__ double dsm[];
-  constexpr int kPBatch = 16 * kWarps;   // columns per P1 batch (16 loads in flight per lane)
+  constexpr int kPBatch = 16 * kWarps / 2;   // columns per P1 batch of a half (16 loads per lane)
   double* cs = dsm;                        // c = T[0:k, j*], zero-padded to a batch multiple
   double* ps = dsm + a.d_max + kPBatch;    // p_{k-1} (pending column), zero-padded
   __shared__ double red[kWarps][kCols];
-  constexpr int kPRows = 32 * VEC;  // rows per P1 block
-  __shared__ double red_c[kWarps][kPRows];
-  __shared__ double red_p[kWarps][kPRows];
+  // P1 block: two warp-halves of 32*VEC rows each (warps 0-3 / 4-7); within a
+  // half the 4 warps split the columns (l = warp%4 mod 4), so every row's sum
+  // runs in the same order whichever half it falls in
+  constexpr int kPHalf = 32 * VEC;
+  constexpr int kPRows = 2 * kPHalf;  // rows per P1 block
+  constexpr int kPW = kWarps / 2;     // warps per half
+  __shared__ double red_c[kWarps][kPHalf];
+  __shared__ double red_p[kWarps][kPHalf];
   __shared__ double smn[kWarps];
   __shared__ Rec smr[kWarps];
   __shared__ long long sh_tile;
@@ -286,15 +291,16 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
     __syncthreads();
     double nacc = 0.0;
     for (long long rb = r_lo; rb < r_hi; rb += kPRows) {
-      // lane owns rows i0 .. i0+VEC-1 (a 16-byte pair when VEC == 2)
-      const long long i0 = rb + (long long)VEC * lane;
+      // lane owns rows i0 .. i0+VEC-1 of its half (a 16-byte pair when VEC == 2)
+      const int half = warp / kPW, wh = warp % kPW;
+      const long long i0 = rb + (long long)half * kPHalf + (long long)VEC * lane;
       const long long iend = (rb + kPRows < r_hi) ? rb + kPRows : r_hi;   // rows of this block
-      // warp 0 finishes the block's rows: their x and w1_{k-1} loads go out
-      // now and land while the block's Y batches stream
+      // the first warp of each half finishes the half's rows: their x and
+      // w1_{k-1} loads go out now and land while the block's Y batches stream
       double xpre[VEC], wpre[VEC];
 #pragma unroll
       for (int v = 0; v < VEC; ++v) {
-        const bool in = warp == 0 && i0 + v < iend;
+        const bool in = wh == 0 && i0 + v < iend;
         xpre[v] = (in && live) ? __ldcg(&x[i0 + v]) : 0.0;
         wpre[v] = (in && pending) ? __ldcg(&a.w[i0 + v]) : 0.0;
       }
@@ -307,13 +313,13 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
       const long long nv_ = iend - i0;
       const int nv = nv_ >= VEC ? VEC : (nv_ > 0 ? (int)nv_ : 0);
       if (nv > 0) {
-        const double* yp = a.Y + i0 + (long long)warp * m;
-        const long long stp = (long long)kWarps * m;
-        for (long long l = warp; l < kb; l += 16 * kWarps) {
+        const double* yp = a.Y + i0 + (long long)wh * m;
+        const long long stp = (long long)kPW * m;
+        for (long long l = wh; l < kb; l += 16 * kPW) {
           double yv[16][VEC];
 #pragma unroll
           for (int q = 0; q < 16; ++q) {
-            const bool ok = l + q * kWarps < kb;
+            const bool ok = l + q * kPW < kb;
             if constexpr (VEC == 2) {
               if (ok && nv == 2) {
                 const double2 t2 = __ldcg(reinterpret_cast<const double2*>(yp + q * stp));
@@ -331,8 +337,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
           for (int q = 0; q < 16; ++q)
 #pragma unroll
             for (int v = 0; v < VEC; ++v) {
-              acc_c[v] = fma(yv[q][v], cs[l + q * kWarps], acc_c[v]);   // zero past kb
-              acc_p[v] = fma(yv[q][v], ps[l + q * kWarps], acc_p[v]);
+              acc_c[v] = fma(yv[q][v], cs[l + q * kPW], acc_c[v]);   // zero past kb
+              acc_p[v] = fma(yv[q][v], ps[l + q * kPW], acc_p[v]);
             }
           yp += 16 * stp;
         }
@@ -343,16 +349,17 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
         red_p[warp][VEC * lane + v] = acc_p[v];
       }
       __syncthreads();
-      if (warp == 0) {
+      if (wh == 0) {
 #pragma unroll
         for (int v = 0; v < VEC; ++v) {
           const long long i = i0 + v;
           if (i >= iend) break;
-          double sc = red_c[0][VEC * lane + v], sp = red_p[0][VEC * lane + v];
+          const int w0 = half * kPW;
+          double sc = red_c[w0][VEC * lane + v], sp = red_p[w0][VEC * lane + v];
 #pragma unroll
-          for (int w = 1; w < kWarps; ++w) {
-            sc += red_c[w][VEC * lane + v];
-            sp += red_p[w][VEC * lane + v];
+          for (int w = 1; w < kPW; ++w) {
+            sc += red_c[w0 + w][VEC * lane + v];
+            sp += red_p[w0 + w][VEC * lane + v];
           }
           if (pending) {
             const double yk1 = (wpre[v] - sp) / wnorm_prev;  // second pass of column k-1
@@ -371,7 +378,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
     pending = 0;
     if (!live) continue;   // materialisation-only pass after the stop
     {
-      const double sblk = block_sum_fixed<kThreads>(warp == 0 ? nacc : 0.0, smn);
+      const double sblk = block_sum_fixed<kThreads>(warp % kPW == 0 ? nacc : 0.0, smn);
       // block_sum_fixed ends with __syncthreads: every P1 write of this CTA
       // (w1 rows, Y column k-1 rows) precedes the release-adds below
       if (tid == 0) {
