@@ -641,7 +641,20 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
     // every CTA: the published decision, the global argmax over the CTA
     // records (workspace.cpp:107-113,123) and the stop test (decompose.cpp:87)
     {
+      // one round trip for all of it: the decision words and the CTA records
       const int bd = __ldcg(&ctl->breakdown);
+      const double nrm = __ldcg(&ctl->norm);
+      const int re = __ldcg(&ctl->reorth);
+      double rv0 = -1.0, rv1 = -1.0;
+      long long rj0 = 0x7fffffffffffffffLL, rj1 = 0x7fffffffffffffffLL;
+      if (tid < G) {
+        rv0 = __ldcg(&a.rec[tid].v);
+        rj0 = __ldcg(&a.rec[tid].j);
+      }
+      if (tid + kThreads < G) {
+        rv1 = __ldcg(&a.rec[tid + kThreads].v);
+        rj1 = __ldcg(&a.rec[tid + kThreads].j);
+      }
       if (bd) {                        // decompose.cpp:90 — keep the d we have
         done = 1;
         breakdown = 1;
@@ -655,11 +668,17 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
         }
         continue;
       }
-      const double nrm = __ldcg(&ctl->norm);
-      const int re = __ldcg(&ctl->reorth);
       double gv = -1.0;
       long long gj = 0x7fffffffffffffffLL;
-      for (int b = tid; b < G; b += kThreads) {
+      if (rec_better(rv0, rj0, gv, gj)) {
+        gv = rv0;
+        gj = rj0;
+      }
+      if (rec_better(rv1, rj1, gv, gj)) {
+        gv = rv1;
+        gj = rj1;
+      }
+      for (int b = tid + 2 * kThreads; b < G; b += kThreads) {   // grids above 512 CTAs
         const double v = __ldcg(&a.rec[b].v);
         const long long jj = __ldcg(&a.rec[b].j);
         if (rec_better(v, jj, gv, gj)) {
