@@ -37,6 +37,8 @@ def parse():
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--d-max", type=int, default=None, help="override d_max (quick runs)")
+    p.add_argument("--ref-seconds", type=float, default=6.0,
+                   help="reference arm: CPU seconds of greedy steps per bench step")
     return p.parse_args()
 
 
@@ -133,7 +135,8 @@ def make_workload(name, device):
         Xd = configs.low_rank_matrix_torch(w.m, w.n, rank, configs.spectrum(key, rank),
                                            {"C2": 1e-8, "C3": 1e-10, "C4": 1e-6}[key], w.seed,
                                            device=device)
-    torch.cuda.synchronize(device)
+    if torch.device(device).type == "cuda":
+        torch.cuda.synchronize(device)
     colmax = float(Xd.norm(dim=0).max())
     return w, Xd, configs.eps_for(w, colmax)
 
@@ -169,7 +172,7 @@ def run_reference(args):
     t0 = time.perf_counter()
     oracle.decompose(X, w.d_max, eps, nthreads=cores, max_steps=2)
     per = max((time.perf_counter() - t0) / 2.0, 1e-4)
-    S = int(max(2, min(w.d_max, 6.0 / per)))
+    S = int(max(2, min(w.d_max, args.ref_seconds / per)))
     for _ in range(args.warmup):
         oracle.decompose(X, w.d_max, eps, nthreads=cores, max_steps=S)
     t0 = time.perf_counter()
