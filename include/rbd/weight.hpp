@@ -1,12 +1,13 @@
-// rbd/weight.hpp — WeightSpec (proj/include/rbd/weight.hpp:16-54). Only the
-// identity weight runs on the B200 path; a diagonal weight is carried for the
-// reference's dimension check (IncompatibleWeight) and is otherwise rejected
-// with InvalidArgument (next row).
+// rbd/weight.hpp — WeightSpec (proj/include/rbd/weight.hpp:16-54). The identity
+// and diagonal weights run on the B200 path (decompose and the ErrorWorkspace);
+// a sparse SPD weight exists only as the external marker of a loaded model.
 #ifndef RBD_B200_WEIGHT_HPP
 #define RBD_B200_WEIGHT_HPP
 
+#include <cmath>
 #include <cstdint>
 
+#include "rbd/errors.hpp"
 #include "rbd/types.hpp"
 
 namespace rbd {
@@ -17,7 +18,11 @@ class WeightSpec {
  public:
   WeightSpec() = default;
   static WeightSpec identity() { return WeightSpec(); }
-  static WeightSpec diagonal(Vector d) {
+  static WeightSpec diagonal(Vector d) {   // weight.cpp:11-21
+    if (d.size() == 0) throw InvalidArgument("diagonal weight must be non-empty");
+    for (Index i = 0; i < d.size(); ++i)
+      if (!(d[i] > 0.0) || !std::isfinite(d[i]))
+        throw InvalidArgument("diagonal weight entries must be strictly positive and finite");
     WeightSpec w;
     w.kind_ = WeightKind::diagonal;
     w.diag_ = std::move(d);

@@ -1,5 +1,6 @@
 // rbd/workspace.hpp — ErrorWorkspace API (proj/include/rbd/workspace.hpp:18-54),
-// identity weight, on the B200 (the workspace owns a device copy of X).
+// identity and diagonal weights, on the B200 (the workspace owns a device copy
+// of X).
 #ifndef RBD_B200_WORKSPACE_HPP
 #define RBD_B200_WORKSPACE_HPP
 
@@ -34,13 +35,19 @@ struct ScanResult {
 inline ErrorWorkspace workspace_init(const Matrix& x, const WeightSpec& a) {   // workspace.cpp:9-41
   if (!a.compatible_with(x.rows()))
     throw IncompatibleWeight("weight dimension does not match matrix rows");
-  if (a.kind() != WeightKind::identity)
-    throw InvalidArgument("workspace_init: only the identity weight runs on the B200 path");
+  if (a.kind() == WeightKind::sparse_spd)
+    throw InvalidArgument("workspace_init: sparse SPD weights are out of scope on the B200 path");
   ErrorWorkspace ws;
+  ws.kind = a.kind();
   ws.m = x.rows();
   ws.n = x.cols();
   rbd_ws_t h = nullptr;
-  detail::check(rbd_ws_init_host(detail::context(), x.data(), ws.m, ws.n, ws.m, ws.n, &h));
+  if (a.kind() == WeightKind::diagonal)
+    detail::check(rbd_ws_init_diag_host(detail::context(), x.data(), ws.m, ws.n, ws.m, ws.n,
+                                        a.diagonal_values().data(), a.diagonal_values().size(),
+                                        &h));
+  else
+    detail::check(rbd_ws_init_host(detail::context(), x.data(), ws.m, ws.n, ws.m, ws.n, &h));
   ws.h = std::shared_ptr<rbd_ws_s>(h, [](rbd_ws_s* p) { rbd_ws_destroy(p); });
   return ws;
 }
@@ -64,7 +71,14 @@ inline ScanResult residual_scan(const ErrorWorkspace& ws, const MatrixRef& t) { 
     throw DimensionMismatch("residual_scan: T shape does not match workspace");
   ScanResult r;
   int64_t arg = 0;
-  detail::check(rbd_ws_scan(ws.h.get(), &r.e_cur, &arg));
+  if (ws.kind == WeightKind::identity) {
+    detail::check(rbd_ws_scan(ws.h.get(), &r.e_cur, &arg));
+  } else {   // general weight: error_sq of every column with c = T[:, j]
+    std::vector<double> trow(static_cast<size_t>(ws.d * ws.n));
+    for (Index k = 0; k < ws.d; ++k)
+      for (Index j = 0; j < ws.n; ++j) trow[static_cast<size_t>(k * ws.n + j)] = t(k, j);
+    detail::check(rbd_ws_scan_T_host(ws.h.get(), trow.data(), &r.e_cur, &arg));
+  }
   r.argmax = arg;
   return r;
 }

@@ -154,6 +154,22 @@ int rbd_mgs_project_host(rbd_ctx_t ctx, const double* hv, int64_t m, const doubl
                          int64_t ldb, double breakdown_tol, int reorthogonalize, double* hxi,
                          double* norm, int* ok);
 /* Workspace over a device copy of host X (owned by the workspace). */
+/* ErrorWorkspace with a diagonal weight (workspace.cpp:24-29 init, 61-79 extend:
+ * the yax row X'(a o xi) and the Y'AY row; 84-99 error_sq with Y'AY). The
+ * residual_sq kept by the identity workspace is not maintained for a weight
+ * (as in the reference): scan with rbd_ws_scan_T. d_diag: diag_len device
+ * doubles (host doubles for _host); InvalidArgument for a bad diagonal,
+ * IncompatibleWeight when diag_len != m. */
+int rbd_ws_init_diag(rbd_ctx_t ctx, const double* dX, int64_t m, int64_t n, int64_t ldx,
+                     int64_t cap, const double* d_diag, int64_t diag_len, rbd_ws_t* out);
+int rbd_ws_init_diag_host(rbd_ctx_t ctx, const double* hX, int64_t m, int64_t n, int64_t ldx,
+                          int64_t cap, const double* h_diag, int64_t diag_len, rbd_ws_t* out);
+/* residual_scan(ws, T) for any weight (workspace.cpp:101-125): error_sq of every
+ * column with c = T[:, j], T the d x n coefficients row-major (device / host). */
+int rbd_ws_scan_T(rbd_ws_t ws, const double* dT, double* e_cur, int64_t* argmax);
+int rbd_ws_scan_T_host(rbd_ws_t ws, const double* hT, double* e_cur, int64_t* argmax);
+/* Y'AY (d x d row-major) of a diagonal workspace. */
+int rbd_ws_read_yay(rbd_ws_t ws, double* h_yay);
 int rbd_ws_init_host(rbd_ctx_t ctx, const double* hX, int64_t m, int64_t n, int64_t ldx,
                      int64_t cap, rbd_ws_t* out);
 int rbd_ws_extend_host(rbd_ws_t ws, const double* hxi);

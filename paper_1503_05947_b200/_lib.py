@@ -142,6 +142,11 @@ _SIGS = {
     "rbd_classify_host": (C.c_int, [_P, _P, _I64, _I64, _P, _I64, _P, _I64, _P, _P]),
     "rbd_nearest_columns": (C.c_int, [_P, _P, _I64, _I64, _I64, _P, _I64, _P, _P]),
     "rbd_compress_device": (C.c_int, [_P, _P, _I64, _I64, _I64, _P, _I64, _I64, _P, _I64]),
+    "rbd_ws_init_diag": (C.c_int, [_P, _P, _I64, _I64, _I64, _I64, _P, _I64, C.POINTER(_P)]),
+    "rbd_ws_init_diag_host": (C.c_int, [_P, _P, _I64, _I64, _I64, _I64, _P, _I64, C.POINTER(_P)]),
+    "rbd_ws_scan_T": (C.c_int, [_P, _P, C.POINTER(C.c_double), C.POINTER(_I64)]),
+    "rbd_ws_scan_T_host": (C.c_int, [_P, _P, C.POINTER(C.c_double), C.POINTER(_I64)]),
+    "rbd_ws_read_yay": (C.c_int, [_P, _P]),
     "rbd_model_write": (C.c_int, [_P, C.c_char_p, _I64, _I64, _I64, _P, _I64, _P, C.c_double, _P,
                                   C.c_int, _P]),
     "rbd_model_read_header": (C.c_int, [C.c_char_p, C.POINTER(_I64), C.POINTER(_I64),

@@ -528,24 +528,35 @@ def mgs_project(v, basis, breakdown_tol: float, reorthogonalize: bool = False,
 
 
 class Workspace:
-    """ErrorWorkspace (workspace.hpp:18-30), identity weight, on device.
+    """ErrorWorkspace (workspace.hpp:18-30) on device, identity or diagonal weight.
 
     workspace_init (workspace.cpp:9-41) at construction; extend(xi)
-    (workspace.cpp:43-60); scan() (workspace.cpp:101-125); error_sq(j, c)
-    (workspace.cpp:84-99)."""
+    (workspace.cpp:43-79); scan() (identity, workspace.cpp:101-113,123) and
+    scan_T(T) (any weight, :101-125); error_sq(j, c) (workspace.cpp:84-99)."""
 
-    def __init__(self, x, cap: Optional[int] = None, ctx: Optional[Context] = None):
+    def __init__(self, x, cap: Optional[int] = None, ctx: Optional[Context] = None, diag=None):
         if not _is_torch_cuda(x):
             raise InvalidArgument("Workspace: pass a torch CUDA tensor")
         self._lib = load_library()
         self.ctx = ctx or default_context(x.device.index or 0)
         self._x, ldx = _col_major_torch(x)
         self.m, self.n = self._x.shape
-        cap = cap if cap is not None else self.n
+        self.cap = cap if cap is not None else self.n
         h = C.c_void_p()
         torch.cuda.current_stream(x.device).synchronize()
-        check(self._lib.rbd_ws_init(self.ctx.handle, C.c_void_p(self._x.data_ptr()), self.m,
-                                    self.n, ldx, cap, C.byref(h)))
+        if diag is None:
+            self.weight_kind = 0
+            check(self._lib.rbd_ws_init(self.ctx.handle, C.c_void_p(self._x.data_ptr()), self.m,
+                                        self.n, ldx, self.cap, C.byref(h)))
+        else:   # WeightSpec::diagonal (workspace.cpp:24-29)
+            self.weight_kind = 1
+            self._diag = torch.as_tensor(diag, dtype=torch.float64,
+                                         device=x.device).reshape(-1).contiguous()
+            torch.cuda.current_stream(x.device).synchronize()
+            check(self._lib.rbd_ws_init_diag(
+                self.ctx.handle, C.c_void_p(self._x.data_ptr()), self.m, self.n, ldx, self.cap,
+                C.c_void_p(self._diag.data_ptr()) if self._diag.numel() else None,
+                self._diag.numel(), C.byref(h)))
         self.handle = h
 
     def close(self):
@@ -575,6 +586,29 @@ class Workspace:
         j = C.c_int64()
         check(self._lib.rbd_ws_scan(self.handle, C.byref(e), C.byref(j)))
         return e.value, j.value
+
+    def scan_T(self, T):
+        """residual_scan(ws, T) for any weight: T is d x n (numpy or CUDA tensor)."""
+        e = C.c_double()
+        j = C.c_int64()
+        if _is_torch_cuda(T):
+            Tc = T.contiguous()
+            torch.cuda.current_stream(T.device).synchronize()
+            check(self._lib.rbd_ws_scan_T(self.handle, C.c_void_p(Tc.data_ptr()), C.byref(e),
+                                          C.byref(j)))
+        else:
+            Th = np.ascontiguousarray(np.asarray(T, dtype=np.float64))
+            if Th.shape != (self.d, self.n):
+                raise DimensionMismatch("residual_scan: T shape does not match workspace")
+            check(self._lib.rbd_ws_scan_T_host(self.handle, _dp(Th) if Th.size else None,
+                                               C.byref(e), C.byref(j)))
+        return e.value, j.value
+
+    def yay(self):
+        """Y'AY (d x d) of a diagonal workspace (workspace.cpp:69-75)."""
+        out = np.zeros((max(self.d, 1), max(self.d, 1)))
+        check(self._lib.rbd_ws_read_yay(self.handle, _dp(out)))
+        return out[: self.d, : self.d]
 
     def error_sq(self, j: int, c) -> float:
         cc = np.ascontiguousarray(np.asarray(c, dtype=np.float64).reshape(-1))

@@ -266,4 +266,121 @@ __global__ void __launch_bounds__(kThreads) k_finalize_diag(FinalizeDiagArgs a) 
   finalize_reduce_tail(f, k, bv, bj, smr, &is_last);
 }
 
+// ---------------------------------------------------------------------------
+// ErrorWorkspace with a diagonal weight (rbd_ws_* on a diagonal workspace;
+// workspace.cpp:24-29, 61-79, 84-99, 101-125).
+// ---------------------------------------------------------------------------
+
+// out[j] = sum over chunks s of partial[s * n + j] (chunks in order).
+__global__ void k_rowsum(const double* __restrict__ partial, long long S, long long n,
+                         double* __restrict__ out) {
+  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < n;
+       j += (long long)gridDim.x * blockDim.x) {
+    double t = 0.0;
+    for (long long s = 0; s < S; ++s) t += partial[s * n + j];
+    out[j] = t;
+  }
+}
+
+// YAY row d (workspace.cpp:69-75): yay[d][k] = yay[k][d] = row[k] (k < d),
+// yay[d][d] = sum of the xi' A xi partials (in order).
+__global__ void k_yay_row(const double* __restrict__ row, long long d, const double* __restrict__ yy_part,
+                          int np, double* __restrict__ yay, long long ld) {
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < d;
+       k += (long long)gridDim.x * blockDim.x) {
+    yay[d * ld + k] = row[k];
+    yay[k * ld + d] = row[k];
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    double s = 0.0;
+    for (int b = 0; b < np; ++b) s += yy_part[b];
+    yay[d * ld + d] = s;
+  }
+}
+
+// error_sq (workspace.cpp:84-99) for one column: cross = c . yax[:, j],
+// quad = c' yay c (yay == nullptr: identity, quad = ||c||^2).
+__global__ void __launch_bounds__(kThreads) k_error_sq_w(const double* __restrict__ yax, long long n,
+                                                         long long d, long long j,
+                                                         const double* __restrict__ c,
+                                                         const double* __restrict__ yay, long long ld,
+                                                         const double* __restrict__ col_sq,
+                                                         double* __restrict__ out) {
+  __shared__ double sm[kWarps];
+  double cross = 0.0, quad = 0.0;
+  for (long long k = threadIdx.x; k < d; k += kThreads) {
+    cross = fma(c[k], yax[k * n + j], cross);
+    double yc = c[k];
+    if (yay) {
+      yc = 0.0;
+      for (long long l = 0; l < d; ++l) yc = fma(yay[k * ld + l], c[l], yc);
+    }
+    quad = fma(c[k], yc, quad);
+  }
+  cross = block_sum_fixed<kThreads>(cross, sm);
+  quad = block_sum_fixed<kThreads>(quad, sm);
+  if (threadIdx.x == 0) {
+    const double e2 = col_sq[j] - 2.0 * cross + quad;   // :95-96
+    out[0] = e2 > 0.0 ? e2 : 0.0;
+  }
+}
+
+// residual_scan for a general weight (workspace.cpp:114-122): error_sq of every
+// column with c = T[:, j] (T row-major d x n), argmax with smallest-index
+// ties, E_cur = sqrt(max(best, 0)) (:123); last-CTA reduction into out.
+__global__ void __launch_bounds__(kThreads) k_scan_T(const double* __restrict__ yax,
+                                                     const double* __restrict__ T, long long n,
+                                                     long long d, const double* __restrict__ yay,
+                                                     long long ld, const double* __restrict__ col_sq,
+                                                     Rec* rec, unsigned* counter, Rec* out) {
+  __shared__ Rec smr[kWarps];
+  __shared__ int is_last;
+  double bv = -1.0;
+  long long bj = 0x7fffffffffffffffLL;
+  for (long long j = blockIdx.x * (long long)kThreads + threadIdx.x; j < n;
+       j += (long long)gridDim.x * kThreads) {
+    double cross = 0.0, quad = 0.0;
+    for (long long k = 0; k < d; ++k) {
+      const double ck = T[k * n + j];
+      cross = fma(ck, yax[k * n + j], cross);
+      double yc = ck;
+      if (yay) {
+        yc = 0.0;
+        for (long long l = 0; l < d; ++l) yc = fma(yay[k * ld + l], T[l * n + j], yc);
+      }
+      quad = fma(ck, yc, quad);
+    }
+    double e2 = col_sq[j] - 2.0 * cross + quad;
+    e2 = e2 > 0.0 ? e2 : 0.0;
+    if (rec_better(e2, j, bv, bj)) {
+      bv = e2;
+      bj = j;
+    }
+  }
+  block_argmax<kThreads>(bv, bj, smr);
+  if (threadIdx.x == 0) {
+    rec[blockIdx.x] = Rec{bv, bj};
+    __threadfence();
+    is_last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  bv = -1.0;
+  bj = 0x7fffffffffffffffLL;
+  for (unsigned b = threadIdx.x; b < gridDim.x; b += kThreads) {
+    const Rec rr{__ldcg(&rec[b].v), __ldcg(&rec[b].j)};
+    if (rec_better(rr.v, rr.j, bv, bj)) {
+      bv = rr.v;
+      bj = rr.j;
+    }
+  }
+  block_argmax<kThreads>(bv, bj, smr);
+  if (threadIdx.x == 0) {
+    *counter = 0u;
+    if (bj == 0x7fffffffffffffffLL) bj = 0;
+    out[0] = Rec{sqrt(bv > 0.0 ? bv : 0.0), bj};
+  }
+}
+
 }  // namespace rbdk

@@ -299,6 +299,36 @@ int main() {
     weighted.weight = WeightSpec::diagonal(Vector{100.0, 1.0, 1.0, 1.0});
     CHECK(decompose(x, weighted).selected[1] == 0);
   }
+  // test_workspace.cpp:39-60 (identity and diagonal kinds) and a weighted scan
+  {
+    const Index m = 11, n = 6;
+    const Matrix x = random_matrix(m, n, 11);
+    const Vector a = random_positive(m, 12);
+    const WeightSpec kinds[] = {WeightSpec::identity(), WeightSpec::diagonal(a)};
+    for (const WeightSpec& w : kinds) {
+      const ErrorWorkspace ws = workspace_init(x, w);
+      const Vector cs = ws.col_sq();
+      for (Index j = 0; j < n; ++j) {
+        double q = 0.0;
+        for (Index i = 0; i < m; ++i)
+          q += (w.kind() == WeightKind::diagonal ? a[i] : 1.0) * x(i, j) * x(i, j);
+        CHECK(std::abs(cs[j] - q) <= 1e-12 * q);
+      }
+    }
+    Vector ones4(4);
+    for (Index i = 0; i < 4; ++i) ones4[i] = 1.0;
+    CHECK_THROWS_AS(workspace_init(random_matrix(5, 3, 14), WeightSpec::diagonal(ones4)),
+                    IncompatibleWeight);
+    CHECK_THROWS_AS(WeightSpec::diagonal(Vector(4)), InvalidArgument);   // test_weight.cpp:21-32
+    RbdConfig cfg = basic(4);
+    cfg.weight = WeightSpec::diagonal(a);
+    const RbdModel model = decompose(x, cfg);
+    ErrorWorkspace ws = workspace_init(x, cfg.weight);
+    for (Index k = 0; k < model.d; ++k) workspace_extend(ws, model.Y.col(k), x, cfg.weight);
+    const ScanResult scan = residual_scan(ws, model.T);
+    CHECK(std::abs(scan.e_cur - model.residual_history.back()) <=
+          1e-9 * std::max(1.0, model.residual_history.back()));
+  }
   // test_io.cpp:273-332: container round trip, size, corruption, missing file
   {
     namespace fs = std::filesystem;

@@ -14,7 +14,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 def declared_symbols():
     src = open(os.path.join(ROOT, "include", "rbd_cuda.h")).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return set(re.findall(r"\b(rbd_[a-z0-9_]+)\s*\(", src))
+    return set(re.findall(r"\b(rbd_[A-Za-z0-9_]+)\s*\(", src))
 
 
 def test_library_exports_every_declared_symbol():
@@ -23,7 +23,7 @@ def test_library_exports_every_declared_symbol():
     assert not missing, missing
     out = subprocess.run(["nm", "-D", "--defined-only", _build.LIB], capture_output=True,
                          text=True, check=True).stdout
-    exported = set(re.findall(r" T (rbd_[a-z0-9_]+)", out))
+    exported = set(re.findall(r" T (rbd_[A-Za-z0-9_]+)", out))
     assert declared_symbols() <= exported
 
 

@@ -137,3 +137,69 @@ def test_y_t_euclidean_and_history_direct_at_scale(cuda):
         R = x - g.Y[:, :k] @ g.T[:k]
         e2 = np.maximum(np.einsum("ij,i,ij->j", R, dg, R), 0.0).max()
         assert abs(g.residual_history[k - 1] ** 2 - e2) <= 1e-12 * colsq_a.max()
+
+
+# ---------------- the diagonal ErrorWorkspace (rbd_ws_* with a weight) ----------------
+
+def _cuda(x):
+    return torch.from_numpy(np.asfortranarray(x)).cuda()
+
+
+def test_workspace_col_sq_weighted(cuda):                        # test_workspace.cpp:39-60
+    m, n = 11, 6
+    x = oracle.random_matrix(m, n, 11)
+    dg = oracle.random_positive(m, 12)
+    ws = rbd.Workspace(_cuda(x), diag=dg)
+    col_sq, resid, _ = ws.read()
+    np.testing.assert_allclose(col_sq, np.einsum("ij,i,ij->j", x, dg, x), rtol=1e-12)
+    np.testing.assert_array_equal(resid, col_sq)
+
+
+def test_workspace_rejects_bad_weights(cuda):                    # test_workspace.cpp:62-66
+    x = _cuda(oracle.random_matrix(5, 3, 14))
+    with pytest.raises(rbd.IncompatibleWeight):
+        rbd.Workspace(x, diag=np.ones(4))
+    with pytest.raises(rbd.InvalidArgument):
+        rbd.Workspace(x, diag=np.r_[np.ones(4), 0.0])
+
+
+@pytest.mark.parametrize("instance", range(12))
+def test_workspace_offline_online_identity(cuda, instance):      # acceptance.cpp:185-231 (diag)
+    rng = np.random.default_rng(2000 + instance)
+    m = int(rng.integers(5, 41))
+    n = int(rng.integers(4, 31))
+    d = 1 + int(rng.integers(0, min(10, m, n)))
+    dg = rng.uniform(0.25, 4.0, m)
+    x = oracle.random_matrix(m, n, 7000 + instance)
+    model = oracle.decompose(x, d, diag=dg)
+    ws = rbd.Workspace(_cuda(x), cap=d, diag=dg)
+    ows = oracle.Workspace(x, diag=dg)
+    for k in range(model.d):
+        ws.extend(torch.from_numpy(model.Y[:, k].copy()).cuda())
+        ows.extend(model.Y[:, k])
+    np.testing.assert_allclose(ws.yay(), ows.yay(), rtol=0, atol=1e-12)
+    _, _, yax = ws.read()
+    for k in range(model.d):
+        np.testing.assert_allclose(yax[k], ows.yax_row(k), rtol=0, atol=1e-12 * max(1, np.abs(x).max()))
+    for j in range(n):
+        c = model.T[:, j].copy()
+        if instance % 2 == 1:
+            c += rng.uniform(-0.5, 0.5, c.shape)
+        fast = ws.error_sq(j, c)
+        r = x[:, j] - model.Y @ c
+        direct = max(float(np.dot(dg * r, r)), 0.0)
+        assert abs(fast - direct) <= 1e-9 * max(1.0, ows.col_sq()[j])
+    e, arg = ws.scan_T(model.T)
+    e_ref, arg_ref = ows.scan_T(model.T)
+    assert arg == arg_ref and e == pytest.approx(e_ref, rel=1e-9, abs=1e-12)
+
+
+def test_workspace_scan_T_identity_matches_scan(cuda):
+    x = oracle.random_matrix(60, 25, 9)
+    model = oracle.decompose(x, 8)
+    ws = rbd.Workspace(_cuda(x), cap=8)
+    for k in range(model.d):
+        ws.extend(torch.from_numpy(model.Y[:, k].copy()).cuda())
+    e1, j1 = ws.scan()
+    e2, j2 = ws.scan_T(model.T)
+    assert j1 == j2 and e1 == pytest.approx(e2, rel=1e-9)
