@@ -87,9 +87,9 @@ __global__ void __launch_bounds__(WARPS_M * WARPS_N * 32, 4)
     if (st < nk) load_stage(st, st);
     cp_async_commit();
   }
-  int koff[4];   // swizzled K-contiguous B stage (BKC), as in K5
+  int koff[4];   // swizzled K-contiguous B stage (BKC, dm_swz): (row, 4q + t)
 #pragma unroll
-  for (int q = 0; q < 4; ++q) koff[q] = 4 * (q ^ (g & 3)) + t;
+  for (int q = 0; q < 4; ++q) koff[q] = 4 * (q ^ (g & 3)) + (t ^ ((g & 1) << 1));
   const int rowA = wm * WM + g, colB = wn * WN + g;
   for (long long kt = 0; kt < nk; ++kt) {
     cp_async_wait<kDmStages - 2>();

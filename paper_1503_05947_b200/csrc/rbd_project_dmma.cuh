@@ -26,9 +26,14 @@ constexpr size_t dm_smem_bytes() {
 }
 
 // XOR swizzle of the 16-double rows: element (row, k) lives at
-// row*16 + (k ^ (4*(row & 3))). Keeps 16-byte chunks intact (cp.async) and
-// makes the m16n8k4 fragment loads (row g / g+8, k = kk + t) conflict free.
-__device__ __forceinline__ int dm_swz(int row, int k) { return row * kDmBK + (k ^ ((row & 3) << 2)); }
+// row*16 + (k ^ 4*(row & 3) ^ 2*(row & 1)). Keeps 16-byte chunks intact
+// (cp.async). K5 permutes k inside a stage (lane t of DMMA step q takes
+// k = 4t + q), so a lane's four elements of a row are one 32-byte group and
+// load as two 16-byte halves; the row-parity bit puts the two rows of an
+// 8-lane phase on different halves, which keeps those loads conflict free.
+__device__ __forceinline__ int dm_swz(int row, int k) {
+  return row * kDmBK + (k ^ ((row & 3) << 2) ^ ((row & 1) << 1));
+}
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -120,12 +125,11 @@ __global__ void __launch_bounds__(WARPS_M * WARPS_N * 32, 4)
     if (st < nk) load_stage(st, st);
     cp_async_commit();
   }
-  // swizzled fragment offsets: every fragment row has (row & 3) == (g & 3),
-  // so (row, 4q + t) sits at row*16 + 4*(q ^ (g & 3)) + t
+  // every fragment row has (row & 3) == (g & 3) and (row & 1) == (g & 1): with
+  // k = 4t + q, elements q = 2h, 2h+1 of the lane's group are the 16 bytes at
+  // row*16 + 4*(t ^ (g & 3)) + 2*(h ^ (g & 1)), in q order
   const int baseA = (wm * WM + g) * kDmBK, baseB = (wn * WN + g) * kDmBK;
-  int koff[4];
-#pragma unroll
-  for (int q = 0; q < 4; ++q) koff[q] = 4 * (q ^ (g & 3)) + t;
+  const int off0 = 4 * (t ^ (g & 3)) + 2 * (g & 1), off1 = 4 * (t ^ (g & 3)) + 2 * ((g & 1) ^ 1);
   for (long long kt = 0; kt < nk; ++kt) {
     cp_async_wait<kDmStages - 2>();
     __syncthreads();
@@ -138,19 +142,25 @@ __global__ void __launch_bounds__(WARPS_M * WARPS_N * 32, 4)
     const double* A = As + sc * BM * kDmBK;
     const double* B = Bs + sc * BN * kDmBK;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      double af[MT][2], bf[NT];
+    for (int h = 0; h < 2; ++h) {   // DMMA steps q = 2h and 2h + 1
+      const int off = h ? off1 : off0;
+      double2 a0[MT], a1[MT], bf[NT];
 #pragma unroll
       for (int a = 0; a < MT; ++a) {
-        af[a][0] = A[baseA + (a * 16) * kDmBK + koff[q]];
-        af[a][1] = A[baseA + (a * 16 + 8) * kDmBK + koff[q]];
+        a0[a] = *reinterpret_cast<const double2*>(A + baseA + (a * 16) * kDmBK + off);
+        a1[a] = *reinterpret_cast<const double2*>(A + baseA + (a * 16 + 8) * kDmBK + off);
       }
 #pragma unroll
-      for (int b = 0; b < NT; ++b) bf[b] = B[baseB + (b * 8) * kDmBK + koff[q]];
+      for (int b = 0; b < NT; ++b)
+        bf[b] = *reinterpret_cast<const double2*>(B + baseB + (b * 8) * kDmBK + off);
 #pragma unroll
       for (int a = 0; a < MT; ++a)
 #pragma unroll
-        for (int b = 0; b < NT; ++b) dmma_16x8x4(acc[a][b], af[a][0], af[a][1], bf[b]);
+        for (int b = 0; b < NT; ++b) dmma_16x8x4(acc[a][b], a0[a].x, a1[a].x, bf[b].x);
+#pragma unroll
+      for (int a = 0; a < MT; ++a)
+#pragma unroll
+        for (int b = 0; b < NT; ++b) dmma_16x8x4(acc[a][b], a0[a].y, a1[a].y, bf[b].y);
     }
     if (do_norm && tid < BN) {
       const double* xr = B + tid * kDmBK;
