@@ -138,6 +138,7 @@ struct rbd_ctx_s {
   // diagonal-weight loop (rbd_weighted.cuh): a o xi, xi'A xi partials, YAX row
   // partials, YAY row, YAX (d_max x n), cross, quad, col_sq_A, host-entry diag
   DevBuf wd_axi, wd_yy, wd_part2, wd_yrow, wd_yax, wd_cross, wd_quad, wd_colsq, wd_diag;
+  DevBuf wd_ppart2, wd_q, wd_yay;           // persistent weighted loop: Y'(a o w1), YAY
   DevBuf nn_part, nn_coords;               // classify: split minima, query coordinates
   DevBuf pj_ws;                            // K5 split-K partial slices
   DevBuf send, recv;                       // sharded mode: payload exchange buffers
@@ -450,14 +451,28 @@ int enqueue_step_diag(rbd_ctx_t ctx, const LoopBufs& L, const double* diag) {
 
 bool use_fused(long long d_max) { return d_max <= kFMaxCoef; }
 
+// Weighted loop: one persistent launch unless its decider's YAY matvec (d^2
+// doubles per step, read by one CTA) would rival the X pass (m n doubles at
+// HBM rate): d^2 <= m n / 256. RBD_DIAG_PATH=persistent|steps overrides.
+bool diag_persistent(rbd_ctx_t ctx, long long d_max, long long m, long long n) {
+  if (ctx->path != 0 || !use_fused(d_max)) return false;
+  if (const char* e = getenv("RBD_DIAG_PATH")) {
+    if (std::string(e) == "persistent") return true;
+    if (std::string(e) == "steps") return false;
+  }
+  return (double)d_max * (double)d_max <= (double)m * (double)n / 256.0;
+}
+
 int fused_grid(rbd_ctx_t ctx, long long m) {
   return (int)std::max<long long>(1, std::min<long long>(cdiv(m, kFRows), ctx->fused_grid_cap));
 }
 
 size_t fused_smem(long long dcap) { return sizeof(double) * 3 * (size_t)std::max<long long>(dcap, 1); }
-// c and p vectors, each zero-padded by one P1 batch (16 loads x kWarps columns)
-size_t persist_smem(long long dcap) {
-  return sizeof(double) * 2 * ((size_t)std::max<long long>(dcap, 1) + 16 * kWarps);
+// c and p vectors, each zero-padded by one P1 batch (16 loads x kWarps columns);
+// weighted: + p_k and the YAY row for the finaliser
+size_t persist_smem(long long dcap, bool diag = false) {
+  const size_t d = (size_t)std::max<long long>(dcap, 1);
+  return sizeof(double) * (2 * (d + 16 * kWarps) + (diag ? 2 * (d + 1) : 0));
 }
 
 // Materialise a pending column / clear the pending flag (used after the loop).
@@ -532,10 +547,14 @@ int enqueue_step_fused(rbd_ctx_t ctx, const LoopBufs& L) {
   return RBD_OK;
 }
 
-int persistent_grid(rbd_ctx_t ctx, int vec, long long d_max) {
+int persistent_grid(rbd_ctx_t ctx, int vec, long long d_max, bool diag = false) {
   int occ = 0;
-  const size_t smem = persist_smem(d_max);
-  if (vec == 2)
+  const size_t smem = persist_smem(d_max, diag);
+  if (diag)
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &occ, vec == 2 ? k_rbd_persistent<2, false, true> : k_rbd_persistent<1, false, true>,
+        kThreads, smem);
+  else if (vec == 2)
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_rbd_persistent<2, false>, kThreads, smem);
   else
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_rbd_persistent<1, false>, kThreads, smem);
@@ -543,11 +562,13 @@ int persistent_grid(rbd_ctx_t ctx, int vec, long long d_max) {
   return occ * ctx->nsm;
 }
 
-// The whole greedy loop in one cooperative launch (single GPU).
-int launch_persistent(rbd_ctx_t ctx, const LoopBufs& L) {
+// The whole greedy loop in one cooperative launch (single GPU); diag != nullptr:
+// the weighted loop (row f1; the caller has sized the wd_* buffers and zeroed
+// cross/quad).
+int launch_persistent(rbd_ctx_t ctx, const LoopBufs& L, const double* diag = nullptr) {
   const int vec = (L.ldx % 2 == 0 && L.m % 2 == 0 && aligned16(L.X) && aligned16(L.Y) &&
-                   aligned16(ctx->w.p)) ? 2 : 1;
-  const int grid = persistent_grid(ctx, vec, L.d_max);
+                   aligned16(ctx->w.p) && (!diag || aligned16(ctx->wd_axi.p))) ? 2 : 1;
+  const int grid = persistent_grid(ctx, vec, L.d_max, diag != nullptr);
   if (grid < 1) return set_err(RBD_ERR_CUDA, "persistent kernel: zero occupancy");
   const long long S = cdiv(L.m, kChunk);
   const long long ngx = cdiv(L.n, kCols);
@@ -586,6 +607,25 @@ int launch_persistent(rbd_ctx_t ctx, const LoopBufs& L) {
   a.d_max = L.d_max;
   a.ctl = ptr<StepCtl>(ctx->ctl);
   a.rdy = ptr<unsigned long long>(ctx->rdy);
+  if (diag) {
+    TRY(ensure(ctx->wd_ppart2, sizeof(double) * (size_t)std::max<long long>(grid, S) * L.d_max));
+    TRY(ensure(ctx->wd_q, sizeof(double) * (size_t)(L.d_max + 1)));
+    TRY(ensure(ctx->wd_yay, sizeof(double) * (size_t)L.d_max * (size_t)L.d_max));
+    TRY(ensure(ctx->wd_yy, sizeof(double) * (size_t)std::max<long long>(grid, diag_vec_grid(ctx, L.m))));
+    CU(cudaMemsetAsync(ctx->wd_part2.p, 0xFF, sizeof(double) * (size_t)S * L.n, ctx->stream));
+    a.diag = diag;
+    a.aw = ptr<double>(ctx->wd_axi);
+    a.npart2 = ptr<double>(ctx->wd_yy);
+    a.ppart2 = ptr<double>(ctx->wd_ppart2);
+    a.q = ptr<double>(ctx->wd_q);
+    a.partial2 = ptr<double>(ctx->wd_part2);
+    a.YAX = ptr<double>(ctx->wd_yax);
+    a.YAY = ptr<double>(ctx->wd_yay);
+    a.yrow = ptr<double>(ctx->wd_yrow);
+    a.cross = ptr<double>(ctx->wd_cross);
+    a.quad = ptr<double>(ctx->wd_quad);
+    a.colsq_a = ptr<double>(ctx->wd_colsq);
+  }
   a.progress = (ctx->ystream_dst && ctx->d_progress) ? ctx->d_progress : nullptr;
   if (a.progress) *(volatile long long*)ctx->h_progress = 0;
   a.phase_ns = nullptr;
@@ -603,12 +643,11 @@ int launch_persistent(rbd_ctx_t ctx, const LoopBufs& L) {
     a.trace_step = atoll(ts);
   }
   void* args[] = {&a};
-  const size_t smem = persist_smem(L.d_max);
-  cudaError_t e = vec == 2
-                      ? cudaLaunchCooperativeKernel((void*)k_rbd_persistent<2, false>, grid,
-                                                    kThreads, args, smem, ctx->stream)
-                      : cudaLaunchCooperativeKernel((void*)k_rbd_persistent<1, false>, grid,
-                                                    kThreads, args, smem, ctx->stream);
+  const size_t smem = persist_smem(L.d_max, diag != nullptr);
+  void* fn = diag ? (vec == 2 ? (void*)k_rbd_persistent<2, false, true>
+                              : (void*)k_rbd_persistent<1, false, true>)
+                  : (vec == 2 ? (void*)k_rbd_persistent<2, false> : (void*)k_rbd_persistent<1, false>);
+  cudaError_t e = cudaLaunchCooperativeKernel(fn, grid, kThreads, args, smem, ctx->stream);
   ctx->launches++;
   if (e != cudaSuccess)
     return set_err(RBD_ERR_CUDA, std::string("persistent launch: ") + cudaGetErrorString(e));
@@ -818,6 +857,10 @@ int rbd_ctx_create(int device, rbd_ctx_t* out) {
                        (int)fused_smem(kFMaxCoef));
   cudaFuncSetAttribute(k_rbd_persistent<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)fused_smem(kFMaxCoef));
+  cudaFuncSetAttribute(k_rbd_persistent<2, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)persist_smem(kFMaxCoef, true));
+  cudaFuncSetAttribute(k_rbd_persistent<1, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)persist_smem(kFMaxCoef, true));
   if (const char* pth = getenv("RBD_PATH")) ctx->path = (std::string(pth) == "graph") ? 1 : 0;
   if (ensure(ctx->bar, 64) == RBD_OK) cudaMemset(ctx->bar.p, 0, 64);
   *out = ctx;
@@ -837,6 +880,7 @@ int rbd_ctx_destroy(rbd_ctx_t ctx) {
                   &ctx->hX,      &ctx->hY,   &ctx->hT,      &ctx->ppart, &ctx->bar,
                   &ctx->wd_axi,  &ctx->wd_yy, &ctx->wd_part2, &ctx->wd_yrow, &ctx->wd_yax,
                   &ctx->wd_cross, &ctx->wd_quad, &ctx->wd_colsq, &ctx->wd_diag,
+                  &ctx->wd_ppart2, &ctx->wd_q, &ctx->wd_yay,
                   &ctx->nn_part, &ctx->nn_coords, &ctx->pj_ws,
                   &ctx->ctl,     &ctx->gcnt, &ctx->ygcnt,   &ctx->rdy,   &ctx->send,  &ctx->recv};
   for (DevBuf* b : bl) release(*b);
@@ -953,6 +997,12 @@ int decompose_device_impl(rbd_ctx_t ctx, const double* dX, int64_t m, int64_t n,
     TRY(ensure(ctx->ppart, sizeof(double) * S * d_cap));
     CU(cudaMemsetAsync(ctx->wd_cross.p, 0, sizeof(double) * n, ctx->stream));
     CU(cudaMemsetAsync(ctx->wd_quad.p, 0, sizeof(double) * n, ctx->stream));
+  }
+  const bool diag_pers = diag && diag_persistent(ctx, cfg->d_max, m, n);
+  if (diag_pers) {   // the weighted loop in one persistent launch
+    CU(cudaEventRecord(ev1, ctx->stream));
+    TRY(launch_persistent(ctx, L, diag));
+  } else if (diag) {
     CU(cudaEventRecord(ev1, ctx->stream));
     // host-driven steps; the done flag is polled every kDiagPoll steps, one
     // batch behind, so the device never waits for the host
@@ -1015,7 +1065,8 @@ int decompose_device_impl(rbd_ctx_t ctx, const double* dX, int64_t m, int64_t n,
   }
   CU(cudaEventRecord(ev2, ctx->stream));
   ctx->ystream_copied = 0;
-  if (ctx->ystream_dst && ctx->d_progress && ctx->path == 0 && use_fused(cfg->d_max) && !diag) {
+  if (ctx->ystream_dst && ctx->d_progress && ctx->path == 0 && use_fused(cfg->d_max) &&
+      (!diag || diag_pers)) {
     // stream finished Y columns to the host while the loop runs (copy engine,
     // second stream), 16 columns or more per copy
     if (!ctx->copy_stream) CU(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));

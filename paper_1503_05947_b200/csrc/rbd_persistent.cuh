@@ -21,9 +21,18 @@
 //           publishes the global argmax (workspace.cpp:107-113,123).
 //   --- barrier ---
 //       every CTA: stop test (decompose.cpp:87) on the published outcome
+//
+// DIAG (diagonal weight A = diag(a), row f1): Y and T stay Euclidean; the scan
+// is on e2_j = ||x_j||_A^2 - 2 cross_j + quad_j (rbd_weighted.cuh). With the
+// lazy xi_k = (w1 - Y p)/||w||, P1 also writes a o w1 and w1'Aw1, the Y'w1 and
+// X tiles take two vectors (w1, a o w1) in the same pass, and
+//   YAX[k, j]   = ((a o w1).x_j - p.YAX[0:k, j]) / ||w||
+//   YAY[k, 0:k] = (q - YAY p) / ||w||,   q = Y'(a o w1)
+//   YAY[k, k]   = (w1'Aw1 - 2 p.q + p'YAY p) / ||w||^2
+// (the decider forms the YAY row; the finaliser carries cross/quad).
 #pragma once
 
-#include "rbd_device.cuh"
+#include "rbd_weighted.cuh"
 
 namespace rbdk {
 
@@ -59,6 +68,19 @@ struct PersistArgs {
   unsigned long long* rdy;       // [0] CTAs through P1, [1 + s] rows of chunk s written by P1
                                  // (monotonic within a decompose, zeroed with ctl)
   long long* progress;           // optional mapped host word: Y columns [0, value) are final
+  // diagonal weight A = diag(a) (DIAG instantiation; see rbd_weighted.cuh)
+  const double* diag;            // a
+  double* aw;                    // a o w1_k (P1)
+  double* npart2;                // [G] P1 shares of w1' A w1
+  double* ppart2;                // [S][d_max] chunk partials of Y'(a o w1)
+  double* q;                     // [d_max] q_k = Y'(a o w1_k)
+  double* partial2;              // [S][n] X-tile partials of (a o w1).x_j (NaN = not written)
+  double* YAX;                   // [d_max][n] YAX[l, j] = (A y_l).x_j
+  double* YAY;                   // [d_max][d_max] Y'AY (symmetric)
+  double* yrow;                  // [d_max + 1] YAY[k, 0:k+1] of the current step
+  double* cross;                 // [n] sum_l T[l,j] YAX[l,j]
+  double* quad;                  // [n] T[:,j]' YAY T[:,j]
+  const double* colsq_a;         // [n] ||x_j||_A^2
 };
 
 __device__ __forceinline__ void red_release_add_u64(unsigned long long* p, unsigned long long v) {
@@ -188,12 +210,76 @@ constexpr int kTraceWords = 256;  // per CTA: [0] count, then (tag<<40 | time) w
 // column x_j, [4+m, 4+m+k+1) the column T[0:k+1, j].
 constexpr int kPayHead = 4;
 
-template <int VEC, bool SHARD>
+// DIAG decider: YAY[k, 0:k+1] = the new row of Y'AY (see the header), into
+// a.yrow and the symmetric YAY. CTA-wide; v = YAY[0:k,0:k] p is read as pairs of
+// YAY columns (coalesced, YAY symmetric) with 8 pairs in flight per thread.
+__device__ __forceinline__ void diag_yay_row(const PersistArgs& a, long long k, int re, double nrm,
+                                             double w1a, const double* p, double* sm) {
+  const long long ld = a.d_max;
+  double pq = 0.0, pv = 0.0;
+  for (long long l0 = 2 * threadIdx.x; l0 < k; l0 += 2 * kThreads) {
+    const bool two = l0 + 1 < k;
+    double v0 = 0.0, v1 = 0.0;
+    if (re) {
+      long long mm = 0;
+      if (two && (ld % 2 == 0)) {
+        for (; mm + 8 <= k; mm += 8) {
+          double2 yv[8];
+          double pm[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            yv[u] = __ldcg(reinterpret_cast<const double2*>(a.YAY + (mm + u) * ld + l0));
+            pm[u] = __ldcg(p + mm + u);
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            v0 = fma(yv[u].x, pm[u], v0);
+            v1 = fma(yv[u].y, pm[u], v1);
+          }
+        }
+      }
+      for (; mm < k; ++mm) {
+        const double pm = __ldcg(p + mm);
+        v0 = fma(__ldcg(a.YAY + mm * ld + l0), pm, v0);
+        if (two) v1 = fma(__ldcg(a.YAY + mm * ld + l0 + 1), pm, v1);
+      }
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const long long l = l0 + h;
+      if (h == 1 && !two) break;
+      const double vl = h ? v1 : v0;
+      const double ql = __ldcg(a.q + l);
+      const double yl = (re ? ql - vl : ql) / nrm;
+      a.yrow[l] = yl;
+      a.YAY[k * ld + l] = yl;
+      a.YAY[l * ld + k] = yl;
+      if (re) {
+        const double pl = __ldcg(p + l);
+        pq = fma(pl, ql, pq);
+        pv = fma(pl, vl, pv);
+      }
+    }
+  }
+  pq = block_sum_fixed<kThreads>(pq, sm);
+  pv = block_sum_fixed<kThreads>(pv, sm);
+  if (threadIdx.x == 0) {
+    const double num = re ? (w1a - 2.0 * pq) + pv : w1a;
+    const double ykk = num / (nrm * nrm);
+    a.yrow[k] = ykk;
+    a.YAY[k * ld + k] = ykk;
+  }
+}
+
+template <int VEC, bool SHARD, bool DIAG = false>
 __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
+  static_assert(!(SHARD && DIAG), "the weighted loop is single-GPU");
   extern __shared__ double dsm[];
   constexpr int kPBatch = 16 * kWarps / 2;   // columns per P1 batch of a half (16 loads per lane)
   double* cs = dsm;                        // c = T[0:k, j*], zero-padded to a batch multiple
   double* ps = dsm + a.d_max + kPBatch;    // p_{k-1} (pending column), zero-padded
+  double* pd = dsm + 2 * (a.d_max + kPBatch);   // DIAG: p_k (finaliser copy)
+  double* yd = pd + a.d_max + 1;                // DIAG: YAY[k, 0:k+1]
   __shared__ double red[kWarps][kCols];
   // P1 block: two warp-halves of 32*VEC rows each (warps 0-3 / 4-7); within a
   // half the 4 warps split the columns (l = warp%4 mod 4), so every row's sum
@@ -207,6 +293,11 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
   __shared__ Rec smr[kWarps];
   __shared__ long long sh_tile;
   __shared__ int sh_ok;
+  __shared__ int sh_dec[2];
+  __shared__ double sh_decd[2];
+  // DIAG two-vector tiles reduce through red_c (free outside P1)
+  double (*red2)[2 * kCols] = reinterpret_cast<double (*)[2 * kCols]>(&red_c[0][0]);
+  static_assert(sizeof(red_c) >= sizeof(double) * kWarps * 2 * kCols, "red2 alias");
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const long long m = a.m, n = a.n;
@@ -289,7 +380,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
     }
     const double* x = SHARD ? pay + kPayHead : a.X + jstar * a.ldx;
     __syncthreads();
-    double nacc = 0.0;
+    double nacc = 0.0, nacc2 = 0.0;
     for (long long rb = r_lo; rb < r_hi; rb += kPRows) {
       // lane owns rows i0 .. i0+VEC-1 of its half (a 16-byte pair when VEC == 2)
       const int half = warp / kPW, wh = warp % kPW;
@@ -297,12 +388,13 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
       const long long iend = (rb + kPRows < r_hi) ? rb + kPRows : r_hi;   // rows of this block
       // the first warp of each half finishes the half's rows: their x and
       // w1_{k-1} loads go out now and land while the block's Y batches stream
-      double xpre[VEC], wpre[VEC];
+      double xpre[VEC], wpre[VEC], apre[VEC];
 #pragma unroll
       for (int v = 0; v < VEC; ++v) {
         const bool in = wh == 0 && i0 + v < iend;
         xpre[v] = (in && live) ? __ldcg(&x[i0 + v]) : 0.0;
         wpre[v] = (in && pending) ? __ldcg(&a.w[i0 + v]) : 0.0;
+        if constexpr (DIAG) apre[v] = (in && live) ? __ldg(&a.diag[i0 + v]) : 0.0;
       }
       double acc_c[VEC], acc_p[VEC];
 #pragma unroll
@@ -370,6 +462,11 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
             const double w1 = xpre[v] - sc;                  // first pass of column k
             a.w[i] = w1;
             nacc = fma(w1, w1, nacc);
+            if constexpr (DIAG) {
+              const double awv = apre[v] * w1;               // a o w1 (weight.cpp:83)
+              a.aw[i] = awv;
+              nacc2 = fma(awv, w1, nacc2);
+            }
           }
         }
       }
@@ -379,6 +476,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
     if (!live) continue;   // materialisation-only pass after the stop
     {
       const double sblk = block_sum_fixed<kThreads>(warp % kPW == 0 ? nacc : 0.0, smn);
+      if constexpr (DIAG) {
+        const double sblk2 = block_sum_fixed<kThreads>(warp % kPW == 0 ? nacc2 : 0.0, smn);
+        if (tid == 0) a.npart2[cta] = sblk2;
+      }
       // block_sum_fixed ends with __syncthreads: every P1 write of this CTA
       // (w1 rows, Y column k-1 rows) precedes the release-adds below
       if (tid == 0) {
@@ -449,6 +550,14 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
       ctl->norm = norm0;
       ctl->reorth = 0;
       ctl->breakdown = (norm0 < tol || norm0 == 0.0) ? 1 : 0;
+      if constexpr (DIAG) {   // YAY[0, 0] = w1'Aw1 / ||w1||^2
+        double w1a = 0.0;
+        for (int b = 0; b < G; ++b) w1a += __ldcg(&a.npart2[b]);
+        const double y00 = w1a / (norm0 * norm0);
+        a.yrow[0] = y00;
+        a.YAY[0] = y00;
+        __threadfence();
+      }
       st_release_s64(&ctl->p_step, k + 1);
     }
     // Groups whose last chunk this CTA swept and that are not finalised yet
@@ -478,6 +587,15 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
       re_s = __ldcg(&ctl->reorth);
       bd_s = __ldcg(&ctl->breakdown);
       nrm_s = __ldcg(&ctl->norm);
+      if constexpr (DIAG) {
+        if (!bd_s) {
+          for (long long l = tid; l <= k; l += kThreads) {
+            pd[l] = (re_s && l < k) ? __ldcg(&pbuf(k)[l]) : 0.0;
+            yd[l] = __ldcg(&a.yrow[l]);
+          }
+          __syncthreads();
+        }
+      }
       p_ready = true;
       return true;
     };
@@ -492,10 +610,35 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
       const long long j = g * kCols + (warp & 3);
       const bool mine = g >= 0 && j < n;
       double sp = 0.0, corr = 0.0, rj = 0.0;
+      double sp2 = 0.0, corr2 = 0.0, gg = 0.0;   // DIAG: (a o w1).x_j, p.YAX[:, j], YAY row . T[:, j]
       if (mine) {   // a chunk partial not written yet is NaN, and so is the sum
         for (long long ss = lane; ss < S; ss += 32) sp += ld_relaxed_f64(&a.partial[ss * n + j]);
-        if (lane == 0) rj = __ldcg(&a.r[j]);
-        if (re_s && !bd_s) {
+        if constexpr (DIAG) {
+          for (long long ss = lane; ss < S; ss += 32) sp2 += ld_relaxed_f64(&a.partial2[ss * n + j]);
+          sp = (sp2 == sp2) ? sp : sp2;   // NaN if either row is incomplete
+          if (!bd_s) {
+            for (long long l0 = 0; l0 < k; l0 += 256) {
+              double tv[8], av[8];
+#pragma unroll
+              for (int u = 0; u < 8; ++u) {
+                const long long l = l0 + lane + 32 * u;
+                tv[u] = (l < k) ? __ldcg(&a.T[l * n + j]) : 0.0;
+                av[u] = (l < k && re_s) ? __ldcg(&a.YAX[l * n + j]) : 0.0;
+              }
+#pragma unroll
+              for (int u = 0; u < 8; ++u) {
+                const long long l = l0 + lane + 32 * u;
+                const double pl = (l < k) ? pd[l] : 0.0, yl = (l < k) ? yd[l] : 0.0;
+                corr = fma(pl, tv[u], corr);
+                corr2 = fma(pl, av[u], corr2);
+                gg = fma(yl, tv[u], gg);
+              }
+            }
+          }
+        } else if (lane == 0) {
+          rj = __ldcg(&a.r[j]);
+        }
+        if (!DIAG && re_s && !bd_s) {
           for (long long l0 = 0; l0 < k; l0 += 512) {
             double tv[16], pv[16];
 #pragma unroll
@@ -515,16 +658,43 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
       if (block && mine && !commit) {
         sp = 0.0;
         for (long long ss = lane; ss < S; ss += 32) sp += poll_f64(&a.partial[ss * n + j]);
+        if constexpr (DIAG) {
+          sp2 = 0.0;
+          for (long long ss = lane; ss < S; ss += 32) sp2 += poll_f64(&a.partial2[ss * n + j]);
+        }
         commit = true;
       }
       if (commit) {
         for (long long ss = lane; ss < S; ss += 32) st_relaxed_f64(&a.partial[ss * n + j], kNaN);
+        if constexpr (DIAG)
+          for (long long ss = lane; ss < S; ss += 32) st_relaxed_f64(&a.partial2[ss * n + j], kNaN);
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) {
           sp += __shfl_xor_sync(0xffffffffu, sp, off);
           corr += __shfl_xor_sync(0xffffffffu, corr, off);
+          if constexpr (DIAG) {
+            sp2 += __shfl_xor_sync(0xffffffffu, sp2, off);
+            corr2 += __shfl_xor_sync(0xffffffffu, corr2, off);
+            gg += __shfl_xor_sync(0xffffffffu, gg, off);
+          }
         }
-        if (lane == 0 && !bd_s) {
+        if (DIAG && lane == 0 && !bd_s) {
+          // weighted bookkeeping (rbd_weighted.cuh; workspace.cpp:61-99)
+          const double tt = (sp - corr) / nrm_s;                 // decompose.cpp:93
+          const double ya = (sp2 - corr2) / nrm_s;               // workspace.cpp:66
+          a.T[k * n + j] = tt;
+          a.YAX[k * n + j] = ya;
+          const double cr = a.cross[j] + tt * ya;
+          const double qd = a.quad[j] + (2.0 * tt * gg + yd[k] * tt * tt);
+          a.cross[j] = cr;
+          a.quad[j] = qd;
+          double e2 = a.colsq_a[j] - 2.0 * cr + qd;              // workspace.cpp:88-97
+          e2 = e2 > 0.0 ? e2 : 0.0;
+          if (rec_better(e2, j, bv, bj)) {
+            bv = e2;
+            bj = j;
+          }
+        } else if (!DIAG && lane == 0 && !bd_s) {
           const double tt = (sp - corr) / nrm_s;
           a.T[k * n + j] = tt;                                   // decompose.cpp:93
           const double sq = __dmul_rn(tt, tt);
@@ -560,16 +730,26 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
       trace(k, 4 | ((unsigned long long)t << 8));
       if (tid == 0) next = (long long)(atomicAdd(&ctl->tile_ctr, 1ull) - tile_base);
       if (t < gy) {
-        for (long long s = 0; s < S; ++s)
-          sweep_tiles<VEC, MODE_DOT, LOAD_CG, true>(a.Y, m, m, k, a.w, a.ppart, a.d_max,
-                                                     s * gy + t, 1LL << 40, red, dummy_nf,
-                                                     dummy_nz);
+        for (long long s = 0; s < S; ++s) {
+          if constexpr (DIAG)
+            sweep_tile_dot2<VEC, LOAD_CG, true>(a.Y, m, m, k, a.w, a.aw, a.ppart, a.ppart2,
+                                                a.d_max, s * gy + t, red2);
+          else
+            sweep_tiles<VEC, MODE_DOT, LOAD_CG, true>(a.Y, m, m, k, a.w, a.ppart, a.d_max,
+                                                       s * gy + t, 1LL << 40, red, dummy_nf,
+                                                       dummy_nz);
+        }
         // the partials of this group were written by this CTA (CTA-visible)
         if (tid < kCols && t * kCols + tid < k) {
           const long long l = t * kCols + tid;
           double v = 0.0;
           for (long long s = 0; s < S; ++s) v += a.ppart[s * a.d_max + l];
           pbuf(k)[l] = v;
+          if constexpr (DIAG) {
+            double v2 = 0.0;
+            for (long long s = 0; s < S; ++s) v2 += a.ppart2[s * a.d_max + l];
+            a.q[l] = v2;
+          }
         }
         __syncthreads();
         if (tid == 0) {
@@ -589,16 +769,34 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
           double w1n2 = 0.0;
           for (int b = tid; b < G; b += kThreads) w1n2 += __ldcg(&a.npart[b]);
           w1n2 = block_sum_fixed<kThreads>(w1n2, smn);
+          double w1a = 0.0;
+          if constexpr (DIAG) {
+            for (int b = tid; b < G; b += kThreads) w1a += __ldcg(&a.npart2[b]);
+            w1a = block_sum_fixed<kThreads>(w1a, smn);
+          }
           if (tid == 0) {
             ctl->ydone = 0u;
             const int re = (cfg_reorth || sqrt(w1n2) < 0.5 * sqrt(xnorm2)) ? 1 : 0;  // :28
             double wn2 = re ? w1n2 - pn : w1n2;
             wn2 = wn2 > 0.0 ? wn2 : 0.0;
             const double nrm = sqrt(wn2);
+            const int bd = (nrm < tol || nrm == 0.0) ? 1 : 0;                       // :29-30
             ctl->norm = nrm;
             ctl->reorth = re;
-            ctl->breakdown = (nrm < tol || nrm == 0.0) ? 1 : 0;                     // :29-30
-            st_release_s64(&ctl->p_step, k + 1);
+            ctl->breakdown = bd;
+            sh_dec[0] = re;
+            sh_dec[1] = bd;
+            sh_decd[0] = nrm;
+            if (!DIAG) st_release_s64(&ctl->p_step, k + 1);
+          }
+          if constexpr (DIAG) {   // the YAY row, then publish
+            __syncthreads();
+            if (!sh_dec[1]) diag_yay_row(a, k, sh_dec[0], sh_decd[0], w1a, pbuf(k), smn);
+            __syncthreads();
+            if (tid == 0) {
+              __threadfence();
+              st_release_s64(&ctl->p_step, k + 1);
+            }
           }
         }
         mark(6);
@@ -610,9 +808,13 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
         // end of the queue
         const long long tx = t - gy;
         const long long g = tx / S, s = tx - g * S;
-        sweep_tiles<VEC, MODE_DOT, LOAD_STREAM, true>(a.X, a.ldx, m, n, a.w, a.partial, n,
-                                                       s * ngx + g, 1LL << 40, red, dummy_nf,
-                                                       dummy_nz);
+        if constexpr (DIAG)
+          sweep_tile_dot2<VEC, LOAD_STREAM, true>(a.X, a.ldx, m, n, a.w, a.aw, a.partial,
+                                                  a.partial2, n, s * ngx + g, red2);
+        else
+          sweep_tiles<VEC, MODE_DOT, LOAD_STREAM, true>(a.X, a.ldx, m, n, a.w, a.partial, n,
+                                                         s * ngx + g, 1LL << 40, red, dummy_nf,
+                                                         dummy_nz);
         mark(7);
         if (npend > 0) finalize_pass(false);
         if (s == S - 1) {

@@ -64,7 +64,9 @@ __global__ void __launch_bounds__(kThreads) k_diag_vec(const double* __restrict_
 // Same thread -> row layout, per-thread fma order (groups ascending, .x then
 // .y) and reduction tree as sweep_tiles<VEC, MODE_DOT>, so `partial` is
 // bit-identical to the identity sweep's; out-of-range rows load 0.
-template <int VEC>
+// ALOAD: LOAD_STREAM (X) or LOAD_CG (Y, written inside the persistent loop);
+// VCOH: the vectors are read L2-coherently (written earlier in the same launch).
+template <int VEC, int ALOAD = LOAD_STREAM, bool VCOH = false>
 __device__ __forceinline__ void sweep_tile_dot2(const double* __restrict__ A, long long lda,
                                                 long long m, long long ncols,
                                                 const double* __restrict__ v,
@@ -100,31 +102,36 @@ __device__ __forceinline__ void sweep_tile_dot2(const double* __restrict__ A, lo
       const long long e = (long long)(tid + (ub + u) * kThreads) * VEC;
       if (e + VEC <= rows) {
         if constexpr (VEC == 2) {
-          const double2 y2 = ld_keep2(vr + e), z2 = ld_keep2(wr + e);
+          const double2 y2 = VCOH ? __ldcg(reinterpret_cast<const double2*>(vr + e)) : ld_keep2(vr + e);
+          const double2 z2 = VCOH ? __ldcg(reinterpret_cast<const double2*>(wr + e)) : ld_keep2(wr + e);
           yv[u][0] = y2.x;
           yv[u][VEC - 1] = y2.y;
           zv[u][0] = z2.x;
           zv[u][VEC - 1] = z2.y;
 #pragma unroll
           for (int c = 0; c < kCols; ++c) {
-            const double2 x2 = ld_stream2(Ac[c] + e);
+            const double2 x2 = ALOAD == LOAD_STREAM ? ld_stream2(Ac[c] + e)
+                               : __ldcg(reinterpret_cast<const double2*>(Ac[c] + e));
             xv[u][c][0] = x2.x;
             xv[u][c][VEC - 1] = x2.y;
           }
         } else {
-          yv[u][0] = ld_keep1(vr + e);
-          zv[u][0] = ld_keep1(wr + e);
+          yv[u][0] = VCOH ? __ldcg(vr + e) : ld_keep1(vr + e);
+          zv[u][0] = VCOH ? __ldcg(wr + e) : ld_keep1(wr + e);
 #pragma unroll
-          for (int c = 0; c < kCols; ++c) xv[u][c][0] = ld_stream1(Ac[c] + e);
+          for (int c = 0; c < kCols; ++c)
+            xv[u][c][0] = ALOAD == LOAD_STREAM ? ld_stream1(Ac[c] + e) : __ldcg(Ac[c] + e);
         }
       } else {
 #pragma unroll
         for (int q = 0; q < VEC; ++q) {
           const bool in = e + q < rows;
-          yv[u][q] = in ? __ldg(vr + e + q) : 0.0;
-          zv[u][q] = in ? __ldg(wr + e + q) : 0.0;
+          yv[u][q] = in ? (VCOH ? __ldcg(vr + e + q) : __ldg(vr + e + q)) : 0.0;
+          zv[u][q] = in ? (VCOH ? __ldcg(wr + e + q) : __ldg(wr + e + q)) : 0.0;
 #pragma unroll
-          for (int c = 0; c < kCols; ++c) xv[u][c][q] = in ? __ldcs(Ac[c] + e + q) : 0.0;
+          for (int c = 0; c < kCols; ++c)
+            xv[u][c][q] = in ? (ALOAD == LOAD_STREAM ? __ldcs(Ac[c] + e + q) : __ldcg(Ac[c] + e + q))
+                             : 0.0;
         }
       }
     }
