@@ -211,53 +211,72 @@ constexpr int kTraceWords = 256;  // per CTA: [0] count, then (tag<<40 | time) w
 constexpr int kPayHead = 4;
 
 // DIAG decider: YAY[k, 0:k+1] = the new row of Y'AY (see the header), into
-// a.yrow and the symmetric YAY. CTA-wide; v = YAY[0:k,0:k] p is read as pairs of
-// YAY columns (coalesced, YAY symmetric) with 8 pairs in flight per thread.
+// a.yrow and the symmetric YAY. CTA-wide: v = YAY[0:k,0:k] p with every warp on
+// 8 column pairs x 4 row residues (lanes 0-7 / 8-15 / ... read 128 contiguous
+// bytes of one row), 8 double2 loads in flight per lane, residues combined by
+// shuffles in a fixed order.
 __device__ __forceinline__ void diag_yay_row(const PersistArgs& a, long long k, int re, double nrm,
                                              double w1a, const double* p, double* sm) {
   const long long ld = a.d_max;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int pr = lane & 7, rs = lane >> 3;   // pair within the warp's 8, row residue mod 4
+  const bool vec2 = (ld % 2) == 0;
   double pq = 0.0, pv = 0.0;
-  for (long long l0 = 2 * threadIdx.x; l0 < k; l0 += 2 * kThreads) {
-    const bool two = l0 + 1 < k;
+  const long long npairs = (k + 1) / 2;
+  for (long long pb = 0; pb < npairs; pb += 8 * kWarps) {
+    const long long pair = pb + warp * 8 + pr;
+    const long long l0 = 2 * pair;
+    const bool have = pair < npairs, two = l0 + 1 < k;
     double v0 = 0.0, v1 = 0.0;
-    if (re) {
-      long long mm = 0;
-      if (two && (ld % 2 == 0)) {
-        for (; mm + 8 <= k; mm += 8) {
-          double2 yv[8];
-          double pm[8];
+    if (re && have) {
+      long long mm = rs;
+      for (; mm + 4 * 7 < k; mm += 4 * 8) {
+        double2 yv[8];
+        double pm[8];
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            yv[u] = __ldcg(reinterpret_cast<const double2*>(a.YAY + (mm + u) * ld + l0));
-            pm[u] = __ldcg(p + mm + u);
+        for (int u = 0; u < 8; ++u) {
+          const double* src = a.YAY + (mm + 4 * u) * ld + l0;
+          if (vec2 && two) {
+            yv[u] = __ldcg(reinterpret_cast<const double2*>(src));
+          } else {
+            yv[u].x = __ldcg(src);
+            yv[u].y = two ? __ldcg(src + 1) : 0.0;
           }
+          pm[u] = __ldcg(p + mm + 4 * u);
+        }
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            v0 = fma(yv[u].x, pm[u], v0);
-            v1 = fma(yv[u].y, pm[u], v1);
-          }
+        for (int u = 0; u < 8; ++u) {
+          v0 = fma(yv[u].x, pm[u], v0);
+          v1 = fma(yv[u].y, pm[u], v1);
         }
       }
-      for (; mm < k; ++mm) {
+      for (; mm < k; mm += 4) {
         const double pm = __ldcg(p + mm);
         v0 = fma(__ldcg(a.YAY + mm * ld + l0), pm, v0);
         if (two) v1 = fma(__ldcg(a.YAY + mm * ld + l0 + 1), pm, v1);
       }
     }
+    // residues 0..3 -> lane pr (fixed order: (r0 + r1) + (r2 + r3))
+    v0 += __shfl_xor_sync(0xffffffffu, v0, 8);
+    v1 += __shfl_xor_sync(0xffffffffu, v1, 8);
+    v0 += __shfl_xor_sync(0xffffffffu, v0, 16);
+    v1 += __shfl_xor_sync(0xffffffffu, v1, 16);
+    if (rs == 0 && have) {
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const long long l = l0 + h;
-      if (h == 1 && !two) break;
-      const double vl = h ? v1 : v0;
-      const double ql = __ldcg(a.q + l);
-      const double yl = (re ? ql - vl : ql) / nrm;
-      a.yrow[l] = yl;
-      a.YAY[k * ld + l] = yl;
-      a.YAY[l * ld + k] = yl;
-      if (re) {
-        const double pl = __ldcg(p + l);
-        pq = fma(pl, ql, pq);
-        pv = fma(pl, vl, pv);
+      for (int h = 0; h < 2; ++h) {
+        const long long l = l0 + h;
+        if (h == 1 && !two) break;
+        const double vl = h ? v1 : v0;
+        const double ql = __ldcg(a.q + l);
+        const double yl = (re ? ql - vl : ql) / nrm;
+        a.yrow[l] = yl;
+        a.YAY[k * ld + l] = yl;
+        a.YAY[l * ld + k] = yl;
+        if (re) {
+          const double pl = __ldcg(p + l);
+          pq = fma(pl, ql, pq);
+          pv = fma(pl, vl, pv);
+        }
       }
     }
   }
@@ -732,8 +751,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
       if (t < gy) {
         for (long long s = 0; s < S; ++s) {
           if constexpr (DIAG)
-            sweep_tile_dot2<VEC, LOAD_CG, true>(a.Y, m, m, k, a.w, a.aw, a.ppart, a.ppart2,
-                                                a.d_max, s * gy + t, red2);
+            sweep_tile_dot2<VEC, LOAD_CG, true, 2>(a.Y, m, m, k, a.w, a.aw, a.ppart, a.ppart2,
+                                                   a.d_max, s * gy + t, red2);
           else
             sweep_tiles<VEC, MODE_DOT, LOAD_CG, true>(a.Y, m, m, k, a.w, a.ppart, a.d_max,
                                                        s * gy + t, 1LL << 40, red, dummy_nf,
@@ -809,8 +828,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
         const long long tx = t - gy;
         const long long g = tx / S, s = tx - g * S;
         if constexpr (DIAG)
-          sweep_tile_dot2<VEC, LOAD_STREAM, true>(a.X, a.ldx, m, n, a.w, a.aw, a.partial,
-                                                  a.partial2, n, s * ngx + g, red2);
+          sweep_tile_dot2<VEC, LOAD_STREAM, true, 2>(a.X, a.ldx, m, n, a.w, a.aw, a.partial,
+                                                     a.partial2, n, s * ngx + g, red2);
         else
           sweep_tiles<VEC, MODE_DOT, LOAD_STREAM, true>(a.X, a.ldx, m, n, a.w, a.partial, n,
                                                          s * ngx + g, 1LL << 40, red, dummy_nf,

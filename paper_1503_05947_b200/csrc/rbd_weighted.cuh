@@ -66,7 +66,7 @@ __global__ void __launch_bounds__(kThreads) k_diag_vec(const double* __restrict_
 // bit-identical to the identity sweep's; out-of-range rows load 0.
 // ALOAD: LOAD_STREAM (X) or LOAD_CG (Y, written inside the persistent loop);
 // VCOH: the vectors are read L2-coherently (written earlier in the same launch).
-template <int VEC, int ALOAD = LOAD_STREAM, bool VCOH = false>
+template <int VEC, int ALOAD = LOAD_STREAM, bool VCOH = false, int UB = 2>
 __device__ __forceinline__ void sweep_tile_dot2(const double* __restrict__ A, long long lda,
                                                 long long m, long long ncols,
                                                 const double* __restrict__ v,
@@ -82,7 +82,7 @@ __device__ __forceinline__ void sweep_tile_dot2(const double* __restrict__ A, lo
   const long long rows = (m - row0 < kChunk) ? m - row0 : kChunk;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int U = kChunk / (VEC * kThreads);
-  constexpr int UB = 2;
+  static_assert(U % UB == 0, "batch must divide the chunk");
   double acc[kCols], acc2[kCols];
   const double* Ac[kCols];
 #pragma unroll
