@@ -95,6 +95,16 @@ int rbd_ctx_destroy(rbd_ctx_t ctx);
 int rbd_ctx_set_stream(rbd_ctx_t ctx, void* cuda_stream);
 /* Number of kernel launches issued by this context since creation (evidence). */
 int64_t rbd_ctx_launch_count(rbd_ctx_t ctx);
+
+/* Test instrumentation for the parity protocol (no reference
+ * counterpart): later decompose calls on ctx start at h_selected[0] and take
+ * h_selected[k] instead of the greedy argmax at step k < count (the residual
+ * history still records the argmax residual, decompose.cpp:97-99). Used to
+ * re-run the B200 loop on the oracle's selection after an admissible near-tie
+ * divergence so Y, T and residuals stay comparable for all steps. Implemented
+ * on the persistent loop (identity and diagonal weight); other paths return
+ * RBD_ERR_INVALID_ARGUMENT. count = 0 clears. */
+int rbd_set_forced_selection(rbd_ctx_t ctx, const int64_t* h_selected, int64_t count);
 int rbd_ctx_synchronize(rbd_ctx_t ctx);
 /* The cudaStream_t the context launches on (for event timing by callers). */
 void* rbd_ctx_stream(rbd_ctx_t ctx);

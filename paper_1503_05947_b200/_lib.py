@@ -132,6 +132,7 @@ _SIGS = {
     "rbd_ctx_destroy": (C.c_int, [_P]),
     "rbd_ctx_set_stream": (C.c_int, [_P, _P]),
     "rbd_ctx_launch_count": (C.c_int64, [_P]),
+    "rbd_set_forced_selection": (C.c_int, [_P, _P, C.c_int64]),
     "rbd_ctx_synchronize": (C.c_int, [_P]),
     "rbd_ctx_stream": (_P, [_P]),
     "rbd_decompose_device": (C.c_int, [_P, _P, _I64, _I64, _I64, C.POINTER(Config), _P, _P, _P, _P,
@@ -254,6 +255,15 @@ class Context:
 
     def synchronize(self):
         check(self._lib.rbd_ctx_synchronize(self.handle))
+
+    def force_selection(self, selected=None):
+        """Parity-protocol instrumentation: later decompose calls on
+        this context follow `selected` instead of the greedy argmax (None clears)."""
+        import numpy as np
+        arr = np.ascontiguousarray(np.asarray([] if selected is None else selected,
+                                              dtype=np.int64).reshape(-1))
+        check(self._lib.rbd_set_forced_selection(
+            self.handle, arr.ctypes.data_as(C.c_void_p) if arr.size else None, arr.size))
 
 
 _tls = threading.local()

@@ -161,12 +161,23 @@ class Model:
 
 def decompose(x, d_max: int, eps_r: float = 0.0, diag=None, sparse=None, start_column: int = 0,
               reorthogonalize: bool = False, breakdown_tol: float = -1.0,
-              start_seed: Optional[int] = None, ctx: Optional[Context] = None) -> Model:
+              start_seed: Optional[int] = None, ctx: Optional[Context] = None,
+              forced_selection=None) -> Model:
     """rbd.decompose (bindings.cpp:69-78) -> rbd::decompose (decompose.cpp:53-111).
 
     numpy input: end-to-end host entry (rbd_decompose_host).
     torch CUDA input: device-resident entry (rbd_decompose_device).
+    forced_selection: parity-test instrumentation; follow this
+    column sequence instead of the greedy argmax (persistent loop only).
     """
+    if forced_selection is not None:
+        ctx = ctx or default_context((x.device.index or 0) if _is_torch_cuda(x) else 0)
+        ctx.force_selection(forced_selection)
+        try:
+            return decompose(x, d_max, eps_r, diag, sparse, start_column, reorthogonalize,
+                             breakdown_tol, start_seed, ctx)
+        finally:
+            ctx.force_selection(None)
     cfg = make_config(d_max, eps_r, start_column, reorthogonalize, breakdown_tol, start_seed,
                       diag, sparse)
     lib = load_library()

@@ -139,6 +139,8 @@ struct rbd_ctx_s {
   // partials, YAY row, YAX (d_max x n), cross, quad, col_sq_A, host-entry diag
   DevBuf wd_axi, wd_yy, wd_part2, wd_yrow, wd_yax, wd_cross, wd_quad, wd_colsq, wd_diag;
   DevBuf wd_ppart2, wd_q, wd_yay;           // persistent weighted loop: Y'(a o w1), YAY
+  DevBuf forced;                             // rbd_set_forced_selection (test instrumentation)
+  std::vector<long long> forced_h;
   DevBuf nn_part, nn_coords;               // classify: split minima, query coordinates
   DevBuf pj_ws;                            // K5 split-K partial slices
   DevBuf send, recv;                       // sharded mode: payload exchange buffers
@@ -607,6 +609,8 @@ int launch_persistent(rbd_ctx_t ctx, const LoopBufs& L, const double* diag = nul
   a.d_max = L.d_max;
   a.ctl = ptr<StepCtl>(ctx->ctl);
   a.rdy = ptr<unsigned long long>(ctx->rdy);
+  a.forced = ctx->forced_h.empty() ? nullptr : ptr<long long>(ctx->forced);
+  a.nforced = (long long)ctx->forced_h.size();
   if (diag) {
     TRY(ensure(ctx->wd_ppart2, sizeof(double) * (size_t)std::max<long long>(grid, S) * L.d_max));
     TRY(ensure(ctx->wd_q, sizeof(double) * (size_t)(L.d_max + 1)));
@@ -880,7 +884,7 @@ int rbd_ctx_destroy(rbd_ctx_t ctx) {
                   &ctx->hX,      &ctx->hY,   &ctx->hT,      &ctx->ppart, &ctx->bar,
                   &ctx->wd_axi,  &ctx->wd_yy, &ctx->wd_part2, &ctx->wd_yrow, &ctx->wd_yax,
                   &ctx->wd_cross, &ctx->wd_quad, &ctx->wd_colsq, &ctx->wd_diag,
-                  &ctx->wd_ppart2, &ctx->wd_q, &ctx->wd_yay,
+                  &ctx->wd_ppart2, &ctx->wd_q, &ctx->wd_yay, &ctx->forced,
                   &ctx->nn_part, &ctx->nn_coords, &ctx->pj_ws,
                   &ctx->ctl,     &ctx->gcnt, &ctx->ygcnt,   &ctx->rdy,   &ctx->send,  &ctx->recv};
   for (DevBuf* b : bl) release(*b);
@@ -901,6 +905,21 @@ int rbd_ctx_set_stream(rbd_ctx_t ctx, void* s) {
 }
 
 int64_t rbd_ctx_launch_count(rbd_ctx_t ctx) { return ctx ? ctx->launches : 0; }
+
+int rbd_set_forced_selection(rbd_ctx_t ctx, const int64_t* h_selected, int64_t count) {
+  if (!ctx) return set_err(RBD_ERR_INVALID_ARGUMENT, "forced selection: null context");
+  if (count < 0 || (count > 0 && !h_selected))
+    return set_err(RBD_ERR_INVALID_ARGUMENT, "forced selection: bad sequence");
+  CU(cudaSetDevice(ctx->device));
+  ctx->forced_h.assign(h_selected, h_selected + count);
+  if (count > 0) {
+    TRY(ensure(ctx->forced, sizeof(long long) * (size_t)count));
+    CU(cudaMemcpyAsync(ctx->forced.p, ctx->forced_h.data(), sizeof(long long) * (size_t)count,
+                       cudaMemcpyHostToDevice, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+  }
+  return RBD_OK;
+}
 
 int rbd_ctx_synchronize(rbd_ctx_t ctx) {
   CU(cudaStreamSynchronize(ctx->stream));
@@ -968,6 +987,16 @@ int decompose_device_impl(rbd_ctx_t ctx, const double* dX, int64_t m, int64_t n,
   const double tol = breakdown_tolerance(cfg, m, max_colsq);
   long long j0 = 0;
   TRY(start_column(cfg, n, &j0));
+  if (!ctx->forced_h.empty()) {   // parity re-run on a given selection sequence
+    for (long long v : ctx->forced_h)
+      if (v < 0 || v >= n) return set_err(RBD_ERR_INDEX_OUT_OF_RANGE, "forced selection index out of range");
+    const bool pers = diag ? diag_persistent(ctx, cfg->d_max, m, n)
+                           : (ctx->path == 0 && use_fused(cfg->d_max));
+    if (!pers)
+      return set_err(RBD_ERR_INVALID_ARGUMENT,
+                     "forced selection is implemented on the persistent loop only");
+    j0 = ctx->forced_h[0];
+  }
 
   // ---- loop state ----
   hs.d = 0;

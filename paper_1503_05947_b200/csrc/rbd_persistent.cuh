@@ -68,6 +68,10 @@ struct PersistArgs {
   unsigned long long* rdy;       // [0] CTAs through P1, [1 + s] rows of chunk s written by P1
                                  // (monotonic within a decompose, zeroed with ctl)
   long long* progress;           // optional mapped host word: Y columns [0, value) are final
+  // test instrumentation (SURVEY §8(c) parity protocol): steps k < nforced
+  // select forced[k] instead of the argmax (history still records the argmax)
+  const long long* forced;
+  long long nforced;
   // diagonal weight A = diag(a) (DIAG instantiation; see rbd_weighted.cuh)
   const double* diag;            // a
   double* aw;                    // a o w1_k (P1)
@@ -939,7 +943,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
         pending = 1;
         reorth_prev = re;
         wnorm_prev = nrm;
-        jstar = gj;                      // :101
+        jstar = (k < a.nforced) ? __ldg(&a.forced[k]) : gj;   // :101 (forced: parity re-run)
         xnorm2 = a.col_sq[gj];
         done = !(k < a.d_max && e_cur > eps_R) ? 1 : 0;   // :87
       }

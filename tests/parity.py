@@ -3,7 +3,8 @@
 * selected: equal step by step, except where the oracle's top-two residual gap
   at that step is within tau * max_j col_sq_j (a near tie, either pick is
   admissible); comparison of Y/T/history stops at the first admissible
-  divergence.
+  divergence, or, given `rerun`, continues over all steps on a B200 re-run
+  forced onto the oracle's selection (rbd_set_forced_selection).
 * Y:        ||y_k^gpu - y_k^ref||_2 <= tol_k,  tol_k = tol + 64 eps kappa_k
             (tol = 1e-10 fp64). kappa_k = ||x_{j_k}|| / ||w_k|| is the factor by
             which step k amplifies roundoff: y_k = w_k/||w_k|| with
@@ -55,8 +56,12 @@ def top2_gap(r: np.ndarray) -> float:
 
 
 def compare(gpu, ref, X, tol: float = 1e-10, tau: float = 1e-12, require_same_d: bool = True,
-            diag=None):
-    """Returns the number of steps compared; raises AssertionError on mismatch."""
+            diag=None, rerun=None):
+    """Returns the number of steps compared; raises AssertionError on mismatch.
+
+    rerun: optional callable(selected) -> gpu model. After an admissible
+    divergence the B200 loop is re-run on the oracle's selection (forced-selection
+    mode, rbd_set_forced_selection) and compared over all steps."""
     X = np.asarray(X, dtype=np.float64)
     gY = np.asarray(gpu.Y.cpu() if hasattr(gpu.Y, "cpu") else gpu.Y)
     gT = np.asarray(gpu.T.cpu() if hasattr(gpu.T, "cpu") else gpu.T)
@@ -78,6 +83,10 @@ def compare(gpu, ref, X, tol: float = 1e-10, tau: float = 1e-12, require_same_d:
                 f"top-two gap {gap:.3e} > {tau * max_colsq:.3e}")
             upto = k
             break
+    if upto < d_cmp and rerun is not None:
+        forced = rerun(list(ref.selected))
+        assert list(forced.selected[:ref.d]) == list(ref.selected[:forced.d])
+        return compare(forced, ref, X, tol, tau, require_same_d, diag)
     if upto == d_cmp and require_same_d:
         assert gpu.d == ref.d, f"d differs: gpu {gpu.d} ref {ref.d}"
     tols = step_tolerances(ref, col_sq, rsteps, tol)

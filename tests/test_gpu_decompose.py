@@ -30,7 +30,8 @@ def test_c0_parity_full(cuda):
     X = configs.c0_matrix()
     g, r = both(X, 64, 1e-6)
     assert g.d == r.d == 64
-    compare(g, r, X)
+    rerun = lambda sel: rbd.decompose(X, d_max=64, eps_r=1e-6, forced_selection=sel)  # noqa: E731
+    assert compare(g, r, X, rerun=rerun) == 64
 
 
 @pytest.mark.parametrize("m,n,d", [(17, 12, 6), (1, 5, 1), (3, 1, 1), (4097, 9, 9), (8193, 7, 7),
@@ -40,7 +41,7 @@ def test_shapes_parity(cuda, m, n, d):
     multi-chunk rows, single row / single column."""
     X = oracle.random_matrix(m, n, 1000 + m + n)
     g, r = both(X, d)
-    compare(g, r, X)
+    assert compare(g, r, X, rerun=lambda sel: rbd.decompose(X, d_max=d, forced_selection=sel)) == r.d
 
 
 def test_padded_leading_dimension_device(cuda):

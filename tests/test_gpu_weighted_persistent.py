@@ -32,7 +32,8 @@ def test_parity_random(persistent, m, n, d, seed):
     x = oracle.random_matrix(m, n, 100 + seed)
     dg = oracle.random_positive(m, 200 + seed)
     g, r = both(x, d, dg)
-    assert compare(g, r, x, diag=dg) == r.d
+    rerun = lambda sel: rbd.decompose(x, d_max=d, diag=dg, forced_selection=sel)  # noqa: E731
+    assert compare(g, r, x, diag=dg, rerun=rerun) == r.d
     assert g.result.launches < 8   # one persistent launch (+ init), not 12 per step
 
 
