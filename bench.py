@@ -120,6 +120,28 @@ def ncu_traffic():
         return None
 
 
+def read_peak_gbs(dev, gib: int = 4, reps: int = 10):
+    import torch
+    try:
+        buf = torch.ones(gib * (1 << 27), dtype=torch.float64, device=dev)
+    except RuntimeError:
+        return None
+    best = float("inf")
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for i in range(reps + 2):
+        torch.cuda.synchronize(dev)
+        e0.record()
+        buf.sum()
+        e1.record()
+        torch.cuda.synchronize(dev)
+        if i >= 2:
+            best = min(best, e0.elapsed_time(e1))
+    nbytes = buf.numel() * 8
+    del buf
+    torch.cuda.empty_cache()
+    return nbytes / (best / 1e3) / 1e9
+
+
 def make_workload(name, device):
     import torch
     from paper_1503_05947_b200 import configs
@@ -284,6 +306,15 @@ def run_b200(args):
     roofline["sweep_kernel"] = {"kernel": "k_sweep<2,MODE_DOT,stream> (K2 standalone)",
                                 "achieved": sw, "frac": sw / peak, "ms_per_launch": ms_sweep.value,
                                 "bytes_per_launch": bytes_per_gstep}
+    # read-only HBM peak (the copy-based peak under-states a pure
+    # read stream): a stock reduction over 4 GiB of fp64, best of 10
+    rp = read_peak_gbs(dev)
+    if rp:
+        roofline["read_peak"] = {"gbs": rp, "frac": ach / rp,
+                                 "how": "torch.sum over a 4 GiB fp64 buffer (read-only), best of 10, "
+                                        "CUDA events"}
+    roofline["frac_of_nominal"] = {"gbs": 7700.0, "frac": ach / 7700.0,
+                                   "note": "nominal HBM3e 7.7 TB/s (HGX), B200_PROFILING.md"}
 
     # ---- e2e through the reference-facing host entry (pinned host X) ----
     e2e = None
