@@ -18,7 +18,13 @@
 namespace rbdk {
 
 constexpr int kDmBK = 16;           // i per stage (row of 16 doubles, no padding)
-constexpr int kDmStages = 3;
+#ifndef RBD_DM_STAGES
+#define RBD_DM_STAGES 3
+#endif
+#ifndef RBD_DM_MINB
+#define RBD_DM_MINB 4
+#endif
+constexpr int kDmStages = RBD_DM_STAGES;
 
 template <int BM, int BN>
 constexpr size_t dm_smem_bytes() {
@@ -72,7 +78,7 @@ __device__ __forceinline__ void dm_load_tile(double* s, const double* __restrict
 }
 
 template <int BM, int BN, int WARPS_M, int WARPS_N>
-__global__ void __launch_bounds__(WARPS_M * WARPS_N * 32, 4)
+__global__ void __launch_bounds__(WARPS_M * WARPS_N * 32, RBD_DM_MINB)
     k_project_dmma(const double* __restrict__ Y, long long m, long long d, long long ldy,
                    const double* __restrict__ Xn, long long N, long long ldx,
                    double* __restrict__ Tn, double* __restrict__ xnorm2, long long kc,
@@ -112,7 +118,11 @@ __global__ void __launch_bounds__(WARPS_M * WARPS_N * 32, 4)
     for (int b = 0; b < NT; ++b)
 #pragma unroll
       for (int e = 0; e < 4; ++e) acc[a][b][e] = 0.0;
-  double xn = 0.0;   // ||x_j||^2: thread tid < BN owns column j0 + tid
+  // ||x_j||^2 (l-tile 0 only): every thread takes half a B row (8 stored
+  // doubles) of column (tid % BN) in two chains; halves combined in order
+  static_assert(NTHREADS == 2 * BN, "two threads per B row");
+  double xa = 0.0, xb = 0.0;
+  __shared__ double xn_half[BN];
   const long long nk = (m + kDmBK - 1) / kDmBK;
   auto load_stage = [&](int st, long long kt) {
     const long long i0 = kt * kDmBK;
@@ -162,10 +172,18 @@ __global__ void __launch_bounds__(WARPS_M * WARPS_N * 32, 4)
 #pragma unroll
         for (int b = 0; b < NT; ++b) dmma_16x8x4(acc[a][b], a0[a].y, a1[a].y, bf[b].y);
     }
-    if (do_norm && tid < BN) {
-      const double* xr = B + tid * kDmBK;
+    if (do_norm) {
+      // stored positions p = 2q + h (the row's half h), rotated by the row so the
+      // lanes of a warp spread over 8 bank pairs instead of one (rows are 128 B)
+      const int row = tid % BN, h = tid / BN;
+      const double* xr = B + row * kDmBK;
 #pragma unroll
-      for (int q = 0; q < kDmBK; ++q) xn = fma(xr[q], xr[q], xn);
+      for (int q = 0; q < kDmBK / 2; q += 2) {
+        const double v0 = xr[(2 * q + h + 2 * row) & (kDmBK - 1)];
+        const double v1 = xr[(2 * q + 2 + h + 2 * row) & (kDmBK - 1)];
+        xa = fma(v0, v0, xa);
+        xb = fma(v1, v1, xb);
+      }
     }
   }
   cp_async_wait<0>();
@@ -180,7 +198,11 @@ __global__ void __launch_bounds__(WARPS_M * WARPS_N * 32, 4)
         const long long j = j0 + wn * WN + b * 8 + t * 2 + (e & 1);
         if (l < d && j < N) Tn[l + j * d] = acc[a][b][e];
       }
-  if (do_norm && tid < BN && j0 + tid < N) xnorm2[j0 + tid] = xn;
+  if (do_norm) {
+    if (tid >= BN) xn_half[tid - BN] = xa + xb;
+    __syncthreads();
+    if (tid < BN && j0 + tid < N) xnorm2[j0 + tid] = (xa + xb) + xn_half[tid];
+  }
 }
 
 // Split-K combine: Tn += workspace slices (and ||x||^2), splits in order.
