@@ -207,6 +207,10 @@ __device__ __forceinline__ bool live_at_exit(int done, int breakdown) {
 }
 
 constexpr int kP3Groups = 4;   // column groups finalised together in P3
+#ifndef RBD_P1_LOADS
+#define RBD_P1_LOADS 16
+#endif
+constexpr int kPLoads = RBD_P1_LOADS;   // P1: Y loads in flight per lane per batch
 constexpr int kTraceWords = 256;  // per CTA: [0] count, then (tag<<40 | time) words
 
 // Payload of a rank in sharded mode (doubles): [0] best residual, [1] global
@@ -298,7 +302,8 @@ template <int VEC, bool SHARD, bool DIAG = false>
 __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
   static_assert(!(SHARD && DIAG), "the weighted loop is single-GPU");
   extern __shared__ double dsm[];
-  constexpr int kPBatch = 16 * kWarps / 2;   // columns per P1 batch of a half (16 loads per lane)
+  constexpr int kPBatch = kPLoads * kWarps / 2;   // columns per P1 batch of a half
+  static_assert(kPBatch <= 16 * kWarps, "P1 batch padding (persist_smem) too small");
   double* cs = dsm;                        // c = T[0:k, j*], zero-padded to a batch multiple
   double* ps = dsm + a.d_max + kPBatch;    // p_{k-1} (pending column), zero-padded
   double* pd = dsm + 2 * (a.d_max + kPBatch);   // DIAG: p_k (finaliser copy)
@@ -430,10 +435,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
       if (nv > 0) {
         const double* yp = a.Y + i0 + (long long)wh * m;
         const long long stp = (long long)kPW * m;
-        for (long long l = wh; l < kb; l += 16 * kPW) {
-          double yv[16][VEC];
+        for (long long l = wh; l < kb; l += kPLoads * kPW) {
+          double yv[kPLoads][VEC];
 #pragma unroll
-          for (int q = 0; q < 16; ++q) {
+          for (int q = 0; q < kPLoads; ++q) {
             const bool ok = l + q * kPW < kb;
             if constexpr (VEC == 2) {
               if (ok && nv == 2) {
@@ -449,13 +454,13 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
             }
           }
 #pragma unroll
-          for (int q = 0; q < 16; ++q)
+          for (int q = 0; q < kPLoads; ++q)
 #pragma unroll
             for (int v = 0; v < VEC; ++v) {
               acc_c[v] = fma(yv[q][v], cs[l + q * kPW], acc_c[v]);   // zero past kb
               acc_p[v] = fma(yv[q][v], ps[l + q * kPW], acc_p[v]);
             }
-          yp += 16 * stp;
+          yp += kPLoads * stp;
         }
       }
 #pragma unroll
