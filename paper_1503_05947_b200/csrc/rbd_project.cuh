@@ -103,18 +103,27 @@ __global__ void k_reconstruct(const double* __restrict__ Y, long long m, long lo
   }
 }
 
-// Split-K factor for the DMMA grid: the smallest of 1..4 whose last wave is
-// >= 97% full (4 CTAs per SM), keeping >= 1024 rows per split.
+// Split-K factor for the DMMA grid (4 CTAs per SM): of 1..4 (>= 1024 rows per
+// split), the one whose waves are best filled; a larger split must fill them
+// by 2 points more (its combine pass and workspace are not free). E.g. C4's
+// 8 x 256 tiles -> 2 (6.92 waves), classify's 7 x 256 -> 4 (12.1 waves, 93 %
+// instead of 3.03 waves at 76 %).
 inline int project_splitk(long long m, long long d, long long N, int nsm) {
   const long long ctas = ((d + 63) / 64) * ((N + 63) / 64);
   const long long slots = 4LL * nsm;
+  int best = 1;
+  double best_eff = 0.0;
   for (int s = 1; s <= 4; ++s) {
     if (s > 1 && m / s < 1024) break;
     const long long c = ctas * s;
     const long long waves = (c + slots - 1) / slots;
-    if ((double)c / (double)(waves * slots) >= 0.97) return s;
+    const double eff = (double)c / (double)(waves * slots);
+    if (s == 1 || eff > best_eff + 0.02) {
+      best = s;
+      best_eff = eff;
+    }
   }
-  return 1;
+  return best;
 }
 
 inline int launch_project_f64(const double* Y, long long m, long long d, long long ldy,
