@@ -2466,10 +2466,42 @@ int rbd_project_batch_f32(rbd_ctx_t ctx, const float* dY, int64_t m, int64_t d, 
     TRY(ensure(ctx->scratch1, sizeof(double) * (size_t)std::max<int64_t>(N, 32)));
     xn = ptr<double>(ctx->scratch1);
   }
-  dim3 grid((unsigned)cdiv(d, kTcBM), (unsigned)cdiv(N, kTcBN));
-  k_project_tf32x3<<<grid, kTcThreads, kTcSmem, ctx->stream>>>(mY, mX, m, d, N, dTn, xn);
+  // split-K over the k-blocks for the best-filled waves (1 CTA per SM): 2 for C4's 4 x 128 tiles
+  const long long nk = cdiv(m, kTcBK);
+  const long long ctas = cdiv(d, kTcBM) * cdiv(N, kTcBN);
+  int sk = 1;
+  {
+    double best_eff = 0.0;
+    for (int s = 1; s <= 4; ++s) {
+      if (s > 1 && nk / s < 64) break;
+      const long long c = ctas * s, waves = cdiv(c, ctx->nsm);
+      const double eff = (double)c / (double)(waves * ctx->nsm);
+      if (s == 1 || eff > best_eff + 0.02) {
+        sk = s;
+        best_eff = eff;
+      }
+    }
+  }
+  const int kb_per = (int)cdiv(nk, sk);
+  sk = (int)cdiv(nk, kb_per);   // every split gets at least one k-block
+  float* Tws = nullptr;
+  double* xws = nullptr;
+  if (sk > 1) {
+    const size_t tbytes = sizeof(float) * (size_t)(sk - 1) * (size_t)(d * N);
+    TRY(ensure(ctx->pj_ws, tbytes + sizeof(double) * (size_t)(sk - 1) * (size_t)N + 16));
+    Tws = ptr<float>(ctx->pj_ws);
+    xws = reinterpret_cast<double*>(reinterpret_cast<char*>(ctx->pj_ws.p) + ((tbytes + 15) & ~(size_t)15));
+  }
+  dim3 grid((unsigned)cdiv(d, kTcBM), (unsigned)cdiv(N, kTcBN), (unsigned)sk);
+  k_project_tf32x3<<<grid, kTcThreads, kTcSmem, ctx->stream>>>(mY, mX, m, d, N, dTn, xn, kb_per,
+                                                                Tws, xws);
   ctx->launches++;
   CU(cudaGetLastError());
+  if (sk > 1) {
+    k_splitk_sum_f32<<<1184, 256, 0, ctx->stream>>>(dTn, Tws, d * N, sk - 1, xn, xws, N);
+    ctx->launches++;
+    CU(cudaGetLastError());
+  }
   if (d_err) {
     k_project_err_f32<<<(unsigned)cdiv(N, 8), 256, 0, ctx->stream>>>(xn, dTn, d, N, d_err);
     ctx->launches++;

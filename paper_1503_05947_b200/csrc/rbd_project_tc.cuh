@@ -122,10 +122,14 @@ __device__ __forceinline__ float tf32_lo(float x) {
   return x - hi;                                                        // exact in fp32
 }
 
+// split-K: blockIdx.z takes k-blocks [z * kb_per, min(nk, (z + 1) * kb_per)) (at
+// least one); split 0 writes Tn / xnorm2, split z > 0 its workspace slices
+// (Tws + (z-1) d N, xws + (z-1) N), added in order by k_splitk_sum_f32.
 __global__ void __launch_bounds__(kTcThreads, 1)
     k_project_tf32x3(const __grid_constant__ CUtensorMap mapY, const __grid_constant__ CUtensorMap mapX,
                      long long m, long long d, long long N, float* __restrict__ Tn,
-                     double* __restrict__ xnorm2) {
+                     double* __restrict__ xnorm2, int kb_per, float* __restrict__ Tws,
+                     double* __restrict__ xws) {
   extern __shared__ __align__(1024) uint8_t tc_smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(tc_smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kTcStages * kTcStageBytes);
@@ -136,7 +140,13 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int l0 = blockIdx.x * kTcBM, j0 = blockIdx.y * kTcBN;
-  const int nk = (int)((m + kTcBK - 1) / kTcBK);
+  const int nk_all = (int)((m + kTcBK - 1) / kTcBK);
+  const int kb0 = (int)blockIdx.z * kb_per;
+  const int nk = (kb0 + kb_per < nk_all ? kb0 + kb_per : nk_all) - kb0;   // local k-blocks (>= 1)
+  if (blockIdx.z > 0) {
+    Tn = Tws + (long long)(blockIdx.z - 1) * d * N;
+    if (xnorm2) xnorm2 = xws + (long long)(blockIdx.z - 1) * N;
+  }
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kTcStages; ++s) {
@@ -171,8 +181,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         const uint32_t ph = (kb / kTcStages) & 1;
         mbar_wait(&empty[s], ph ^ 1);
         mbar_expect_tx(&full[s], 2 * kTcTileBytes);
-        tma_load_2d(stageA(s), &mapY, &full[s], kb * kTcBK, l0);
-        tma_load_2d(stageB(s), &mapX, &full[s], kb * kTcBK, j0);
+        tma_load_2d(stageA(s), &mapY, &full[s], (kb0 + kb) * kTcBK, l0);
+        tma_load_2d(stageB(s), &mapX, &full[s], (kb0 + kb) * kTcBK, j0);
       }
     }
   } else if (warp == 1) {
@@ -271,6 +281,23 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTcBN));
+  }
+}
+
+// Split-K combine: Tn += fp32 workspace slices and xn += fp64 slices, in split order.
+__global__ void k_splitk_sum_f32(float* __restrict__ Tn, const float* __restrict__ Tws, long long dN,
+                                 int nws, double* __restrict__ xn, const double* __restrict__ xws,
+                                 long long N) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < dN;
+       e += (long long)gridDim.x * blockDim.x) {
+    float v = Tn[e];
+    for (int z = 0; z < nws; ++z) v += Tws[(long long)z * dN + e];
+    Tn[e] = v;
+    if (xn && e < N) {
+      double x = xn[e];
+      for (int z = 0; z < nws; ++z) x += xws[(long long)z * N + e];
+      xn[e] = x;
+    }
   }
 }
 
