@@ -1675,10 +1675,30 @@ int rbd_nearest_columns(rbd_ctx_t ctx, const double* dC, int64_t d, int64_t Q, i
   CU(cudaSetDevice(ctx->device));
   const long long gx = cdiv(Q, kNnTile);
   const long long tiles = cdiv(n_train, kNnTile);
-  // split the training columns so the grid covers ~4 CTAs per SM
-  long long nsplit = std::max<long long>(1, std::min<long long>(tiles, cdiv(4LL * ctx->nsm, gx)));
-  const long long per = cdiv(tiles, nsplit) * kNnTile;
-  nsplit = cdiv(n_train, per);
+  // split the training columns for the best-filled waves (resident CTAs per SM
+  // from the occupancy API); a larger split must fill them by 2 points more
+  static int nn_occ = 0;
+  if (nn_occ == 0) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nn_occ, k_nearest, kThreads, 0) != cudaSuccess ||
+        nn_occ < 1)
+      nn_occ = 1;
+  }
+  const long long slots = (long long)nn_occ * ctx->nsm;
+  long long nsplit = 1, per = tiles * kNnTile;
+  {
+    double best_eff = 0.0;
+    for (long long sp = 1; sp <= std::min<long long>(tiles, 16); ++sp) {
+      const long long pr = cdiv(tiles, sp) * kNnTile;
+      const long long ns = cdiv(n_train, pr);
+      const long long c = gx * ns, waves = cdiv(c, slots);
+      const double eff = (double)c / (double)(waves * slots);
+      if (sp == 1 || eff > best_eff + 0.02) {
+        best_eff = eff;
+        nsplit = ns;
+        per = pr;
+      }
+    }
+  }
   if (gx > 0x7fffffffLL || nsplit > 65535)
     return set_err(RBD_ERR_INVALID_ARGUMENT, "nearest: problem too large for one launch");
   TRY(ensure(ctx->nn_part, sizeof(NnRec) * (size_t)nsplit * (size_t)Q));
