@@ -52,13 +52,30 @@ def _stale(target, deps) -> bool:
 
 
 def build_library(force: bool = False, verbose: bool = False) -> str:
+    """Compile every translation unit of csrc/ in parallel (one nvcc per unit),
+    then link the shared library; the result replaces LIB atomically."""
     if not force and not _stale(LIB, _deps()):
         return LIB
-    cmd = [_nvcc(), *NVCC_FLAGS, "-shared", "-I", INCLUDE, "-I", CSRC, *_sources(),
-           "-o", LIB + ".tmp", "-ldl"]
-    if verbose:
-        print(" ".join(cmd))
-    subprocess.run(cmd, check=True, cwd=ROOT)
+    import tempfile
+    from concurrent.futures import ThreadPoolExecutor
+    with tempfile.TemporaryDirectory(prefix="rbd_build_") as tmp:
+        def compile_one(src):
+            obj = os.path.join(tmp, os.path.basename(src) + ".o")
+            cmd = [_nvcc(), *NVCC_FLAGS, "-Xcompiler", "-fPIC", "-c", "-I", INCLUDE, "-I", CSRC,
+                   src, "-o", obj]
+            if verbose:
+                print(" ".join(cmd))
+            r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True)
+            if r.returncode != 0:
+                raise RuntimeError(f"nvcc failed on {src}:\n{r.stderr[-4000:]}")
+            return obj
+        srcs = _sources()
+        with ThreadPoolExecutor(max_workers=max(1, min(len(srcs), os.cpu_count() or 1))) as ex:
+            objs = list(ex.map(compile_one, srcs))
+        cmd = [_nvcc(), *NVCC_FLAGS, "-shared", *objs, "-o", LIB + ".tmp", "-ldl"]
+        if verbose:
+            print(" ".join(cmd))
+        subprocess.run(cmd, check=True, cwd=ROOT)
     os.replace(LIB + ".tmp", LIB)
     return LIB
 

@@ -1,169 +1,15 @@
 // rbd_capi.cu — host runtime of the B200 RBD path behind the C ABI in
 // include/rbd_cuda.h: context, scratch management, the CUDA-graph-captured
 // greedy step loop, the workspace API and out-of-sample projection.
-#include <cuda_runtime.h>
-#include <dlfcn.h>
-
-#include <algorithm>
-#include <cmath>
-#include <cstdio>
-#include <cstring>
-#include <limits>
-#include <random>
-#include <string>
-#include <vector>
-
-#include "rbd_cuda.h"
-#include "rbd_internal.h"
-#include "rbd_device.cuh"
-#include "rbd_project.cuh"
+#include "rbd_capi_internal.h"
 #include "rbd_persistent.cuh"
-#include "rbd_project_tc.cuh"
-#include "rbd_weighted.cuh"
-#include "rbd_classify.cuh"
-#include "rbd_compress_dmma.cuh"
-
-#include <cudaTypedefs.h>
-
-using namespace rbdk;
-
-void rbd_comm_release(rbd_ctx_t ctx);
+#include "rbd_project.cuh"
 
 namespace {
-
 thread_local std::string g_err;
-
-int set_err(int code, const std::string& msg) {
-  g_err = msg;
-  return code;
-}
-
-#define CU(call)                                                                          \
-  do {                                                                                    \
-    cudaError_t e_ = (call);                                                              \
-    if (e_ != cudaSuccess)                                                                \
-      return set_err(e_ == cudaErrorMemoryAllocation ? RBD_ERR_OUT_OF_MEMORY : RBD_ERR_CUDA, \
-                     std::string(#call) + ": " + cudaGetErrorString(e_));                 \
-  } while (0)
-
-#define TRY(expr)            \
-  do {                       \
-    int s_ = (expr);         \
-    if (s_ != RBD_OK) return s_; \
-  } while (0)
-
-struct DevBuf {
-  void* p = nullptr;
-  size_t bytes = 0;
-};
-
-int ensure(DevBuf& b, size_t bytes) {
-  if (bytes == 0) bytes = 16;
-  if (b.bytes >= bytes) return RBD_OK;
-  if (b.p) cudaFree(b.p);
-  b.p = nullptr;
-  b.bytes = 0;
-  cudaError_t e = cudaMalloc(&b.p, bytes);
-  if (e != cudaSuccess)
-    return set_err(RBD_ERR_OUT_OF_MEMORY, std::string("cudaMalloc(") + std::to_string(bytes) +
-                                              "): " + cudaGetErrorString(e));
-  b.bytes = bytes;
-  return RBD_OK;
-}
-
-void release(DevBuf& b) {
-  if (b.p) cudaFree(b.p);
-  b.p = nullptr;
-  b.bytes = 0;
-}
-
-template <typename T>
-T* ptr(DevBuf& b) {
-  return static_cast<T*>(b.p);
-}
-
-long long cdiv(long long a, long long b) { return (a + b - 1) / b; }
-
-bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
-
-struct GraphKey {
-  const void* X = nullptr;
-  const void* Y = nullptr;
-  const void* T = nullptr;
-  long long m = 0, n = 0, ldx = 0, d_max = 0;
-  const void* bufs[8] = {};
-  cudaStream_t stream = nullptr;
-  int steps = 0;
-  bool operator==(const GraphKey& o) const {
-    if (X != o.X || Y != o.Y || T != o.T || m != o.m || n != o.n || ldx != o.ldx ||
-        d_max != o.d_max || stream != o.stream || steps != o.steps)
-      return false;
-    for (int i = 0; i < 8; ++i)
-      if (bufs[i] != o.bufs[i]) return false;
-    return true;
-  }
-};
-
 }  // namespace
 
-struct rbd_ctx_s {
-  int device = 0;
-  int nsm = 148;
-  cudaStream_t own_stream = nullptr;
-  cudaStream_t stream = nullptr;
-  DevBuf partial, rec, counter, state, colsq, resid, w, c, p, nrm, hist, sel, out_rec, scratch1;
-  DevBuf hX, hY, hT;  // cached device copies for the host entry
-  DevBuf ppart;       // fused-extension partials
-  DevState* h_state = nullptr;  // pinned
-  // host entry with a page-locked Y: the loop posts its progress to a mapped
-  // word and finished Y columns are copied out on a second stream meanwhile
-  long long* h_progress = nullptr;
-  long long* d_progress = nullptr;
-  cudaStream_t copy_stream = nullptr;
-  double* ystream_dst = nullptr;   // host Y (ld m) to stream into, or null
-  double* tstream_dst = nullptr;   // host T (row-major, n per row), or null
-  long long ystream_copied = 0;    // Y columns / T rows already copied (or in flight)
-  Rec* h_rec = nullptr;         // pinned
-  cudaGraphExec_t gexec = nullptr;
-  GraphKey gkey;
-  long long graph_nodes = 0;
-  long long launches = 0;
-  int occ_sweep2 = 2, occ_sweep1 = 2;
-  int fused_grid_cap = 296;
-  int persist_occ2 = 0, persist_occ1 = 0;  // co-resident CTAs/SM of the persistent kernel
-  int path = 0;                            // 0 persistent, 1 graph of per-phase kernels
-  DevBuf bar;                              // grid-barrier words
-  DevBuf ctl, gcnt, ygcnt;                 // persistent loop: ctl words, p (x2), CTA records
-  DevBuf rdy;                              // persistent loop: P1 readiness counters
-  // diagonal-weight loop (rbd_weighted.cuh): a o xi, xi'A xi partials, YAX row
-  // partials, YAY row, YAX (d_max x n), cross, quad, col_sq_A, host-entry diag
-  DevBuf wd_axi, wd_yy, wd_part2, wd_yrow, wd_yax, wd_cross, wd_quad, wd_colsq, wd_diag;
-  DevBuf wd_ppart2, wd_q, wd_yay;           // persistent weighted loop: Y'(a o w1), YAY
-  DevBuf forced;                             // rbd_set_forced_selection (test instrumentation)
-  std::vector<long long> forced_h;
-  DevBuf nn_part, nn_coords;               // classify: split minima, query coordinates
-  DevBuf pj_ws;                            // K5 split-K partial slices
-  DevBuf send, recv;                       // sharded mode: payload exchange buffers
-  // multi-GPU
-  void* comm = nullptr;                    // ncclComm_t (dlopen'ed NCCL)
-  int rank = 0, world = 1;
-  std::vector<rbd_ctx_s*> virt;            // virtual ranks (single-device sharded mode)
-};
-
-struct rbd_ws_s {
-  rbd_ctx_t ctx;
-  const double* X;
-  long long m, n, ldx, cap, d;
-  DevBuf T, colsq, resid, partial, rec, counter, out, tmp;
-  DevBuf Xown;   // host-entry workspaces own a device copy of X
-  // diagonal weight (kind 1, workspace.hpp:18-30): the weight, the basis vectors
-  // passed to extend (for Y'AY), a o xi scratch and its partials, Y'AY (cap x cap),
-  // a row scratch
-  int kind = 0;
-  DevBuf diag, basis, axi, yy, yay, row;
-};
-
-namespace {
+namespace rbdc {
 
 // ---------------------------------------------------------------------------
 // Launch helpers (each increments the context's launch counter)
@@ -472,7 +318,7 @@ int fused_grid(rbd_ctx_t ctx, long long m) {
 size_t fused_smem(long long dcap) { return sizeof(double) * 3 * (size_t)std::max<long long>(dcap, 1); }
 // c and p vectors, each zero-padded by one P1 batch (16 loads x kWarps columns);
 // weighted: + p_k and the YAY row for the finaliser
-size_t persist_smem(long long dcap, bool diag = false) {
+size_t persist_smem(long long dcap, bool diag) {
   const size_t d = (size_t)std::max<long long>(dcap, 1);
   return sizeof(double) * (2 * (d + 16 * kWarps) + (diag ? 2 * (d + 1) : 0));
 }
@@ -549,7 +395,7 @@ int enqueue_step_fused(rbd_ctx_t ctx, const LoopBufs& L) {
   return RBD_OK;
 }
 
-int persistent_grid(rbd_ctx_t ctx, int vec, long long d_max, bool diag = false) {
+int persistent_grid(rbd_ctx_t ctx, int vec, long long d_max, bool diag) {
   int occ = 0;
   const size_t smem = persist_smem(d_max, diag);
   if (diag)
@@ -747,7 +593,7 @@ int get_step_graph(rbd_ctx_t ctx, const LoopBufs& L) {
 // Validation shared by the single- and multi-GPU entries: reference order of
 // decompose.cpp:56-64 after the K1 flags are known.
 int validate_after_init(const rbd_config_t* cfg, long long m, long long n, const DevState& hs,
-                        bool diag_supplied = false) {
+                        bool diag_supplied) {
   if (hs.flags_nonfinite)
     return set_err(RBD_ERR_INVALID_ARGUMENT, "decompose: matrix has non-finite entries");
   if (cfg->d_max < 1 || cfg->d_max > n)
@@ -789,7 +635,17 @@ double breakdown_tolerance(const rbd_config_t* cfg, long long m, double max_cols
   return std::max(cfg->breakdown_tol < 0.0 ? cfg->eps_R : cfg->breakdown_tol, noise_floor);
 }
 
-}  // namespace
+// diagonal weight values: positive and finite (weight.cpp:11-17)
+int check_diagonal(const double* h, int64_t len) {
+  if (len <= 0) return set_err(RBD_ERR_INVALID_ARGUMENT, "diagonal weight must be non-empty");
+  for (int64_t i = 0; i < len; ++i)
+    if (!(h[i] > 0.0) || !std::isfinite(h[i]))
+      return set_err(RBD_ERR_INVALID_ARGUMENT,
+                     "diagonal weight entries must be strictly positive and finite");
+  return RBD_OK;
+}
+
+}  // namespace rbdc
 
 // ===========================================================================
 // C ABI
@@ -800,7 +656,8 @@ const char* rbd_last_error(void) { return g_err.c_str(); }
 
 // for the library's other translation units (csrc/rbd_internal.h)
 __attribute__((visibility("hidden"))) int rbd_internal_set_error(int code, const char* msg) {
-  return set_err(code, msg);
+  g_err = msg;
+  return code;
 }
 int rbd_abi_version(void) { return RBD_ABI_VERSION; }
 
@@ -1142,14 +999,6 @@ int decompose_device_impl(rbd_ctx_t ctx, const double* dX, int64_t m, int64_t n,
 }
 
 // WeightSpec::diagonal validation (weight.cpp:11-17) on host values.
-int check_diagonal(const double* h, int64_t len) {
-  if (len <= 0) return set_err(RBD_ERR_INVALID_ARGUMENT, "diagonal weight must be non-empty");
-  for (int64_t i = 0; i < len; ++i)
-    if (!(h[i] > 0.0) || !std::isfinite(h[i]))
-      return set_err(RBD_ERR_INVALID_ARGUMENT,
-                     "diagonal weight entries must be strictly positive and finite");
-  return RBD_OK;
-}
 }  // namespace
 
 int rbd_decompose_device(rbd_ctx_t ctx, const double* dX, int64_t m, int64_t n, int64_t ldx,
@@ -1350,892 +1199,6 @@ int rbd_mgs_project(rbd_ctx_t ctx, const double* dv, int64_t m, const double* dB
   return RBD_OK;
 }
 
-// ---------------------------------------------------------------------------
-// Workspace API
-// ---------------------------------------------------------------------------
-int rbd_ws_init(rbd_ctx_t ctx, const double* dX, int64_t m, int64_t n, int64_t ldx, int64_t cap,
-                rbd_ws_t* out) {
-  if (!ctx || !out) return set_err(RBD_ERR_INVALID_ARGUMENT, "null argument");
-  if (m < 1 || n < 1) return set_err(RBD_ERR_INVALID_ARGUMENT, "workspace_init: empty matrix");
-  if (ldx < m) return set_err(RBD_ERR_DIMENSION_MISMATCH, "workspace_init: ldx < m");
-  CU(cudaSetDevice(ctx->device));
-  auto* ws = new rbd_ws_s();
-  ws->ctx = ctx;
-  ws->X = dX;
-  ws->m = m;
-  ws->n = n;
-  ws->ldx = ldx;
-  ws->cap = std::max<int64_t>(cap, 1);
-  ws->d = 0;
-  const long long S = cdiv(m, kChunk);
-  int rc = RBD_OK;
-  if ((rc = ensure(ws->T, sizeof(double) * ws->cap * n)) ||
-      (rc = ensure(ws->colsq, sizeof(double) * n)) || (rc = ensure(ws->resid, sizeof(double) * n)) ||
-      (rc = ensure(ws->partial, sizeof(double) * S * n)) ||
-      (rc = ensure(ws->rec, sizeof(Rec) * (size_t)ctx->nsm * 8)) ||
-      (rc = ensure(ws->counter, 64)) || (rc = ensure(ws->out, 64)) ||
-      (rc = ensure(ws->tmp, sizeof(DevState) + 64))) {
-    rbd_ws_destroy(ws);
-    return rc;
-  }
-  cudaMemsetAsync(ws->counter.p, 0, 64, ctx->stream);
-  cudaMemsetAsync(ws->tmp.p, 0, sizeof(DevState), ctx->stream);
-  rc = enqueue_init(ctx, dX, m, n, ldx, ptr<double>(ws->partial), ptr<double>(ws->colsq),
-                    ptr<double>(ws->resid), ptr<DevState>(ws->tmp));
-  if (rc == RBD_OK && cudaStreamSynchronize(ctx->stream) != cudaSuccess)
-    rc = set_err(RBD_ERR_CUDA, "workspace_init: kernel failure");
-  if (rc != RBD_OK) {
-    rbd_ws_destroy(ws);
-    return rc;
-  }
-  *out = ws;
-  return RBD_OK;
-}
-
-int rbd_ws_destroy(rbd_ws_t ws) {
-  if (!ws) return RBD_OK;
-  DevBuf* bl[] = {&ws->T,       &ws->colsq, &ws->resid, &ws->partial, &ws->rec,
-                  &ws->counter, &ws->out,   &ws->tmp,   &ws->Xown,    &ws->diag,
-                  &ws->basis,   &ws->axi,   &ws->yy,    &ws->yay,     &ws->row};
-  for (DevBuf* b : bl) release(*b);
-  delete ws;
-  return RBD_OK;
-}
-
-int64_t rbd_ws_d(rbd_ws_t ws) { return ws ? ws->d : 0; }
-
-int rbd_ws_extend(rbd_ws_t ws, const double* dxi) {
-  if (!ws) return set_err(RBD_ERR_INVALID_ARGUMENT, "null workspace");
-  if (ws->d >= ws->cap) return set_err(RBD_ERR_INVALID_ARGUMENT, "workspace_extend: capacity exhausted");
-  rbd_ctx_t ctx = ws->ctx;
-  CU(cudaSetDevice(ctx->device));
-  if (ws->kind == 1) {   // diagonal, workspace.cpp:61-79
-    const long long m = ws->m, n = ws->n, d = ws->d, S = cdiv(m, kChunk);
-    double* basis = ptr<double>(ws->basis);
-    CU(cudaMemcpyAsync(basis + d * m, dxi, sizeof(double) * m, cudaMemcpyDeviceToDevice,
-                       ctx->stream));
-    // a o xi (weight.cpp:83) and xi'A xi (:75): k_diag_vec reads column st->d of
-    // its "Y" argument; the workspace's scratch state has d = 0, done = 0
-    DevState* st0 = ptr<DevState>(ws->tmp);
-    const int gv = diag_vec_grid(ctx, m);
-    k_diag_vec<<<gv, kThreads, 0, ctx->stream>>>(basis + d * m, m, ptr<double>(ws->diag),
-                                                 ptr<double>(ws->axi), ptr<double>(ws->yy), st0);
-    ctx->launches++;
-    // YAX row d = X'(a o xi) (:66)
-    const int vx = (ws->ldx % 2 == 0 && aligned16(ws->X) && aligned16(ws->axi.p)) ? 2 : 1;
-    SweepArgs s{};
-    s.A = ws->X;
-    s.lda = ws->ldx;
-    s.m = m;
-    s.ncols = n;
-    s.v = ptr<double>(ws->axi);
-    s.partial = ptr<double>(ws->partial);
-    s.pstride = n;
-    s.gate = GATE_NONE;
-    TRY(launch_sweep(ctx, s, vx, MODE_DOT, true, n));
-    const int gr = (int)std::max<long long>(1, std::min<long long>(cdiv(n, 256), (long long)ctx->nsm * 4));
-    k_rowsum<<<gr, 256, 0, ctx->stream>>>(ptr<double>(ws->partial), S, n, ptr<double>(ws->T) + d * n);
-    ctx->launches++;
-    // YAY row d (:69-75): the earlier basis vectors against a o xi
-    if (d > 0) {
-      const int vb = (m % 2 == 0 && aligned16(ws->basis.p) && aligned16(ws->axi.p)) ? 2 : 1;
-      SweepArgs b{};
-      b.A = basis;
-      b.lda = m;
-      b.m = m;
-      b.ncols = d;
-      b.v = ptr<double>(ws->axi);
-      b.partial = ptr<double>(ws->partial);
-      b.pstride = d;
-      b.gate = GATE_NONE;
-      TRY(launch_sweep(ctx, b, vb, MODE_DOT, false, d));
-      k_rowsum<<<(unsigned)std::max<long long>(1, cdiv(d, 256)), 256, 0, ctx->stream>>>(
-          ptr<double>(ws->partial), S, d, ptr<double>(ws->row));
-      ctx->launches++;
-    }
-    k_yay_row<<<(unsigned)std::max<long long>(1, cdiv(d, 256)), 256, 0, ctx->stream>>>(
-        ptr<double>(ws->row), d, ptr<double>(ws->yy), gv, ptr<double>(ws->yay), ws->cap);
-    ctx->launches++;
-    CU(cudaGetLastError());
-    CU(cudaStreamSynchronize(ctx->stream));
-    ws->d += 1;
-    return RBD_OK;
-  }
-  const int vec = (ws->ldx % 2 == 0 && aligned16(ws->X) && aligned16(dxi)) ? 2 : 1;
-  SweepArgs s{};
-  s.A = ws->X;
-  s.lda = ws->ldx;
-  s.m = ws->m;
-  s.ncols = ws->n;
-  s.v = dxi;
-  s.partial = ptr<double>(ws->partial);
-  s.pstride = ws->n;
-  s.st = nullptr;
-  s.gate = GATE_NONE;
-  TRY(launch_sweep(ctx, s, vec, MODE_DOT, true, ws->n));
-  FinalizeArgs f{};
-  f.partial = ptr<double>(ws->partial);
-  f.S = cdiv(ws->m, kChunk);
-  f.n = ws->n;
-  f.T = ptr<double>(ws->T);
-  f.krow = ws->d;
-  f.r = ptr<double>(ws->resid);
-  f.col_sq = ptr<double>(ws->colsq);
-  f.st = nullptr;
-  f.mode = 1;
-  k_finalize<<<finalize_grid(ctx, ws->n), kThreads, 0, ctx->stream>>>(f);
-  ctx->launches++;
-  CU(cudaGetLastError());
-  CU(cudaStreamSynchronize(ctx->stream));
-  ws->d += 1;
-  return RBD_OK;
-}
-
-int rbd_ws_scan(rbd_ws_t ws, double* e_cur, int64_t* argmax) {
-  if (!ws) return set_err(RBD_ERR_INVALID_ARGUMENT, "null workspace");
-  rbd_ctx_t ctx = ws->ctx;
-  CU(cudaSetDevice(ctx->device));
-  const int g = finalize_grid(ctx, ws->n);
-  k_scan_only<<<g, kThreads, 0, ctx->stream>>>(ptr<double>(ws->resid), ws->n, ptr<Rec>(ws->rec),
-                                                ptr<unsigned>(ws->counter), ptr<Rec>(ws->out));
-  ctx->launches++;
-  CU(cudaGetLastError());
-  CU(cudaMemcpyAsync(ctx->h_rec, ws->out.p, sizeof(Rec), cudaMemcpyDeviceToHost, ctx->stream));
-  CU(cudaStreamSynchronize(ctx->stream));
-  if (e_cur) *e_cur = ctx->h_rec->v;
-  if (argmax) *argmax = ctx->h_rec->j;
-  return RBD_OK;
-}
-
-int rbd_ws_error_sq(rbd_ws_t ws, int64_t j, const double* h_c, int64_t clen, double* out) {
-  if (!ws) return set_err(RBD_ERR_INVALID_ARGUMENT, "null workspace");
-  if (j < 0 || j >= ws->n) return set_err(RBD_ERR_INDEX_OUT_OF_RANGE, "error_sq: column index out of range");
-  if (clen != ws->d) return set_err(RBD_ERR_DIMENSION_MISMATCH, "error_sq: coefficient length != d");
-  rbd_ctx_t ctx = ws->ctx;
-  CU(cudaSetDevice(ctx->device));
-  double* dc = reinterpret_cast<double*>(static_cast<char*>(ws->tmp.p) + sizeof(DevState));
-  DevBuf cbuf;
-  if (clen > 0) {
-    TRY(ensure(cbuf, sizeof(double) * clen));
-    CU(cudaMemcpyAsync(cbuf.p, h_c, sizeof(double) * clen, cudaMemcpyHostToDevice, ctx->stream));
-  }
-  if (ws->kind == 1)
-    k_error_sq_w<<<1, kThreads, 0, ctx->stream>>>(ptr<double>(ws->T), ws->n, ws->d, j,
-                                                  ptr<double>(cbuf), ptr<double>(ws->yay), ws->cap,
-                                                  ptr<double>(ws->colsq), dc);
-  else
-    k_error_sq<<<1, kThreads, 0, ctx->stream>>>(ptr<double>(ws->T), ws->n, ws->d, j,
-                                                ptr<double>(cbuf), ptr<double>(ws->colsq), dc);
-  ctx->launches++;
-  CU(cudaGetLastError());
-  CU(cudaMemcpyAsync(out, dc, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
-  CU(cudaStreamSynchronize(ctx->stream));
-  release(cbuf);
-  return RBD_OK;
-}
-
-int rbd_ws_read(rbd_ws_t ws, double* h_col_sq, double* h_residual_sq, double* h_yax) {
-  if (!ws) return set_err(RBD_ERR_INVALID_ARGUMENT, "null workspace");
-  rbd_ctx_t ctx = ws->ctx;
-  CU(cudaSetDevice(ctx->device));
-  if (h_col_sq) CU(cudaMemcpyAsync(h_col_sq, ws->colsq.p, sizeof(double) * ws->n, cudaMemcpyDeviceToHost, ctx->stream));
-  if (h_residual_sq)
-    CU(cudaMemcpyAsync(h_residual_sq, ws->resid.p, sizeof(double) * ws->n, cudaMemcpyDeviceToHost, ctx->stream));
-  if (h_yax && ws->d > 0)
-    CU(cudaMemcpyAsync(h_yax, ws->T.p, sizeof(double) * ws->d * ws->n, cudaMemcpyDeviceToHost, ctx->stream));
-  CU(cudaStreamSynchronize(ctx->stream));
-  return RBD_OK;
-}
-
-int rbd_ws_init_diag(rbd_ctx_t ctx, const double* dX, int64_t m, int64_t n, int64_t ldx,
-                     int64_t cap, const double* d_diag, int64_t diag_len, rbd_ws_t* out) {
-  if (!ctx || !out) return set_err(RBD_ERR_INVALID_ARGUMENT, "null argument");
-  CU(cudaSetDevice(ctx->device));
-  std::vector<double> h((size_t)std::max<int64_t>(diag_len, 0));
-  if (diag_len > 0) {
-    if (!d_diag) return set_err(RBD_ERR_INVALID_ARGUMENT, "workspace_init: null diagonal");
-    CU(cudaMemcpyAsync(h.data(), d_diag, sizeof(double) * diag_len, cudaMemcpyDeviceToHost,
-                       ctx->stream));
-    CU(cudaStreamSynchronize(ctx->stream));
-  }
-  TRY(check_diagonal(h.data(), diag_len));                              // weight.cpp:11-17
-  if (m < 1 || n < 1) return set_err(RBD_ERR_INVALID_ARGUMENT, "workspace_init: empty matrix");
-  if (diag_len != m)                                                    // workspace.cpp:12-13
-    return set_err(RBD_ERR_INCOMPATIBLE_WEIGHT, "weight dimension does not match matrix rows");
-  rbd_ws_t ws = nullptr;
-  TRY(rbd_ws_init(ctx, dX, m, n, ldx, cap, &ws));
-  int rc = RBD_OK;
-  const long long c = ws->cap;
-  if ((rc = ensure(ws->diag, sizeof(double) * m)) || (rc = ensure(ws->basis, sizeof(double) * m * c)) ||
-      (rc = ensure(ws->axi, sizeof(double) * m)) ||
-      (rc = ensure(ws->yy, sizeof(double) * diag_vec_grid(ctx, m))) ||
-      (rc = ensure(ws->yay, sizeof(double) * c * c)) ||
-      (rc = ensure(ws->row, sizeof(double) * std::max<long long>(c, 1))) ||
-      (rc = ensure(ws->partial, sizeof(double) * cdiv(m, kChunk) * std::max<long long>(n, c)))) {
-    rbd_ws_destroy(ws);
-    return rc;
-  }
-  ws->kind = 1;
-  cudaMemcpyAsync(ws->diag.p, d_diag, sizeof(double) * m, cudaMemcpyDeviceToDevice, ctx->stream);
-  cudaMemsetAsync(ws->yay.p, 0, sizeof(double) * c * c, ctx->stream);
-  // col_sq = diag(X'AX) (workspace.cpp:24-29), residual_sq = col_sq (:38)
-  const int g = (int)std::max<long long>(1, std::min<long long>(n, (long long)ctx->nsm * 8));
-  k_colsq_diag<<<g, kThreads, 0, ctx->stream>>>(dX, ldx, m, n, ptr<double>(ws->diag),
-                                                ptr<double>(ws->colsq));
-  ctx->launches++;
-  cudaMemcpyAsync(ws->resid.p, ws->colsq.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->stream);
-  if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(ctx->stream) != cudaSuccess) {
-    rbd_ws_destroy(ws);
-    return set_err(RBD_ERR_CUDA, "workspace_init: kernel failure");
-  }
-  *out = ws;
-  return RBD_OK;
-}
-
-int rbd_ws_scan_T(rbd_ws_t ws, const double* dT, double* e_cur, int64_t* argmax) {
-  if (!ws) return set_err(RBD_ERR_INVALID_ARGUMENT, "null workspace");
-  if (ws->d > 0 && !dT) return set_err(RBD_ERR_DIMENSION_MISMATCH, "residual_scan: T shape does not match workspace");
-  rbd_ctx_t ctx = ws->ctx;
-  CU(cudaSetDevice(ctx->device));
-  const int g = finalize_grid(ctx, ws->n);
-  k_scan_T<<<g, kThreads, 0, ctx->stream>>>(ptr<double>(ws->T), dT, ws->n, ws->d,
-                                            ws->kind == 1 ? ptr<double>(ws->yay) : nullptr, ws->cap,
-                                            ptr<double>(ws->colsq), ptr<Rec>(ws->rec),
-                                            ptr<unsigned>(ws->counter), ptr<Rec>(ws->out));
-  ctx->launches++;
-  CU(cudaGetLastError());
-  CU(cudaMemcpyAsync(ctx->h_rec, ws->out.p, sizeof(Rec), cudaMemcpyDeviceToHost, ctx->stream));
-  CU(cudaStreamSynchronize(ctx->stream));
-  if (e_cur) *e_cur = ctx->h_rec->v;
-  if (argmax) *argmax = ctx->h_rec->j;
-  return RBD_OK;
-}
-
-int rbd_ws_scan_T_host(rbd_ws_t ws, const double* hT, double* e_cur, int64_t* argmax) {
-  if (!ws) return set_err(RBD_ERR_INVALID_ARGUMENT, "null workspace");
-  rbd_ctx_t ctx = ws->ctx;
-  CU(cudaSetDevice(ctx->device));
-  DevBuf tb;
-  if (ws->d > 0) {
-    TRY(ensure(tb, sizeof(double) * ws->d * ws->n));
-    if (cudaMemcpyAsync(tb.p, hT, sizeof(double) * ws->d * ws->n, cudaMemcpyHostToDevice,
-                        ctx->stream) != cudaSuccess) {
-      release(tb);
-      return set_err(RBD_ERR_CUDA, "residual_scan: H2D failed");
-    }
-  }
-  const int rc = rbd_ws_scan_T(ws, ws->d > 0 ? ptr<double>(tb) : nullptr, e_cur, argmax);
-  release(tb);
-  return rc;
-}
-
-int rbd_ws_read_yay(rbd_ws_t ws, double* h_yay) {
-  if (!ws) return set_err(RBD_ERR_INVALID_ARGUMENT, "null workspace");
-  if (ws->kind != 1) return set_err(RBD_ERR_INVALID_ARGUMENT, "read_yay: identity workspace (Y'AY = I)");
-  rbd_ctx_t ctx = ws->ctx;
-  CU(cudaSetDevice(ctx->device));
-  if (ws->d > 0)
-    CU(cudaMemcpy2DAsync(h_yay, sizeof(double) * ws->d, ws->yay.p, sizeof(double) * ws->cap,
-                         sizeof(double) * ws->d, ws->d, cudaMemcpyDeviceToHost, ctx->stream));
-  CU(cudaStreamSynchronize(ctx->stream));
-  return RBD_OK;
-}
-
-// ---------------------------------------------------------------------------
-// Out-of-sample compression (K5) and reconstruct
-// ---------------------------------------------------------------------------
-int rbd_project_batch(rbd_ctx_t ctx, const double* dY, int64_t m, int64_t d, int64_t ldy,
-                      const double* dXn, int64_t N, int64_t ldx, double* dTn, double* d_err) {
-  if (!ctx) return set_err(RBD_ERR_INVALID_ARGUMENT, "null context");
-  if (m < 1 || d < 1 || N < 0) return set_err(RBD_ERR_DIMENSION_MISMATCH, "project: bad sizes");
-  if (ldy < m || ldx < m) return set_err(RBD_ERR_DIMENSION_MISMATCH, "project: vector length != m");
-  if (N == 0) return RBD_OK;
-  CU(cudaSetDevice(ctx->device));
-  long long nl = 0;
-  if (d_err) TRY(ensure(ctx->scratch1, sizeof(double) * (size_t)std::max<int64_t>(N, 32)));
-  // split the K = m reduction when the DMMA grid would leave a partial last wave
-  int sk = rbdk::project_splitk(m, d, N, ctx->nsm);
-  if (sk > 1 && ensure(ctx->pj_ws, sizeof(double) * (size_t)(sk - 1) * (size_t)(d * N + N)) != RBD_OK)
-    sk = 1;
-  int rc = rbdk::launch_project_f64(dY, m, d, ldy, dXn, N, ldx, dTn, d_err, ctx->stream, &nl,
-                                    d_err ? ptr<double>(ctx->scratch1) : nullptr, sk,
-                                    sk > 1 ? ptr<double>(ctx->pj_ws) : nullptr);
-  ctx->launches += nl;
-  if (rc != 0) return set_err(RBD_ERR_CUDA, std::string("project kernel: ") + cudaGetErrorString((cudaError_t)rc));
-  return RBD_OK;
-}
-
-int rbd_nearest_columns(rbd_ctx_t ctx, const double* dC, int64_t d, int64_t Q, int64_t ldc,
-                        const double* dT, int64_t n_train, int64_t* d_best, double* d_dist) {
-  if (!ctx) return set_err(RBD_ERR_INVALID_ARGUMENT, "null context");
-  if (d < 1 || n_train < 1 || Q < 0 || ldc < d)
-    return set_err(RBD_ERR_DIMENSION_MISMATCH, "nearest: bad sizes");
-  if (Q == 0) return RBD_OK;
-  if (!dC || !dT || !d_best) return set_err(RBD_ERR_INVALID_ARGUMENT, "nearest: null buffer");
-  CU(cudaSetDevice(ctx->device));
-  const long long gx = cdiv(Q, kNnTile);
-  const long long tiles = cdiv(n_train, kNnTile);
-  // split the training columns for the best-filled waves (resident CTAs per SM
-  // from the occupancy API); a larger split must fill them by 2 points more
-  static int nn_occ = 0;
-  if (nn_occ == 0) {
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nn_occ, k_nearest, kThreads, 0) != cudaSuccess ||
-        nn_occ < 1)
-      nn_occ = 1;
-  }
-  const long long slots = (long long)nn_occ * ctx->nsm;
-  long long nsplit = 1, per = tiles * kNnTile;
-  {
-    double best_eff = 0.0;
-    for (long long sp = 1; sp <= std::min<long long>(tiles, 16); ++sp) {
-      const long long pr = cdiv(tiles, sp) * kNnTile;
-      const long long ns = cdiv(n_train, pr);
-      const long long c = gx * ns, waves = cdiv(c, slots);
-      const double eff = (double)c / (double)(waves * slots);
-      if (sp == 1 || eff > best_eff + 0.02) {
-        best_eff = eff;
-        nsplit = ns;
-        per = pr;
-      }
-    }
-  }
-  if (gx > 0x7fffffffLL || nsplit > 65535)
-    return set_err(RBD_ERR_INVALID_ARGUMENT, "nearest: problem too large for one launch");
-  TRY(ensure(ctx->nn_part, sizeof(NnRec) * (size_t)nsplit * (size_t)Q));
-  k_nearest<<<dim3((unsigned)gx, (unsigned)nsplit), kThreads, 0, ctx->stream>>>(
-      dC, ldc, dT, n_train, d, Q, per, ptr<NnRec>(ctx->nn_part));
-  const int gr = (int)std::max<long long>(1, std::min<long long>(cdiv(Q, 256), (long long)ctx->nsm * 4));
-  k_nearest_reduce<<<gr, 256, 0, ctx->stream>>>(ptr<NnRec>(ctx->nn_part), Q, (int)nsplit,
-                                                reinterpret_cast<long long*>(d_best),
-                                                d_dist);
-  ctx->launches += 2;
-  CU(cudaGetLastError());
-  return RBD_OK;
-}
-
-int rbd_classify_batch(rbd_ctx_t ctx, const double* dY, int64_t m, int64_t d, int64_t ldy,
-                       const double* dT, int64_t n_train, const double* dQ, int64_t Q,
-                       int64_t ldq, int64_t* d_best, double* d_dist) {
-  if (!ctx) return set_err(RBD_ERR_INVALID_ARGUMENT, "null context");
-  if (m < 1 || d < 1 || n_train < 1 || Q < 0)
-    return set_err(RBD_ERR_DIMENSION_MISMATCH, "classify: bad sizes");
-  if (ldy < m || ldq < m)
-    return set_err(RBD_ERR_DIMENSION_MISMATCH, "classify: test dimension != training dimension");
-  if (Q == 0) return RBD_OK;
-  CU(cudaSetDevice(ctx->device));
-  TRY(ensure(ctx->nn_coords, sizeof(double) * (size_t)d * (size_t)Q));
-  double* C = ptr<double>(ctx->nn_coords);
-  TRY(rbd_project_batch(ctx, dY, m, d, ldy, dQ, Q, ldq, C, nullptr));   // c = Y'v (K5)
-  return rbd_nearest_columns(ctx, C, d, Q, d, dT, n_train, d_best, d_dist);
-}
-
-int rbd_classify_host(rbd_ctx_t ctx, const double* hY, int64_t m, int64_t d, const double* hT,
-                      int64_t n_train, const double* hQ, int64_t Q, int64_t* h_best,
-                      double* h_dist) {
-  if (!ctx) return set_err(RBD_ERR_INVALID_ARGUMENT, "null context");
-  if (m < 1 || d < 1 || n_train < 1 || Q < 0)
-    return set_err(RBD_ERR_DIMENSION_MISMATCH, "classify: bad sizes");
-  if (Q == 0) return RBD_OK;
-  CU(cudaSetDevice(ctx->device));
-  DevBuf bY, bT, bQ, bB, bD;
-  auto fin = [&](int rc) {
-    release(bY);
-    release(bT);
-    release(bQ);
-    release(bB);
-    release(bD);
-    return rc;
-  };
-  const long long ldm = (m % 2 == 0) ? m : m + 1;   // 16-byte aligned columns for K5
-  int rc;
-  if ((rc = ensure(bY, sizeof(double) * ldm * d)) || (rc = ensure(bT, sizeof(double) * d * n_train)) ||
-      (rc = ensure(bQ, sizeof(double) * ldm * Q)) || (rc = ensure(bB, sizeof(int64_t) * Q)) ||
-      (rc = ensure(bD, sizeof(double) * Q)))
-    return fin(rc);
-  if (cudaMemcpy2DAsync(bY.p, sizeof(double) * ldm, hY, sizeof(double) * m, sizeof(double) * m, d,
-                        cudaMemcpyHostToDevice, ctx->stream) ||
-      cudaMemcpyAsync(bT.p, hT, sizeof(double) * d * n_train, cudaMemcpyHostToDevice, ctx->stream) ||
-      cudaMemcpy2DAsync(bQ.p, sizeof(double) * ldm, hQ, sizeof(double) * m, sizeof(double) * m, Q,
-                        cudaMemcpyHostToDevice, ctx->stream))
-    return fin(set_err(RBD_ERR_CUDA, "classify_host: H2D failed"));
-  rc = rbd_classify_batch(ctx, ptr<double>(bY), m, d, ldm, ptr<double>(bT), n_train, ptr<double>(bQ),
-                          Q, ldm, ptr<int64_t>(bB), ptr<double>(bD));
-  if (rc) return fin(rc);
-  if (cudaMemcpyAsync(h_best, bB.p, sizeof(int64_t) * Q, cudaMemcpyDeviceToHost, ctx->stream) ||
-      (h_dist && cudaMemcpyAsync(h_dist, bD.p, sizeof(double) * Q, cudaMemcpyDeviceToHost,
-                                 ctx->stream)) ||
-      cudaStreamSynchronize(ctx->stream))
-    return fin(set_err(RBD_ERR_CUDA, "classify_host: D2H failed"));
-  return fin(RBD_OK);
-}
-
-int rbd_reconstruct(rbd_ctx_t ctx, const double* dY, int64_t m, int64_t d, int64_t ldy,
-                    const double* dc, double* dv) {
-  if (!ctx) return set_err(RBD_ERR_INVALID_ARGUMENT, "null context");
-  if (ldy < m) return set_err(RBD_ERR_DIMENSION_MISMATCH, "reconstruct: ldy < m");
-  CU(cudaSetDevice(ctx->device));
-  long long nl = 0;
-  int rc = rbdk::launch_reconstruct_f64(dY, m, d, ldy, dc, dv, ctx->stream, &nl);
-  ctx->launches += nl;
-  if (rc != 0) return set_err(RBD_ERR_CUDA, std::string("reconstruct kernel: ") + cudaGetErrorString((cudaError_t)rc));
-  return RBD_OK;
-}
-
-}  // extern "C"
-
-extern "C" {
-
-int rbd_project_host(rbd_ctx_t ctx, const double* hY, int64_t m, int64_t d, const double* hXn,
-                     int64_t N, double* hTn, double* h_err) {
-  if (!ctx) return set_err(RBD_ERR_INVALID_ARGUMENT, "null context");
-  if (m < 1 || d < 1 || N < 0) return set_err(RBD_ERR_DIMENSION_MISMATCH, "project: bad sizes");
-  if (N == 0) return RBD_OK;
-  CU(cudaSetDevice(ctx->device));
-  DevBuf bY, bX, bT, bE;
-  auto fin = [&](int rc) {
-    release(bY);
-    release(bX);
-    release(bT);
-    release(bE);
-    return rc;
-  };
-  int rc;
-  if ((rc = ensure(bY, sizeof(double) * m * d)) || (rc = ensure(bX, sizeof(double) * m * N)) ||
-      (rc = ensure(bT, sizeof(double) * d * N)) || (rc = ensure(bE, sizeof(double) * N)))
-    return fin(rc);
-  if (cudaMemcpyAsync(bY.p, hY, sizeof(double) * m * d, cudaMemcpyHostToDevice, ctx->stream) ||
-      cudaMemcpyAsync(bX.p, hXn, sizeof(double) * m * N, cudaMemcpyHostToDevice, ctx->stream))
-    return fin(set_err(RBD_ERR_CUDA, "project_host: H2D failed"));
-  rc = rbd_project_batch(ctx, ptr<double>(bY), m, d, m, ptr<double>(bX), N, m, ptr<double>(bT),
-                         h_err ? ptr<double>(bE) : nullptr);
-  if (rc) return fin(rc);
-  if (hTn && cudaMemcpyAsync(hTn, bT.p, sizeof(double) * d * N, cudaMemcpyDeviceToHost, ctx->stream))
-    return fin(set_err(RBD_ERR_CUDA, "project_host: D2H failed"));
-  if (h_err && cudaMemcpyAsync(h_err, bE.p, sizeof(double) * N, cudaMemcpyDeviceToHost, ctx->stream))
-    return fin(set_err(RBD_ERR_CUDA, "project_host: D2H failed"));
-  if (cudaStreamSynchronize(ctx->stream)) return fin(set_err(RBD_ERR_CUDA, "project_host: sync failed"));
-  return fin(RBD_OK);
-}
-
-int rbd_reconstruct_host(rbd_ctx_t ctx, const double* hY, int64_t m, int64_t d, const double* hc,
-                         double* hv) {
-  if (!ctx) return set_err(RBD_ERR_INVALID_ARGUMENT, "null context");
-  if (m < 1 || d < 0) return set_err(RBD_ERR_DIMENSION_MISMATCH, "reconstruct: bad sizes");
-  CU(cudaSetDevice(ctx->device));
-  DevBuf bY, bc, bv;
-  auto fin = [&](int rc) {
-    release(bY);
-    release(bc);
-    release(bv);
-    return rc;
-  };
-  int rc;
-  if ((rc = ensure(bY, sizeof(double) * m * std::max<int64_t>(d, 1))) ||
-      (rc = ensure(bc, sizeof(double) * std::max<int64_t>(d, 1))) || (rc = ensure(bv, sizeof(double) * m)))
-    return fin(rc);
-  if (d > 0 && (cudaMemcpyAsync(bY.p, hY, sizeof(double) * m * d, cudaMemcpyHostToDevice, ctx->stream) ||
-                cudaMemcpyAsync(bc.p, hc, sizeof(double) * d, cudaMemcpyHostToDevice, ctx->stream)))
-    return fin(set_err(RBD_ERR_CUDA, "reconstruct_host: H2D failed"));
-  rc = rbd_reconstruct(ctx, ptr<double>(bY), m, d, m, ptr<double>(bc), ptr<double>(bv));
-  if (rc) return fin(rc);
-  if (cudaMemcpyAsync(hv, bv.p, sizeof(double) * m, cudaMemcpyDeviceToHost, ctx->stream) ||
-      cudaStreamSynchronize(ctx->stream))
-    return fin(set_err(RBD_ERR_CUDA, "reconstruct_host: D2H failed"));
-  return fin(RBD_OK);
-}
-
-int rbd_time_sweep(rbd_ctx_t ctx, const double* dX, int64_t m, int64_t n, int64_t ldx,
-                   const double* dy, int reps, double* ms_per_launch) {
-  if (!ctx || reps < 1) return set_err(RBD_ERR_INVALID_ARGUMENT, "time_sweep: bad arguments");
-  CU(cudaSetDevice(ctx->device));
-  TRY(ensure(ctx->partial, sizeof(double) * cdiv(m, kChunk) * n));
-  const int vec = (ldx % 2 == 0 && aligned16(dX) && aligned16(dy)) ? 2 : 1;
-  SweepArgs s{};
-  s.A = dX;
-  s.lda = ldx;
-  s.m = m;
-  s.ncols = n;
-  s.v = dy;
-  s.partial = ptr<double>(ctx->partial);
-  s.pstride = n;
-  s.gate = GATE_NONE;
-  TRY(launch_sweep(ctx, s, vec, MODE_DOT, true, n));  // warm-up
-  cudaEvent_t a, b;
-  CU(cudaEventCreate(&a));
-  CU(cudaEventCreate(&b));
-  cudaEventRecord(a, ctx->stream);
-  for (int r = 0; r < reps; ++r) {
-    int rc = launch_sweep(ctx, s, vec, MODE_DOT, true, n);
-    if (rc) {
-      cudaEventDestroy(a);
-      cudaEventDestroy(b);
-      return rc;
-    }
-  }
-  cudaEventRecord(b, ctx->stream);
-  cudaError_t e = cudaEventSynchronize(b);
-  float ms = 0.f;
-  cudaEventElapsedTime(&ms, a, b);
-  cudaEventDestroy(a);
-  cudaEventDestroy(b);
-  if (e != cudaSuccess) return set_err(RBD_ERR_CUDA, std::string("time_sweep: ") + cudaGetErrorString(e));
-  *ms_per_launch = ms / reps;
-  return RBD_OK;
-}
-
-}  // extern "C"
-
-// ===========================================================================
-// Sharded (multi-GPU) greedy loop — SURVEY.md §8(e)
-//
-// X is split by contiguous column blocks, Y is replicated. Each step every
-// rank runs the one-step mode of the persistent kernel on its shard
-// (k_rbd_persistent<VEC, true>): the replicated extension pass, the replicated
-// Y'w1 tiles (identical bits on every rank), the local X'w1 sweep and
-// finalisation, and packs a payload = (its best residual, global index,
-// col_sq, x_j, T[0:k+1, j]). One allgather of payloads replaces the max-loc
-// allreduce + owner broadcast (exact: no arithmetic on the data), and
-// k_shard_select picks the winner identically on every rank. Per-column sums
-// depend on m only, so results are bit-identical for any number of shards.
-//
-// Two exchanges: NCCL (one process per GPU, NCCL loaded with dlopen) and
-// virtual ranks (R shards in one process on one device, stepped in lockstep on
-// one stream — no kernel ever waits for another rank).
-// ===========================================================================
-#include <nccl.h>
-
-namespace {
-
-struct NcclApi {
-  void* h = nullptr;
-  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
-  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
-  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
-                            cudaStream_t) = nullptr;
-  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
-  const char* (*GetErrorString)(ncclResult_t) = nullptr;
-  bool ok = false;
-};
-
-NcclApi& nccl() {
-  static NcclApi api = [] {
-    NcclApi a;
-    const char* names[] = {"libnccl.so.2", "libnccl.so"};
-    for (const char* nm : names)
-      if ((a.h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL))) break;
-    if (!a.h) return a;
-    a.GetUniqueId = (decltype(a.GetUniqueId))dlsym(a.h, "ncclGetUniqueId");
-    a.CommInitRank = (decltype(a.CommInitRank))dlsym(a.h, "ncclCommInitRank");
-    a.AllGather = (decltype(a.AllGather))dlsym(a.h, "ncclAllGather");
-    a.CommDestroy = (decltype(a.CommDestroy))dlsym(a.h, "ncclCommDestroy");
-    a.GetErrorString = (decltype(a.GetErrorString))dlsym(a.h, "ncclGetErrorString");
-    a.ok = a.GetUniqueId && a.CommInitRank && a.AllGather && a.CommDestroy && a.GetErrorString;
-    return a;
-  }();
-  return api;
-}
-
-struct Exchange {
-  virtual ~Exchange() = default;
-  virtual int world() const = 0;
-  // every rank's `count` doubles of send -> slot [rank] of every rank's recv
-  virtual int allgather(std::vector<rbd_ctx_t>& R, long long count) = 0;
-};
-
-struct LocalExchange : Exchange {
-  int R;
-  explicit LocalExchange(int r) : R(r) {}
-  int world() const override { return R; }
-  int allgather(std::vector<rbd_ctx_t>& ranks, long long count) override {
-    for (int r = 0; r < R; ++r)
-      for (int s = 0; s < R; ++s)
-        CU(cudaMemcpyAsync(ptr<double>(ranks[r]->recv) + (long long)s * count, ranks[s]->send.p,
-                           sizeof(double) * count, cudaMemcpyDeviceToDevice, ranks[r]->stream));
-    return RBD_OK;
-  }
-};
-
-struct NcclExchange : Exchange {
-  int W;
-  explicit NcclExchange(int w) : W(w) {}
-  int world() const override { return W; }
-  int allgather(std::vector<rbd_ctx_t>& ranks, long long count) override {
-    rbd_ctx_t c = ranks[0];
-    ncclResult_t r = nccl().AllGather(c->send.p, c->recv.p, (size_t)count, ncclDouble,
-                                      (ncclComm_t)c->comm, c->stream);
-    if (r != ncclSuccess) return set_err(RBD_ERR_NCCL, std::string("ncclAllGather: ") + nccl().GetErrorString(r));
-    return RBD_OK;
-  }
-};
-
-struct Shard {
-  const double* X;
-  long long n_local;
-  long long col_offset;
-  double* Y;
-  double* T;
-};
-
-int shard_step_launch(rbd_ctx_t c, const Shard& sh, long long m, long long ldx, long long d_max,
-                      long long pay_stride, int vec, int grid) {
-  PersistArgs a{};
-  a.X = sh.X;
-  a.ldx = ldx;
-  a.m = m;
-  a.n = sh.n_local;
-  a.Y = sh.Y;
-  a.T = sh.T;
-  a.w = ptr<double>(c->w);
-  a.p = ptr<double>(c->gcnt);
-  a.ppart = ptr<double>(c->ppart);
-  a.npart = ptr<double>(c->nrm);
-  a.partial = ptr<double>(c->partial);
-  a.r = ptr<double>(c->resid);
-  a.col_sq = ptr<double>(c->colsq);
-  a.rec = ptr<Rec>(c->ygcnt);
-  a.history = ptr<double>(c->hist);
-  a.selected = ptr<long long>(c->sel);
-  a.st = ptr<DevState>(c->state);
-  a.bar = ptr<unsigned>(c->bar);
-  a.d_max = d_max;
-  a.ctl = ptr<StepCtl>(c->ctl);
-  a.rdy = ptr<unsigned long long>(c->rdy);
-  a.recv = ptr<double>(c->recv);
-  a.send = ptr<double>(c->send);
-  a.pay_stride = pay_stride;
-  a.col_offset = sh.col_offset;
-  void* args[] = {&a};
-  const size_t smem = persist_smem(d_max);
-  cudaError_t e = vec == 2 ? cudaLaunchCooperativeKernel((void*)k_rbd_persistent<2, true>, grid,
-                                                         kThreads, args, smem, c->stream)
-                           : cudaLaunchCooperativeKernel((void*)k_rbd_persistent<1, true>, grid,
-                                                         kThreads, args, smem, c->stream);
-  c->launches++;
-  if (e != cudaSuccess)
-    return set_err(RBD_ERR_CUDA, std::string("sharded step launch: ") + cudaGetErrorString(e));
-  return RBD_OK;
-}
-
-int sharded_decompose(std::vector<rbd_ctx_t>& R, Exchange& ex, std::vector<Shard>& sh, long long m,
-                      long long ldx, long long n_global, const rbd_config_t* cfg,
-                      int64_t* h_selected, double* h_history, rbd_result_t* result) {
-  if (m < 1 || n_global < 1) return set_err(RBD_ERR_INVALID_ARGUMENT, "decompose: matrix must be non-empty");
-  const int nl = (int)R.size();
-  const long long d_cap = std::max<long long>(1, std::min<long long>(cfg->d_max, n_global));
-  if (d_cap > kFMaxCoef)
-    return set_err(RBD_ERR_INVALID_ARGUMENT, "sharded decompose: d_max above the fused-path limit");
-  const long long pay_stride = ((kPayHead + m + d_cap + 1) + 1) / 2 * 2;
-  bool vec2 = (ldx % 2 == 0) && (m % 2 == 0);
-  for (auto& s : sh) vec2 = vec2 && aligned16(s.X) && aligned16(s.Y);
-  const int vec = vec2 ? 2 : 1;
-  // ---- K1 on every shard, then a global combine of (finite, nonzero, max col_sq) ----
-  for (int r = 0; r < nl; ++r) {
-    rbd_ctx_t c = R[r];
-    CU(cudaSetDevice(c->device));
-    const long long nloc = std::max<long long>(sh[r].n_local, 1);
-    TRY(ensure_loop_buffers(c, m, nloc, d_cap));
-    TRY(ensure(c->send, sizeof(double) * pay_stride));
-    TRY(ensure(c->recv, sizeof(double) * pay_stride * ex.world()));
-    TRY(ensure(c->ctl, sizeof(StepCtl)));
-    TRY(ensure(c->gcnt, sizeof(double) * 2 * (size_t)(d_cap + 1)));
-    TRY(ensure(c->rdy, sizeof(unsigned long long) * (size_t)(cdiv(m, kChunk) + 1)));
-    const int grid = persistent_grid(c, vec, d_cap);
-    TRY(ensure(c->ppart, sizeof(double) * (size_t)std::max<long long>(grid, cdiv(m, kChunk)) * d_cap));
-    TRY(ensure(c->nrm, sizeof(double) * std::max<long long>(gemv_grid(m), grid)));
-    TRY(ensure(c->ygcnt, sizeof(Rec) * (size_t)grid));
-    DevState* st = ptr<DevState>(c->state);
-    CU(cudaMemsetAsync(st, 0, sizeof(DevState), c->stream));
-    CU(cudaMemsetAsync(c->ctl.p, 0, sizeof(StepCtl), c->stream));
-    CU(cudaMemsetAsync(c->rdy.p, 0, sizeof(unsigned long long) * (size_t)(cdiv(m, kChunk) + 1),
-                       c->stream));
-    CU(cudaMemsetAsync(c->bar.p, 0, 64, c->stream));
-    CU(cudaMemsetAsync(c->partial.p, 0xFF, sizeof(double) * (size_t)cdiv(m, kChunk) * nloc, c->stream));
-    if (sh[r].n_local > 0)
-      TRY(enqueue_init(c, sh[r].X, m, sh[r].n_local, ldx, ptr<double>(c->partial),
-                       ptr<double>(c->colsq), ptr<double>(c->resid), st));
-    CU(cudaMemsetAsync(c->partial.p, 0xFF, sizeof(double) * (size_t)cdiv(m, kChunk) * nloc, c->stream));
-    CU(cudaMemsetAsync(c->counter.p, 0, 64, c->stream));
-    CU(cudaMemcpyAsync(c->h_state, st, sizeof(DevState), cudaMemcpyDeviceToHost, c->stream));
-    CU(cudaStreamSynchronize(c->stream));
-    double head[4] = {(double)c->h_state->flags_nonfinite, (double)c->h_state->flags_nonzero, 0.0, 0.0};
-    std::memcpy(&head[2], &c->h_state->max_colsq_bits, sizeof(double));
-    CU(cudaMemcpyAsync(c->send.p, head, sizeof(head), cudaMemcpyHostToDevice, c->stream));
-    CU(cudaStreamSynchronize(c->stream));   // head is a stack buffer
-  }
-  TRY(ex.allgather(R, 4));
-  std::vector<double> all(4 * (size_t)ex.world());
-  CU(cudaMemcpyAsync(all.data(), R[0]->recv.p, sizeof(double) * all.size(), cudaMemcpyDeviceToHost,
-                     R[0]->stream));
-  CU(cudaStreamSynchronize(R[0]->stream));
-  DevState hs{};
-  double max_colsq = 0.0;
-  for (int w = 0; w < ex.world(); ++w) {
-    hs.flags_nonfinite |= all[4 * w] != 0.0;
-    hs.flags_nonzero |= all[4 * w + 1] != 0.0;
-    max_colsq = std::max(max_colsq, all[4 * w + 2]);
-  }
-  TRY(validate_after_init(cfg, m, n_global, hs));
-  const double tol = breakdown_tolerance(cfg, m, max_colsq);
-  long long j0 = 0;
-  TRY(start_column(cfg, n_global, &j0));
-  // ---- loop state + seed exchange (the owner of the start column publishes it) ----
-  for (int r = 0; r < nl; ++r) {
-    rbd_ctx_t c = R[r];
-    DevState s0{};
-    s0.d = 0;
-    s0.jstar = j0;
-    s0.d_max = cfg->d_max;
-    s0.e_cur = std::numeric_limits<double>::infinity();
-    s0.eps_R = cfg->eps_R;
-    s0.breakdown_tol = tol;
-    s0.done = !(0 < cfg->d_max && s0.e_cur > cfg->eps_R) ? 1 : 0;
-    s0.cfg_reorth = cfg->reorthogonalize ? 1 : 0;
-    s0.wnorm = 1.0;
-    *c->h_state = s0;
-    CU(cudaMemcpyAsync(c->state.p, c->h_state, sizeof(DevState), cudaMemcpyHostToDevice, c->stream));
-    const long long jl = (j0 >= sh[r].col_offset && j0 < sh[r].col_offset + sh[r].n_local)
-                             ? j0 - sh[r].col_offset : -1;
-    k_shard_seed_pack<<<64, 256, 0, c->stream>>>(sh[r].X, ldx, m, jl, sh[r].col_offset,
-                                                 ptr<double>(c->colsq), ptr<double>(c->send));
-    c->launches++;
-    CU(cudaStreamSynchronize(c->stream));   // pinned h_state reused below
-  }
-  TRY(ex.allgather(R, pay_stride));
-  for (int r = 0; r < nl; ++r) {
-    k_shard_seed_select<<<1, 32, 0, R[r]->stream>>>(ptr<DevState>(R[r]->state), ptr<double>(R[r]->recv),
-                                                    pay_stride, ex.world());
-    R[r]->launches++;
-  }
-  // ---- greedy loop: step kernels, payload allgather, winner selection ----
-  std::vector<int> grids(nl);
-  for (int r = 0; r < nl; ++r) grids[r] = persistent_grid(R[r], vec, d_cap);
-  for (long long step = 0; step < cfg->d_max; ++step) {
-    for (int r = 0; r < nl; ++r)
-      TRY(shard_step_launch(R[r], sh[r], m, ldx, d_cap, pay_stride, vec, grids[r]));
-    TRY(ex.allgather(R, pay_stride));
-    for (int r = 0; r < nl; ++r) {
-      k_shard_select<<<1, 32, 0, R[r]->stream>>>(ptr<DevState>(R[r]->state), ptr<double>(R[r]->recv),
-                                                 pay_stride, ex.world(), ptr<double>(R[r]->hist),
-                                                 ptr<long long>(R[r]->sel));
-      R[r]->launches++;
-    }
-    CU(cudaGetLastError());
-    if ((step & 3) == 3 || step + 1 == cfg->d_max) {
-      CU(cudaMemcpyAsync((void*)&R[0]->h_state->done, &ptr<DevState>(R[0]->state)->done, sizeof(int),
-                         cudaMemcpyDeviceToHost, R[0]->stream));
-      CU(cudaStreamSynchronize(R[0]->stream));
-      if (R[0]->h_state->done) break;
-    }
-  }
-  // the last accepted column's second pass
-  for (int r = 0; r < nl; ++r) TRY(shard_step_launch(R[r], sh[r], m, ldx, d_cap, pay_stride, vec, grids[r]));
-  for (int r = 0; r < nl; ++r) CU(cudaStreamSynchronize(R[r]->stream));
-  rbd_ctx_t c0 = R[0];
-  CU(cudaMemcpy(c0->h_state, c0->state.p, sizeof(DevState), cudaMemcpyDeviceToHost));
-  const long long d = c0->h_state->d;
-  if (d == 0)
-    return set_err(RBD_ERR_DEGENERATE_INPUT, "decompose: start column is numerically zero, no basis built");
-  if (h_selected) CU(cudaMemcpy(h_selected, c0->sel.p, sizeof(long long) * d, cudaMemcpyDeviceToHost));
-  if (h_history) CU(cudaMemcpy(h_history, c0->hist.p, sizeof(double) * d, cudaMemcpyDeviceToHost));
-  if (result) {
-    result->d = d;
-    result->breakdown = c0->h_state->breakdown;
-    result->breakdown_tol = tol;
-    result->max_col_norm = std::sqrt(max_colsq);
-    result->launches = 0;
-    for (auto c : R) result->launches += c->launches;
-  }
-  return RBD_OK;
-}
-
-}  // namespace
-
-void rbd_comm_release(rbd_ctx_t ctx) {
-  if (ctx && ctx->comm && nccl().ok) {
-    nccl().CommDestroy((ncclComm_t)ctx->comm);
-    ctx->comm = nullptr;
-  }
-}
-
-extern "C" {
-
-int rbd_comm_unique_id(char out[RBD_UNIQUE_ID_BYTES]) {
-  if (!nccl().ok) return set_err(RBD_ERR_NCCL, "NCCL (libnccl.so.2) could not be loaded");
-  ncclUniqueId id;
-  ncclResult_t r = nccl().GetUniqueId(&id);
-  if (r != ncclSuccess) return set_err(RBD_ERR_NCCL, std::string("ncclGetUniqueId: ") + nccl().GetErrorString(r));
-  static_assert(sizeof(ncclUniqueId) == RBD_UNIQUE_ID_BYTES, "unique id size");
-  std::memcpy(out, &id, RBD_UNIQUE_ID_BYTES);
-  return RBD_OK;
-}
-
-int rbd_ctx_init_comm(rbd_ctx_t ctx, int rank, int world, const char id[RBD_UNIQUE_ID_BYTES]) {
-  if (!ctx || world < 1 || rank < 0 || rank >= world)
-    return set_err(RBD_ERR_INVALID_ARGUMENT, "init_comm: bad rank/world");
-  if (!nccl().ok) return set_err(RBD_ERR_NCCL, "NCCL (libnccl.so.2) could not be loaded");
-  CU(cudaSetDevice(ctx->device));
-  ncclUniqueId uid;
-  std::memcpy(&uid, id, RBD_UNIQUE_ID_BYTES);
-  ncclComm_t comm;
-  ncclResult_t r = nccl().CommInitRank(&comm, world, uid, rank);
-  if (r != ncclSuccess) return set_err(RBD_ERR_NCCL, std::string("ncclCommInitRank: ") + nccl().GetErrorString(r));
-  rbd_comm_release(ctx);
-  ctx->comm = comm;
-  ctx->rank = rank;
-  ctx->world = world;
-  return RBD_OK;
-}
-
-int rbd_decompose_sharded(rbd_ctx_t ctx, const double* dX_local, int64_t m, int64_t n_local,
-                          int64_t ldx, int64_t col_offset, int64_t n_global,
-                          const rbd_config_t* cfg, double* dY, double* dT_local,
-                          int64_t* h_selected, double* h_history, rbd_result_t* result) {
-  if (!ctx || !cfg) return set_err(RBD_ERR_INVALID_ARGUMENT, "decompose: null context/config");
-  if (!ctx->comm) return set_err(RBD_ERR_NCCL, "sharded decompose: call rbd_ctx_init_comm first");
-  if (ldx < m) return set_err(RBD_ERR_DIMENSION_MISMATCH, "decompose: ldx < m");
-  std::vector<rbd_ctx_t> R{ctx};
-  std::vector<Shard> sh{Shard{dX_local, n_local, col_offset, dY, dT_local}};
-  NcclExchange ex(ctx->world);
-  return sharded_decompose(R, ex, sh, m, ldx, n_global, cfg, h_selected, h_history, result);
-}
-
-int rbd_decompose_sharded_virtual(rbd_ctx_t ctx, int nranks, const double* const* dX_shards,
-                                  const int64_t* n_locals, int64_t m, int64_t ldx,
-                                  const rbd_config_t* cfg, double* const* dY_ranks,
-                                  double* const* dT_ranks, int64_t* h_selected, double* h_history,
-                                  rbd_result_t* result) {
-  if (!ctx || !cfg || nranks < 1) return set_err(RBD_ERR_INVALID_ARGUMENT, "virtual sharded: bad arguments");
-  if (ldx < m) return set_err(RBD_ERR_DIMENSION_MISMATCH, "decompose: ldx < m");
-  CU(cudaSetDevice(ctx->device));
-  while ((int)ctx->virt.size() < nranks) {
-    auto* sub = new rbd_ctx_s();
-    sub->device = ctx->device;
-    sub->nsm = ctx->nsm;
-    sub->occ_sweep2 = ctx->occ_sweep2;
-    sub->occ_sweep1 = ctx->occ_sweep1;
-    sub->fused_grid_cap = ctx->fused_grid_cap;
-    sub->stream = ctx->stream;
-    cudaMallocHost(&sub->h_state, sizeof(DevState));
-    cudaMallocHost(&sub->h_rec, sizeof(Rec) * 4);
-    if (ensure(sub->bar, 64) == RBD_OK) cudaMemset(sub->bar.p, 0, 64);
-    ctx->virt.push_back(sub);
-  }
-  std::vector<rbd_ctx_t> R(ctx->virt.begin(), ctx->virt.begin() + nranks);
-  for (auto c : R) c->stream = ctx->stream;
-  std::vector<Shard> sh(nranks);
-  long long off = 0;
-  for (int r = 0; r < nranks; ++r) {
-    sh[r] = Shard{dX_shards[r], n_locals[r], off, dY_ranks[r], dT_ranks[r]};
-    off += n_locals[r];
-  }
-  LocalExchange ex(nranks);
-  const long long l0 = 0;
-  for (auto c : R) c->launches = l0;
-  int rc = sharded_decompose(R, ex, sh, m, ldx, off, cfg, h_selected, h_history, result);
-  for (auto c : R) ctx->launches += c->launches;
-  return rc;
-}
-
 }  // extern "C"
 
 extern "C" {
@@ -2272,262 +1235,6 @@ int rbd_mgs_project_host(rbd_ctx_t ctx, const double* hv, int64_t m, const doubl
   if (ok) *ok = okv;
   if (norm) *norm = nv;
   return fin(RBD_OK);
-}
-
-int rbd_ws_init_host(rbd_ctx_t ctx, const double* hX, int64_t m, int64_t n, int64_t ldx,
-                     int64_t cap, rbd_ws_t* out) {
-  if (!ctx || !out) return set_err(RBD_ERR_INVALID_ARGUMENT, "null argument");
-  if (m < 1 || n < 1) return set_err(RBD_ERR_INVALID_ARGUMENT, "workspace_init: empty matrix");
-  if (ldx < m) return set_err(RBD_ERR_DIMENSION_MISMATCH, "workspace_init: ldx < m");
-  CU(cudaSetDevice(ctx->device));
-  DevBuf xb;
-  TRY(ensure(xb, sizeof(double) * m * n));
-  if (cudaMemcpy2DAsync(xb.p, sizeof(double) * m, hX, sizeof(double) * ldx, sizeof(double) * m, n,
-                        cudaMemcpyHostToDevice, ctx->stream) != cudaSuccess) {
-    release(xb);
-    return set_err(RBD_ERR_CUDA, "workspace_init: H2D failed");
-  }
-  rbd_ws_t ws = nullptr;
-  int rc = rbd_ws_init(ctx, ptr<double>(xb), m, n, m, cap, &ws);
-  if (rc) {
-    release(xb);
-    return rc;
-  }
-  ws->Xown = xb;
-  *out = ws;
-  return RBD_OK;
-}
-
-int rbd_ws_init_diag_host(rbd_ctx_t ctx, const double* hX, int64_t m, int64_t n, int64_t ldx,
-                          int64_t cap, const double* h_diag, int64_t diag_len, rbd_ws_t* out) {
-  if (!ctx || !out) return set_err(RBD_ERR_INVALID_ARGUMENT, "null argument");
-  TRY(check_diagonal(h_diag, diag_len));
-  if (m < 1 || n < 1) return set_err(RBD_ERR_INVALID_ARGUMENT, "workspace_init: empty matrix");
-  if (ldx < m) return set_err(RBD_ERR_DIMENSION_MISMATCH, "workspace_init: ldx < m");
-  if (diag_len != m)
-    return set_err(RBD_ERR_INCOMPATIBLE_WEIGHT, "weight dimension does not match matrix rows");
-  CU(cudaSetDevice(ctx->device));
-  DevBuf xb, db;
-  TRY(ensure(xb, sizeof(double) * m * n));
-  if (ensure(db, sizeof(double) * m) != RBD_OK ||
-      cudaMemcpy2DAsync(xb.p, sizeof(double) * m, hX, sizeof(double) * ldx, sizeof(double) * m, n,
-                        cudaMemcpyHostToDevice, ctx->stream) != cudaSuccess ||
-      cudaMemcpyAsync(db.p, h_diag, sizeof(double) * m, cudaMemcpyHostToDevice, ctx->stream) !=
-          cudaSuccess) {
-    release(xb);
-    release(db);
-    return set_err(RBD_ERR_CUDA, "workspace_init: H2D failed");
-  }
-  rbd_ws_t ws = nullptr;
-  int rc = rbd_ws_init_diag(ctx, ptr<double>(xb), m, n, m, cap, ptr<double>(db), m, &ws);
-  release(db);   // the workspace keeps its own copy of the weight
-  if (rc) {
-    release(xb);
-    return rc;
-  }
-  ws->Xown = xb;
-  *out = ws;
-  return RBD_OK;
-}
-
-int rbd_ws_extend_host(rbd_ws_t ws, const double* hxi) {
-  if (!ws) return set_err(RBD_ERR_INVALID_ARGUMENT, "null workspace");
-  DevBuf b;
-  TRY(ensure(b, sizeof(double) * ws->m));
-  // on the workspace's stream (a pageable-source cudaMemcpy may return before its
-  // DMA lands, and the context stream does not wait for the legacy stream)
-  if (cudaMemcpyAsync(b.p, hxi, sizeof(double) * ws->m, cudaMemcpyHostToDevice,
-                      ws->ctx->stream) != cudaSuccess) {
-    release(b);
-    return set_err(RBD_ERR_CUDA, "workspace_extend: H2D failed");
-  }
-  int rc = rbd_ws_extend(ws, ptr<double>(b));
-  release(b);
-  return rc;
-}
-
-int rbd_reconstruct_batch(rbd_ctx_t ctx, const double* dY, int64_t m, int64_t d, int64_t ldy,
-                          const double* dC, int64_t N, double* dV) {
-  if (!ctx) return set_err(RBD_ERR_INVALID_ARGUMENT, "null context");
-  if (ldy < m || m < 1 || N < 0) return set_err(RBD_ERR_DIMENSION_MISMATCH, "compress: bad sizes");
-  if (N == 0) return RBD_OK;
-  CU(cudaSetDevice(ctx->device));
-  if (d >= 1 && launch_compress_dmma<true>(dY, m, d, ldy, dC, N, d, dV, m, ctx->stream)) {
-    ctx->launches += cdiv(cdiv(N, 64), 65535);
-    CU(cudaGetLastError());
-    return RBD_OK;
-  }
-  const long long gx = std::min<long long>(cdiv(m, 256), 1024);
-  for (long long j0 = 0; j0 < N; j0 += 65535) {
-    const long long nb = std::min<long long>(65535, N - j0);
-    k_reconstruct_batch<<<dim3((unsigned)gx, (unsigned)nb), 256, 0, ctx->stream>>>(
-        dY, m, d, ldy, dC + j0 * d, nb, dV + j0 * m);
-    ctx->launches++;
-  }
-  CU(cudaGetLastError());
-  return RBD_OK;
-}
-
-int rbd_compress_device(rbd_ctx_t ctx, const double* dY, int64_t m, int64_t d, int64_t ldy,
-                        const double* dT, int64_t n, int64_t ldt, double* dV, int64_t ldv) {
-  if (!ctx) return set_err(RBD_ERR_INVALID_ARGUMENT, "null context");
-  if (m < 1 || d < 1 || n < 0 || ldy < m || ldt < n || ldv < m)
-    return set_err(RBD_ERR_DIMENSION_MISMATCH, "compress: bad sizes");
-  if (n == 0) return RBD_OK;
-  CU(cudaSetDevice(ctx->device));
-  if (launch_compress_dmma<false>(dY, m, d, ldy, dT, n, ldt, dV, ldv, ctx->stream)) {
-    ctx->launches += cdiv(cdiv(n, 64), 65535);
-    CU(cudaGetLastError());
-    return RBD_OK;
-  }
-  // unaligned operands: transpose T into column-major coefficients, SIMT path
-  DevBuf c;
-  TRY(ensure(c, sizeof(double) * (size_t)d * (size_t)n));
-  for (int64_t k = 0; k < d; ++k)   // row k of T -> element k of every column
-    CU(cudaMemcpy2DAsync(ptr<double>(c) + k, sizeof(double) * d, dT + k * ldt, sizeof(double),
-                         sizeof(double), n, cudaMemcpyDeviceToDevice, ctx->stream));
-  int rc = RBD_OK;
-  if (ldv == m) {
-    rc = rbd_reconstruct_batch(ctx, dY, m, d, ldy, ptr<double>(c), n, dV);
-  } else {
-    rc = set_err(RBD_ERR_INVALID_ARGUMENT, "compress: unaligned operands need ldv == m");
-  }
-  cudaStreamSynchronize(ctx->stream);
-  release(c);
-  return rc;
-}
-
-int rbd_compress_host(rbd_ctx_t ctx, const double* hY, int64_t m, int64_t d, const double* hC,
-                      int64_t N, double* hV) {
-  if (!ctx) return set_err(RBD_ERR_INVALID_ARGUMENT, "null context");
-  if (m < 1 || d < 1 || N < 1) return set_err(RBD_ERR_DIMENSION_MISMATCH, "compress: bad sizes");
-  CU(cudaSetDevice(ctx->device));
-  DevBuf bY, bC, bV;
-  auto fin = [&](int rc) {
-    release(bY);
-    release(bC);
-    release(bV);
-    return rc;
-  };
-  int rc;
-  if ((rc = ensure(bY, sizeof(double) * m * d)) || (rc = ensure(bC, sizeof(double) * d * N)) ||
-      (rc = ensure(bV, sizeof(double) * m * N)))
-    return fin(rc);
-  if (cudaMemcpyAsync(bY.p, hY, sizeof(double) * m * d, cudaMemcpyHostToDevice, ctx->stream) ||
-      cudaMemcpyAsync(bC.p, hC, sizeof(double) * d * N, cudaMemcpyHostToDevice, ctx->stream))
-    return fin(set_err(RBD_ERR_CUDA, "compress_host: H2D failed"));
-  rc = rbd_reconstruct_batch(ctx, ptr<double>(bY), m, d, m, ptr<double>(bC), N, ptr<double>(bV));
-  if (rc) return fin(rc);
-  if (cudaMemcpyAsync(hV, bV.p, sizeof(double) * m * N, cudaMemcpyDeviceToHost, ctx->stream) ||
-      cudaStreamSynchronize(ctx->stream))
-    return fin(set_err(RBD_ERR_CUDA, "compress_host: D2H failed"));
-  return fin(RBD_OK);
-}
-
-}  // extern "C"
-
-// ===========================================================================
-// fp32 out-of-sample compression on tcgen05 (K6)
-// ===========================================================================
-namespace {
-
-PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
-        q != cudaDriverEntryPointSuccess)
-      return (PFN_cuTensorMapEncodeTiled_v12000) nullptr;
-    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-  }();
-  return fn;
-}
-
-// 2-D fp32 column-major operand (rows = contiguous dim of length `inner`,
-// `outer` columns, leading dimension ld), box 32 x 128, 128-byte swizzle.
-int make_map_f32(CUtensorMap* map, const float* base, long long inner, long long outer, long long ld) {
-  auto enc = tensor_map_encoder();
-  if (!enc) return set_err(RBD_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-  cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
-  cuuint64_t strides[1] = {(cuuint64_t)ld * sizeof(float)};
-  cuuint32_t box[2] = {(cuuint32_t)kTcBK, (cuuint32_t)kTcBM};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides,
-                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return set_err(RBD_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
-  return RBD_OK;
-}
-
-}  // namespace
-
-extern "C" {
-
-int rbd_project_batch_f32(rbd_ctx_t ctx, const float* dY, int64_t m, int64_t d, int64_t ldy,
-                          const float* dXn, int64_t N, int64_t ldx, float* dTn, double* d_err) {
-  if (!ctx) return set_err(RBD_ERR_INVALID_ARGUMENT, "null context");
-  if (m < 1 || d < 1 || N < 0) return set_err(RBD_ERR_DIMENSION_MISMATCH, "project: bad sizes");
-  if (ldy < m || ldx < m) return set_err(RBD_ERR_DIMENSION_MISMATCH, "project: vector length != m");
-  if (N == 0) return RBD_OK;
-  if ((ldy % 4) || (ldx % 4) || !aligned16(dY) || !aligned16(dXn))
-    return set_err(RBD_ERR_INVALID_ARGUMENT,
-                   "project f32: leading dimensions must be multiples of 4 floats and bases 16-byte aligned (TMA)");
-  CU(cudaSetDevice(ctx->device));
-  CUtensorMap mY, mX;
-  TRY(make_map_f32(&mY, dY, m, d, ldy));
-  TRY(make_map_f32(&mX, dXn, m, N, ldx));
-  static bool attr = false;
-  if (!attr) {
-    CU(cudaFuncSetAttribute(k_project_tf32x3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTcSmem));
-    attr = true;
-  }
-  double* xn = nullptr;
-  if (d_err) {
-    TRY(ensure(ctx->scratch1, sizeof(double) * (size_t)std::max<int64_t>(N, 32)));
-    xn = ptr<double>(ctx->scratch1);
-  }
-  // split-K over the k-blocks for the best-filled waves (1 CTA per SM): 2 for C4's 4 x 128 tiles
-  const long long nk = cdiv(m, kTcBK);
-  const long long ctas = cdiv(d, kTcBM) * cdiv(N, kTcBN);
-  int sk = 1;
-  {
-    double best_eff = 0.0;
-    for (int s = 1; s <= 4; ++s) {
-      if (s > 1 && nk / s < 64) break;
-      const long long c = ctas * s, waves = cdiv(c, ctx->nsm);
-      const double eff = (double)c / (double)(waves * ctx->nsm);
-      if (s == 1 || eff > best_eff + 0.02) {
-        sk = s;
-        best_eff = eff;
-      }
-    }
-  }
-  const int kb_per = (int)cdiv(nk, sk);
-  sk = (int)cdiv(nk, kb_per);   // every split gets at least one k-block
-  float* Tws = nullptr;
-  double* xws = nullptr;
-  if (sk > 1) {
-    const size_t tbytes = sizeof(float) * (size_t)(sk - 1) * (size_t)(d * N);
-    TRY(ensure(ctx->pj_ws, tbytes + sizeof(double) * (size_t)(sk - 1) * (size_t)N + 16));
-    Tws = ptr<float>(ctx->pj_ws);
-    xws = reinterpret_cast<double*>(reinterpret_cast<char*>(ctx->pj_ws.p) + ((tbytes + 15) & ~(size_t)15));
-  }
-  dim3 grid((unsigned)cdiv(d, kTcBM), (unsigned)cdiv(N, kTcBN), (unsigned)sk);
-  k_project_tf32x3<<<grid, kTcThreads, kTcSmem, ctx->stream>>>(mY, mX, m, d, N, dTn, xn, kb_per,
-                                                                Tws, xws);
-  ctx->launches++;
-  CU(cudaGetLastError());
-  if (sk > 1) {
-    k_splitk_sum_f32<<<1184, 256, 0, ctx->stream>>>(dTn, Tws, d * N, sk - 1, xn, xws, N);
-    ctx->launches++;
-    CU(cudaGetLastError());
-  }
-  if (d_err) {
-    k_project_err_f32<<<(unsigned)cdiv(N, 8), 256, 0, ctx->stream>>>(xn, dTn, d, N, d_err);
-    ctx->launches++;
-    CU(cudaGetLastError());
-  }
-  return RBD_OK;
 }
 
 }  // extern "C"

@@ -32,7 +32,7 @@ __device__ __forceinline__ bool nn_better(double av, long long aj, double bv, lo
 // C: d x Q coordinates, column-major (ld ldc). Tt: d x n_tr, row-major (T[k*n_tr + j]).
 // out[split * Q + q] = best (distance, column) of query q over the columns of
 // split `blockIdx.y` (cols_per_split, a multiple of kNnTile).
-__global__ void __launch_bounds__(kThreads) k_nearest(const double* __restrict__ C, long long ldc,
+static __global__ void __launch_bounds__(kThreads) k_nearest(const double* __restrict__ C, long long ldc,
                                                       const double* __restrict__ Tt,
                                                       long long n_tr, long long d, long long Q,
                                                       long long cols_per_split,
@@ -120,7 +120,7 @@ __global__ void __launch_bounds__(kThreads) k_nearest(const double* __restrict__
 }
 
 // best[q] / dist[q] = the minimum over the splits (order-independent total order).
-__global__ void k_nearest_reduce(const NnRec* __restrict__ part, long long Q, int nsplit,
+static __global__ void k_nearest_reduce(const NnRec* __restrict__ part, long long Q, int nsplit,
                                  long long* __restrict__ best, double* __restrict__ dist) {
   for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < Q;
        q += (long long)gridDim.x * blockDim.x) {

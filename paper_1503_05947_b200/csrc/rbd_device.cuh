@@ -399,7 +399,7 @@ __device__ __forceinline__ void block_argmax(double& v, long long& j, Rec* sm) {
 // ---------------------------------------------------------------------------
 // K1 finish: col_sq = sum of chunk partials, residual_sq = col_sq, max col_sq.
 // ---------------------------------------------------------------------------
-__global__ void k_init_finish(const double* __restrict__ partial, long long S, long long n,
+static __global__ void k_init_finish(const double* __restrict__ partial, long long S, long long n,
                               double* __restrict__ col_sq, double* __restrict__ resid,
                               DevState* st) {
   __shared__ double sm[kWarps];
@@ -452,7 +452,7 @@ struct FinalizeArgs {
   int mode;
 };
 
-__device__ void finalize_state(const FinalizeArgs& a, double best, long long arg) {
+static __device__ void finalize_state(const FinalizeArgs& a, double best, long long arg) {
   DevState* st = a.st;
   const long long k = st->d;
   const double e_cur = sqrt(best > 0.0 ? best : 0.0);  // workspace.cpp:123
@@ -466,7 +466,7 @@ __device__ void finalize_state(const FinalizeArgs& a, double best, long long arg
 __device__ __forceinline__ void finalize_reduce_tail(const FinalizeArgs& a, long long k, double bv,
                                                      long long bj, Rec* smr, int* is_last_s);
 
-__global__ void __launch_bounds__(kThreads) k_finalize(FinalizeArgs a) {
+static __global__ void __launch_bounds__(kThreads) k_finalize(FinalizeArgs a) {
   if (a.mode != 1 && a.st->done) return;
   __shared__ Rec smr[kWarps];
   __shared__ int is_last;
@@ -558,7 +558,7 @@ struct ExtArgs {
   int pass;             // 1 or 2
 };
 
-__global__ void __launch_bounds__(kThreads) k_ext_gemv_n(ExtArgs a) {
+static __global__ void __launch_bounds__(kThreads) k_ext_gemv_n(ExtArgs a) {
   if (gate_skip(a.st, a.gate)) return;
   const long long k = a.st->d;
   const long long m = a.m;
@@ -624,7 +624,7 @@ __device__ __forceinline__ double sum_parts(const double* p, long long np, doubl
 }
 
 // After pass 1: decide the second pass exactly as decompose.cpp:28 does.
-__global__ void __launch_bounds__(kThreads) k_ext_decide(const double* nrm_part, long long np,
+static __global__ void __launch_bounds__(kThreads) k_ext_decide(const double* nrm_part, long long np,
                                                          DevState* st) {
   if (st->done) return;
   __shared__ double sm[kWarps];
@@ -637,7 +637,7 @@ __global__ void __launch_bounds__(kThreads) k_ext_decide(const double* nrm_part,
 }
 
 // Second-pass coefficients p[l] = sum_s partial[s*pstride + l] (fixed order).
-__global__ void k_coef_combine(const double* __restrict__ partial, long long S, long long pstride,
+static __global__ void k_coef_combine(const double* __restrict__ partial, long long S, long long pstride,
                                double* __restrict__ p, DevState* st, int gate) {
   if (gate_skip(st, gate)) return;
   const long long k = st->d;
@@ -650,7 +650,7 @@ __global__ void k_coef_combine(const double* __restrict__ partial, long long S, 
 }
 
 // Norm + breakdown test (decompose.cpp:29-30); on success record selected.
-__global__ void __launch_bounds__(kThreads) k_ext_finish(const double* nrm_part, long long np,
+static __global__ void __launch_bounds__(kThreads) k_ext_finish(const double* nrm_part, long long np,
                                                          DevState* st, long long* selected) {
   if (st->done) return;
   __shared__ double sm[kWarps];
@@ -669,7 +669,7 @@ __global__ void __launch_bounds__(kThreads) k_ext_finish(const double* nrm_part,
 }
 
 // y = w / norm into the output column (decompose.cpp:31,92).
-__global__ void k_normalize(const double* __restrict__ w, double* __restrict__ ybase,
+static __global__ void k_normalize(const double* __restrict__ w, double* __restrict__ ybase,
                             long long ystride, long long m, DevState* st, int use_d) {
   if (st->done) return;
   const double norm = st->wnorm;
@@ -680,7 +680,7 @@ __global__ void k_normalize(const double* __restrict__ w, double* __restrict__ y
 }
 
 // Entry norm for standalone mgs_project: xnorm2 = ||v||^2 (fixed order).
-__global__ void __launch_bounds__(kThreads) k_norm2_single(const double* v, long long m,
+static __global__ void __launch_bounds__(kThreads) k_norm2_single(const double* v, long long m,
                                                            DevState* st) {
   __shared__ double sm[kWarps];
   double s = 0.0;
@@ -690,7 +690,7 @@ __global__ void __launch_bounds__(kThreads) k_norm2_single(const double* v, long
 }
 
 // Workspace scan (residual_scan identity, workspace.cpp:101-125) into out.
-__global__ void __launch_bounds__(kThreads) k_scan_only(const double* r, long long n, Rec* rec,
+static __global__ void __launch_bounds__(kThreads) k_scan_only(const double* r, long long n, Rec* rec,
                                                         unsigned* counter, Rec* out) {
   __shared__ Rec smr[kWarps];
   __shared__ int is_last;
@@ -729,7 +729,7 @@ __global__ void __launch_bounds__(kThreads) k_scan_only(const double* r, long lo
 }
 
 // Identity error_sq (workspace.cpp:84-99) for one column from the T rows.
-__global__ void k_error_sq(const double* T, long long n, long long d, long long j,
+static __global__ void k_error_sq(const double* T, long long n, long long d, long long j,
                            const double* c, const double* col_sq, double* out) {
   __shared__ double sm[kWarps];
   double cross = 0.0, quad = 0.0;
@@ -784,7 +784,7 @@ struct FusedArgs {
   long long dcap;         // coefficient capacity (= d_max) of the smem arrays
 };
 
-__global__ void __launch_bounds__(kThreads) k_ext_fused(FusedArgs a) {
+static __global__ void __launch_bounds__(kThreads) k_ext_fused(FusedArgs a) {
   DevState* st = a.st;
   const int pending = st->pending;
   const int live = !st->done;
@@ -927,7 +927,7 @@ struct ReduceArgs {
   long long* selected;
 };
 
-__global__ void __launch_bounds__(kThreads) k_ext_reduce(ReduceArgs a) {
+static __global__ void __launch_bounds__(kThreads) k_ext_reduce(ReduceArgs a) {
   DevState* st = a.st;
   __shared__ double sred[kWarps][32];
   __shared__ double smn[kWarps];
@@ -1011,7 +1011,7 @@ struct Finalize2Args {
 };
 
 constexpr int kF2Cols = 32;   // columns per CTA
-__global__ void __launch_bounds__(kThreads) k_finalize_fused(Finalize2Args a) {
+static __global__ void __launch_bounds__(kThreads) k_finalize_fused(Finalize2Args a) {
   DevState* st = a.st;
   if (st->done) return;
   __shared__ double scorr[kWarps][kF2Cols];

@@ -971,7 +971,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
 
 // Sharded mode: winner selection after the payload allgather (every rank runs
 // it on identical data, so every rank takes the same decision).
-__global__ void k_shard_select(DevState* st, const double* recv, long long pay_stride, int nranks,
+static __global__ void k_shard_select(DevState* st, const double* recv, long long pay_stride, int nranks,
                                double* history, long long* selected) {
   if (threadIdx.x != 0 || st->done) return;
   double bv = -1.0;
@@ -1001,7 +1001,7 @@ __global__ void k_shard_select(DevState* st, const double* recv, long long pay_s
 }
 
 // Sharded mode, before step 0: the owner of the start column publishes it.
-__global__ void k_shard_seed_pack(const double* X, long long ldx, long long m, long long jlocal,
+static __global__ void k_shard_seed_pack(const double* X, long long ldx, long long m, long long jlocal,
                                   long long col_offset, const double* col_sq, double* send) {
   const long long i0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i0 == 0) {
@@ -1015,7 +1015,7 @@ __global__ void k_shard_seed_pack(const double* X, long long ldx, long long m, l
     send[kPayHead + i] = X[jlocal * ldx + i];
 }
 
-__global__ void k_shard_seed_select(DevState* st, const double* recv, long long pay_stride,
+static __global__ void k_shard_seed_select(DevState* st, const double* recv, long long pay_stride,
                                     int nranks) {
   if (threadIdx.x != 0) return;
   for (int r = 0; r < nranks; ++r) {

@@ -17,7 +17,7 @@ constexpr int kPjBM = 64;   // rows of T_new (basis index k) per CTA
 constexpr int kPjBN = 64;   // columns of T_new (new vectors) per CTA
 constexpr int kPjBK = 16;   // reduction depth per stage (rows i of Y / X_new)
 
-__global__ void __launch_bounds__(256) k_project_f64(const double* __restrict__ Y, long long m,
+static __global__ void __launch_bounds__(256) k_project_f64(const double* __restrict__ Y, long long m,
                                                      long long d, long long ldy,
                                                      const double* __restrict__ Xn, long long N,
                                                      long long ldx, double* __restrict__ Tn) {
@@ -73,7 +73,7 @@ __global__ void __launch_bounds__(256) k_project_f64(const double* __restrict__ 
 }
 
 // err_j = max(||x_j||^2 - ||t_j||^2, 0), one warp per column (fixed order).
-__global__ void k_project_err(const double* __restrict__ Xn, long long m, long long ldx,
+static __global__ void k_project_err(const double* __restrict__ Xn, long long m, long long ldx,
                               const double* __restrict__ Tn, long long d, long long N,
                               double* __restrict__ err) {
   const long long j = (long long)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
@@ -93,7 +93,7 @@ __global__ void k_project_err(const double* __restrict__ Xn, long long m, long l
   }
 }
 
-__global__ void k_reconstruct(const double* __restrict__ Y, long long m, long long d,
+static __global__ void k_reconstruct(const double* __restrict__ Y, long long m, long long d,
                               long long ldy, const double* __restrict__ c, double* __restrict__ v) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m;
        i += (long long)gridDim.x * blockDim.x) {
@@ -173,7 +173,7 @@ inline int launch_project_f64(const double* Y, long long m, long long d, long lo
 }
 
 // V = Y C (decompose.cpp:119-125): thread per row i, one column j per grid.y.
-__global__ void k_reconstruct_batch(const double* __restrict__ Y, long long m, long long d,
+static __global__ void k_reconstruct_batch(const double* __restrict__ Y, long long m, long long d,
                                     long long ldy, const double* __restrict__ C, long long N,
                                     double* __restrict__ V) {
   const long long j = blockIdx.y;

@@ -206,7 +206,7 @@ __global__ void __launch_bounds__(WARPS_M * WARPS_N * 32, RBD_DM_MINB)
 }
 
 // Split-K combine: Tn += workspace slices (and ||x||^2), splits in order.
-__global__ void k_splitk_sum(double* __restrict__ Tn, const double* __restrict__ Tws,
+static __global__ void k_splitk_sum(double* __restrict__ Tn, const double* __restrict__ Tws,
                              long long dN, int nws, double* __restrict__ xn,
                              const double* __restrict__ xws, long long N) {
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < dN;
@@ -223,7 +223,7 @@ __global__ void k_splitk_sum(double* __restrict__ Tn, const double* __restrict__
 }
 
 // err_j = max(||x_j||^2 - ||t_j||^2, 0) from the fused ||x||^2 (one warp per column).
-__global__ void k_project_err_fused(const double* __restrict__ xnorm2, const double* __restrict__ Tn,
+static __global__ void k_project_err_fused(const double* __restrict__ xnorm2, const double* __restrict__ Tn,
                                     long long d, long long N, double* __restrict__ err) {
   const long long j = (long long)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
   const int lane = threadIdx.x & 31;

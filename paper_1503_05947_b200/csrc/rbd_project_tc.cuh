@@ -125,7 +125,7 @@ __device__ __forceinline__ float tf32_lo(float x) {
 // split-K: blockIdx.z takes k-blocks [z * kb_per, min(nk, (z + 1) * kb_per)) (at
 // least one); split 0 writes Tn / xnorm2, split z > 0 its workspace slices
 // (Tws + (z-1) d N, xws + (z-1) N), added in order by k_splitk_sum_f32.
-__global__ void __launch_bounds__(kTcThreads, 1)
+static __global__ void __launch_bounds__(kTcThreads, 1)
     k_project_tf32x3(const __grid_constant__ CUtensorMap mapY, const __grid_constant__ CUtensorMap mapX,
                      long long m, long long d, long long N, float* __restrict__ Tn,
                      double* __restrict__ xnorm2, int kb_per, float* __restrict__ Tws,
@@ -285,7 +285,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 }
 
 // Split-K combine: Tn += fp32 workspace slices and xn += fp64 slices, in split order.
-__global__ void k_splitk_sum_f32(float* __restrict__ Tn, const float* __restrict__ Tws, long long dN,
+static __global__ void k_splitk_sum_f32(float* __restrict__ Tn, const float* __restrict__ Tws, long long dN,
                                  int nws, double* __restrict__ xn, const double* __restrict__ xws,
                                  long long N) {
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < dN;
@@ -302,7 +302,7 @@ __global__ void k_splitk_sum_f32(float* __restrict__ Tn, const float* __restrict
 }
 
 // err_j = max(||x_j||^2 - ||t_j||^2, 0), fp64 accumulation (the subtraction cancels).
-__global__ void k_project_err_f32(const double* __restrict__ xnorm2, const float* __restrict__ Tn,
+static __global__ void k_project_err_f32(const double* __restrict__ xnorm2, const float* __restrict__ Tn,
                                   long long d, long long N, double* __restrict__ err) {
   const long long j = (long long)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
   const int lane = threadIdx.x & 31;

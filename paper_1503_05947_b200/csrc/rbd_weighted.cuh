@@ -20,7 +20,7 @@ namespace rbdk {
 
 // col_sq_A[j] = max(sum_i x_ij^2 a_i, 0) (workspace.cpp:24-29,37); one CTA per
 // column, fixed per-thread row order and a fixed reduction tree.
-__global__ void __launch_bounds__(kThreads) k_colsq_diag(const double* __restrict__ X, long long ldx,
+static __global__ void __launch_bounds__(kThreads) k_colsq_diag(const double* __restrict__ X, long long ldx,
                                                          long long m, long long n,
                                                          const double* __restrict__ diag,
                                                          double* __restrict__ colsq_a) {
@@ -39,7 +39,7 @@ __global__ void __launch_bounds__(kThreads) k_colsq_diag(const double* __restric
 
 // a_xi = a o xi (weight.cpp:83) for the vector just written to Y[:, st->d];
 // yy_part[b] = this CTA's share of xi' A xi (workspace.cpp:75). Fixed grid.
-__global__ void __launch_bounds__(kThreads) k_diag_vec(const double* __restrict__ Y, long long m,
+static __global__ void __launch_bounds__(kThreads) k_diag_vec(const double* __restrict__ Y, long long m,
                                                        const double* __restrict__ diag,
                                                        double* __restrict__ axi,
                                                        double* __restrict__ yy_part,
@@ -208,7 +208,7 @@ struct FinalizeDiagArgs {
 // CTA = 32 columns; g_j = YAY[d,0:d] . T[0:d,j] is split over the 8 warps
 // (l = warp, warp+8, ...; coalesced T rows) and combined in warp order.
 constexpr int kFdCols = 32;
-__global__ void __launch_bounds__(kThreads) k_finalize_diag(FinalizeDiagArgs a) {
+static __global__ void __launch_bounds__(kThreads) k_finalize_diag(FinalizeDiagArgs a) {
   const FinalizeArgs& f = a.f;
   if (f.st->done) return;
   __shared__ Rec smr[kWarps];
@@ -279,7 +279,7 @@ __global__ void __launch_bounds__(kThreads) k_finalize_diag(FinalizeDiagArgs a) 
 // ---------------------------------------------------------------------------
 
 // out[j] = sum over chunks s of partial[s * n + j] (chunks in order).
-__global__ void k_rowsum(const double* __restrict__ partial, long long S, long long n,
+static __global__ void k_rowsum(const double* __restrict__ partial, long long S, long long n,
                          double* __restrict__ out) {
   for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < n;
        j += (long long)gridDim.x * blockDim.x) {
@@ -291,7 +291,7 @@ __global__ void k_rowsum(const double* __restrict__ partial, long long S, long l
 
 // YAY row d (workspace.cpp:69-75): yay[d][k] = yay[k][d] = row[k] (k < d),
 // yay[d][d] = sum of the xi' A xi partials (in order).
-__global__ void k_yay_row(const double* __restrict__ row, long long d, const double* __restrict__ yy_part,
+static __global__ void k_yay_row(const double* __restrict__ row, long long d, const double* __restrict__ yy_part,
                           int np, double* __restrict__ yay, long long ld) {
   for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < d;
        k += (long long)gridDim.x * blockDim.x) {
@@ -307,7 +307,7 @@ __global__ void k_yay_row(const double* __restrict__ row, long long d, const dou
 
 // error_sq (workspace.cpp:84-99) for one column: cross = c . yax[:, j],
 // quad = c' yay c (yay == nullptr: identity, quad = ||c||^2).
-__global__ void __launch_bounds__(kThreads) k_error_sq_w(const double* __restrict__ yax, long long n,
+static __global__ void __launch_bounds__(kThreads) k_error_sq_w(const double* __restrict__ yax, long long n,
                                                          long long d, long long j,
                                                          const double* __restrict__ c,
                                                          const double* __restrict__ yay, long long ld,
@@ -335,7 +335,7 @@ __global__ void __launch_bounds__(kThreads) k_error_sq_w(const double* __restric
 // residual_scan for a general weight (workspace.cpp:114-122): error_sq of every
 // column with c = T[:, j] (T row-major d x n), argmax with smallest-index
 // ties, E_cur = sqrt(max(best, 0)) (:123); last-CTA reduction into out.
-__global__ void __launch_bounds__(kThreads) k_scan_T(const double* __restrict__ yax,
+static __global__ void __launch_bounds__(kThreads) k_scan_T(const double* __restrict__ yax,
                                                      const double* __restrict__ T, long long n,
                                                      long long d, const double* __restrict__ yay,
                                                      long long ld, const double* __restrict__ col_sq,
