@@ -29,13 +29,14 @@ sys.path.insert(0, ROOT)
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--steps", type=int, default=20)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
     p.add_argument("--workload", default="C1-image-like")
     p.add_argument("--cpu-seconds", type=float, default=15.0)
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-f32", action="store_true", help="skip the fp32 storage-mode line")
     p.add_argument("--d-max", type=int, default=None, help="override d_max (quick runs)")
     p.add_argument("--ref-seconds", type=float, default=6.0,
                    help="reference arm: CPU seconds of greedy steps per bench step")
@@ -72,6 +73,14 @@ class ClockSampler:
         except Exception:
             self.proc = None
 
+    def wait_first(self, timeout: float = 3.0):
+        """Block until nvidia-smi has produced its first sample (its start-up
+        takes longer than a short timed region), so the samples cover it."""
+        t0 = time.perf_counter()
+        while self.proc is not None and not self.lines and time.perf_counter() - t0 < timeout:
+            time.sleep(0.02)
+        self.begin = len(self.lines)   # samples from here on fall in the timed region
+
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
@@ -86,7 +95,8 @@ class ClockSampler:
             self.proc.kill()
         sm, smax, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        lines = self.lines[getattr(self, "begin", 0):] or self.lines
+        for ln in lines:
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 9:
                 continue
@@ -252,6 +262,7 @@ def run_b200(args):
     barrier()
     torch.cuda.synchronize(dev)
     clocks.start()
+    clocks.wait_first()
     launches0 = ctx.launches
     e0.record(stream)
     ds = []
@@ -316,6 +327,37 @@ def run_b200(args):
     roofline["frac_of_nominal"] = {"gbs": 7700.0, "frac": ach / 7700.0,
                                    "note": "nominal HBM3e 7.7 TB/s (HGX), B200_PROFILING.md"}
 
+    # ---- fp32 storage mode (rbd_decompose_device_f32), same workload rounded
+    #      to fp32: half the X bytes per sweep, fp64 arithmetic; reported beside
+    #      the fp64 headline (metric bytes at 4 B/element) ----
+    f32_mode = None
+    if not args.no_f32:
+        Xf = Xd.float()
+        for _ in range(2):
+            gf = rbd.decompose(Xf, d_max=w.d_max, eps_r=eps, ctx=ctx)
+        torch.cuda.synchronize(dev)
+        e0.record(stream)
+        fl, fd = [], []
+        for _ in range(max(1, args.steps)):
+            gf = rbd.decompose(Xf, d_max=w.d_max, eps_r=eps, ctx=ctx)
+            fd.append(gf.d)
+            fl.append(gf.result.loop_ms)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        msf = e0.elapsed_time(e1)
+        fbytes = m * n * 4
+        floop = float(np.mean(fl))
+        f32_mode = {"storage": "f32 X, f64 arithmetic (rbd_decompose_device_f32)",
+                    "value": fbytes * sum(fd) / (msf / 1e3) / 1e9, "unit": "GB/s",
+                    "ms_per_step": msf / len(fd), "loop_ms_mean": floop,
+                    "roofline_frac": fbytes * float(np.mean(fd)) / (floop / 1e3) / 1e9 / peak,
+                    "d_reached": int(np.mean(fd)),
+                    "same_selection_as_f64_run_on_f32_values": None}
+        g64 = rbd.decompose(Xf.double(), d_max=w.d_max, eps_r=eps, ctx=ctx)
+        f32_mode["same_selection_as_f64_run_on_f32_values"] = g64.selected == gf.selected
+        del Xf, g64
+        torch.cuda.empty_cache()
+
     # ---- e2e through the reference-facing host entry (pinned host X) ----
     e2e = None
     if not args.no_e2e:
@@ -373,7 +415,7 @@ def run_b200(args):
                        "describe": w.describe},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk, "loop_ms_mean": float(np.mean(loop_ms)),
-            "d_per_step": ds,
+            "d_per_step": ds, "f32_mode": f32_mode,
         }
         print(json.dumps(line), flush=True)
     ctx.close()
@@ -426,6 +468,7 @@ def run_sharded(args):
     barrier()
     torch.cuda.synchronize(dev)
     clocks.start()
+    clocks.wait_first()
     stream = torch.cuda.ExternalStream(ctx.stream, device=dev)
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)

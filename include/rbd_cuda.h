@@ -123,6 +123,21 @@ int rbd_decompose_host(rbd_ctx_t ctx, const double* hX, int64_t m, int64_t n, in
                        const rbd_config_t* cfg, double* hY, double* hT, int64_t* h_selected,
                        double* h_history, rbd_result_t* result);
 
+/* fp32 storage mode of rbd::decompose (BASELINE north_star's optional fp32
+ * mode; same contract as rbd_decompose_device / _host otherwise): X is held
+ * in fp32 (half the HBM bytes the per-step sweep streams), every product and
+ * sum is fp64 on the exact value of each element, and Y, T, the residuals and
+ * the history are fp64. The result is therefore the fp64 algorithm run on the
+ * fp32-valued matrix (parity: the fp64 oracle on X rounded to fp32, to the
+ * fp64 tolerances). Identity weight, persistent loop (d_max <= 4096);
+ * otherwise RBD_ERR_INVALID_ARGUMENT. */
+int rbd_decompose_device_f32(rbd_ctx_t ctx, const float* dX, int64_t m, int64_t n, int64_t ldx,
+                             const rbd_config_t* cfg, double* dY, double* dT, int64_t* h_selected,
+                             double* h_history, rbd_result_t* result);
+int rbd_decompose_host_f32(rbd_ctx_t ctx, const float* hX, int64_t m, int64_t n, int64_t ldx,
+                           const rbd_config_t* cfg, double* hY, double* hT, int64_t* h_selected,
+                           double* h_history, rbd_result_t* result);
+
 /* rbd::decompose with cfg.weight = WeightSpec::diagonal(diag) (
  * reference decompose.cpp:53-111, weight.cpp:11-21, workspace.cpp:24-29,61-99,
  * 114-122). Y and T are Euclidean as in the reference; the weight steers the

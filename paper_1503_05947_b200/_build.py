@@ -28,6 +28,11 @@ NVCC_FLAGS = [
 ]
 
 
+def _extra_flags():
+    """Experiment knobs (e.g. RBD_NVCC_DEFS="-DRBD_RING=1"); empty by default."""
+    return os.environ.get("RBD_NVCC_DEFS", "").split()
+
+
 def _nvcc() -> str:
     for cand in (shutil.which("nvcc"), "/usr/local/cuda/bin/nvcc"):
         if cand and os.path.exists(cand):
@@ -61,7 +66,7 @@ def build_library(force: bool = False, verbose: bool = False) -> str:
     with tempfile.TemporaryDirectory(prefix="rbd_build_") as tmp:
         def compile_one(src):
             obj = os.path.join(tmp, os.path.basename(src) + ".o")
-            cmd = [_nvcc(), *NVCC_FLAGS, "-Xcompiler", "-fPIC", "-c", "-I", INCLUDE, "-I", CSRC,
+            cmd = [_nvcc(), *NVCC_FLAGS, *_extra_flags(), "-Xcompiler", "-fPIC", "-c", "-I", INCLUDE, "-I", CSRC,
                    src, "-o", obj]
             if verbose:
                 print(" ".join(cmd))

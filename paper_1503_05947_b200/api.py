@@ -36,9 +36,10 @@ def _col_major_np(x) -> np.ndarray:
     return np.asfortranarray(np.asarray(x, dtype=np.float64))
 
 
-def _col_major_torch(x):
-    if x.dtype != torch.float64:
-        x = x.to(torch.float64)
+def _col_major_torch(x, dtype=None):
+    dtype = dtype or torch.float64
+    if x.dtype != dtype:
+        x = x.to(dtype)
     if x.dim() != 2:
         raise InvalidArgument("decompose: X must be a 2-D matrix")
     m = x.shape[0]
@@ -162,11 +163,14 @@ class Model:
 def decompose(x, d_max: int, eps_r: float = 0.0, diag=None, sparse=None, start_column: int = 0,
               reorthogonalize: bool = False, breakdown_tol: float = -1.0,
               start_seed: Optional[int] = None, ctx: Optional[Context] = None,
-              forced_selection=None) -> Model:
+              forced_selection=None, storage: Optional[str] = None) -> Model:
     """rbd.decompose (bindings.cpp:69-78) -> rbd::decompose (decompose.cpp:53-111).
 
     numpy input: end-to-end host entry (rbd_decompose_host).
     torch CUDA input: device-resident entry (rbd_decompose_device).
+    storage: "f64" or "f32" (default: "f32" for float32 input, else "f64").
+    "f32" keeps X in fp32 on the device (rbd_decompose_*_f32: half the bytes
+    per sweep, fp64 arithmetic on the fp32 values; identity weight only).
     forced_selection: parity-test instrumentation; follow this
     column sequence instead of the greedy argmax (persistent loop only).
     """
@@ -175,9 +179,18 @@ def decompose(x, d_max: int, eps_r: float = 0.0, diag=None, sparse=None, start_c
         ctx.force_selection(forced_selection)
         try:
             return decompose(x, d_max, eps_r, diag, sparse, start_column, reorthogonalize,
-                             breakdown_tol, start_seed, ctx)
+                             breakdown_tol, start_seed, ctx, storage=storage)
         finally:
             ctx.force_selection(None)
+    if storage is None:
+        dt = getattr(x, "dtype", None)
+        storage = "f32" if dt in ((torch.float32,) if torch is not None else ()) + (np.float32,) \
+            else "f64"
+    if storage not in ("f32", "f64"):
+        raise InvalidArgument("decompose: storage must be 'f32' or 'f64'")
+    f32 = storage == "f32"
+    if f32 and (diag is not None or sparse is not None):
+        raise InvalidArgument("decompose: fp32 storage mode supports the identity weight only")
     cfg = make_config(d_max, eps_r, start_column, reorthogonalize, breakdown_tol, start_seed,
                       diag, sparse)
     lib = load_library()
@@ -185,7 +198,7 @@ def decompose(x, d_max: int, eps_r: float = 0.0, diag=None, sparse=None, start_c
     if _is_torch_cuda(x):
         dev = x.device.index or 0
         ctx = ctx or default_context(dev)
-        xc, ldx = _col_major_torch(x)
+        xc, ldx = _col_major_torch(x, torch.float32 if f32 else torch.float64)
         m, n = xc.shape
         cap = max(1, min(int(d_max), n)) if n > 0 else 1
         Y = torch.empty((cap, max(m, 1)), dtype=torch.float64, device=x.device).t()
@@ -202,14 +215,14 @@ def decompose(x, d_max: int, eps_r: float = 0.0, diag=None, sparse=None, start_c
                 C.c_void_p(Y.data_ptr()), C.c_void_p(T.data_ptr()), _dp(sel), _dp(hist),
                 C.byref(res)))
         else:
-            check(lib.rbd_decompose_device(ctx.handle, C.c_void_p(xc.data_ptr()), m, n, ldx,
-                                           C.byref(cfg), C.c_void_p(Y.data_ptr()),
-                                           C.c_void_p(T.data_ptr()), _dp(sel), _dp(hist),
-                                           C.byref(res)))
+            fn = lib.rbd_decompose_device_f32 if f32 else lib.rbd_decompose_device
+            check(fn(ctx.handle, C.c_void_p(xc.data_ptr()), m, n, ldx, C.byref(cfg),
+                     C.c_void_p(Y.data_ptr()), C.c_void_p(T.data_ptr()), _dp(sel), _dp(hist),
+                     C.byref(res)))
         d = res.d
         return Model(Y, T, d, sel[:d], hist[:d], res, ctx, 1 if diag is not None else 0, diag)
     ctx = ctx or default_context(0)
-    xa = _col_major_np(x)
+    xa = np.asfortranarray(np.asarray(x, dtype=np.float32)) if f32 else _col_major_np(x)
     if xa.ndim != 2:
         raise InvalidArgument("decompose: X must be a 2-D matrix")
     m, n = xa.shape
@@ -223,8 +236,9 @@ def decompose(x, d_max: int, eps_r: float = 0.0, diag=None, sparse=None, start_c
                                           _dp(dg) if dg.size else None, dg.size, _dp(Y), _dp(T),
                                           _dp(sel), _dp(hist), C.byref(res)))
     else:
-        check(lib.rbd_decompose_host(ctx.handle, _dp(xa), m, n, max(m, 1), C.byref(cfg),
-                                     _dp(Y), _dp(T), _dp(sel), _dp(hist), C.byref(res)))
+        fn = lib.rbd_decompose_host_f32 if f32 else lib.rbd_decompose_host
+        check(fn(ctx.handle, _dp(xa), m, n, max(m, 1), C.byref(cfg), _dp(Y), _dp(T), _dp(sel),
+                 _dp(hist), C.byref(res)))
     d = res.d
     return Model(Y, T, d, sel[:d], hist[:d], res, ctx, 1 if diag is not None else 0, diag)
 

@@ -52,6 +52,20 @@ long long gemv_grid(long long m) { return cdiv(m, kGemvRows); }
 // ---------------------------------------------------------------------------
 // K1: init pass over X (col_sq, residual, flags, max col_sq)
 // ---------------------------------------------------------------------------
+int enqueue_init_f32(rbd_ctx_t ctx, const float* X, long long m, long long n, long long ldx,
+                     double* partial, double* colsq, double* resid, DevState* st) {
+  const int vec4 = (ldx % 4 == 0 && aligned16(X)) ? 1 : 0;
+  const int grid = sweep_grid(ctx, m, n, 2);
+  k_sweep_init_f32<<<grid, kThreads, 0, ctx->stream>>>(X, ldx, m, n, partial, st, vec4);
+  ctx->launches++;
+  CU(cudaGetLastError());
+  const int g = (int)std::max<long long>(1, std::min<long long>(cdiv(n, 256), 1024));
+  k_init_finish<<<g, 256, 0, ctx->stream>>>(partial, cdiv(m, kChunk), n, colsq, resid, st);
+  ctx->launches++;
+  CU(cudaGetLastError());
+  return RBD_OK;
+}
+
 int enqueue_init(rbd_ctx_t ctx, const double* X, long long m, long long n, long long ldx,
                  double* partial, double* colsq, double* resid, DevState* st) {
   const int vec = (ldx % 2 == 0 && aligned16(X)) ? 2 : 1;
@@ -150,6 +164,7 @@ struct LoopBufs {
   long long m, n, ldx, d_max;
   double* Y;
   double* T;
+  const float* Xf = nullptr;   // fp32 storage mode (X == nullptr): persistent loop only
 };
 
 // One greedy step: extension (K4) + fused sweep (K2) + finalize/argmax (K3).
@@ -318,9 +333,10 @@ int fused_grid(rbd_ctx_t ctx, long long m) {
 size_t fused_smem(long long dcap) { return sizeof(double) * 3 * (size_t)std::max<long long>(dcap, 1); }
 // c and p vectors, each zero-padded by one P1 batch (16 loads x kWarps columns);
 // weighted: + p_k and the YAY row for the finaliser
-size_t persist_smem(long long dcap, bool diag) {
+size_t persist_smem(long long dcap, bool diag, bool ring) {
   const size_t d = (size_t)std::max<long long>(dcap, 1);
-  return sizeof(double) * (2 * (d + 16 * kWarps) + (diag ? 2 * (d + 1) : 0));
+  return (ring ? (size_t)kRingBytes : 0) +
+         sizeof(double) * (2 * (d + 16 * kWarps) + (diag ? 2 * (d + 1) : 0));
 }
 
 // Materialise a pending column / clear the pending flag (used after the loop).
@@ -395,10 +411,15 @@ int enqueue_step_fused(rbd_ctx_t ctx, const LoopBufs& L) {
   return RBD_OK;
 }
 
-int persistent_grid(rbd_ctx_t ctx, int vec, long long d_max, bool diag) {
+int persistent_grid(rbd_ctx_t ctx, int vec, long long d_max, bool diag, bool xf32) {
   int occ = 0;
-  const size_t smem = persist_smem(d_max, diag);
-  if (diag)
+  const size_t smem = persist_smem(d_max, diag,
+                                   xf32 ? ring_on<false, false, true>() : (!diag && ring_on<false, false, false>()));
+  if (xf32)
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &occ, vec == 2 ? k_rbd_persistent<2, false, false, true> : k_rbd_persistent<1, false, false, true>,
+        kThreads, smem);
+  else if (diag)
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(
         &occ, vec == 2 ? k_rbd_persistent<2, false, true> : k_rbd_persistent<1, false, true>,
         kThreads, smem);
@@ -414,9 +435,13 @@ int persistent_grid(rbd_ctx_t ctx, int vec, long long d_max, bool diag) {
 // the weighted loop (row f1; the caller has sized the wd_* buffers and zeroed
 // cross/quad).
 int launch_persistent(rbd_ctx_t ctx, const LoopBufs& L, const double* diag = nullptr) {
-  const int vec = (L.ldx % 2 == 0 && L.m % 2 == 0 && aligned16(L.X) && aligned16(L.Y) &&
-                   aligned16(ctx->w.p) && (!diag || aligned16(ctx->wd_axi.p))) ? 2 : 1;
-  const int grid = persistent_grid(ctx, vec, L.d_max, diag != nullptr);
+  const bool xf32 = L.Xf != nullptr;
+  // VEC: 16-byte pairs of Y / w rows in P1 (and of X in the fp64 sweep; the
+  // fp32 sweep picks float4 loads separately, so its VEC never depends on ldx)
+  const bool xpairs = xf32 || (L.ldx % 2 == 0 && aligned16(L.X));
+  const int vec = (xpairs && L.m % 2 == 0 && aligned16(L.Y) && aligned16(ctx->w.p) &&
+                   (!diag || aligned16(ctx->wd_axi.p))) ? 2 : 1;
+  const int grid = persistent_grid(ctx, vec, L.d_max, diag != nullptr, xf32);
   if (grid < 1) return set_err(RBD_ERR_CUDA, "persistent kernel: zero occupancy");
   const long long S = cdiv(L.m, kChunk);
   const long long ngx = cdiv(L.n, kCols);
@@ -435,6 +460,8 @@ int launch_persistent(rbd_ctx_t ctx, const LoopBufs& L, const double* diag = nul
   TRY(ensure(ctx->rec, sizeof(Rec) * (size_t)std::max(grid, ctx->nsm * 8)));
   PersistArgs a{};
   a.X = L.X;
+  a.Xf = L.Xf;
+  a.xvec4 = (xf32 && L.ldx % 4 == 0 && aligned16(L.Xf)) ? 1 : 0;
   a.ldx = L.ldx;
   a.m = L.m;
   a.n = L.n;
@@ -493,8 +520,12 @@ int launch_persistent(rbd_ctx_t ctx, const LoopBufs& L, const double* diag = nul
     a.trace_step = atoll(ts);
   }
   void* args[] = {&a};
-  const size_t smem = persist_smem(L.d_max, diag != nullptr);
-  void* fn = diag ? (vec == 2 ? (void*)k_rbd_persistent<2, false, true>
+  const size_t smem = persist_smem(L.d_max, diag != nullptr,
+                                   xf32 ? ring_on<false, false, true>()
+                                        : (!diag && ring_on<false, false, false>()));
+  void* fn = xf32 ? (vec == 2 ? (void*)k_rbd_persistent<2, false, false, true>
+                              : (void*)k_rbd_persistent<1, false, false, true>)
+             : diag ? (vec == 2 ? (void*)k_rbd_persistent<2, false, true>
                               : (void*)k_rbd_persistent<1, false, true>)
                   : (vec == 2 ? (void*)k_rbd_persistent<2, false> : (void*)k_rbd_persistent<1, false>);
   cudaError_t e = cudaLaunchCooperativeKernel(fn, grid, kThreads, args, smem, ctx->stream);
@@ -710,18 +741,23 @@ int rbd_ctx_create(int device, rbd_ctx_t* out) {
   cudaFuncSetAttribute(k_ext_fused, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)fused_smem(kFMaxCoef));
   ctx->fused_grid_cap = 2 * ctx->nsm;
-  cudaFuncSetAttribute(k_rbd_persistent<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)fused_smem(kFMaxCoef));
-  cudaFuncSetAttribute(k_rbd_persistent<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)fused_smem(kFMaxCoef));
-  cudaFuncSetAttribute(k_rbd_persistent<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)fused_smem(kFMaxCoef));
-  cudaFuncSetAttribute(k_rbd_persistent<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)fused_smem(kFMaxCoef));
+  {
+    const int sm_id = (int)persist_smem(kFMaxCoef, false, ring_on<false, false, false>());
+    const int sm_sh = (int)persist_smem(kFMaxCoef, false, ring_on<true, false, false>());
+    const int sm_f32 = (int)persist_smem(kFMaxCoef, false, ring_on<false, false, true>());
+    cudaFuncSetAttribute(k_rbd_persistent<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_id);
+    cudaFuncSetAttribute(k_rbd_persistent<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_id);
+    cudaFuncSetAttribute(k_rbd_persistent<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_sh);
+    cudaFuncSetAttribute(k_rbd_persistent<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_sh);
+    cudaFuncSetAttribute(k_rbd_persistent<2, false, false, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, sm_f32);
+    cudaFuncSetAttribute(k_rbd_persistent<1, false, false, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, sm_f32);
+  }
   cudaFuncSetAttribute(k_rbd_persistent<2, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)persist_smem(kFMaxCoef, true));
+                       (int)persist_smem(kFMaxCoef, true, false));
   cudaFuncSetAttribute(k_rbd_persistent<1, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)persist_smem(kFMaxCoef, true));
+                       (int)persist_smem(kFMaxCoef, true, false));
   if (const char* pth = getenv("RBD_PATH")) ctx->path = (std::string(pth) == "graph") ? 1 : 0;
   if (ensure(ctx->bar, 64) == RBD_OK) cudaMemset(ctx->bar.p, 0, 64);
   *out = ctx;
@@ -791,11 +827,19 @@ namespace {
 // already validated as a WeightSpec::diagonal).
 int decompose_device_impl(rbd_ctx_t ctx, const double* dX, int64_t m, int64_t n, int64_t ldx,
                           const rbd_config_t* cfg, const double* diag, double* dY, double* dT,
-                          int64_t* h_selected, double* h_history, rbd_result_t* result) {
+                          int64_t* h_selected, double* h_history, rbd_result_t* result,
+                          const float* dXf = nullptr) {
   if (!ctx || !cfg) return set_err(RBD_ERR_INVALID_ARGUMENT, "decompose: null context/config");
   if (m < 1 || n < 1) return set_err(RBD_ERR_INVALID_ARGUMENT, "decompose: matrix must be non-empty");
   if (ldx < m) return set_err(RBD_ERR_DIMENSION_MISMATCH, "decompose: ldx < m");
   CU(cudaSetDevice(ctx->device));
+  if (dXf) {   // fp32 storage mode runs on the persistent identity loop only
+    if (cfg->weight_kind != RBD_WEIGHT_IDENTITY)
+      return set_err(RBD_ERR_INVALID_ARGUMENT, "decompose: fp32 storage mode supports the identity weight only");
+    if (!(ctx->path == 0 && use_fused(cfg->d_max)))
+      return set_err(RBD_ERR_INVALID_ARGUMENT,
+                     "decompose: fp32 storage mode runs on the persistent loop (d_max <= 4096)");
+  }
   const long long d_cap = std::max<long long>(1, std::min<long long>(cfg->d_max, n));
   TRY(ensure_loop_buffers(ctx, m, n, d_cap));
   DevState* st = ptr<DevState>(ctx->state);
@@ -816,8 +860,12 @@ int decompose_device_impl(rbd_ctx_t ctx, const double* dX, int64_t m, int64_t n,
   // ---- K1 ----
   CU(cudaMemsetAsync(st, 0, sizeof(DevState), ctx->stream));
   CU(cudaEventRecord(ev0, ctx->stream));
-  TRY(enqueue_init(ctx, dX, m, n, ldx, ptr<double>(ctx->partial), ptr<double>(ctx->colsq),
-                   ptr<double>(ctx->resid), st));
+  if (dXf)
+    TRY(enqueue_init_f32(ctx, dXf, m, n, ldx, ptr<double>(ctx->partial), ptr<double>(ctx->colsq),
+                         ptr<double>(ctx->resid), st));
+  else
+    TRY(enqueue_init(ctx, dX, m, n, ldx, ptr<double>(ctx->partial), ptr<double>(ctx->colsq),
+                     ptr<double>(ctx->resid), st));
   if (diag) {   // workspace_init, diagonal kind (workspace.cpp:24-29)
     TRY(ensure(ctx->wd_colsq, sizeof(double) * n));
     const int g = (int)std::max<long long>(1, std::min<long long>(n, (long long)ctx->nsm * 8));
@@ -870,7 +918,7 @@ int decompose_device_impl(rbd_ctx_t ctx, const double* dX, int64_t m, int64_t n,
   *ctx->h_state = hs;
   CU(cudaMemcpyAsync(st, ctx->h_state, sizeof(DevState), cudaMemcpyHostToDevice, ctx->stream));
 
-  LoopBufs L{dX, m, n, ldx, cfg->d_max, dY, dT};
+  LoopBufs L{dX, m, n, ldx, cfg->d_max, dY, dT, dXf};
   if (diag) {
     const long long S = cdiv(m, kChunk);
     TRY(ensure(ctx->wd_axi, sizeof(double) * m));
@@ -1008,6 +1056,14 @@ int rbd_decompose_device(rbd_ctx_t ctx, const double* dX, int64_t m, int64_t n, 
                                result);
 }
 
+int rbd_decompose_device_f32(rbd_ctx_t ctx, const float* dX, int64_t m, int64_t n, int64_t ldx,
+                             const rbd_config_t* cfg, double* dY, double* dT, int64_t* h_selected,
+                             double* h_history, rbd_result_t* result) {
+  if (!dX) return set_err(RBD_ERR_INVALID_ARGUMENT, "decompose: null X");
+  return decompose_device_impl(ctx, nullptr, m, n, ldx, cfg, nullptr, dY, dT, h_selected, h_history,
+                               result, dX);
+}
+
 int rbd_decompose_diag_device(rbd_ctx_t ctx, const double* dX, int64_t m, int64_t n, int64_t ldx,
                               const rbd_config_t* cfg, const double* d_diag, int64_t diag_len,
                               double* dY, double* dT, int64_t* h_selected, double* h_history,
@@ -1037,21 +1093,23 @@ namespace {
 int decompose_host_impl(rbd_ctx_t ctx, const double* hX, int64_t m, int64_t n, int64_t ldx,
                         const rbd_config_t* cfg, const double* h_diag, int64_t diag_len,
                         double* hY, double* hT, int64_t* h_selected, double* h_history,
-                        rbd_result_t* result) {
+                        rbd_result_t* result, const float* hXf = nullptr) {
   if (!ctx || !cfg) return set_err(RBD_ERR_INVALID_ARGUMENT, "decompose: null context/config");
   if (m < 1 || n < 1) return set_err(RBD_ERR_INVALID_ARGUMENT, "decompose: matrix must be non-empty");
   if (ldx < m) return set_err(RBD_ERR_DIMENSION_MISMATCH, "decompose: ldx < m");
   CU(cudaSetDevice(ctx->device));
   const long long d_cap = std::max<long long>(1, std::min<long long>(cfg->d_max, n));
-  const long long ldd = (m % 2 == 0) ? m : m + 1;  // keep columns 16-byte aligned on device
-  TRY(ensure(ctx->hX, sizeof(double) * ldd * n));
+  // keep device columns 16-byte aligned (2 doubles / 4 floats)
+  const size_t es = hXf ? sizeof(float) : sizeof(double);
+  const long long ldd = hXf ? (m + 3) / 4 * 4 : (m % 2 == 0 ? m : m + 1);
+  TRY(ensure(ctx->hX, es * ldd * n));
   TRY(ensure(ctx->hY, sizeof(double) * m * d_cap));
   TRY(ensure(ctx->hT, sizeof(double) * d_cap * n));
   double* dX = ptr<double>(ctx->hX);
   double* dY = ptr<double>(ctx->hY);
   double* dT = ptr<double>(ctx->hT);
-  cudaError_t e = cudaMemcpy2DAsync(dX, sizeof(double) * ldd, hX, sizeof(double) * ldx,
-                                    sizeof(double) * m, n, cudaMemcpyHostToDevice, ctx->stream);
+  cudaError_t e = cudaMemcpy2DAsync(dX, es * ldd, hXf ? (const void*)hXf : (const void*)hX, es * ldx,
+                                    es * m, n, cudaMemcpyHostToDevice, ctx->stream);
   if (e != cudaSuccess) return set_err(RBD_ERR_CUDA, std::string("H2D X: ") + cudaGetErrorString(e));
   rbd_result_t r{};
   int rc;
@@ -1079,7 +1137,9 @@ int decompose_host_impl(rbd_ctx_t ctx, const double* hX, int64_t m, int64_t n, i
         cudaGetLastError();
       }
     }
-    rc = rbd_decompose_device(ctx, dX, m, n, ldd, cfg, dY, dT, h_selected, h_history, &r);
+    rc = hXf ? decompose_device_impl(ctx, nullptr, m, n, ldd, cfg, nullptr, dY, dT, h_selected,
+                                     h_history, &r, reinterpret_cast<const float*>(dX))
+             : rbd_decompose_device(ctx, dX, m, n, ldd, cfg, dY, dT, h_selected, h_history, &r);
     t_streamed = ctx->tstream_dst != nullptr;
     ctx->ystream_dst = nullptr;
     ctx->tstream_dst = nullptr;
@@ -1111,6 +1171,14 @@ int rbd_decompose_host(rbd_ctx_t ctx, const double* hX, int64_t m, int64_t n, in
                        double* h_history, rbd_result_t* result) {
   return decompose_host_impl(ctx, hX, m, n, ldx, cfg, nullptr, 0, hY, hT, h_selected, h_history,
                              result);
+}
+
+int rbd_decompose_host_f32(rbd_ctx_t ctx, const float* hX, int64_t m, int64_t n, int64_t ldx,
+                           const rbd_config_t* cfg, double* hY, double* hT, int64_t* h_selected,
+                           double* h_history, rbd_result_t* result) {
+  if (!hX) return set_err(RBD_ERR_INVALID_ARGUMENT, "decompose: null X");
+  return decompose_host_impl(ctx, nullptr, m, n, ldx, cfg, nullptr, 0, hY, hT, h_selected,
+                             h_history, result, hX);
 }
 
 int rbd_decompose_diag_host(rbd_ctx_t ctx, const double* hX, int64_t m, int64_t n, int64_t ldx,

@@ -352,6 +352,171 @@ __global__ void __launch_bounds__(kThreads, 2) k_sweep(SweepArgs a) {
 }
 
 // ---------------------------------------------------------------------------
+// fp32 storage mode of X (rbd_decompose_*_f32): the matrix is held in fp32
+// (half the HBM bytes per step), every product and sum is fp64 on the exact
+// fp64 value of each element, so the arithmetic is the fp64 path's on the
+// fp32-valued matrix. Same tiles (kChunk rows x kCols columns) and partial
+// layout as sweep_tiles; a thread owns rows e..e+3, e = 4*(tid + u*kThreads),
+// read as one float4 per column when the group is in range and the column
+// start is 16-byte aligned (vec4), else as four predicated scalars — the fma
+// order is the same either way, so the bits are too.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float4 ld_stream4f(const float* p) {
+  return __ldcs(reinterpret_cast<const float4*>(p));
+}
+__device__ __forceinline__ bool is_nonfinite_f(float x) {
+  return (__float_as_uint(x) & 0x7f800000u) == 0x7f800000u;
+}
+
+// KC = columns per tile: 4 (K1) or 8 (the greedy loop: 128 KB per tile, the
+// fp64 tile's bytes, loaded as two batches of 16 float4 per thread — row
+// groups 0-1 then 2-3 — so per-tile costs are amortised as in fp64). A
+// column's sum does not depend on KC.
+template <int MODE, bool VCOH = false, int KC = kCols>
+__device__ __forceinline__ void sweep_tiles_f32(const float* __restrict__ A, long long lda,
+                                                long long m, long long ncols,
+                                                const double* __restrict__ v,
+                                                double* __restrict__ partial, long long pstride,
+                                                long long tile_begin, long long tile_stride,
+                                                double (*red)[KC], unsigned& nonfinite,
+                                                unsigned& nonzero, bool vec4) {
+  constexpr int U = kChunk / (4 * kThreads);   // row groups of 4 per thread per column
+  constexpr int UB = 16 / KC;                  // row groups per load batch (16 float4 in flight)
+  static_assert(U % UB == 0, "batches");
+  const long long S = (m + kChunk - 1) / kChunk;
+  const long long G = (ncols + KC - 1) / KC;
+  const long long ntiles = S * G;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  for (long long tile = tile_begin; tile < ntiles; tile += tile_stride) {
+    const long long s = tile / G;
+    const long long g = tile - s * G;
+    const long long row0 = s * kChunk;
+    const long long col0 = g * KC;
+    const long long rows = (m - row0 < kChunk) ? m - row0 : kChunk;
+    double acc[KC];
+#pragma unroll
+    for (int c = 0; c < KC; ++c) acc[c] = 0.0;
+    const float* Ac[KC];
+#pragma unroll
+    for (int c = 0; c < KC; ++c) {
+      const long long cc = (col0 + c < ncols) ? col0 + c : col0;  // clamp (result unused)
+      Ac[c] = A + cc * lda + row0;
+    }
+    const double* vr = (MODE == MODE_DOT) ? v + row0 : nullptr;
+    auto accum = [&](int c, float4 x, double2 y0, double2 y1) {
+      if constexpr (MODE == MODE_DOT) {
+        acc[c] = fma((double)x.x, y0.x, acc[c]);
+        acc[c] = fma((double)x.y, y0.y, acc[c]);
+        acc[c] = fma((double)x.z, y1.x, acc[c]);
+        acc[c] = fma((double)x.w, y1.y, acc[c]);
+      } else {
+        acc[c] = fma((double)x.x, (double)x.x, acc[c]);
+        acc[c] = fma((double)x.y, (double)x.y, acc[c]);
+        acc[c] = fma((double)x.z, (double)x.z, acc[c]);
+        acc[c] = fma((double)x.w, (double)x.w, acc[c]);
+        nonfinite |= is_nonfinite_f(x.x) | is_nonfinite_f(x.y) | is_nonfinite_f(x.z) |
+                     is_nonfinite_f(x.w);
+        nonzero |= (x.x != 0.f) | (x.y != 0.f) | (x.z != 0.f) | (x.w != 0.f);
+      }
+    };
+    auto ldv = [&](const double* p) {
+      return VCOH ? __ldcg(reinterpret_cast<const double2*>(p)) : ld_keep2(p);
+    };
+    if (vec4 && rows == kChunk) {
+      // whole tile in range: batches of UB row groups x KC columns in flight
+#pragma unroll
+      for (int ub = 0; ub < U; ub += UB) {
+        float4 xv[UB][KC];
+        double2 y0[UB], y1[UB];
+#pragma unroll
+        for (int u = 0; u < UB; ++u) {
+          const int e = (tid + (ub + u) * kThreads) * 4;
+          if constexpr (MODE == MODE_DOT) {
+            y0[u] = ldv(vr + e);
+            y1[u] = ldv(vr + e + 2);
+          } else {
+            y0[u] = y1[u] = make_double2(0.0, 0.0);
+          }
+#pragma unroll
+          for (int c = 0; c < KC; ++c) xv[u][c] = ld_stream4f(Ac[c] + e);
+        }
+#pragma unroll
+        for (int u = 0; u < UB; ++u)
+#pragma unroll
+          for (int c = 0; c < KC; ++c) accum(c, xv[u][c], y0[u], y1[u]);
+      }
+    } else {
+#pragma unroll 1
+      for (int u = 0; u < U; ++u) {
+        const long long e = (long long)(tid + u * kThreads) * 4;
+        if (e >= rows) break;   // rows past e contribute +0 (a no-op on every sum)
+        double2 y0 = make_double2(0.0, 0.0), y1 = make_double2(0.0, 0.0);
+        float4 x[KC];
+        if (vec4 && e + 4 <= rows) {
+          if constexpr (MODE == MODE_DOT) {
+            y0 = ldv(vr + e);
+            y1 = ldv(vr + e + 2);
+          }
+#pragma unroll
+          for (int c = 0; c < KC; ++c) x[c] = ld_stream4f(Ac[c] + e);
+        } else {
+          if constexpr (MODE == MODE_DOT) {
+            y0.x = __ldcg(vr + e);
+            y0.y = (e + 1 < rows) ? __ldcg(vr + e + 1) : 0.0;
+            y1.x = (e + 2 < rows) ? __ldcg(vr + e + 2) : 0.0;
+            y1.y = (e + 3 < rows) ? __ldcg(vr + e + 3) : 0.0;
+          }
+#pragma unroll
+          for (int c = 0; c < KC; ++c) {
+            x[c].x = __ldcg(Ac[c] + e);
+            x[c].y = (e + 1 < rows) ? __ldcg(Ac[c] + e + 1) : 0.f;
+            x[c].z = (e + 2 < rows) ? __ldcg(Ac[c] + e + 2) : 0.f;
+            x[c].w = (e + 3 < rows) ? __ldcg(Ac[c] + e + 3) : 0.f;
+          }
+        }
+#pragma unroll
+        for (int c = 0; c < KC; ++c) accum(c, x[c], y0, y1);
+      }
+    }
+    // CTA reduction in a fixed order: xor-butterfly in the warp, then warps 0..7.
+#pragma unroll
+    for (int c = 0; c < KC; ++c) {
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], off);
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int c = 0; c < KC; ++c) red[warp][c] = acc[c];
+    }
+    __syncthreads();
+    if (tid < KC && col0 + tid < ncols) {
+      double sum = red[0][tid];
+#pragma unroll
+      for (int w = 1; w < kWarps; ++w) sum += red[w][tid];
+      partial[s * pstride + col0 + tid] = sum;
+    }
+    __syncthreads();
+  }
+}
+
+// K1 over an fp32 matrix (col_sq in fp64, finite / nonzero flags).
+static __global__ void __launch_bounds__(kThreads, 2)
+    k_sweep_init_f32(const float* __restrict__ A, long long lda, long long m, long long n,
+                     double* __restrict__ partial, DevState* st, int vec4) {
+  __shared__ double red[kWarps][kCols];
+  unsigned nonfinite = 0, nonzero = 0;
+  sweep_tiles_f32<MODE_INIT>(A, lda, m, n, nullptr, partial, n, blockIdx.x, gridDim.x, red,
+                             nonfinite, nonzero, vec4 != 0);
+  const int any_nf = __syncthreads_or(nonfinite);
+  const int any_nz = __syncthreads_or(nonzero);
+  if (threadIdx.x == 0) {
+    if (any_nf) atomicOr(&st->flags_nonfinite, 1u);
+    if (any_nz) atomicOr(&st->flags_nonzero, 1u);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Block-level helpers
 // ---------------------------------------------------------------------------
 template <int NT>

@@ -14,6 +14,8 @@ dmax = int(sys.argv[2]) if len(sys.argv) > 2 else None
 w = configs.WORKLOADS[name]
 X = configs.c1_matrix(n=w.n, seed=w.seed, device="cuda")
 eps = configs.eps_for(w, float(X.norm(dim=0).max()))
+if len(sys.argv) > 3 and sys.argv[3] == "f32":   # fp32 storage mode
+    X = X.float()
 ctx = rbd.Context(0)
 for it in range(2):
     t = time.perf_counter()
