@@ -336,7 +336,8 @@ size_t fused_smem(long long dcap) { return sizeof(double) * 3 * (size_t)std::max
 size_t persist_smem(long long dcap, bool diag, bool ring) {
   const size_t d = (size_t)std::max<long long>(dcap, 1);
   return (ring ? (size_t)kRingBytes : 0) +
-         sizeof(double) * (2 * (d + 16 * kWarps) + (diag ? 2 * (d + 1) : 0));
+         sizeof(double) * (2 * (d + 16 * kWarps) + (diag ? 2 * (d + 1) + 2 : 0)) +
+         (diag ? (size_t)kSvBytes : 0);   // DIAG: X-tile vector slots (rbd_weighted.cuh)
 }
 
 // Materialise a pending column / clear the pending flag (used after the loop).

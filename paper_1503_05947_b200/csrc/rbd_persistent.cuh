@@ -383,6 +383,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
   double* ps = cs + a.d_max + kPBatch;     // p_{k-1} (pending column), zero-padded
   double* pd = cs + 2 * (a.d_max + kPBatch);    // DIAG: p_k (finaliser copy)
   double* yd = pd + a.d_max + 1;                // DIAG: YAY[k, 0:k+1]
+  // DIAG, VEC 2: per-thread cp.async slots of the X tiles' two vectors
+  double2* svec = reinterpret_cast<double2*>(cs + ((2 * (a.d_max + 16 * kWarps) + 2 * (a.d_max + 1) + 1) & ~1LL));
   __shared__ double red[kWarps][kCols];
   // P1 block: two warp-halves of 32*VEC rows each (warps 0-3 / 4-7); within a
   // half the 4 warps split the columns (l = warp%4 mod 4), so every row's sum
@@ -1158,7 +1160,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
         // end of the queue
         const long long tx = t - gy;
         const long long g = tx / S, s = tx - g * S;
-        if constexpr (DIAG)
+        if constexpr (DIAG && VEC == 2)
+          sweep_tile_dot2_sv(a.X, a.ldx, m, n, a.w, a.aw, a.partial, a.partial2, n, s * ngx + g,
+                             red2, svec);
+        else if constexpr (DIAG)
           sweep_tile_dot2<VEC, LOAD_STREAM, true, 2>(a.X, a.ldx, m, n, a.w, a.aw, a.partial,
                                                      a.partial2, n, s * ngx + g, red2);
         else if constexpr (XF32)   // g: an 8-column tile = finalisation groups 2g, 2g+1

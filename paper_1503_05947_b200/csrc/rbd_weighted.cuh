@@ -172,6 +172,109 @@ __device__ __forceinline__ void sweep_tile_dot2(const double* __restrict__ A, lo
   __syncthreads();
 }
 
+// sweep_tile_dot2 for the persistent weighted loop's X tiles (VEC 2): the two
+// vectors travel by per-thread cp.async into this thread's own shared-memory
+// slots (no CTA barrier needed), so registers hold only X while the loads are
+// in flight and a batch keeps UB x kCols 16-byte X loads outstanding (UB 4:
+// the identity sweep's depth). Same row layout, fma order and reduction as
+// sweep_tile_dot2, hence the same bits. sv: [UB][2][kThreads] double2.
+constexpr int kSvUB = 4;
+constexpr int kSvBytes = kSvUB * 2 * kThreads * 16;   // 32 KiB per CTA
+template <int UB = kSvUB>
+__device__ __forceinline__ void sweep_tile_dot2_sv(const double* __restrict__ A, long long lda,
+                                                   long long m, long long ncols,
+                                                   const double* __restrict__ v,
+                                                   const double* __restrict__ v2,
+                                                   double* __restrict__ partial,
+                                                   double* __restrict__ partial2, long long pstride,
+                                                   long long tile, double (*red)[2 * kCols],
+                                                   double2* __restrict__ sv) {
+  constexpr int VEC = 2;
+  const long long G = (ncols + kCols - 1) / kCols;
+  const long long s = tile / G;
+  const long long g = tile - s * G;
+  const long long row0 = s * kChunk;
+  const long long col0 = g * kCols;
+  const long long rows = (m - row0 < kChunk) ? m - row0 : kChunk;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int U = kChunk / (VEC * kThreads);
+  static_assert(U % UB == 0, "batch must divide the chunk");
+  double acc[kCols], acc2[kCols];
+  const double* Ac[kCols];
+#pragma unroll
+  for (int c = 0; c < kCols; ++c) {
+    acc[c] = acc2[c] = 0.0;
+    const long long cc = (col0 + c < ncols) ? col0 + c : col0;   // clamp (result unused)
+    Ac[c] = A + cc * lda + row0;
+  }
+  const double* vr = v + row0;
+  const double* wr = v2 + row0;
+#pragma unroll 1
+  for (int ub = 0; ub < U; ub += UB) {
+    if ((long long)ub * VEC * kThreads >= rows) break;
+    double2 xv[UB][kCols];
+#pragma unroll
+    for (int u = 0; u < UB; ++u) {
+      const long long e = (long long)(tid + (ub + u) * kThreads) * VEC;
+      double2* s0 = sv + (2 * u) * kThreads + tid;
+      double2* s1 = sv + (2 * u + 1) * kThreads + tid;
+      if (e + VEC <= rows) {
+        const unsigned a0 = (unsigned)__cvta_generic_to_shared(s0);
+        const unsigned a1 = (unsigned)__cvta_generic_to_shared(s1);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(a0), "l"(vr + e) : "memory");
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(a1), "l"(wr + e) : "memory");
+#pragma unroll
+        for (int c = 0; c < kCols; ++c) xv[u][c] = ld_stream2(Ac[c] + e);
+      } else {
+        const bool in0 = e < rows, in1 = e + 1 < rows;
+        *s0 = make_double2(in0 ? __ldcg(vr + e) : 0.0, in1 ? __ldcg(vr + e + 1) : 0.0);
+        *s1 = make_double2(in0 ? __ldcg(wr + e) : 0.0, in1 ? __ldcg(wr + e + 1) : 0.0);
+#pragma unroll
+        for (int c = 0; c < kCols; ++c)
+          xv[u][c] = make_double2(in0 ? __ldcs(Ac[c] + e) : 0.0, in1 ? __ldcs(Ac[c] + e + 1) : 0.0);
+      }
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+#pragma unroll
+    for (int u = 0; u < UB; ++u) {
+      const double2 y2 = sv[(2 * u) * kThreads + tid];
+      const double2 z2 = sv[(2 * u + 1) * kThreads + tid];
+#pragma unroll
+      for (int c = 0; c < kCols; ++c) {
+        acc[c] = fma(xv[u][c].x, y2.x, acc[c]);
+        acc2[c] = fma(xv[u][c].x, z2.x, acc2[c]);
+        acc[c] = fma(xv[u][c].y, y2.y, acc[c]);
+        acc2[c] = fma(xv[u][c].y, z2.y, acc2[c]);
+      }
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < kCols; ++c)
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], off);
+      acc2[c] += __shfl_xor_sync(0xffffffffu, acc2[c], off);
+    }
+  if (lane == 0) {
+#pragma unroll
+    for (int c = 0; c < kCols; ++c) {
+      red[warp][c] = acc[c];
+      red[warp][kCols + c] = acc2[c];
+    }
+  }
+  __syncthreads();
+  if (tid < 2 * kCols) {
+    const int c = tid % kCols;
+    if (col0 + c < ncols) {
+      double sum = red[0][tid];
+#pragma unroll
+      for (int w = 1; w < kWarps; ++w) sum += red[w][tid];
+      (tid < kCols ? partial : partial2)[s * pstride + col0 + c] = sum;
+    }
+  }
+  __syncthreads();
+}
+
 // One X pass for both new rows: T row partials (xi . x_j, decompose.cpp:93) and
 // YAX row partials ((A xi) . x_j, workspace.cpp:66).
 template <int VEC>

@@ -37,7 +37,43 @@ __global__ void __launch_bounds__(kT, 2) k_stream(const XT* __restrict__ X, long
 #pragma unroll
       for (int e = 0; e < XV; ++e) acc[c] = fma((double)xs[c][e], vr[e], acc[c]);
   };
-  if (MODE == 0) {
+  if (MODE == 3) {   // fp32-style 8-column tiles, two batches of (Q/2 row groups x 8 columns)
+    const long long G8 = n / 8, total8 = S * G8;
+    double acc8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    while (true) {
+      if (tid == 0) sh_t = (long long)atomicAdd(ctr, 1ull);
+      __syncthreads();
+      const long long t = sh_t;
+      __syncthreads();
+      if (t >= total8) break;
+      const long long s = t / G8, g = t % G8;
+#pragma unroll
+      for (int b = 0; b < 2; ++b) {
+        uint4 xr[Q / 2][8];
+        double2 wv[Q / 2][XV / 2];
+#pragma unroll
+        for (int q = 0; q < Q / 2; ++q) {
+          const long long row = s * kChunk + (b * Q / 2 + q) * SR + tid * XV;
+#pragma unroll
+          for (int h = 0; h < XV / 2; ++h) wv[q][h] = __ldcg(reinterpret_cast<const double2*>(v + row) + h);
+#pragma unroll
+          for (int c = 0; c < 8; ++c)
+            xr[q][c] = __ldcs(reinterpret_cast<const uint4*>(X + (g * 8 + c) * m + row));
+        }
+#pragma unroll
+        for (int q = 0; q < Q / 2; ++q)
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const XT* xs = reinterpret_cast<const XT*>(&xr[q][c]);
+            const double* ws = reinterpret_cast<const double*>(&wv[q][0]);
+#pragma unroll
+            for (int e = 0; e < XV; ++e) acc8[c] = fma((double)xs[e], ws[e], acc8[c]);
+          }
+      }
+      __syncthreads();
+    }
+    acc[0] = acc8[0] + acc8[1] + acc8[2] + acc8[3] + acc8[4] + acc8[5] + acc8[6] + acc8[7];
+  } else if (MODE == 0) {
     while (true) {
       if (tid == 0) sh_t = (long long)atomicAdd(ctr, 1ull);
       __syncthreads();
@@ -188,6 +224,8 @@ int main(int argc, char** argv) {
   cudaMemset(Xd, 0, sizeof(double) * m * n);
   cudaMemset(Xf, 0, sizeof(float) * m * n);
   cudaMemset(v, 0, sizeof(double) * m);
+  if (sel < 0 || sel == 10) run<3, 1, double>("regs 8col 2 batches", Xd, m, n, v, out, ctr, sms);
+  if (sel < 0 || sel == 11) run<3, 1, float>("regs 8col 2 batches", Xf, m, n, v, out, ctr, sms);
   if (sel < 0 || sel == 0) run<0, 1, double>("regs", Xd, m, n, v, out, ctr, sms);
   if (sel < 0 || sel == 1) run<1, 4, double>("tma ring 4", Xd, m, n, v, out, ctr, sms);
   if (sel < 0 || sel == 2) run<1, 6, double>("tma ring 6", Xd, m, n, v, out, ctr, sms);
