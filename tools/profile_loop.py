@@ -14,11 +14,19 @@ dmax = int(sys.argv[2]) if len(sys.argv) > 2 else None
 w = configs.WORKLOADS[name]
 X = configs.c1_matrix(n=w.n, seed=w.seed, device="cuda")
 eps = configs.eps_for(w, float(X.norm(dim=0).max()))
-if len(sys.argv) > 3 and sys.argv[3] == "f32":   # fp32 storage mode
+mode = sys.argv[3] if len(sys.argv) > 3 else "f64"
+diag = None
+if mode == "f32":     # fp32 storage mode
     X = X.float()
+elif mode == "diag":  # row f1: bench_diag.py's pixel-importance weight
+    import numpy as np
+    h, wd = configs.FRAME
+    yy, xx = np.meshgrid(np.linspace(-1, 1, h), np.linspace(-1, 1, wd), indexing="ij")
+    mask = 0.5 + 2.0 * np.exp(-(xx ** 2 + yy ** 2) / 0.3)
+    diag = torch.from_numpy(mask.reshape(-1, order="F")[:X.shape[0]].astype(np.float64)).cuda()
 ctx = rbd.Context(0)
 for it in range(2):
     t = time.perf_counter()
-    g = rbd.decompose(X, d_max=dmax or w.d_max, eps_r=eps, ctx=ctx)
+    g = rbd.decompose(X, d_max=dmax or w.d_max, eps_r=eps, ctx=ctx, diag=diag)
     print(f"run {it}: d={g.d} loop_ms={g.result.loop_ms:.2f} init_ms={g.result.init_ms:.2f} "
           f"launches={g.result.launches} wall={time.perf_counter() - t:.3f}s", flush=True)
