@@ -150,3 +150,38 @@ def test_c1_f32_prefix_parity_and_full_properties(cuda):
     assert g64.selected == g.selected
     assert orthonormality_defect(g.Y.cpu().numpy()) < 1e-10
     assert float((g64.Y - g.Y).abs().max()) < 1e-9
+
+
+@pytest.mark.parametrize("kw", [dict(start_seed=12345), dict(start_column=7), dict(reorthogonalize=True),
+                                dict(breakdown_tol=1e-3)])
+def test_f32_config_fields_match_oracle(cuda, kw):
+    """RbdConfig fields (start spec, reorthogonalize, breakdown_tol) in the fp32
+    storage mode: same bits as the fp64 oracle on the fp32 values (to 1e-10)."""
+    X32 = f32(configs.c0_matrix(m=3000, n=200, rank=24, seed=9))
+    g, r = run_both(X32, 24, 0.0, **kw)
+    rerun = lambda sel: rbd.decompose(X32, d_max=24, forced_selection=sel, **kw)  # noqa: E731
+    assert compare(g, r, X32, rerun=rerun) == r.d
+
+
+def test_f32_certified_stop(cuda):
+    """Stop at eps_R: every column's fp64 residual against the fp32 values is
+    within eps (+ roundoff), as test_decompose.cpp:88-111 for fp64."""
+    X32 = f32(configs.c0_matrix(m=2048, n=300, rank=20, seed=4))
+    X = X32.astype(np.float64)
+    eps = 5e-2   # just above the noise floor: stops after ~60 of 200 steps
+    g = rbd.decompose(X32, d_max=200, eps_r=eps)
+    assert g.d < 200 and g.residual_history[-1] <= eps
+    R = X - g.Y @ g.T
+    assert np.sqrt((R * R).sum(0)).max() <= eps + 1e-10 * np.sqrt((X * X).sum(0)).max()
+
+
+def test_f32_host_entry_pinned_outputs_equal_device_entry(cuda):
+    """Page-locked Y/T stream out of the fp32 loop (host entry) with the same
+    bits as the device entry."""
+    import torch
+    m, n, d = 20000, 600, 120
+    X32 = f32(oracle.random_matrix(m, n, 17))
+    a = rbd.decompose(X32, d_max=d)    # pinned outputs (>= 1 Mi elements)
+    b = rbd.decompose(torch.as_tensor(np.ascontiguousarray(X32.T), device=cuda).t(), d_max=d)
+    assert a.selected == b.selected
+    assert np.array_equal(a.Y, b.Y.cpu().numpy()) and np.array_equal(a.T, b.T.cpu().numpy())
