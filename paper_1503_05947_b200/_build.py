@@ -29,7 +29,7 @@ NVCC_FLAGS = [
 
 
 def _extra_flags():
-    """Experiment knobs (e.g. RBD_NVCC_DEFS="-DRBD_RING=1"); empty by default."""
+    """Experiment knobs (e.g. RBD_NVCC_DEFS="-DRBD_P1_LOADS=20"); empty by default."""
     return os.environ.get("RBD_NVCC_DEFS", "").split()
 
 

@@ -333,10 +333,9 @@ int fused_grid(rbd_ctx_t ctx, long long m) {
 size_t fused_smem(long long dcap) { return sizeof(double) * 3 * (size_t)std::max<long long>(dcap, 1); }
 // c and p vectors, each zero-padded by one P1 batch (16 loads x kWarps columns);
 // weighted: + p_k and the YAY row for the finaliser
-size_t persist_smem(long long dcap, bool diag, bool ring) {
+size_t persist_smem(long long dcap, bool diag) {
   const size_t d = (size_t)std::max<long long>(dcap, 1);
-  return (ring ? (size_t)kRingBytes : 0) +
-         sizeof(double) * (2 * (d + 16 * kWarps) + (diag ? 2 * (d + 1) + 2 : 0)) +
+  return sizeof(double) * (2 * (d + 16 * kWarps) + (diag ? 2 * (d + 1) + 2 : 0)) +
          (diag ? (size_t)kSvBytes : 0);   // DIAG: X-tile vector slots (rbd_weighted.cuh)
 }
 
@@ -414,8 +413,7 @@ int enqueue_step_fused(rbd_ctx_t ctx, const LoopBufs& L) {
 
 int persistent_grid(rbd_ctx_t ctx, int vec, long long d_max, bool diag, bool xf32) {
   int occ = 0;
-  const size_t smem = persist_smem(d_max, diag,
-                                   xf32 ? ring_on<false, false, true>() : (!diag && ring_on<false, false, false>()));
+  const size_t smem = persist_smem(d_max, diag);
   if (xf32)
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(
         &occ, vec == 2 ? k_rbd_persistent<2, false, false, true> : k_rbd_persistent<1, false, false, true>,
@@ -521,9 +519,7 @@ int launch_persistent(rbd_ctx_t ctx, const LoopBufs& L, const double* diag = nul
     a.trace_step = atoll(ts);
   }
   void* args[] = {&a};
-  const size_t smem = persist_smem(L.d_max, diag != nullptr,
-                                   xf32 ? ring_on<false, false, true>()
-                                        : (!diag && ring_on<false, false, false>()));
+  const size_t smem = persist_smem(L.d_max, diag != nullptr);
   void* fn = xf32 ? (vec == 2 ? (void*)k_rbd_persistent<2, false, false, true>
                               : (void*)k_rbd_persistent<1, false, false, true>)
              : diag ? (vec == 2 ? (void*)k_rbd_persistent<2, false, true>
@@ -743,9 +739,9 @@ int rbd_ctx_create(int device, rbd_ctx_t* out) {
                        (int)fused_smem(kFMaxCoef));
   ctx->fused_grid_cap = 2 * ctx->nsm;
   {
-    const int sm_id = (int)persist_smem(kFMaxCoef, false, ring_on<false, false, false>());
-    const int sm_sh = (int)persist_smem(kFMaxCoef, false, ring_on<true, false, false>());
-    const int sm_f32 = (int)persist_smem(kFMaxCoef, false, ring_on<false, false, true>());
+    const int sm_id = (int)persist_smem(kFMaxCoef, false);
+    const int sm_sh = sm_id;
+    const int sm_f32 = sm_id;
     cudaFuncSetAttribute(k_rbd_persistent<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_id);
     cudaFuncSetAttribute(k_rbd_persistent<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_id);
     cudaFuncSetAttribute(k_rbd_persistent<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm_sh);
@@ -756,9 +752,9 @@ int rbd_ctx_create(int device, rbd_ctx_t* out) {
                          cudaFuncAttributeMaxDynamicSharedMemorySize, sm_f32);
   }
   cudaFuncSetAttribute(k_rbd_persistent<2, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)persist_smem(kFMaxCoef, true, false));
+                       (int)persist_smem(kFMaxCoef, true));
   cudaFuncSetAttribute(k_rbd_persistent<1, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)persist_smem(kFMaxCoef, true, false));
+                       (int)persist_smem(kFMaxCoef, true));
   if (const char* pth = getenv("RBD_PATH")) ctx->path = (std::string(pth) == "graph") ? 1 : 0;
   if (ensure(ctx->bar, 64) == RBD_OK) cudaMemset(ctx->bar.p, 0, 64);
   *out = ctx;

@@ -215,69 +215,6 @@ constexpr int kP3Groups = 4;   // column groups finalised together in P3
 constexpr int kPLoads = RBD_P1_LOADS;   // P1: Y loads in flight per lane per batch
 constexpr int kTraceWords = 256;  // per CTA: [0] count, then (tag<<40 | time) words
 
-// ---- X-tile staging ring (TMA bulk copies into shared memory) ----
-// A tile (kChunk rows x kCols columns) is streamed as stages of kRingStageCol
-// bytes per column (1024 rows fp32 / 512 rows fp64); the CTA keeps up to
-// kRingStages stages in flight, fed across tile boundaries from the claim
-// queue, so HBM requests stay outstanding while the CTA reduces, finalises
-// and claims. A thread reads the same rows of a stage as the register sweep
-// gives it (e = q*SR + VEC*tid), so the per-column sums are bit-identical to
-// sweep_tiles / sweep_tiles_f32.
-// Measured SLOWER than the register sweep on B200 (C1 loop: fp64 46.9 ->
-// 60.3 ms, fp32 37.4 -> 47.5 ms; tools/microbench/stream_ring.cu: a TMA
-// bulk ring streams 5.9-6.5 TB/s and a cp.async ring 5.3-6.0 TB/s where
-// plain 16-byte register loads reach 7.0 TB/s), so it is off by default and
-// kept as an experiment (RBD_RING=1 enables it for the fp64 loop; the fp32
-// measurement above was taken with 4-column fp32 tiles).
-#ifndef RBD_RING
-#define RBD_RING 0
-#endif
-constexpr int kRingStages = 4;
-constexpr int kRingStageCol = 4096;
-constexpr int kRingBytes = kRingStages * kCols * kRingStageCol;   // 64 KiB
-constexpr int kRingTiles = 4;                                      // tile FIFO depth
-template <bool SHARD, bool DIAG, bool XF32>
-__host__ __device__ constexpr bool ring_on() {
-  return !DIAG && !XF32 && RBD_RING != 0;   // (fp32 tiles are 8 columns wide)
-}
-
-__device__ __forceinline__ unsigned ring_smem_u32(const void* p) {
-  return (unsigned)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void ring_bar_init(unsigned long long* bar) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(ring_smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void ring_expect_tx(unsigned long long* bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(ring_smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void ring_bulk_load(void* dst, const void* src, unsigned bytes,
-                                               unsigned long long* bar, unsigned long long pol) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], "
-      "%2, [%3], %4;" ::"r"(ring_smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(ring_smem_u32(bar)), "l"(pol)
-      : "memory");
-}
-__device__ __forceinline__ void ring_wait(unsigned long long* bar, unsigned parity) {
-  unsigned ok = 0;
-  unsigned long long t0 = 0;
-  unsigned spins = 0;
-  while (true) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(ok)
-        : "r"(ring_smem_u32(bar)), "r"(parity)
-        : "memory");
-    if (ok) return;
-    if (spins == 0) t0 = globaltimer();
-    if ((++spins & 0xfffu) == 0 && globaltimer() - t0 > 30000000000ull) __trap();
-  }
-}
-
 // Payload of a rank in sharded mode (doubles): [0] best residual, [1] global
 // column index (bits), [2] col_sq of that column, [3] pad, [4, 4+m) the
 // column x_j, [4+m, 4+m+k+1) the column T[0:k+1, j].
@@ -368,18 +305,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
   static_assert(!(SHARD && DIAG), "the weighted loop is single-GPU");
   static_assert(!XF32 || (!SHARD && !DIAG), "fp32 storage: single-GPU identity loop");
   extern __shared__ __align__(128) double dsm[];
-  constexpr bool RING = ring_on<SHARD, DIAG, XF32>();
-  constexpr int kXE = XF32 ? 4 : 8;                    // bytes per X element
-  constexpr int kXV = 16 / kXE;                        // X elements per 16-byte load
-  constexpr int kSR = kRingStageCol / kXE;             // rows per ring stage
-  constexpr int kQ = kChunk / kSR;                     // ring stages per full tile
-  static_assert(kSR == kXV * kThreads, "a stage is one 16-byte load per thread and column");
-  unsigned char* ring = reinterpret_cast<unsigned char*>(dsm);
-  __shared__ __align__(8) unsigned long long ring_bar[kRingStages];
-  __shared__ long long ring_tf[kRingTiles];
   constexpr int kPBatch = kPLoads * kWarps / 2;   // columns per P1 batch of a half
   static_assert(kPBatch <= 16 * kWarps, "P1 batch padding (persist_smem) too small");
-  double* cs = dsm + (RING ? kRingBytes / 8 : 0);   // c = T[0:k, j*], zero-padded to a batch multiple
+  double* cs = dsm;                        // c = T[0:k, j*], zero-padded to a batch multiple
   double* ps = cs + a.d_max + kPBatch;     // p_{k-1} (pending column), zero-padded
   double* pd = cs + 2 * (a.d_max + kPBatch);    // DIAG: p_k (finaliser copy)
   double* yd = pd + a.d_max + 1;                // DIAG: YAY[k, 0:k+1]
@@ -415,21 +343,6 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
   // in sharded mode CTA 0 rezeroes it after the step's last barrier), and
   // advances by exactly total + G per step
   unsigned long long tile_base = 0;
-  // ring (RING builds): consumed stages and popped tiles are uniform across the
-  // CTA; issued stages and pushed tiles are the producer's (tid 0). Running
-  // totals over the whole launch: slot = count % kRingStages, mbarrier phase
-  // parity = (count / kRingStages) & 1.
-  unsigned long long rc_cons = 0, rc_iss = 0, tf_pop = 0, tf_push = 0;
-  unsigned long long xpol = 0;
-  const bool ring_ok = RING && (XF32 ? a.xvec4 != 0 : VEC == 2);
-  if constexpr (RING) {
-    if (tid == 0) {
-      for (int i = 0; i < kRingStages; ++i) ring_bar_init(&ring_bar[i]);
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-      asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(xpol));
-    }
-    __syncthreads();
-  }
 
   // ---- loop state: identical in every CTA (and, sharded, on every rank) ----
   long long k = st->d;
@@ -927,232 +840,6 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
         }
         mark(6);
         trace(k, 5);
-      } else if (RING && ring_ok) {
-        // ---- ring mode: t and every later claim of this step are X tiles ----
-        // tid 0 produces (claims, arms the stage barriers, issues the bulk
-        // copies); every thread consumes tiles in claim order from the FIFO.
-        long long p_tile = t, p_next = next;
-        int p_q = 0, p_qf = 0;
-        bool p_done = false;
-        auto qf_of = [&](long long tile) -> int {   // full ring stages of a tile
-          const long long sc = (tile - gy) % S;
-          const long long rw = (m - sc * kChunk < kChunk) ? m - sc * kChunk : kChunk;
-          return (int)(rw / kSR);
-        };
-        auto produce = [&]() {   // tid 0
-          // (a slot is refilled only after the CTA barrier that follows every
-          // thread's reads of it; no proxy fence: it would wait for the copies
-          // in flight)
-          while (rc_iss - rc_cons < (unsigned long long)kRingStages) {
-            if (p_q < p_qf) {
-              const unsigned slot = (unsigned)(rc_iss % kRingStages);
-              const long long tx = p_tile - gy;
-              const long long g = tx / S, sc = tx - g * S;
-              const long long r0 = sc * kChunk + (long long)p_q * kSR;
-              unsigned char* dst = ring + (size_t)slot * (kCols * kRingStageCol);
-              ring_expect_tx(&ring_bar[slot], kCols * kRingStageCol);
-#pragma unroll
-              for (int c = 0; c < kCols; ++c) {
-                long long col = g * kCols + c;
-                if (col >= n) col = g * kCols;   // clamp (result unused)
-                const void* src = XF32 ? (const void*)(a.Xf + col * a.ldx + r0)
-                                       : (const void*)(a.X + col * a.ldx + r0);
-                ring_bulk_load(dst + c * kRingStageCol, src, kRingStageCol, &ring_bar[slot], xpol);
-              }
-              ++rc_iss;
-              ++p_q;
-              continue;
-            }
-            if (p_done || tf_push - tf_pop >= (unsigned long long)kRingTiles) return;
-            const long long nt = p_next;
-            if (nt >= total) {
-              p_done = true;
-              ring_tf[tf_push % kRingTiles] = -1;
-              ++tf_push;
-              return;
-            }
-            p_next = (long long)(atomicAdd(&ctl->tile_ctr, 1ull) - tile_base);
-            p_tile = nt;
-            p_q = 0;
-            p_qf = qf_of(nt);
-            ring_tf[tf_push % kRingTiles] = nt;
-            ++tf_push;
-          }
-        };
-        if (tid == 0) {
-          p_qf = qf_of(t);
-          ring_tf[tf_push % kRingTiles] = t;
-          ++tf_push;
-        }
-        while (true) {
-          if (tid == 0) produce();
-          __syncthreads();
-          const long long tt = ring_tf[tf_pop % kRingTiles];
-          ++tf_pop;
-          if (tt < 0) break;
-          if (tid == 0) wait_inputs(tt, gy, total);
-          __syncthreads();
-          trace(k, 4 | ((unsigned long long)tt << 8));
-          const long long tx = tt - gy;
-          const long long g = tx / S, sc = tx - g * S;
-          const long long row0 = sc * kChunk, col0 = g * kCols;
-          const long long rows = (m - row0 < kChunk) ? m - row0 : kChunk;
-          const int qf = (int)(rows / kSR);
-          const double* vr = a.w + row0;
-          double acc[kCols];
-#pragma unroll
-          for (int c = 0; c < kCols; ++c) acc[c] = 0.0;
-          // the tile's w1 rows of the ring stages, one L2 round trip per tile
-          double2 wv[kQ][kXV / 2];
-#pragma unroll
-          for (int q = 0; q < kQ; ++q)
-#pragma unroll
-            for (int h = 0; h < kXV / 2; ++h)
-              wv[q][h] = (q < qf) ? __ldcg(reinterpret_cast<const double2*>(vr + q * kSR + kXV * tid + 2 * h))
-                                  : make_double2(0.0, 0.0);
-#pragma unroll
-          for (int q = 0; q < kQ; ++q) {
-            if (q < qf) {
-              const unsigned slot = (unsigned)(rc_cons % kRingStages);
-              ring_wait(&ring_bar[slot], (unsigned)((rc_cons / kRingStages) & 1ull));
-              const unsigned char* sp = ring + (size_t)slot * (kCols * kRingStageCol) + 16 * tid;
-              if constexpr (XF32) {
-                float4 xr[kCols];
-#pragma unroll
-                for (int c = 0; c < kCols; ++c)
-                  xr[c] = *reinterpret_cast<const float4*>(sp + c * kRingStageCol);
-                ++rc_cons;
-                __syncthreads();   // slot free
-                if (tid == 0) produce();
-#pragma unroll
-                for (int c = 0; c < kCols; ++c) {
-                  acc[c] = fma((double)xr[c].x, wv[q][0].x, acc[c]);
-                  acc[c] = fma((double)xr[c].y, wv[q][0].y, acc[c]);
-                  acc[c] = fma((double)xr[c].z, wv[q][kXV / 2 - 1].x, acc[c]);
-                  acc[c] = fma((double)xr[c].w, wv[q][kXV / 2 - 1].y, acc[c]);
-                }
-              } else {
-                double2 xr[kCols];
-#pragma unroll
-                for (int c = 0; c < kCols; ++c)
-                  xr[c] = *reinterpret_cast<const double2*>(sp + c * kRingStageCol);
-                ++rc_cons;
-                __syncthreads();   // slot free
-                if (tid == 0) produce();
-#pragma unroll
-                for (int c = 0; c < kCols; ++c) {
-                  acc[c] = fma(xr[c].x, wv[q][0].x, acc[c]);
-                  acc[c] = fma(xr[c].y, wv[q][0].y, acc[c]);
-                }
-              }
-            }
-          }
-          // rows past the full stages (the partial last chunk): the register
-          // sweep's own per-thread order, loads straight from global memory
-          if (qf < kQ) {
-            if constexpr (XF32) {
-#pragma unroll 1
-              for (int u = qf; u < kQ; ++u) {   // sweep_tiles_f32's fallback branch
-                const long long e = (long long)(tid + u * kThreads) * 4;
-                if (e >= rows) break;
-                double2 y0 = make_double2(0.0, 0.0), y1 = make_double2(0.0, 0.0);
-                float4 x[kCols];
-                if (e + 4 <= rows) {
-                  y0 = __ldcg(reinterpret_cast<const double2*>(vr + e));
-                  y1 = __ldcg(reinterpret_cast<const double2*>(vr + e + 2));
-#pragma unroll
-                  for (int c = 0; c < kCols; ++c) {
-                    long long col = col0 + c;
-                    if (col >= n) col = col0;
-                    x[c] = ld_stream4f(a.Xf + col * a.ldx + row0 + e);
-                  }
-                } else {
-                  y0.x = __ldcg(vr + e);
-                  y0.y = (e + 1 < rows) ? __ldcg(vr + e + 1) : 0.0;
-                  y1.x = (e + 2 < rows) ? __ldcg(vr + e + 2) : 0.0;
-                  y1.y = (e + 3 < rows) ? __ldcg(vr + e + 3) : 0.0;
-#pragma unroll
-                  for (int c = 0; c < kCols; ++c) {
-                    long long col = col0 + c;
-                    if (col >= n) col = col0;
-                    const float* xc = a.Xf + col * a.ldx + row0;
-                    x[c].x = __ldcg(xc + e);
-                    x[c].y = (e + 1 < rows) ? __ldcg(xc + e + 1) : 0.f;
-                    x[c].z = (e + 2 < rows) ? __ldcg(xc + e + 2) : 0.f;
-                    x[c].w = (e + 3 < rows) ? __ldcg(xc + e + 3) : 0.f;
-                  }
-                }
-#pragma unroll
-                for (int c = 0; c < kCols; ++c) {
-                  acc[c] = fma((double)x[c].x, y0.x, acc[c]);
-                  acc[c] = fma((double)x[c].y, y0.y, acc[c]);
-                  acc[c] = fma((double)x[c].z, y1.x, acc[c]);
-                  acc[c] = fma((double)x[c].w, y1.y, acc[c]);
-                }
-              }
-            } else {
-              // sweep_tiles<2>: batches of 4 groups; a batch wholly past the
-              // rows is skipped, groups of the straddling batch past the rows
-              // add +0 (fma(0, 0, acc)), exactly as the register sweep does
-              constexpr int UB = 4;
-#pragma unroll 1
-              for (int u = qf; u < kQ; ++u) {
-                if ((long long)(u / UB) * UB * kSR >= rows) break;
-                const long long e = (long long)(tid + u * kThreads) * 2;
-                if ((long long)(u + 1) * kSR <= rows) {
-                  const double2 y2 = __ldcg(reinterpret_cast<const double2*>(vr + e));
-#pragma unroll
-                  for (int c = 0; c < kCols; ++c) {
-                    long long col = col0 + c;
-                    if (col >= n) col = col0;
-                    const double2 x2 = ld_stream2(a.X + col * a.ldx + row0 + e);
-                    acc[c] = fma(x2.x, y2.x, acc[c]);
-                    acc[c] = fma(x2.y, y2.y, acc[c]);
-                  }
-                } else {
-                  const double y0 = (e < rows) ? __ldcg(vr + e) : 0.0;
-                  const double y1 = (e + 1 < rows) ? __ldcg(vr + e + 1) : 0.0;
-#pragma unroll
-                  for (int c = 0; c < kCols; ++c) {
-                    long long col = col0 + c;
-                    if (col >= n) col = col0;
-                    const double* xc = a.X + col * a.ldx + row0;
-                    const double x0 = (e < rows) ? __ldcg(xc + e) : 0.0;
-                    const double x1 = (e + 1 < rows) ? __ldcg(xc + e + 1) : 0.0;
-                    acc[c] = fma(x0, y0, acc[c]);
-                    acc[c] = fma(x1, y1, acc[c]);
-                  }
-                }
-              }
-            }
-          }
-          // CTA reduction, as sweep_tiles: xor-butterfly, then warps 0..7 in order
-#pragma unroll
-          for (int c = 0; c < kCols; ++c) {
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], off);
-          }
-          if (lane == 0) {
-#pragma unroll
-            for (int c = 0; c < kCols; ++c) red[warp][c] = acc[c];
-          }
-          __syncthreads();
-          if (tid < kCols && col0 + tid < n) {
-            double sum = red[0][tid];
-#pragma unroll
-            for (int w = 1; w < kWarps; ++w) sum += red[w][tid];
-            a.partial[sc * n + col0 + tid] = sum;
-          }
-          __syncthreads();
-          mark(7);
-          if (npend > 0) finalize_pass(false);
-          if (sc == S - 1) {
-            if (npend == kPend) finalize_pass(true);   // full: retire the two oldest
-            pend[npend++] = g;
-          }
-          trace(k, 5);
-        }
-        break;   // this CTA's claims of the step are exhausted
       } else {
         // X tiles group-major (contiguous column runs per group); the claimer of
         // a group's last chunk finalises it after its NEXT tile (deferred), so

@@ -123,7 +123,7 @@ int shard_step_launch(rbd_ctx_t c, const Shard& sh, long long m, long long ldx, 
   a.pay_stride = pay_stride;
   a.col_offset = sh.col_offset;
   void* args[] = {&a};
-  const size_t smem = persist_smem(d_max, false, ring_on<true, false, false>());
+  const size_t smem = persist_smem(d_max);
   cudaError_t e = vec == 2 ? cudaLaunchCooperativeKernel((void*)k_rbd_persistent<2, true>, grid,
                                                          kThreads, args, smem, c->stream)
                            : cudaLaunchCooperativeKernel((void*)k_rbd_persistent<1, true>, grid,
