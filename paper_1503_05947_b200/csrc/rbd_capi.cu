@@ -493,6 +493,8 @@ int launch_persistent(rbd_ctx_t ctx, const LoopBufs& L, const double* diag = nul
     a.aw = ptr<double>(ctx->wd_axi);
     a.npart2 = ptr<double>(ctx->wd_yy);
     a.ppart2 = ptr<double>(ctx->wd_ppart2);
+    TRY(ensure(ctx->wd_yslice, sizeof(double) * 2 * (size_t)(L.d_max / kYSlice + 2)));
+    a.yslice = ptr<double>(ctx->wd_yslice);
     a.q = ptr<double>(ctx->wd_q);
     a.partial2 = ptr<double>(ctx->wd_part2);
     a.YAX = ptr<double>(ctx->wd_yax);
@@ -774,7 +776,7 @@ int rbd_ctx_destroy(rbd_ctx_t ctx) {
                   &ctx->hX,      &ctx->hY,   &ctx->hT,      &ctx->ppart, &ctx->bar,
                   &ctx->wd_axi,  &ctx->wd_yy, &ctx->wd_part2, &ctx->wd_yrow, &ctx->wd_yax,
                   &ctx->wd_cross, &ctx->wd_quad, &ctx->wd_colsq, &ctx->wd_diag,
-                  &ctx->wd_ppart2, &ctx->wd_q, &ctx->wd_yay, &ctx->forced,
+                  &ctx->wd_ppart2, &ctx->wd_q, &ctx->wd_yay, &ctx->wd_yslice, &ctx->forced,
                   &ctx->nn_part, &ctx->nn_coords, &ctx->pj_ws,
                   &ctx->ctl,     &ctx->gcnt, &ctx->ygcnt,   &ctx->rdy,   &ctx->send,  &ctx->recv};
   for (DevBuf* b : bl) release(*b);

@@ -139,6 +139,7 @@ struct rbd_ctx_s {
   // partials, YAY row, YAX (d_max x n), cross, quad, col_sq_A, host-entry diag
   DevBuf wd_axi, wd_yy, wd_part2, wd_yrow, wd_yax, wd_cross, wd_quad, wd_colsq, wd_diag;
   DevBuf wd_ppart2, wd_q, wd_yay;           // persistent weighted loop: Y'(a o w1), YAY
+  DevBuf wd_yslice;                          // persistent weighted loop: YAY-row slice partials
   DevBuf forced;                             // rbd_set_forced_selection (test instrumentation)
   std::vector<long long> forced_h;
   DevBuf nn_part, nn_coords;               // classify: split minima, query coordinates

@@ -87,6 +87,7 @@ struct PersistArgs {
   double* cross;                 // [n] sum_l T[l,j] YAX[l,j]
   double* quad;                  // [n] T[:,j]' YAY T[:,j]
   const double* colsq_a;         // [n] ||x_j||_A^2
+  double* yslice;                // [d_max / kYSlice + 2][2] per-slice (p.q, p.v) of the YAY row
 };
 
 __device__ __forceinline__ void red_release_add_u64(unsigned long long* p, unsigned long long v) {
@@ -160,6 +161,12 @@ struct StepCtl {
   long long r_step;
   double e_cur;
   long long jstar;
+  // DIAG: the YAY row of the step, computed in slices by every CTA after the
+  // decision; the CTA finishing the last slice publishes it, tagged step+1
+  unsigned yslices;              // CTAs through their slices this step
+  unsigned pad3;
+  long long y_step;
+  double w1a;                    // w1'Aw1 (the decider's sum)
 };
 
 __device__ __forceinline__ long long ld_acquire_s64(const long long* p) {
@@ -213,92 +220,13 @@ constexpr int kP3Groups = 4;   // column groups finalised together in P3
 #define RBD_P1_LOADS 16
 #endif
 constexpr int kPLoads = RBD_P1_LOADS;   // P1: Y loads in flight per lane per batch
+constexpr int kYSlice = kWarps;         // DIAG: YAY-row entries per slice (one warp each)
 constexpr int kTraceWords = 256;  // per CTA: [0] count, then (tag<<40 | time) words
 
 // Payload of a rank in sharded mode (doubles): [0] best residual, [1] global
 // column index (bits), [2] col_sq of that column, [3] pad, [4, 4+m) the
 // column x_j, [4+m, 4+m+k+1) the column T[0:k+1, j].
 constexpr int kPayHead = 4;
-
-// DIAG decider: YAY[k, 0:k+1] = the new row of Y'AY (see the header), into
-// a.yrow and the symmetric YAY. CTA-wide: v = YAY[0:k,0:k] p with every warp on
-// 8 column pairs x 4 row residues (lanes 0-7 / 8-15 / ... read 128 contiguous
-// bytes of one row), 8 double2 loads in flight per lane, residues combined by
-// shuffles in a fixed order.
-__device__ __forceinline__ void diag_yay_row(const PersistArgs& a, long long k, int re, double nrm,
-                                             double w1a, const double* p, double* sm) {
-  const long long ld = a.d_max;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int pr = lane & 7, rs = lane >> 3;   // pair within the warp's 8, row residue mod 4
-  const bool vec2 = (ld % 2) == 0;
-  double pq = 0.0, pv = 0.0;
-  const long long npairs = (k + 1) / 2;
-  for (long long pb = 0; pb < npairs; pb += 8 * kWarps) {
-    const long long pair = pb + warp * 8 + pr;
-    const long long l0 = 2 * pair;
-    const bool have = pair < npairs, two = l0 + 1 < k;
-    double v0 = 0.0, v1 = 0.0;
-    if (re && have) {
-      long long mm = rs;
-      for (; mm + 4 * 7 < k; mm += 4 * 8) {
-        double2 yv[8];
-        double pm[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const double* src = a.YAY + (mm + 4 * u) * ld + l0;
-          if (vec2 && two) {
-            yv[u] = __ldcg(reinterpret_cast<const double2*>(src));
-          } else {
-            yv[u].x = __ldcg(src);
-            yv[u].y = two ? __ldcg(src + 1) : 0.0;
-          }
-          pm[u] = __ldcg(p + mm + 4 * u);
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          v0 = fma(yv[u].x, pm[u], v0);
-          v1 = fma(yv[u].y, pm[u], v1);
-        }
-      }
-      for (; mm < k; mm += 4) {
-        const double pm = __ldcg(p + mm);
-        v0 = fma(__ldcg(a.YAY + mm * ld + l0), pm, v0);
-        if (two) v1 = fma(__ldcg(a.YAY + mm * ld + l0 + 1), pm, v1);
-      }
-    }
-    // residues 0..3 -> lane pr (fixed order: (r0 + r1) + (r2 + r3))
-    v0 += __shfl_xor_sync(0xffffffffu, v0, 8);
-    v1 += __shfl_xor_sync(0xffffffffu, v1, 8);
-    v0 += __shfl_xor_sync(0xffffffffu, v0, 16);
-    v1 += __shfl_xor_sync(0xffffffffu, v1, 16);
-    if (rs == 0 && have) {
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const long long l = l0 + h;
-        if (h == 1 && !two) break;
-        const double vl = h ? v1 : v0;
-        const double ql = __ldcg(a.q + l);
-        const double yl = (re ? ql - vl : ql) / nrm;
-        a.yrow[l] = yl;
-        a.YAY[k * ld + l] = yl;
-        a.YAY[l * ld + k] = yl;
-        if (re) {
-          const double pl = __ldcg(p + l);
-          pq = fma(pl, ql, pq);
-          pv = fma(pl, vl, pv);
-        }
-      }
-    }
-  }
-  pq = block_sum_fixed<kThreads>(pq, sm);
-  pv = block_sum_fixed<kThreads>(pv, sm);
-  if (threadIdx.x == 0) {
-    const double num = re ? (w1a - 2.0 * pq) + pv : w1a;
-    const double ykk = num / (nrm * nrm);
-    a.yrow[k] = ykk;
-    a.YAY[k * ld + k] = ykk;
-  }
-}
 
 template <int VEC, bool SHARD, bool DIAG = false, bool XF32 = false>
 __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
@@ -598,6 +526,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
         __threadfence();
       }
       st_release_s64(&ctl->p_step, k + 1);
+      if (DIAG) st_release_s64(&ctl->y_step, k + 1);
     }
     // Groups whose last chunk this CTA swept and that are not finalised yet
     // (FIFO, uniform across the CTA). Finalisation is attempted after the next
@@ -628,14 +557,105 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
       nrm_s = __ldcg(&ctl->norm);
       if constexpr (DIAG) {
         if (!bd_s) {
-          for (long long l = tid; l <= k; l += kThreads) {
+          for (long long l = tid; l <= k; l += kThreads)
             pd[l] = (re_s && l < k) ? __ldcg(&pbuf(k)[l]) : 0.0;
-            yd[l] = __ldcg(&a.yrow[l]);
-          }
           __syncthreads();
         }
       }
       p_ready = true;
+      return true;
+    };
+    // DIAG: the YAY row YAY[k, 0:k+1] (see the header), distributed: slice sl
+    // (kYSlice entries, one warp per entry l) is computed by CTA sl % G once
+    // the decision is out: v_l = YAY[l, 0:k] . p (lane-strided, xor-butterfly),
+    // YAY[k, l] = (q_l - v_l) / ||w|| (q_l when there is no second pass); the
+    // slice's p.q and p.v go to yslice[sl]. The CTA completing the last slice
+    // sums them in slice order for YAY[k, k] and publishes the row. Every CTA
+    // does its slices before it waits on the row or on the step barrier, so
+    // no wait can cycle.
+    bool y_mine = false, y_ready = false;
+    auto yay_slices = [&](const bool block) {
+      if (!DIAG || y_mine) return;
+      if (k == 0) {   // row [YAY[0, 0]] published with the decision
+        y_mine = true;
+        return;
+      }
+      if (!ensure_p(block)) return;
+      y_mine = true;
+      if (bd_s) return;
+      const long long ld = a.d_max;
+      const long long nsl = (k + kYSlice - 1) / kYSlice;
+      for (long long sl = cta; sl < nsl; sl += G) {
+        const long long l = sl * kYSlice + warp;
+        double v = 0.0;
+        if (re_s && l < k)
+          for (long long mm = lane; mm < k; mm += 32) v = fma(__ldcg(&a.YAY[l * ld + mm]), pd[mm], v);
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+        if (lane == 0) smn[warp] = v;
+        __syncthreads();
+        if (tid == 0) {
+          double pq = 0.0, pv = 0.0;
+          for (int w = 0; w < kYSlice; ++w) {
+            const long long ll = sl * kYSlice + w;
+            if (ll >= k) break;
+            const double ql = __ldcg(a.q + ll), vl = smn[w];
+            const double yl = (re_s ? ql - vl : ql) / nrm_s;
+            a.yrow[ll] = yl;
+            a.YAY[k * ld + ll] = yl;
+            a.YAY[ll * ld + k] = yl;
+            if (re_s) {
+              pq = fma(pd[ll], ql, pq);
+              pv = fma(pd[ll], vl, pv);
+            }
+          }
+          a.yslice[2 * sl] = pq;
+          a.yslice[2 * sl + 1] = pv;
+        }
+        __syncthreads();
+      }
+      if (tid == 0) {
+        __threadfence();
+        if (atomicAdd(&ctl->yslices, 1u) == (unsigned)(G - 1)) {   // last: YAY[k, k]
+          __threadfence();
+          double pq = 0.0, pv = 0.0;
+          for (long long sl = 0; sl < nsl; ++sl) {
+            pq += __ldcg(&a.yslice[2 * sl]);
+            pv += __ldcg(&a.yslice[2 * sl + 1]);
+          }
+          const double w1a = __ldcg(&ctl->w1a);
+          const double num = re_s ? (w1a - 2.0 * pq) + pv : w1a;
+          const double ykk = num / (nrm_s * nrm_s);
+          a.yrow[k] = ykk;
+          a.YAY[k * ld + k] = ykk;
+          ctl->yslices = 0u;
+          __threadfence();
+          st_release_s64(&ctl->y_step, k + 1);
+        }
+      }
+      trace(k, 12);
+    };
+    auto ensure_y = [&](const bool block) -> bool {
+      if (y_ready) return true;
+      yay_slices(block);
+      if (!y_mine) return false;
+      if (bd_s) {
+        y_ready = true;
+        return true;
+      }
+      if (tid == 0) {
+        int ok = ld_acquire_s64(&ctl->y_step) == k + 1;
+        if (!ok && block) {
+          wait_step(&ctl->y_step, k + 1);
+          ok = 1;
+        }
+        sh_ok = ok;
+      }
+      __syncthreads();
+      if (!sh_ok) return false;
+      for (long long l = tid; l <= k; l += kThreads) yd[l] = __ldcg(&a.yrow[l]);
+      __syncthreads();
+      y_ready = true;
       return true;
     };
     // Finalise up to two groups at once (warps 0-3: pend[0], warps 4-7:
@@ -644,17 +664,24 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
     // unless block. Returns the number of groups retired from the FIFO front.
     auto finalize_pass = [&](const bool block) {
       if (!ensure_p(block)) return;
+      if (DIAG && !ensure_y(block)) return;
       const int q = warp >> 2;
       const long long g = q < npend ? pend[q] : -1;
       const long long j = g * kCols + (warp & 3);
       const bool mine = g >= 0 && j < n;
       double sp = 0.0, corr = 0.0, rj = 0.0;
       double sp2 = 0.0, corr2 = 0.0, gg = 0.0;   // DIAG: (a o w1).x_j, p.YAX[:, j], YAY row . T[:, j]
+      double cr0 = 0.0, qd0 = 0.0, ca0 = 0.0;      // DIAG (lane 0): cross_j, quad_j, col_sq_A[j]
       if (mine) {   // a chunk partial not written yet is NaN, and so is the sum
         for (long long ss = lane; ss < S; ss += 32) sp += ld_relaxed_f64(&a.partial[ss * n + j]);
         if constexpr (DIAG) {
+          // every load of the pass goes out before any is used: one L2 round trip
           for (long long ss = lane; ss < S; ss += 32) sp2 += ld_relaxed_f64(&a.partial2[ss * n + j]);
-          sp = (sp2 == sp2) ? sp : sp2;   // NaN if either row is incomplete
+          if (lane == 0) {   // carried sums: only this group's finaliser writes them
+            cr0 = __ldcg(&a.cross[j]);
+            qd0 = __ldcg(&a.quad[j]);
+            ca0 = __ldg(&a.colsq_a[j]);
+          }
           if (!bd_s) {
             for (long long l0 = 0; l0 < k; l0 += 256) {
               double tv[8], av[8];
@@ -674,6 +701,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
               }
             }
           }
+          sp = (sp2 == sp2) ? sp : sp2;   // NaN if either row is incomplete
         } else if (lane == 0) {
           rj = __ldcg(&a.r[j]);
         }
@@ -723,11 +751,11 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
           const double ya = (sp2 - corr2) / nrm_s;               // workspace.cpp:66
           a.T[k * n + j] = tt;
           a.YAX[k * n + j] = ya;
-          const double cr = a.cross[j] + tt * ya;
-          const double qd = a.quad[j] + (2.0 * tt * gg + yd[k] * tt * tt);
+          const double cr = cr0 + tt * ya;
+          const double qd = qd0 + (2.0 * tt * gg + yd[k] * tt * tt);
           a.cross[j] = cr;
           a.quad[j] = qd;
-          double e2 = a.colsq_a[j] - 2.0 * cr + qd;              // workspace.cpp:88-97
+          double e2 = ca0 - 2.0 * cr + qd;                       // workspace.cpp:88-97
           e2 = e2 > 0.0 ? e2 : 0.0;
           if (rec_better(e2, j, bv, bj)) {
             bv = e2;
@@ -826,17 +854,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
             sh_dec[0] = re;
             sh_dec[1] = bd;
             sh_decd[0] = nrm;
-            if (!DIAG) st_release_s64(&ctl->p_step, k + 1);
+            if (DIAG) ctl->w1a = w1a;
+            st_release_s64(&ctl->p_step, k + 1);
           }
-          if constexpr (DIAG) {   // the YAY row, then publish
-            __syncthreads();
-            if (!sh_dec[1]) diag_yay_row(a, k, sh_dec[0], sh_decd[0], w1a, pbuf(k), smn);
-            __syncthreads();
-            if (tid == 0) {
-              __threadfence();
-              st_release_s64(&ctl->p_step, k + 1);
-            }
-          }
+          trace(k, 11);
         }
         mark(6);
         trace(k, 5);
@@ -861,6 +882,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
                                                          s * ngx + g, 1LL << 40, red, dummy_nf,
                                                          dummy_nz);
         mark(7);
+        if (DIAG) yay_slices(false);   // this CTA's share of the YAY row, once decided
         if (npend > 0) finalize_pass(false);
         if (s == S - 1) {
           constexpr int per = kXT / kCols;   // finalisation groups this tile completes
@@ -872,6 +894,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
       }
     }
     while (npend > 0) finalize_pass(true);
+    if (DIAG) yay_slices(true);   // others may be waiting on this CTA's slices
     block_argmax<kThreads>(bv, bj, smr);
     if (tid == 0) a.rec[cta] = Rec{bv, bj};
     tile_base += (unsigned long long)(total + G);

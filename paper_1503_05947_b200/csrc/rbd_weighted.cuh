@@ -180,7 +180,7 @@ __device__ __forceinline__ void sweep_tile_dot2(const double* __restrict__ A, lo
 // sweep_tile_dot2, hence the same bits. sv: [UB][2][kThreads] double2.
 constexpr int kSvUB = 4;
 constexpr int kSvBytes = kSvUB * 2 * kThreads * 16;   // 32 KiB per CTA
-template <int UB = kSvUB>
+template <int ALOAD = LOAD_STREAM, int UB = kSvUB>
 __device__ __forceinline__ void sweep_tile_dot2_sv(const double* __restrict__ A, long long lda,
                                                    long long m, long long ncols,
                                                    const double* __restrict__ v,
@@ -224,14 +224,18 @@ __device__ __forceinline__ void sweep_tile_dot2_sv(const double* __restrict__ A,
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(a0), "l"(vr + e) : "memory");
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(a1), "l"(wr + e) : "memory");
 #pragma unroll
-        for (int c = 0; c < kCols; ++c) xv[u][c] = ld_stream2(Ac[c] + e);
+        for (int c = 0; c < kCols; ++c)
+          xv[u][c] = ALOAD == LOAD_STREAM ? ld_stream2(Ac[c] + e)
+                                          : __ldcg(reinterpret_cast<const double2*>(Ac[c] + e));
       } else {
         const bool in0 = e < rows, in1 = e + 1 < rows;
         *s0 = make_double2(in0 ? __ldcg(vr + e) : 0.0, in1 ? __ldcg(vr + e + 1) : 0.0);
         *s1 = make_double2(in0 ? __ldcg(wr + e) : 0.0, in1 ? __ldcg(wr + e + 1) : 0.0);
 #pragma unroll
         for (int c = 0; c < kCols; ++c)
-          xv[u][c] = make_double2(in0 ? __ldcs(Ac[c] + e) : 0.0, in1 ? __ldcs(Ac[c] + e + 1) : 0.0);
+          xv[u][c] = ALOAD == LOAD_STREAM
+                         ? make_double2(in0 ? __ldcs(Ac[c] + e) : 0.0, in1 ? __ldcs(Ac[c] + e + 1) : 0.0)
+                         : make_double2(in0 ? __ldcg(Ac[c] + e) : 0.0, in1 ? __ldcg(Ac[c] + e + 1) : 0.0);
       }
     }
     asm volatile("cp.async.wait_all;" ::: "memory");

@@ -19,13 +19,14 @@ for c in range(G):
         if tag & 0xFF == 10:
             si += 1
 names = {1: "P1 start", 2: "P1 end", 3: "bar1 out", 6: "P2 end", 7: "bar2 out", 8: "P3 end",
+         11: "decided", 12: "YAY row",
          9: "bar3 out", 10: "step end"}
 for si, ev in enumerate(steps):
     if not ev:
         continue
     t0 = min(e[3] for e in ev if e[1] == 1)
     print(f"--- step {si}")
-    for tag in [1, 2, 3, 6, 7, 8, 9, 10]:
+    for tag in [1, 2, 3, 11, 12, 6, 7, 8, 9, 10]:
         ts = np.array([e[3] - t0 for e in ev if e[1] == tag]) / 1e3
         if len(ts):
             print(f"{names[tag]:10s} min={ts.min():8.2f} med={np.median(ts):8.2f} max={ts.max():8.2f} us")
