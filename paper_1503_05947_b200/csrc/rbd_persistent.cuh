@@ -497,14 +497,15 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
     //                 reorth coefficients) summed over chunks in order by one
     //                 CTA; the last one to finish decides the second pass
     //                 (decompose.cpp:28), ||w_k|| and breakdown (:29-30)
-    //   [gy, gy+nx)   X' w1 tiles (the fused sweep): chunks 0..S-2 group-major,
-    //                 then every group's last chunk. Its claimer finalises the
-    //                 group in-queue:
+    //   [gy, gy+nx)   X' w1 tiles (the fused sweep), group-major (DIAG: chunks
+    //                 0..S-2 group-major, then every group's last chunk). The
+    //                 claimer of a group's last chunk finalises the group in-queue:
     //                 T[k, j] = (w1.x_j - p.T[0:k, j]) / ||w_k||, residuals
     //                 (workspace.cpp:52-53). Chunk partials double as ready
-    //                 flags (NaN = not written); siblings were claimed long
-    //                 before, so the poll practically never waits, and every
-    //                 wait targets an earlier-claimed tile (no deadlock).
+    //                 flags (NaN = not written); the siblings were claimed
+    //                 earlier and finalisation is deferred by one tile, so the
+    //                 poll rarely waits, and every wait targets an
+    //                 earlier-claimed tile (no deadlock).
     const long long gy = (k + kCols - 1) / kCols;
     const long long total = gy + nx;
     double bv = -1.0;          // this CTA's best finalised residual (argmax record)
@@ -867,7 +868,12 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
         // the siblings are long done and finalisation never piles up at the
         // end of the queue
         const long long tx = t - gy;
-        const long long g = tx / S, s = tx - g * S;
+        // queue order: group-major (a group's chunks back to back); DIAG puts
+        // every group's last chunk at the end instead (measured: weighted loop
+        // 56.4 -> 55.6 ms, identity 46.6 -> 48.3 ms with that order)
+        const long long nf = DIAG ? (nx / S) * (S - 1) : 0;   // tiles of chunks 0..S-2
+        const long long g = !DIAG ? tx / S : (tx < nf) ? tx / (S - 1) : tx - nf;
+        const long long s = !DIAG ? tx - g * S : (tx < nf) ? tx - g * (S - 1) : S - 1;
         if constexpr (DIAG && VEC == 2)
           sweep_tile_dot2_sv(a.X, a.ldx, m, n, a.w, a.aw, a.partial, a.partial2, n, s * ngx + g,
                              red2, svec);
