@@ -138,6 +138,22 @@ int rbd_decompose_host_f32(rbd_ctx_t ctx, const float* hX, int64_t m, int64_t n,
                            const rbd_config_t* cfg, double* hY, double* hT, int64_t* h_selected,
                            double* h_history, rbd_result_t* result);
 
+/* rbd::decompose over a sequence of `count` host matrices of one shape and
+ * config (the end-to-end entry for a stream of inputs): the H2D upload of
+ * matrix i+1 runs on a second stream (copy engine) while matrix i's greedy
+ * loop runs, with two device X buffers. Per matrix the outputs and errors are
+ * rbd_decompose_host's (hY[i], hT[i], h_selected[i], h_history[i],
+ * results[i]; any of the pointer arrays may be NULL). Page-locked X is needed
+ * for the overlap. Stops at the first failing matrix and returns its status. */
+int rbd_decompose_host_many(rbd_ctx_t ctx, int64_t count, const double* const* hX, int64_t m,
+                            int64_t n, int64_t ldx, const rbd_config_t* cfg, double* const* hY,
+                            double* const* hT, int64_t* const* h_selected, double* const* h_history,
+                            rbd_result_t* results);
+int rbd_decompose_host_many_f32(rbd_ctx_t ctx, int64_t count, const float* const* hX, int64_t m,
+                                int64_t n, int64_t ldx, const rbd_config_t* cfg, double* const* hY,
+                                double* const* hT, int64_t* const* h_selected,
+                                double* const* h_history, rbd_result_t* results);
+
 /* rbd::decompose with cfg.weight = WeightSpec::diagonal(diag) (
  * reference decompose.cpp:53-111, weight.cpp:11-21, workspace.cpp:24-29,61-99,
  * 114-122). Y and T are Euclidean as in the reference; the weight steers the

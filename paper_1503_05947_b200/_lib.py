@@ -139,6 +139,10 @@ _SIGS = {
                                        C.POINTER(Result)]),
     "rbd_decompose_host": (C.c_int, [_P, _P, _I64, _I64, _I64, C.POINTER(Config), _P, _P, _P, _P,
                                      C.POINTER(Result)]),
+    "rbd_decompose_host_many": (C.c_int, [_P, _I64, _P, _I64, _I64, _I64, C.POINTER(Config), _P, _P,
+                                          _P, _P, _P]),
+    "rbd_decompose_host_many_f32": (C.c_int, [_P, _I64, _P, _I64, _I64, _I64, C.POINTER(Config), _P,
+                                              _P, _P, _P, _P]),
     "rbd_decompose_host_f32": (C.c_int, [_P, _P, _I64, _I64, _I64, C.POINTER(Config), _P, _P, _P, _P,
                                      C.POINTER(Result)]),
     "rbd_decompose_device_f32": (C.c_int, [_P, _P, _I64, _I64, _I64, C.POINTER(Config), _P, _P, _P, _P,

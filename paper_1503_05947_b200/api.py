@@ -243,6 +243,52 @@ def decompose(x, d_max: int, eps_r: float = 0.0, diag=None, sparse=None, start_c
     return Model(Y, T, d, sel[:d], hist[:d], res, ctx, 1 if diag is not None else 0, diag)
 
 
+def decompose_many(xs, d_max: int, eps_r: float = 0.0, start_column: int = 0,
+                   reorthogonalize: bool = False, breakdown_tol: float = -1.0,
+                   start_seed: Optional[int] = None, ctx: Optional[Context] = None,
+                   storage: Optional[str] = None):
+    """rbd::decompose over a sequence of host matrices of one shape
+    (rbd_decompose_host_many): the upload of matrix i+1 overlaps the greedy
+    loop of matrix i. Returns one Model per matrix. Page-locked inputs (e.g.
+    ``torch.empty(..., pin_memory=True).numpy()``) are needed for the overlap."""
+    xs = list(xs)
+    if not xs:
+        return []
+    if storage is None:
+        storage = "f32" if all(getattr(x, "dtype", None) == np.float32 for x in xs) else "f64"
+    if storage not in ("f32", "f64"):
+        raise InvalidArgument("decompose: storage must be 'f32' or 'f64'")
+    f32 = storage == "f32"
+    dt = np.float32 if f32 else np.float64
+    arrs = []
+    for x in xs:
+        a = x if (isinstance(x, np.ndarray) and x.dtype == dt and x.flags["F_CONTIGUOUS"]) \
+            else np.asfortranarray(np.asarray(x, dtype=dt))
+        if a.ndim != 2 or a.shape != np.shape(arrs[0] if arrs else a):
+            raise InvalidArgument("decompose_many: matrices must be 2-D and of one shape")
+        arrs.append(a)
+    m, n = arrs[0].shape
+    cfg = make_config(d_max, eps_r, start_column, reorthogonalize, breakdown_tol, start_seed)
+    lib = load_library()
+    ctx = ctx or default_context(0)
+    cap = max(1, min(int(d_max), n)) if n > 0 else 1
+    cnt = len(arrs)
+    outs = [_host_outputs(m, n, cap) for _ in range(cnt)]
+    sels = [np.zeros(cap, dtype=np.int64) for _ in range(cnt)]
+    hists = [np.zeros(cap, dtype=np.float64) for _ in range(cnt)]
+    res = (Result * cnt)()
+    P = C.c_void_p * cnt
+    xp = P(*[a.ctypes.data for a in arrs])
+    yp = P(*[o[0].ctypes.data for o in outs])
+    tp = P(*[o[1].ctypes.data for o in outs])
+    sp = P(*[v.ctypes.data for v in sels])
+    hp = P(*[v.ctypes.data for v in hists])
+    fn = lib.rbd_decompose_host_many_f32 if f32 else lib.rbd_decompose_host_many
+    check(fn(ctx.handle, cnt, xp, m, n, max(m, 1), C.byref(cfg), yp, tp, sp, hp, res))
+    return [Model(outs[i][0], outs[i][1], res[i].d, sels[i][:res[i].d], hists[i][:res[i].d],
+                  res[i], ctx) for i in range(cnt)]
+
+
 def _ptr(a):
     return C.c_void_p(a.data_ptr()) if hasattr(a, "data_ptr") else _dp(a)
 

@@ -773,7 +773,7 @@ int rbd_ctx_destroy(rbd_ctx_t ctx) {
   DevBuf* bl[] = {&ctx->partial, &ctx->rec,  &ctx->counter, &ctx->state, &ctx->colsq,
                   &ctx->resid,   &ctx->w,    &ctx->c,       &ctx->p,     &ctx->nrm,
                   &ctx->hist,    &ctx->sel,  &ctx->out_rec, &ctx->scratch1,
-                  &ctx->hX,      &ctx->hY,   &ctx->hT,      &ctx->ppart, &ctx->bar,
+                  &ctx->hX,      &ctx->hX2,  &ctx->hY,      &ctx->hT,    &ctx->ppart, &ctx->bar,
                   &ctx->wd_axi,  &ctx->wd_yy, &ctx->wd_part2, &ctx->wd_yrow, &ctx->wd_yax,
                   &ctx->wd_cross, &ctx->wd_quad, &ctx->wd_colsq, &ctx->wd_diag,
                   &ctx->wd_ppart2, &ctx->wd_q, &ctx->wd_yay, &ctx->wd_yslice, &ctx->forced,
@@ -783,6 +783,7 @@ int rbd_ctx_destroy(rbd_ctx_t ctx) {
   if (ctx->h_state) cudaFreeHost(ctx->h_state);
   if (ctx->h_progress) cudaFreeHost(ctx->h_progress);
   if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+  if (ctx->up_stream) cudaStreamDestroy(ctx->up_stream);
   if (ctx->h_rec) cudaFreeHost(ctx->h_rec);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   rbd_comm_release(ctx);
@@ -1089,6 +1090,16 @@ int rbd_decompose_diag_device(rbd_ctx_t ctx, const double* dX, int64_t m, int64_
 }
 
 namespace {
+// Device leading dimension of an uploaded X: columns stay 16-byte aligned.
+long long upload_ld(long long m, bool f32) { return f32 ? (m + 3) / 4 * 4 : (m % 2 == 0 ? m : m + 1); }
+
+// The host entry after the upload: X already sits in dXbuf (ld = upload_ld);
+// runs the decompose and brings Y/T/selected/history back (Y and T stream out
+// during the loop when the host buffers are page-locked).
+int run_uploaded(rbd_ctx_t ctx, void* dXbuf, int64_t m, int64_t n, const rbd_config_t* cfg,
+                 const double* h_diag, int64_t diag_len, double* hY, double* hT, int64_t* h_selected,
+                 double* h_history, rbd_result_t* result, bool f32);
+
 int decompose_host_impl(rbd_ctx_t ctx, const double* hX, int64_t m, int64_t n, int64_t ldx,
                         const rbd_config_t* cfg, const double* h_diag, int64_t diag_len,
                         double* hY, double* hT, int64_t* h_selected, double* h_history,
@@ -1097,19 +1108,28 @@ int decompose_host_impl(rbd_ctx_t ctx, const double* hX, int64_t m, int64_t n, i
   if (m < 1 || n < 1) return set_err(RBD_ERR_INVALID_ARGUMENT, "decompose: matrix must be non-empty");
   if (ldx < m) return set_err(RBD_ERR_DIMENSION_MISMATCH, "decompose: ldx < m");
   CU(cudaSetDevice(ctx->device));
-  const long long d_cap = std::max<long long>(1, std::min<long long>(cfg->d_max, n));
-  // keep device columns 16-byte aligned (2 doubles / 4 floats)
   const size_t es = hXf ? sizeof(float) : sizeof(double);
-  const long long ldd = hXf ? (m + 3) / 4 * 4 : (m % 2 == 0 ? m : m + 1);
+  const long long ldd = upload_ld(m, hXf != nullptr);
   TRY(ensure(ctx->hX, es * ldd * n));
+  cudaError_t e = cudaMemcpy2DAsync(ctx->hX.p, es * ldd, hXf ? (const void*)hXf : (const void*)hX,
+                                    es * ldx, es * m, n, cudaMemcpyHostToDevice, ctx->stream);
+  if (e != cudaSuccess) return set_err(RBD_ERR_CUDA, std::string("H2D X: ") + cudaGetErrorString(e));
+  return run_uploaded(ctx, ctx->hX.p, m, n, cfg, h_diag, diag_len, hY, hT, h_selected, h_history,
+                      result, hXf != nullptr);
+}
+
+int run_uploaded(rbd_ctx_t ctx, void* dXbuf, int64_t m, int64_t n, const rbd_config_t* cfg,
+                 const double* h_diag, int64_t diag_len, double* hY, double* hT, int64_t* h_selected,
+                 double* h_history, rbd_result_t* result, bool f32) {
+  const long long d_cap = std::max<long long>(1, std::min<long long>(cfg->d_max, n));
+  const long long ldd = upload_ld(m, f32);
+  const float* dXf = f32 ? reinterpret_cast<const float*>(dXbuf) : nullptr;   // fp32 storage mode
   TRY(ensure(ctx->hY, sizeof(double) * m * d_cap));
   TRY(ensure(ctx->hT, sizeof(double) * d_cap * n));
-  double* dX = ptr<double>(ctx->hX);
+  double* dX = reinterpret_cast<double*>(dXbuf);
   double* dY = ptr<double>(ctx->hY);
   double* dT = ptr<double>(ctx->hT);
-  cudaError_t e = cudaMemcpy2DAsync(dX, es * ldd, hXf ? (const void*)hXf : (const void*)hX, es * ldx,
-                                    es * m, n, cudaMemcpyHostToDevice, ctx->stream);
-  if (e != cudaSuccess) return set_err(RBD_ERR_CUDA, std::string("H2D X: ") + cudaGetErrorString(e));
+  cudaError_t e = cudaSuccess;
   rbd_result_t r{};
   int rc;
   bool t_streamed = false;
@@ -1136,8 +1156,8 @@ int decompose_host_impl(rbd_ctx_t ctx, const double* hX, int64_t m, int64_t n, i
         cudaGetLastError();
       }
     }
-    rc = hXf ? decompose_device_impl(ctx, nullptr, m, n, ldd, cfg, nullptr, dY, dT, h_selected,
-                                     h_history, &r, reinterpret_cast<const float*>(dX))
+    rc = dXf ? decompose_device_impl(ctx, nullptr, m, n, ldd, cfg, nullptr, dY, dT, h_selected,
+                                     h_history, &r, dXf)
              : rbd_decompose_device(ctx, dX, m, n, ldd, cfg, dY, dT, h_selected, h_history, &r);
     t_streamed = ctx->tstream_dst != nullptr;
     ctx->ystream_dst = nullptr;
@@ -1178,6 +1198,76 @@ int rbd_decompose_host_f32(rbd_ctx_t ctx, const float* hX, int64_t m, int64_t n,
   if (!hX) return set_err(RBD_ERR_INVALID_ARGUMENT, "decompose: null X");
   return decompose_host_impl(ctx, nullptr, m, n, ldx, cfg, nullptr, 0, hY, hT, h_selected,
                              h_history, result, hX);
+}
+
+namespace {
+// Pipelined host entry: the upload of matrix i+1 (second stream, copy engine)
+// overlaps the greedy loop of matrix i; two device X buffers alternate. Each
+// decompose is synchronous, so buffer (i+1) % 2 — last read by decompose
+// i-1 — is free when its upload is enqueued.
+int decompose_host_many_impl(rbd_ctx_t ctx, int64_t count, const void* const* hX, int64_t m,
+                             int64_t n, int64_t ldx, const rbd_config_t* cfg, double* const* hY,
+                             double* const* hT, int64_t* const* h_selected,
+                             double* const* h_history, rbd_result_t* results, bool f32) {
+  if (!ctx || !cfg) return set_err(RBD_ERR_INVALID_ARGUMENT, "decompose: null context/config");
+  if (count < 0 || (count > 0 && !hX)) return set_err(RBD_ERR_INVALID_ARGUMENT, "decompose_many: bad list");
+  if (count == 0) return RBD_OK;
+  if (m < 1 || n < 1) return set_err(RBD_ERR_INVALID_ARGUMENT, "decompose: matrix must be non-empty");
+  if (ldx < m) return set_err(RBD_ERR_DIMENSION_MISMATCH, "decompose: ldx < m");
+  for (int64_t i = 0; i < count; ++i)
+    if (!hX[i]) return set_err(RBD_ERR_INVALID_ARGUMENT, "decompose: null X");
+  CU(cudaSetDevice(ctx->device));
+  const size_t es = f32 ? sizeof(float) : sizeof(double);
+  const long long ldd = upload_ld(m, f32);
+  const size_t bytes = es * (size_t)ldd * (size_t)n;
+  TRY(ensure(ctx->hX2, 2 * bytes));
+  if (!ctx->up_stream) CU(cudaStreamCreateWithFlags(&ctx->up_stream, cudaStreamNonBlocking));
+  cudaEvent_t up[2];
+  CU(cudaEventCreateWithFlags(&up[0], cudaEventDisableTiming));
+  CU(cudaEventCreateWithFlags(&up[1], cudaEventDisableTiming));
+  struct EvGuard {
+    cudaEvent_t* e;
+    cudaStream_t s;
+    ~EvGuard() {
+      cudaStreamSynchronize(s);   // no upload may outlive the call
+      cudaEventDestroy(e[0]);
+      cudaEventDestroy(e[1]);
+    }
+  } guard{up, ctx->up_stream};
+  char* buf = static_cast<char*>(ctx->hX2.p);
+  auto upload = [&](int64_t i) -> int {
+    cudaError_t e = cudaMemcpy2DAsync(buf + (i % 2) * bytes, es * ldd, hX[i], es * ldx, es * m, n,
+                                      cudaMemcpyHostToDevice, ctx->up_stream);
+    if (e == cudaSuccess) e = cudaEventRecord(up[i % 2], ctx->up_stream);
+    if (e != cudaSuccess) return set_err(RBD_ERR_CUDA, std::string("H2D X: ") + cudaGetErrorString(e));
+    return RBD_OK;
+  };
+  TRY(upload(0));
+  for (int64_t i = 0; i < count; ++i) {
+    CU(cudaStreamWaitEvent(ctx->stream, up[i % 2], 0));
+    if (i + 1 < count) TRY(upload(i + 1));
+    TRY(run_uploaded(ctx, buf + (i % 2) * bytes, m, n, cfg, nullptr, 0, hY ? hY[i] : nullptr,
+                     hT ? hT[i] : nullptr, h_selected ? h_selected[i] : nullptr,
+                     h_history ? h_history[i] : nullptr, results ? &results[i] : nullptr, f32));
+  }
+  return RBD_OK;
+}
+}  // namespace
+
+int rbd_decompose_host_many(rbd_ctx_t ctx, int64_t count, const double* const* hX, int64_t m,
+                            int64_t n, int64_t ldx, const rbd_config_t* cfg, double* const* hY,
+                            double* const* hT, int64_t* const* h_selected, double* const* h_history,
+                            rbd_result_t* results) {
+  return decompose_host_many_impl(ctx, count, reinterpret_cast<const void* const*>(hX), m, n, ldx,
+                                  cfg, hY, hT, h_selected, h_history, results, false);
+}
+
+int rbd_decompose_host_many_f32(rbd_ctx_t ctx, int64_t count, const float* const* hX, int64_t m,
+                                int64_t n, int64_t ldx, const rbd_config_t* cfg, double* const* hY,
+                                double* const* hT, int64_t* const* h_selected,
+                                double* const* h_history, rbd_result_t* results) {
+  return decompose_host_many_impl(ctx, count, reinterpret_cast<const void* const*>(hX), m, n, ldx,
+                                  cfg, hY, hT, h_selected, h_history, results, true);
 }
 
 int rbd_decompose_diag_host(rbd_ctx_t ctx, const double* hX, int64_t m, int64_t n, int64_t ldx,

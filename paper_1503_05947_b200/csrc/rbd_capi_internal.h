@@ -120,6 +120,8 @@ struct rbd_ctx_s {
   long long* h_progress = nullptr;
   long long* d_progress = nullptr;
   cudaStream_t copy_stream = nullptr;
+  cudaStream_t up_stream = nullptr;    // rbd_decompose_host_many: uploads of the next X
+  DevBuf hX2;                          // rbd_decompose_host_many: two device X buffers
   double* ystream_dst = nullptr;   // host Y (ld m) to stream into, or null
   double* tstream_dst = nullptr;   // host T (row-major, n per row), or null
   long long ystream_copied = 0;    // Y columns / T rows already copied (or in flight)

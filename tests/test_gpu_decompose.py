@@ -402,3 +402,34 @@ def test_host_entry_pinned_outputs_stream_y_from_the_loop(cuda):
     assert h.selected == dv.selected
     np.testing.assert_array_equal(h.Y, dv.Y.cpu().numpy())
     np.testing.assert_array_equal(h.T, dv.T.cpu().numpy())
+
+
+def test_host_many_pipelined_equals_single_calls(cuda):
+    """rbd_decompose_host_many (upload of matrix i+1 during matrix i's loop,
+    two device X buffers) gives every matrix the bits of a single host call;
+    pinned and pageable inputs, fp64 and fp32 storage."""
+    import torch
+    m, n, d = 9000, 260, 40
+    xs = []
+    for i in range(5):
+        a = oracle.random_matrix(m, n, 500 + i)
+        if i % 2 == 0:   # page-locked
+            t = torch.empty((n, m), dtype=torch.float64, pin_memory=True)
+            t.copy_(torch.from_numpy(np.ascontiguousarray(a.T)))
+            a = t.numpy().T
+        xs.append(a)
+    many = rbd.decompose_many(xs, d_max=d, eps_r=1e-9)
+    assert len(many) == len(xs)
+    for x, g in zip(xs, many):
+        s = rbd.decompose(np.asfortranarray(x), d_max=d, eps_r=1e-9)
+        assert g.selected == s.selected and g.d == s.d
+        assert np.array_equal(g.Y, s.Y) and np.array_equal(g.T, s.T)
+        assert g.residual_history == s.residual_history
+    xs32 = [np.asfortranarray(x, dtype=np.float32) for x in xs[:3]]
+    many32 = rbd.decompose_many(xs32, d_max=d)
+    for x, g in zip(xs32, many32):
+        s = rbd.decompose(x, d_max=d)
+        assert g.selected == s.selected and np.array_equal(g.Y, s.Y) and np.array_equal(g.T, s.T)
+    assert rbd.decompose_many([], d_max=3) == []
+    with pytest.raises(rbd.InvalidArgument):
+        rbd.decompose_many([xs[0], xs[1][:, :10]], d_max=3)
