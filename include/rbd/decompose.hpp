@@ -76,7 +76,8 @@ inline std::optional<MgsResult> mgs_project(const VectorRef& v, const MatrixRef&
   return MgsResult{std::move(xi), norm};
 }
 
-inline RbdModel decompose(const Matrix& x, const RbdConfig& cfg) {
+namespace detail {
+inline rbd_config_t to_c(const RbdConfig& cfg) {
   rbd_config_t c;
   rbd_config_default(&c);
   c.d_max = cfg.d_max;
@@ -89,6 +90,71 @@ inline RbdModel decompose(const Matrix& x, const RbdConfig& cfg) {
   c.breakdown_tol = cfg.breakdown_tol;
   c.weight_kind = static_cast<int32_t>(cfg.weight.kind());
   c.weight_dim = cfg.weight.dim();
+  return c;
+}
+
+// RbdModel from the C ABI's outputs (Y column-major m x cap, T row-major cap x n).
+inline RbdModel to_model(const rbd_result_t& r, Index m, Index n, const std::vector<double>& Yb,
+                         const std::vector<double>& Tb, const std::vector<int64_t>& sel,
+                         const std::vector<double>& hist, const WeightSpec& weight) {
+  RbdModel model;
+  model.d = r.d;
+  model.weight = weight;
+  model.Y = Matrix(m, r.d);
+  for (Index j = 0; j < r.d; ++j)
+    for (Index i = 0; i < m; ++i) model.Y(i, j) = Yb[static_cast<size_t>(i + j * m)];
+  model.T = Matrix(r.d, n);
+  for (Index k = 0; k < r.d; ++k)
+    for (Index j = 0; j < n; ++j) model.T(k, j) = Tb[static_cast<size_t>(k * n + j)];
+  model.selected.assign(sel.begin(), sel.begin() + r.d);
+  model.residual_history.assign(hist.begin(), hist.begin() + r.d);
+  return model;
+}
+}  // namespace detail
+
+// A caller's loop of decompose() over matrices of one shape and config, with
+// the upload of matrix i+1 overlapping matrix i's greedy loop
+// (rbd_decompose_host_many; identity weight). Same results as decompose() on
+// each matrix.
+inline std::vector<RbdModel> decompose_many(const std::vector<Matrix>& xs, const RbdConfig& cfg) {
+  std::vector<RbdModel> out;
+  if (xs.empty()) return out;
+  if (cfg.weight.kind() != WeightKind::identity)
+    throw InvalidArgument("decompose_many: identity weight only");
+  const Index m = xs[0].rows(), n = xs[0].cols();
+  for (const Matrix& x : xs)
+    if (x.rows() != m || x.cols() != n) throw InvalidArgument("decompose_many: matrices must be of one shape");
+  const rbd_config_t c = detail::to_c(cfg);
+  const Index cap = std::max<Index>(1, std::min<Index>(cfg.d_max, std::max<Index>(n, 1)));
+  const size_t cnt = xs.size();
+  std::vector<std::vector<double>> Yb(cnt), Tb(cnt), hist(cnt);
+  std::vector<std::vector<int64_t>> sel(cnt);
+  std::vector<const double*> xp(cnt);
+  std::vector<double*> yp(cnt), tp(cnt), hp(cnt);
+  std::vector<int64_t*> sp(cnt);
+  std::vector<rbd_result_t> r(cnt);
+  for (size_t i = 0; i < cnt; ++i) {
+    Yb[i].resize(static_cast<size_t>(std::max<Index>(m, 1) * cap));
+    Tb[i].resize(static_cast<size_t>(cap * std::max<Index>(n, 1)));
+    sel[i].resize(static_cast<size_t>(cap));
+    hist[i].resize(static_cast<size_t>(cap));
+    xp[i] = xs[i].data();
+    yp[i] = Yb[i].data();
+    tp[i] = Tb[i].data();
+    sp[i] = sel[i].data();
+    hp[i] = hist[i].data();
+  }
+  detail::check(rbd_decompose_host_many(detail::context(), static_cast<int64_t>(cnt), xp.data(), m, n,
+                                        std::max<Index>(m, 1), &c, yp.data(), tp.data(), sp.data(),
+                                        hp.data(), r.data()));
+  out.reserve(cnt);
+  for (size_t i = 0; i < cnt; ++i)
+    out.push_back(detail::to_model(r[i], m, n, Yb[i], Tb[i], sel[i], hist[i], cfg.weight));
+  return out;
+}
+
+inline RbdModel decompose(const Matrix& x, const RbdConfig& cfg) {
+  const rbd_config_t c = detail::to_c(cfg);
   const Index m = x.rows(), n = x.cols();
   const Index cap = std::max<Index>(1, std::min<Index>(cfg.d_max, std::max<Index>(n, 1)));
   std::vector<double> Yb(static_cast<size_t>(std::max<Index>(m, 1) * cap));
@@ -105,18 +171,7 @@ inline RbdModel decompose(const Matrix& x, const RbdConfig& cfg) {
     detail::check(rbd_decompose_host(detail::context(), x.data(), m, n, std::max<Index>(m, 1),
                                      &c, Yb.data(), Tb.data(), sel.data(), hist.data(), &r));
   }
-  RbdModel model;
-  model.d = r.d;
-  model.weight = cfg.weight;
-  model.Y = Matrix(m, r.d);
-  for (Index j = 0; j < r.d; ++j)
-    for (Index i = 0; i < m; ++i) model.Y(i, j) = Yb[static_cast<size_t>(i + j * m)];
-  model.T = Matrix(r.d, n);   // device T is row-major (T[k*n + j])
-  for (Index k = 0; k < r.d; ++k)
-    for (Index j = 0; j < n; ++j) model.T(k, j) = Tb[static_cast<size_t>(k * n + j)];
-  model.selected.assign(sel.begin(), sel.begin() + r.d);
-  model.residual_history.assign(hist.begin(), hist.begin() + r.d);
-  return model;
+  return detail::to_model(r, m, n, Yb, Tb, sel, hist, cfg.weight);   // device T is row-major
 }
 
 inline Vector project(const RbdModel& model, const VectorRef& v) {     // decompose.cpp:113-117

@@ -100,6 +100,21 @@ static RbdConfig basic(Index d_max, double eps = 0.0) {
 }
 
 int main() {
+  // decompose_many (the pipelined host entry) == decompose per matrix, bit for bit
+  {
+    std::vector<Matrix> xs;
+    for (std::uint64_t seed : {700u, 701u, 702u}) xs.push_back(random_matrix(300, 40, seed));
+    const std::vector<RbdModel> many = decompose_many(xs, basic(15));
+    CHECK(many.size() == xs.size());
+    for (size_t i = 0; i < xs.size() && i < many.size(); ++i) {
+      const RbdModel one = decompose(xs[i], basic(15));
+      CHECK(many[i].d == one.d);
+      CHECK(many[i].selected == one.selected);
+      CHECK(max_abs_diff(many[i].Y, one.Y) == 0.0);
+      CHECK(max_abs_diff(many[i].T, one.T) == 0.0);
+    }
+    CHECK_THROWS_AS(decompose_many({xs[0], random_matrix(30, 4, 9)}, basic(3)), InvalidArgument);
+  }
   // test_decompose.cpp:29-40 rank-1 outer product
   {
     const Vector u = random_matrix(30, 1, 100).col(0);
