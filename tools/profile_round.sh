@@ -5,9 +5,9 @@
 set -u
 R=${1:-r01d}
 O=gpurun_out
-python bench.py --no-cpu > $O/${R}_bench.json 2> $O/${R}_bench.err || exit 1
+python bench.py > $O/${R}_bench.json 2> $O/${R}_bench.err || exit 1
 python tools/bench_diag.py 3 > $O/${R}_diag.json 2>&1 || exit 1
-for mode in f32 diag; do
+for mode in f64 f32 diag; do
   python tools/profile_loop.py C1-image-like 400 $mode > $O/${R}_loop_$mode.txt 2>&1 || exit 1
   ncu --set full --clock-control none --import-source on -k regex:k_rbd_persistent --launch-skip 1 -c 1 \
       -f -o $O/${R}_prof_$mode python tools/profile_loop.py C1-image-like 400 $mode > $O/${R}_ncu_$mode.log 2>&1
