@@ -147,13 +147,44 @@ __device__ __forceinline__ void sweep_tiles(const double* __restrict__ A, long l
     double acc[KC];
 #pragma unroll
     for (int c = 0; c < KC; ++c) acc[c] = 0.0;
+    const double* vr = (MODE == MODE_DOT) ? v + row0 : nullptr;
+    if (VEC == 2 && MODE == MODE_DOT && rows == kChunk && col0 + KC <= ncols &&
+        lda <= (1LL << 27)) {
+      // full tile (the common case): one base pointer and 32-bit column
+      // offsets keep fewer registers live; same loads and fma order as below
+      const double* A0 = A + col0 * lda + row0;
+      const int ld32 = (int)lda;
+#pragma unroll 1
+      for (int ub = 0; ub < U; ub += UB) {
+        double2 yv[UB];
+        double2 xv[UB][KC];
+#pragma unroll
+        for (int u = 0; u < UB; ++u) {
+          const int e = (tid + (ub + u) * kThreads) * 2;
+          yv[u] = VCOH ? __ldcg(reinterpret_cast<const double2*>(vr + e)) : ld_keep2(vr + e);
+#pragma unroll
+          for (int c = 0; c < KC; ++c) {
+            const double* pc = A0 + (c * ld32 + e);
+            xv[u][c] = ALOAD == LOAD_STREAM ? ld_stream2(pc)
+                       : ALOAD == LOAD_CG   ? __ldcg(reinterpret_cast<const double2*>(pc))
+                                            : ld_keep2(pc);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < UB; ++u)
+#pragma unroll
+          for (int c = 0; c < KC; ++c) {
+            acc[c] = fma(xv[u][c].x, yv[u].x, acc[c]);
+            acc[c] = fma(xv[u][c].y, yv[u].y, acc[c]);
+          }
+      }
+    } else {
     const double* Ac[KC];
 #pragma unroll
     for (int c = 0; c < KC; ++c) {
       const long long cc = (col0 + c < ncols) ? col0 + c : col0;  // clamp (result unused)
       Ac[c] = A + cc * lda + row0;
     }
-    const double* vr = (MODE == MODE_DOT) ? v + row0 : nullptr;
     // Batches of UB element groups; a batch lying entirely inside the matrix
     // takes the vector path, the (at most one) straddling batch the
     // predicated path. Both use the same per-thread fma order, out-of-range
@@ -309,6 +340,7 @@ __device__ __forceinline__ void sweep_tiles(const double* __restrict__ A, long l
         }
       }
     }
+    }   // general path
     // CTA reduction in a fixed order: xor-butterfly in the warp, then warps 0..7.
 #pragma unroll
     for (int c = 0; c < KC; ++c) {
@@ -423,8 +455,11 @@ __device__ __forceinline__ void sweep_tiles_f32(const float* __restrict__ A, lon
     auto ldv = [&](const double* p) {
       return VCOH ? __ldcg(reinterpret_cast<const double2*>(p)) : ld_keep2(p);
     };
-    if (vec4 && rows == kChunk) {
-      // whole tile in range: batches of UB row groups x KC columns in flight
+    if (vec4 && rows == kChunk && col0 + KC <= ncols && lda <= (1LL << 27)) {
+      // whole tile in range: batches of UB row groups x KC columns in flight;
+      // one base pointer and 32-bit column offsets (fewer live registers)
+      const float* A0 = A + col0 * lda + row0;
+      const int ld32 = (int)lda;
 #pragma unroll
       for (int ub = 0; ub < U; ub += UB) {
         float4 xv[UB][KC];
@@ -439,7 +474,7 @@ __device__ __forceinline__ void sweep_tiles_f32(const float* __restrict__ A, lon
             y0[u] = y1[u] = make_double2(0.0, 0.0);
           }
 #pragma unroll
-          for (int c = 0; c < KC; ++c) xv[u][c] = ld_stream4f(Ac[c] + e);
+          for (int c = 0; c < KC; ++c) xv[u][c] = ld_stream4f(A0 + (c * ld32 + e));
         }
 #pragma unroll
         for (int u = 0; u < UB; ++u)
