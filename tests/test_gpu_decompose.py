@@ -433,3 +433,16 @@ def test_host_many_pipelined_equals_single_calls(cuda):
     assert rbd.decompose_many([], d_max=3) == []
     with pytest.raises(rbd.InvalidArgument):
         rbd.decompose_many([xs[0], xs[1][:, :10]], d_max=3)
+
+
+def test_host_many_stops_at_a_failing_matrix(cuda):
+    """A non-finite matrix in the middle of the sequence raises the reference's
+    InvalidArgument (decompose.cpp:57); the uploads still in flight are drained
+    and the context stays usable."""
+    xs = [oracle.random_matrix(500, 30, 900 + i) for i in range(3)]
+    xs[1] = xs[1].copy()
+    xs[1][7, 3] = np.nan
+    with pytest.raises(rbd.InvalidArgument):
+        rbd.decompose_many(xs, d_max=5)
+    ok = rbd.decompose_many([xs[0], xs[2]], d_max=5)
+    assert [g.d for g in ok] == [5, 5]

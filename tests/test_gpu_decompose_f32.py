@@ -185,3 +185,29 @@ def test_f32_host_entry_pinned_outputs_equal_device_entry(cuda):
     b = rbd.decompose(torch.as_tensor(np.ascontiguousarray(X32.T), device=cuda).t(), d_max=d)
     assert a.selected == b.selected
     assert np.array_equal(a.Y, b.Y.cpu().numpy()) and np.array_equal(a.T, b.T.cpu().numpy())
+
+
+@pytest.mark.slow
+def test_c2_f32_prefix_parity(cuda):
+    """C2 (1 048 576 x 4 096) in fp32 storage at full size: the first 8 greedy
+    steps against the fp64 oracle on the fp32-valued matrix."""
+    import torch
+    w = configs.C2
+    Xd = configs.low_rank_matrix_torch(w.m, w.n, 1024, configs.spectrum("C2", 1024), 1e-8,
+                                       w.seed, device=cuda)
+    Xf = Xd.float()
+    del Xd
+    torch.cuda.empty_cache()
+    g = rbd.decompose(Xf, d_max=8)
+    Xh = torch.empty((w.n, w.m), dtype=torch.float32, pin_memory=True)
+    Xh.copy_(Xf.t())
+    del Xf
+    X = Xh.numpy().T.astype(np.float64, order="F")
+    r = oracle.decompose(X, 8, nthreads=os.cpu_count() or 1)
+
+    class P:
+        pass
+    gp = P()
+    gp.Y, gp.T, gp.d = g.Y.cpu().numpy(), g.T.cpu().numpy(), g.d
+    gp.selected, gp.residual_history = g.selected, g.residual_history
+    assert compare(gp, r, X) == 8
