@@ -17,6 +17,8 @@ rng = np.random.default_rng(0)
 for (m, n, d) in [(300, 40, 12), (4097, 33, 20), (33, 5, 5)]:
     x = rng.standard_normal((m, n))
     g = rbd.decompose(x, d_max=d)
+    rbd.decompose(x.astype(np.float32), d_max=d)            # fp32 storage mode
+    rbd.decompose_many([x, x[:, ::-1]], d_max=d)             # pipelined host entry
     rbd.decompose(x, d_max=d, reorthogonalize=True)
     rbd.decompose(x, d_max=d, diag=rng.uniform(0.5, 2.0, m))
     g.compress()
