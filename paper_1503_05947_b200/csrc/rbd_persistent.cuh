@@ -305,6 +305,22 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
   constexpr int kXT = XF32 ? 2 * kCols : kCols;    // columns per X tile (fp32: 128 KB tiles)
   const long long ngt = (n + kXT - 1) / kXT;       // X tile columns
   const long long nx = ngt * S;                    // X tiles
+  // X claim index tx (counted after the Y'w1 groups) -> column group g and
+  // chunk s; used for the tile and for its P1-readiness wait. Group-major; DIAG
+  // puts every group's last chunk at the end instead (measured: weighted loop
+  // 56.4 -> 55.6 ms, identity 46.6 -> 48.3 ms with that order). Claiming the
+  // last G tiles as 2-column halves (a shorter last wave, same bits) measured
+  // slower: 46.3 -> 47.8 ms.
+  auto x_tile = [&](long long tx, long long& g, long long& s) {
+    if (DIAG) {
+      const long long nf = (nx / S) * (S - 1);   // tiles of chunks 0..S-2
+      g = (tx < nf) ? tx / (S - 1) : tx - nf;
+      s = (tx < nf) ? tx - g * (S - 1) : S - 1;
+    } else {
+      g = tx / S;
+      s = tx - g * S;
+    }
+  };
   unsigned dummy_nf = 0, dummy_nz = 0;
   const bool timing = (a.phase_ns != nullptr) && cta == 0 && tid == 0;
   unsigned long long tp = timing ? globaltimer() : 0ull;
@@ -482,7 +498,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
         wait_ge(&a.rdy[0], (unsigned long long)G * ord);
         all_rdy = true;
       } else {
-        const long long sc = (t - gy_) % S;
+        long long gx, sc;
+        x_tile(t - gy_, gx, sc);
         const long long rows = (m - sc * kChunk < kChunk) ? m - sc * kChunk : kChunk;
         wait_ge(&a.rdy[1 + sc], (unsigned long long)rows * ord);
       }
@@ -867,13 +884,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
         // a group's last chunk finalises it after its NEXT tile (deferred), so
         // the siblings are long done and finalisation never piles up at the
         // end of the queue
-        const long long tx = t - gy;
-        // queue order: group-major (a group's chunks back to back); DIAG puts
-        // every group's last chunk at the end instead (measured: weighted loop
-        // 56.4 -> 55.6 ms, identity 46.6 -> 48.3 ms with that order)
-        const long long nf = DIAG ? (nx / S) * (S - 1) : 0;   // tiles of chunks 0..S-2
-        const long long g = !DIAG ? tx / S : (tx < nf) ? tx / (S - 1) : tx - nf;
-        const long long s = !DIAG ? tx - g * S : (tx < nf) ? tx - g * (S - 1) : S - 1;
+        long long g, s;
+        x_tile(t - gy, g, s);
         if constexpr (DIAG && VEC == 2)
           sweep_tile_dot2_sv(a.X, a.ldx, m, n, a.w, a.aw, a.partial, a.partial2, n, s * ngx + g,
                              red2, svec);
