@@ -551,8 +551,15 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
     // tile without waiting; it blocks only when the FIFO is full or the queue
     // is exhausted. Every wait targets an earlier-claimed tile (a sibling
     // chunk, or the Y'w1 groups that precede all X tiles): no cycles.
-    constexpr int kPend = 4;
-    long long pend[kPend] = {-1, -1, -1, -1};
+    // pending-group FIFO depth and when a tile's finalisation attempt runs
+    // (before or after the tile's own group is queued): measured per loop,
+    // C1 fp64 46.3 -> 46.1 ms and weighted 55.8 -> 55.3 ms with (2, after);
+    // the fp32 loop keeps (4, before): 33.8 ms against 34.6 ms
+    constexpr int kPend = XF32 ? 4 : 2;
+    constexpr bool kFinFirst = XF32;
+    long long pend[kPend];
+#pragma unroll
+    for (int i = 0; i < kPend; ++i) pend[i] = -1;
     int npend = 0;
     // the step's published decision, read once per CTA
     bool p_ready = false;
@@ -901,13 +908,14 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
                                                          dummy_nz);
         mark(7);
         if (DIAG) yay_slices(false);   // this CTA's share of the YAY row, once decided
-        if (npend > 0) finalize_pass(false);
+        if (kFinFirst && npend > 0) finalize_pass(false);
         if (s == S - 1) {
           constexpr int per = kXT / kCols;   // finalisation groups this tile completes
           if (npend > kPend - per) finalize_pass(true);   // retire the two oldest
           for (int h = 0; h < per; ++h)
             if (g * per + h < ngx) pend[npend++] = g * per + h;
         }
+        if (!kFinFirst && npend > 0) finalize_pass(false);
         trace(k, 5);
       }
     }
