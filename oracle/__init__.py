@@ -50,6 +50,11 @@ def lib():
         L.orc_decompose_steps.argtypes = [P, I64, I64, I64, I64, D, I, I64, C.c_uint64, I, D, I, I64,
                                           P, P, P, P, P]
         L.orc_decompose_steps.restype = I
+        L.orc_decompose_ex.argtypes = [P, I64, I64, I64, I64, D, I, I64, C.c_uint64, I, D, I, I64,
+                                       I, P, P, P, P, P, P, P]
+        L.orc_decompose_ex.restype = I
+        L.orc_column_pass.argtypes = [P, I64, I64, I64, I, P, P, P]
+        L.orc_gemv_t.argtypes = [P, I64, I64, I64, P, P, I]
         L.orc_mgs_project.argtypes = [P, I64, P, I64, I64, D, I, P, P]
         L.orc_mgs_project.restype = I
         L.orc_ws_init.argtypes = [P, I64, I64, I64]
@@ -102,13 +107,18 @@ class OracleModel:
     selected: List[int]
     residual_history: List[float]
     d: int = 0
+    t_init_s: float = 0.0         # validation + workspace_init wall time
+    t_loop_s: float = 0.0         # greedy loop wall time
 
 
 def decompose(x, d_max: int, eps_r: float = 0.0, start_column: int = 0,
               start_seed: Optional[int] = None, reorthogonalize: bool = False,
               breakdown_tol: float = -1.0, nthreads: int = 1,
-              max_steps: Optional[int] = None, diag=None) -> OracleModel:
-    """rbd::decompose restated (decompose.cpp:53-111); diag = WeightSpec::diagonal."""
+              max_steps: Optional[int] = None, diag=None, x_passes: int = 2) -> OracleModel:
+    """rbd::decompose restated (decompose.cpp:53-111); diag = WeightSpec::diagonal.
+
+    x_passes=2 keeps the reference's two X passes per step (decompose.cpp:93,
+    workspace.cpp:51); 1 reuses the first pass (same bits, half the time)."""
     xa = np.asfortranarray(np.asarray(x, dtype=np.float64))
     m, n = xa.shape if xa.ndim == 2 else (0, 0)
     cap = max(1, min(int(d_max), max(n, 1)))
@@ -120,6 +130,7 @@ def decompose(x, d_max: int, eps_r: float = 0.0, start_column: int = 0,
     steps = int(max_steps if max_steps is not None else 2**62)
     seed = int(start_seed or 0) & 0xFFFFFFFFFFFFFFFF
     kind = 1 if start_seed is not None else 0
+    ti, tl = C.c_double(), C.c_double()
     if diag is not None:
         dg = np.ascontiguousarray(np.asarray(diag, dtype=np.float64).reshape(-1))
         rc = lib().orc_decompose_diag(
@@ -127,15 +138,109 @@ def decompose(x, d_max: int, eps_r: float = 0.0, start_column: int = 0,
             float(eps_r), kind, int(start_column), seed, 1 if reorthogonalize else 0,
             float(breakdown_tol), steps, _p(Y), _p(T), _p(sel), _p(hist), C.byref(d))
     else:
-        rc = lib().orc_decompose_steps(
+        rc = lib().orc_decompose_ex(
             _p(xa), m, n, max(m, 1), int(d_max), float(eps_r), kind, int(start_column), seed,
             1 if reorthogonalize else 0, float(breakdown_tol), int(nthreads), steps,
-            _p(Y), _p(T), _p(sel), _p(hist), C.byref(d))
+            int(x_passes), _p(Y), _p(T), _p(sel), _p(hist), C.byref(d), C.byref(ti), C.byref(tl))
     if rc != ORC_OK:
         raise OracleError(rc, lib().orc_last_error().decode())
     k = d.value
     return OracleModel(Y[:, :k].copy(order="F"), T[:k, :n].copy(), [int(s) for s in sel[:k]],
-                       [float(h) for h in hist[:k]], k)
+                       [float(h) for h in hist[:k]], k, ti.value, tl.value)
+
+
+def decompose_blocked(get_block, blocks, m: int, n: int, d_max: int, eps_r: float = 0.0,
+                      start_column: int = 0, nthreads: int = 1,
+                      max_steps: Optional[int] = None, get_column=None) -> OracleModel:
+    """rbd::decompose (decompose.cpp:53-111, identity weight, fixed start
+    column, default config) over an X that is only available in column blocks:
+    ``blocks`` is a list of (col_offset, n_cols) covering [0, n) in order and
+    ``get_block(i)`` returns block i as an m x n_cols column-major float64
+    array (``get_column(j)``, optional, column j alone). Each greedy step streams every block once (the reference's two
+    passes per step compute identical values, so the second is reused). Used
+    for config 3 (128 GiB of X) by the parity tests; the arithmetic is the
+    whole-matrix oracle's (per-column dot8 sums, the same mgs_project)."""
+    L = lib()
+    steps = int(max_steps if max_steps is not None else 2**62)
+    # ---- validation (decompose.cpp:56-64) and workspace_init (workspace.cpp:21-23) ----
+    if m < 1 or n < 1:
+        raise OracleError(1, "decompose: matrix must be non-empty")
+    sq = np.zeros(n)
+    fin, zero = True, True
+    for b, (o, nb) in enumerate(blocks):
+        xb = get_block(b)
+        f, z = C.c_int(), C.c_int()
+        L.orc_column_pass(_p(xb), m, nb, xb.strides[1] // 8, int(nthreads),
+                          _p(sq[o:o + nb]), C.byref(f), C.byref(z))
+        fin, zero = fin and bool(f.value), zero and bool(z.value)
+    if not fin:
+        raise OracleError(1, "decompose: matrix has non-finite entries")
+    if d_max < 1 or d_max > n:
+        raise OracleError(1, "decompose: d_max must satisfy 1 <= d_max <= n")
+    if not eps_r >= 0.0:
+        raise OracleError(1, "decompose: eps_R must be >= 0")
+    if zero:
+        raise OracleError(3, "decompose: zero matrix, no basis can be built")
+    max_col_norm = float(np.sqrt(sq).max())                                 # :70
+    noise_floor = max_col_norm * np.sqrt(float(m)) * np.finfo(np.float64).eps * 16.0
+    breakdown_tol = max(eps_r, noise_floor)                                  # :73-74
+    col_sq = np.maximum(sq, 0.0)                                             # workspace.cpp:37
+    residual = col_sq.copy()
+    if not 0 <= start_column < n:
+        raise OracleError(4, "start column index out of range")
+    i = int(start_column)
+    cap = min(int(d_max), steps)
+    Y = np.zeros((m, max(cap, 1)), order="F")
+    T = np.zeros((max(cap, 1), n))
+    sel, hist = [], []
+    d = 0
+    e_cur = np.inf
+
+    def column(j):
+        if get_column is not None:
+            return np.ascontiguousarray(get_column(j), dtype=np.float64)
+        for b, (o, nb) in enumerate(blocks):
+            if o <= j < o + nb:
+                return np.ascontiguousarray(get_block(b)[:, j - o])
+        raise IndexError(j)
+
+    xi = np.zeros(m)
+    nrm = C.c_double()
+    while d < d_max and e_cur > eps_r and d < steps:                         # :87
+        v = column(i)
+        ok = L.orc_mgs_project(_p(v), m, _p(Y), d, m, float(breakdown_tol), 0, _p(xi),
+                               C.byref(nrm))
+        if not ok:
+            break                                                            # :90
+        Y[:, d] = xi                                                         # :92
+        for b, (o, nb) in enumerate(blocks):                                 # :93
+            xb = get_block(b)
+            L.orc_gemv_t(_p(xb), m, nb, xb.strides[1] // 8, _p(xi), _p(T[d, o:o + nb]),
+                         int(nthreads))
+        sel.append(i)
+        residual = np.maximum(residual - T[d] * T[d], 0.0)                   # workspace.cpp:52-53
+        d += 1
+        arg = int(np.argmax(residual))            # strict '>' scan from j = 0 (workspace.cpp:107-113)
+        best = float(residual[arg])
+        e_cur = float(np.sqrt(best if best > 0.0 else 0.0))
+        hist.append(e_cur)
+        i = arg
+    if d == 0:
+        raise OracleError(3, "decompose: start column is numerically zero, no basis built")
+    out = OracleModel(Y[:, :d].copy(order="F"), T[:d].copy(), sel, hist, d)
+    out.col_sq = col_sq
+    return out
+
+
+def column_sq(x, nthreads: int = 1) -> np.ndarray:
+    """||x_j||^2 per column in the oracle's dot8 order (workspace.cpp:22)."""
+    xa = np.asfortranarray(np.asarray(x, dtype=np.float64))
+    m, n = xa.shape
+    out = np.zeros(n)
+    f, z = C.c_int(), C.c_int()
+    lib().orc_column_pass(_p(xa), m, n, xa.strides[1] // 8 if n > 1 else m, int(nthreads),
+                          _p(out), C.byref(f), C.byref(z))
+    return out
 
 
 def mgs_project(v, basis, breakdown_tol: float, reorthogonalize: bool = False):

@@ -15,6 +15,7 @@
 #include <limits>
 #include <random>
 #include <string>
+#include <ctime>
 #include <vector>
 
 #ifdef _OPENMP
@@ -91,34 +92,60 @@ int64_t orc_seeded_start(uint64_t seed, int64_t n) {
   return static_cast<int64_t>(std::uniform_int_distribution<long>(0, static_cast<long>(n) - 1)(rng));
 }
 
-int orc_decompose_steps(const double* X, int64_t m, int64_t n, int64_t ldx, int64_t d_max,
-                        double eps_R, int start_kind, int64_t start_column,
-                        uint64_t start_seed, int reorthogonalize, double cfg_breakdown_tol,
-                        int nthreads, int64_t max_steps, double* Y, double* T,
-                        int64_t* selected, double* history, int64_t* d_out) {
-  // ---- validation, decompose.cpp:56-64 (same order) ----
+// Column pass shared by validation and workspace_init: sq[j] = ||x_j||^2 in
+// dot8 order (the value decompose.cpp:70 takes the root of and
+// workspace.cpp:22 stores), plus the allFinite (decompose.cpp:57) and
+// all-zero (:63-64) flags. Per-column results do not depend on nthreads.
+static void column_pass(const double* X, int64_t m, int64_t n, int64_t ldx, int nthreads,
+                        double* sq, int* all_finite, int* all_zero) {
+  int fin = 1, zero = 1;
+#ifdef _OPENMP
+#pragma omp parallel for num_threads(nthreads) schedule(static) reduction(&& : fin, zero) if (nthreads > 1)
+#endif
+  for (int64_t j = 0; j < n; ++j) {
+    const double* x = X + j * ldx;
+    bool f = true, z = true;
+    for (int64_t i = 0; i < m; ++i) {
+      f = f && std::isfinite(x[i]);
+      z = z && x[i] == 0.0;
+    }
+    fin = fin && f;
+    zero = zero && z;
+    sq[j] = sqnorm(x, m);
+  }
+  *all_finite = fin;
+  *all_zero = zero;
+  (void)nthreads;
+}
+
+static double now_s() {
+  timespec ts;
+  clock_gettime(CLOCK_MONOTONIC, &ts);
+  return static_cast<double>(ts.tv_sec) + 1e-9 * static_cast<double>(ts.tv_nsec);
+}
+
+int orc_decompose_ex(const double* X, int64_t m, int64_t n, int64_t ldx, int64_t d_max,
+                     double eps_R, int start_kind, int64_t start_column, uint64_t start_seed,
+                     int reorthogonalize, double cfg_breakdown_tol, int nthreads,
+                     int64_t max_steps, int x_passes, double* Y, double* T, int64_t* selected,
+                     double* history, int64_t* d_out, double* t_init_s, double* t_loop_s) {
+  const double t0 = now_s();
+  // ---- validation, decompose.cpp:56-64 (same order; the column flags are
+  //      computed in one pass and reported in the reference's order) ----
   if (m < 1 || n < 1) return fail(ORC_INVALID_ARGUMENT, "decompose: matrix must be non-empty");
-  for (int64_t j = 0; j < n; ++j)
-    for (int64_t i = 0; i < m; ++i)
-      if (!std::isfinite(X[i + j * ldx]))
-        return fail(ORC_INVALID_ARGUMENT, "decompose: matrix has non-finite entries");
+  std::vector<double> sq(n);
+  int all_finite = 1, all_zero = 1;
+  column_pass(X, m, n, ldx, nthreads, sq.data(), &all_finite, &all_zero);
+  if (!all_finite) return fail(ORC_INVALID_ARGUMENT, "decompose: matrix has non-finite entries");
   if (d_max < 1 || d_max > n)
     return fail(ORC_INVALID_ARGUMENT, "decompose: d_max must satisfy 1 <= d_max <= n");
   if (!(eps_R >= 0.0)) return fail(ORC_INVALID_ARGUMENT, "decompose: eps_R must be >= 0");
   // identity weight is always compatible (weight.cpp:71-74)
-  bool all_zero = true;
-  for (int64_t j = 0; j < n && all_zero; ++j)
-    for (int64_t i = 0; i < m; ++i)
-      if (X[i + j * ldx] != 0.0) {
-        all_zero = false;
-        break;
-      }
   if (all_zero) return fail(ORC_DEGENERATE_INPUT, "decompose: zero matrix, no basis can be built");
 
   // ---- noise floor / breakdown tolerance, decompose.cpp:70-74 ----
   double max_col_norm = 0.0;
-  for (int64_t j = 0; j < n; ++j)
-    max_col_norm = std::max(max_col_norm, std::sqrt(sqnorm(X + j * ldx, m)));
+  for (int64_t j = 0; j < n; ++j) max_col_norm = std::max(max_col_norm, std::sqrt(sq[j]));
   const double noise_floor =
       max_col_norm * std::sqrt(static_cast<double>(m)) * std::numeric_limits<double>::epsilon() * 16.0;
   const double breakdown_tol =
@@ -127,7 +154,7 @@ int orc_decompose_steps(const double* X, int64_t m, int64_t n, int64_t ldx, int6
   // ---- workspace_init (identity), workspace.cpp:21-23,36-40 ----
   std::vector<double> col_sq(n), residual_sq(n);
   for (int64_t j = 0; j < n; ++j) {
-    col_sq[j] = std::max(sqnorm(X + j * ldx, m), 0.0);
+    col_sq[j] = std::max(sq[j], 0.0);
     residual_sq[j] = col_sq[j];
   }
 
@@ -140,6 +167,7 @@ int orc_decompose_steps(const double* X, int64_t m, int64_t n, int64_t ldx, int6
   } else {
     i = orc_seeded_start(start_seed, n);
   }
+  const double t1 = now_s();
 
   int64_t d = 0;
   double e_cur = std::numeric_limits<double>::infinity();
@@ -153,10 +181,17 @@ int orc_decompose_steps(const double* X, int64_t m, int64_t n, int64_t ldx, int6
     gemv_t(X, m, n, ldx, xi.data(), row.data(), nthreads);  // :93 T.row(d) = xi' X
     std::memcpy(T + d * n, row.data(), sizeof(double) * n);
     selected[d] = i;                                      // :94
-    // workspace_extend identity, workspace.cpp:50-53: second X pass
-    gemv_t(X, m, n, ldx, xi.data(), row2.data(), nthreads);
+    // workspace_extend identity, workspace.cpp:50-53: the reference's second X
+    // pass (x_passes == 2). It recomputes the same values with the same
+    // summation order, so x_passes == 1 (parity tests at config scale) reuses
+    // `row` and gives identical bits at half the CPU time.
+    const double* r2 = row.data();
+    if (x_passes != 1) {
+      gemv_t(X, m, n, ldx, xi.data(), row2.data(), nthreads);
+      r2 = row2.data();
+    }
     for (int64_t j = 0; j < n; ++j) {
-      residual_sq[j] -= row2[j] * row2[j];
+      residual_sq[j] -= r2[j] * r2[j];
       residual_sq[j] = std::max(residual_sq[j], 0.0);
     }
     ++d;                                                  // :96
@@ -172,10 +207,35 @@ int orc_decompose_steps(const double* X, int64_t m, int64_t n, int64_t ldx, int6
     history[d - 1] = e_cur;                               // :99
     i = arg;                                              // :101
   }
+  if (t_init_s) *t_init_s = t1 - t0;
+  if (t_loop_s) *t_loop_s = now_s() - t1;
   if (d == 0)
     return fail(ORC_DEGENERATE_INPUT, "decompose: start column is numerically zero, no basis built");
   *d_out = d;
   return ORC_OK;
+}
+
+int orc_decompose_steps(const double* X, int64_t m, int64_t n, int64_t ldx, int64_t d_max,
+                        double eps_R, int start_kind, int64_t start_column,
+                        uint64_t start_seed, int reorthogonalize, double cfg_breakdown_tol,
+                        int nthreads, int64_t max_steps, double* Y, double* T,
+                        int64_t* selected, double* history, int64_t* d_out) {
+  return orc_decompose_ex(X, m, n, ldx, d_max, eps_R, start_kind, start_column, start_seed,
+                          reorthogonalize, cfg_breakdown_tol, nthreads, max_steps, 2, Y, T,
+                          selected, history, d_out, nullptr, nullptr);
+}
+
+// Pieces of the same loop for a caller that streams X in column blocks (the
+// config-3 parity test: 128 GiB of X never sits in host memory at once). The
+// caller restates decompose.cpp:53-111 around them; every value is the one the
+// whole-matrix loop computes (per-column sums only, same dot8 order).
+void orc_column_pass(const double* X, int64_t m, int64_t n, int64_t ldx, int nthreads, double* sq,
+                     int* all_finite, int* all_zero) {
+  column_pass(X, m, n, ldx, nthreads, sq, all_finite, all_zero);
+}
+void orc_gemv_t(const double* X, int64_t m, int64_t n, int64_t ldx, const double* xi, double* row,
+                int nthreads) {
+  gemv_t(X, m, n, ldx, xi, row, nthreads);
 }
 
 int orc_decompose(const double* X, int64_t m, int64_t n, int64_t ldx, int64_t d_max,
@@ -413,20 +473,63 @@ void orc_reconstruct(const double* Y, int64_t m, int64_t d, const double* c, dou
 }
 // Batched out-of-sample projection: Tn (d x N, column-major ld d) = Y' Xn and
 // err_j = max(||x_j||^2 - ||t_j||^2, 0) (identity Eq.(3), workspace.cpp:88-97).
+// Every Tn[k, j] is dot8(Y[:, k], x_j, m) — the per-vector project of
+// decompose.cpp:113-117 — with the same 8 lane sums accumulated in the same row
+// order; the loops are only tiled (row chunks x basis blocks x column blocks,
+// lane sums carried across chunks) so that a config-4 batch (65536 x 16384
+// against d = 512) finishes in seconds instead of re-reading Y per column.
 void orc_project_batch(const double* Y, int64_t m, int64_t d, const double* Xn, int64_t N,
                        int64_t ldx, int nthreads, double* Tn, double* err) {
+  constexpr int64_t JB = 32;    // columns per task
+  constexpr int64_t KB = 128;    // basis vectors per task
+  constexpr int64_t RC = 2048;  // rows per chunk (multiple of 8)
+  const int64_t m8 = m - (m % 8);
+  const int64_t nj = (N + JB - 1) / JB, nk = (d + KB - 1) / KB;
+#ifdef _OPENMP
+#pragma omp parallel for num_threads(nthreads) schedule(dynamic, 1) if (nthreads > 1)
+#endif
+  for (int64_t task = 0; task < nj * nk; ++task) {
+    const int64_t j0 = (task / nk) * JB, k0 = (task % nk) * KB;
+    const int64_t jn = std::min(JB, N - j0), kn = std::min(KB, d - k0);
+    std::vector<double> acc(static_cast<size_t>(KB * JB * 8), 0.0);
+    for (int64_t r0 = 0; r0 < m8; r0 += RC) {
+      const int64_t r1 = std::min(m8, r0 + RC);
+      for (int64_t jj = 0; jj < jn; ++jj) {
+        const double* x = Xn + (j0 + jj) * ldx;
+        for (int64_t kk = 0; kk < kn; ++kk) {
+          const double* y = Y + (k0 + kk) * m;
+          double* s = acc.data() + (kk * JB + jj) * 8;
+          double t[8];
+          for (int l = 0; l < 8; ++l) t[l] = s[l];
+          for (int64_t i = r0; i < r1; i += 8)
+            for (int l = 0; l < 8; ++l) t[l] += y[i + l] * x[i + l];
+          for (int l = 0; l < 8; ++l) s[l] = t[l];
+        }
+      }
+    }
+    for (int64_t jj = 0; jj < jn; ++jj) {
+      const double* x = Xn + (j0 + jj) * ldx;
+      for (int64_t kk = 0; kk < kn; ++kk) {
+        const double* y = Y + (k0 + kk) * m;
+        const double* s = acc.data() + (kk * JB + jj) * 8;
+        double tail = 0.0;
+        for (int64_t i = m8; i < m; ++i) tail += y[i] * x[i];
+        Tn[(k0 + kk) + (j0 + jj) * d] =
+            (((s[0] + s[4]) + (s[1] + s[5])) + ((s[2] + s[6]) + (s[3] + s[7]))) + tail;
+      }
+    }
+  }
 #ifdef _OPENMP
 #pragma omp parallel for num_threads(nthreads) schedule(static) if (nthreads > 1)
 #endif
   for (int64_t j = 0; j < N; ++j) {
-    const double* x = Xn + j * ldx;
+    if (!err) continue;
     double tt = 0.0;
     for (int64_t k = 0; k < d; ++k) {
-      const double t = dot8(Y + k * m, x, m);
-      Tn[k + j * d] = t;
+      const double t = Tn[k + j * d];
       tt += t * t;
     }
-    const double e = sqnorm(x, m) - tt;
+    const double e = sqnorm(Xn + j * ldx, m) - tt;
     err[j] = e > 0.0 ? e : 0.0;
   }
   (void)nthreads;

@@ -58,6 +58,25 @@ int orc_decompose_steps(const double* X, int64_t m, int64_t n, int64_t ldx, int6
                         int nthreads, int64_t max_steps, double* Y, double* T,
                         int64_t* selected, double* history, int64_t* d_out);
 
+/* Same loop with the options the config-scale parity tests and the CPU
+ * baseline need: x_passes = 2 is the reference's two X passes per step
+ * (decompose.cpp:93 and workspace.cpp:51); 1 reuses the first pass's values
+ * (identical bits, half the CPU time). t_init_s / t_loop_s (may be NULL): wall
+ * time of validation + workspace_init and of the greedy loop. */
+int orc_decompose_ex(const double* X, int64_t m, int64_t n, int64_t ldx, int64_t d_max,
+                     double eps_R, int start_kind, int64_t start_column, uint64_t start_seed,
+                     int reorthogonalize, double breakdown_tol, int nthreads, int64_t max_steps,
+                     int x_passes, double* Y, double* T, int64_t* selected, double* history,
+                     int64_t* d_out, double* t_init_s, double* t_loop_s);
+
+/* Column-block pieces of the same loop (for X streamed in blocks):
+ * sq[j] = ||x_j||^2 (dot8 order) with the allFinite / all-zero flags, and
+ * row[j] = xi . x_j. */
+void orc_column_pass(const double* X, int64_t m, int64_t n, int64_t ldx, int nthreads, double* sq,
+                     int* all_finite, int* all_zero);
+void orc_gemv_t(const double* X, int64_t m, int64_t n, int64_t ldx, const double* xi, double* row,
+                int nthreads);
+
 /* rbd::decompose with WeightSpec::diagonal(diag) (decompose.cpp:53-111,
  * weight.cpp:11-21, workspace.cpp:24-29,61-99,114-122). Single-threaded;
  * Y/T/selected/history as orc_decompose. */

@@ -60,6 +60,17 @@ def _host_outputs(m: int, n: int, cap: int):
             np.zeros((cap, n), dtype=np.float64))
 
 
+F32_MAX_D = 4096   # the persistent loop's limit (kFMaxCoef, csrc/rbd_device.cuh)
+
+
+def _auto_storage(x, d_max, identity: bool) -> str:
+    dt = getattr(x, "dtype", None)
+    is32 = dt in ((torch.float32,) if torch is not None else ()) + (np.float32,)
+    if is32 and identity and int(d_max) <= F32_MAX_D and os.environ.get("RBD_PATH", "") != "graph":
+        return "f32"
+    return "f64"
+
+
 def make_config(d_max: int, eps_r: float = 0.0, start_column: int = 0,
                 reorthogonalize: bool = False, breakdown_tol: float = -1.0,
                 start_seed: Optional[int] = None, diag=None, sparse=None) -> Config:
@@ -168,7 +179,10 @@ def decompose(x, d_max: int, eps_r: float = 0.0, diag=None, sparse=None, start_c
 
     numpy input: end-to-end host entry (rbd_decompose_host).
     torch CUDA input: device-resident entry (rbd_decompose_device).
-    storage: "f64" or "f32" (default: "f32" for float32 input, else "f64").
+    storage: "f64" or "f32". Default: "f32" for float32 input when the fp32
+    mode applies (identity weight, persistent loop: d_max <= 4096 and
+    RBD_PATH unset), else "f64" — float32 input is widened exactly, as the
+    reference's binding converts it to a double Matrix.
     "f32" keeps X in fp32 on the device (rbd_decompose_*_f32: half the bytes
     per sweep, fp64 arithmetic on the fp32 values; identity weight only).
     forced_selection: parity-test instrumentation; follow this
@@ -183,9 +197,7 @@ def decompose(x, d_max: int, eps_r: float = 0.0, diag=None, sparse=None, start_c
         finally:
             ctx.force_selection(None)
     if storage is None:
-        dt = getattr(x, "dtype", None)
-        storage = "f32" if dt in ((torch.float32,) if torch is not None else ()) + (np.float32,) \
-            else "f64"
+        storage = _auto_storage(x, d_max, diag is None and sparse is None)
     if storage not in ("f32", "f64"):
         raise InvalidArgument("decompose: storage must be 'f32' or 'f64'")
     f32 = storage == "f32"
@@ -255,7 +267,7 @@ def decompose_many(xs, d_max: int, eps_r: float = 0.0, start_column: int = 0,
     if not xs:
         return []
     if storage is None:
-        storage = "f32" if all(getattr(x, "dtype", None) == np.float32 for x in xs) else "f64"
+        storage = "f32" if all(_auto_storage(x, d_max, True) == "f32" for x in xs) else "f64"
     if storage not in ("f32", "f64"):
         raise InvalidArgument("decompose: storage must be 'f32' or 'f64'")
     f32 = storage == "f32"

@@ -160,3 +160,44 @@ def low_rank_shard_torch(m: int, n: int, rank: int, s, noise_var: float, seed: i
         Xt[lo - col_offset:hi - col_offset] = blk
     del U, V
     return Xt.t()
+
+
+# ---- config 4: the RBD stage and the out-of-sample stream ----
+C4_RANK = 512
+C4_BATCH = 16384
+C4_NEW_COLUMNS = 262144
+
+
+def c4_stage_matrix(device="cuda"):
+    """The C4 RBD stage (65536 x 8192, rank 512, s_i = 2^(-i/4), N(0,1e-6)) — the
+    same X as ``low_rank_matrix_torch`` builds for bench / tools."""
+    w = C4
+    return low_rank_matrix_torch(w.m, w.n, C4_RANK, spectrum("C4", C4_RANK), 1e-6, w.seed,
+                                 device=device)
+
+
+def c4_basis(device="cuda"):
+    """U (m x 512) and s of the C4 low-rank model (the first draws of the seed-4
+    generator, as in low_rank_matrix_torch)."""
+    import torch
+    g = torch.Generator(device=device)
+    g.manual_seed(C4.seed)
+    U = torch.linalg.qr(torch.randn(C4.m, C4_RANK, dtype=torch.float64, device=device,
+                                    generator=g))[0]
+    s = torch.as_tensor(spectrum("C4", C4_RANK), device=device)
+    return U, s
+
+
+def c4_new_batch(U, s, b: int, batch: int = C4_BATCH, device="cuda"):
+    """Out-of-sample batch b of C4: x = U diag(s) g + e with g ~ N(0, I)/sqrt(8192)
+    (the stage's column distribution) and e ~ N(0, 1e-6); column-major m x batch.
+    Each batch has its own generator keyed by (seed, b), so any batch can be
+    regenerated alone."""
+    import torch
+    g = torch.Generator(device=device)
+    g.manual_seed(C4.seed * 1000003 + 7919 + b)
+    coef = torch.randn(batch, C4_RANK, dtype=torch.float64, device=device, generator=g)
+    coef /= float(np.sqrt(C4.n))
+    Xt = (coef * s) @ U.t()                                   # batch x m == X col-major
+    Xt += 1e-3 * torch.randn(Xt.shape, dtype=torch.float64, device=device, generator=g)
+    return Xt.t()

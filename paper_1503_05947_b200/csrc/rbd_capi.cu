@@ -623,7 +623,7 @@ int get_step_graph(rbd_ctx_t ctx, const LoopBufs& L) {
 // Validation shared by the single- and multi-GPU entries: reference order of
 // decompose.cpp:56-64 after the K1 flags are known.
 int validate_after_init(const rbd_config_t* cfg, long long m, long long n, const DevState& hs,
-                        bool diag_supplied) {
+                        bool diag_supplied, double diag_max) {
   if (hs.flags_nonfinite)
     return set_err(RBD_ERR_INVALID_ARGUMENT, "decompose: matrix has non-finite entries");
   if (cfg->d_max < 1 || cfg->d_max > n)
@@ -641,6 +641,23 @@ int validate_after_init(const rbd_config_t* cfg, long long m, long long n, const
   }
   if (!hs.flags_nonzero)
     return set_err(RBD_ERR_DEGENERATE_INPUT, "decompose: zero matrix, no basis can be built");
+  // A finite X whose largest column norm overflows (entries beyond ~1e154):
+  // in the reference max_col_norm = inf makes breakdown_tol = inf
+  // (decompose.cpp:70-74), so the first mgs_project breaks down and the call
+  // ends in DegenerateInput (:104-105). Stop here with that outcome: the
+  // device loop would otherwise meet inf - inf = NaN dot products, and its
+  // chunk partials use NaN to mean "not written yet".
+  double max_colsq;
+  std::memcpy(&max_colsq, &hs.max_colsq_bits, sizeof(double));
+  if (!std::isfinite(max_colsq))
+    return set_err(RBD_ERR_DEGENERATE_INPUT,
+                   "decompose: start column is numerically zero, no basis built "
+                   "(max column norm overflows, breakdown tolerance is inf)");
+  // Weighted sums a_i x_ij y_i (workspace.cpp:24-29,61-79) stay finite when
+  // max_i a_i * max_j ||x_j||^2 does (Cauchy-Schwarz with ||y|| <= ||x||).
+  if (diag_max > 0.0 && !std::isfinite(diag_max * max_colsq))
+    return set_err(RBD_ERR_INVALID_ARGUMENT,
+                   "decompose: weighted column norms overflow (max a_i * max ||x_j||^2 is not finite)");
   return RBD_OK;
 }
 
@@ -828,7 +845,7 @@ namespace {
 int decompose_device_impl(rbd_ctx_t ctx, const double* dX, int64_t m, int64_t n, int64_t ldx,
                           const rbd_config_t* cfg, const double* diag, double* dY, double* dT,
                           int64_t* h_selected, double* h_history, rbd_result_t* result,
-                          const float* dXf = nullptr) {
+                          const float* dXf = nullptr, double diag_max = 0.0) {
   if (!ctx || !cfg) return set_err(RBD_ERR_INVALID_ARGUMENT, "decompose: null context/config");
   if (m < 1 || n < 1) return set_err(RBD_ERR_INVALID_ARGUMENT, "decompose: matrix must be non-empty");
   if (ldx < m) return set_err(RBD_ERR_DIMENSION_MISMATCH, "decompose: ldx < m");
@@ -883,7 +900,7 @@ int decompose_device_impl(rbd_ctx_t ctx, const double* dX, int64_t m, int64_t n,
     cudaEventElapsedTime(&t, ev0, ev1);
     init_ms = t;
   }
-  TRY(validate_after_init(cfg, m, n, hs, diag != nullptr));
+  TRY(validate_after_init(cfg, m, n, hs, diag != nullptr, diag ? diag_max : 0.0));
   double max_colsq;
   {
     unsigned long long b = hs.max_colsq_bits;
@@ -1085,8 +1102,9 @@ int rbd_decompose_diag_device(rbd_ctx_t ctx, const double* dX, int64_t m, int64_
     return decompose_device_impl(ctx, dX, m, n, ldx, &c, nullptr, dY, dT, h_selected, h_history,
                                  result);
   }
+  const double diag_max = *std::max_element(h.begin(), h.end());
   return decompose_device_impl(ctx, dX, m, n, ldx, &c, d_diag, dY, dT, h_selected, h_history,
-                               result);
+                               result, nullptr, diag_max);
 }
 
 namespace {

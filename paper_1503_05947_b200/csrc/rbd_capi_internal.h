@@ -181,7 +181,7 @@ size_t persist_smem(long long dcap, bool diag = false);
 int persistent_grid(rbd_ctx_t ctx, int vec, long long d_max, bool diag = false, bool xf32 = false);
 int ensure_loop_buffers(rbd_ctx_t ctx, long long m, long long n, long long d_max);
 int validate_after_init(const rbd_config_t* cfg, long long m, long long n, const DevState& hs,
-                        bool diag_supplied = false);
+                        bool diag_supplied = false, double diag_max = 0.0);
 int start_column(const rbd_config_t* cfg, long long n, long long* out);
 double breakdown_tolerance(const rbd_config_t* cfg, long long m, double max_colsq);
 int check_diagonal(const double* h, int64_t len);

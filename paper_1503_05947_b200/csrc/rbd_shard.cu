@@ -190,8 +190,11 @@ int sharded_decompose(std::vector<rbd_ctx_t>& R, Exchange& ex, std::vector<Shard
   for (int w = 0; w < ex.world(); ++w) {
     hs.flags_nonfinite |= all[4 * w] != 0.0;
     hs.flags_nonzero |= all[4 * w + 1] != 0.0;
-    max_colsq = std::max(max_colsq, all[4 * w + 2]);
+    const double v = all[4 * w + 2];
+    max_colsq = (std::isfinite(v) && std::isfinite(max_colsq)) ? std::max(max_colsq, v)
+                                                               : INFINITY;
   }
+  std::memcpy(&hs.max_colsq_bits, &max_colsq, sizeof(double));
   TRY(validate_after_init(cfg, m, n_global, hs));
   const double tol = breakdown_tolerance(cfg, m, max_colsq);
   long long j0 = 0;

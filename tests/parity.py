@@ -26,10 +26,12 @@ from __future__ import annotations
 import numpy as np
 
 
-def running_residuals(X: np.ndarray, T: np.ndarray):
-    """Oracle-side residual_sq after each step (workspace.cpp:52-53)."""
-    col_sq = np.einsum("ij,ij->j", X, X)
-    r = col_sq.copy()
+def running_residuals(X: np.ndarray, T: np.ndarray, col_sq=None):
+    """Oracle-side residual_sq after each step (workspace.cpp:52-53). col_sq
+    (||x_j||^2) may be given instead of X (X streamed in blocks)."""
+    if col_sq is None:
+        col_sq = np.einsum("ij,ij->j", X, X)
+    r = np.asarray(col_sq, dtype=np.float64).copy()
     out = []
     for k in range(T.shape[0]):
         r = np.maximum(r - T[k] * T[k], 0.0)
@@ -56,16 +58,18 @@ def top2_gap(r: np.ndarray) -> float:
 
 
 def compare(gpu, ref, X, tol: float = 1e-10, tau: float = 1e-12, require_same_d: bool = True,
-            diag=None, rerun=None):
+            diag=None, rerun=None, col_sq=None):
     """Returns the number of steps compared; raises AssertionError on mismatch.
 
     rerun: optional callable(selected) -> gpu model. After an admissible
     divergence the B200 loop is re-run on the oracle's selection (forced-selection
-    mode, rbd_set_forced_selection) and compared over all steps."""
-    X = np.asarray(X, dtype=np.float64)
+    mode, rbd_set_forced_selection) and compared over all steps.
+    col_sq: ||x_j||^2 in place of X (identity weight; X too large for the host)."""
+    if col_sq is None:
+        X = np.asarray(X, dtype=np.float64)
     gY = np.asarray(gpu.Y.cpu() if hasattr(gpu.Y, "cpu") else gpu.Y)
     gT = np.asarray(gpu.T.cpu() if hasattr(gpu.T, "cpu") else gpu.T)
-    col_sq, rsteps = running_residuals(X, ref.T)
+    col_sq, rsteps = running_residuals(X, ref.T, col_sq)
     colnorm = np.sqrt(col_sq)
     if diag is None:
         sel_sq, ssteps = col_sq, rsteps
@@ -86,7 +90,7 @@ def compare(gpu, ref, X, tol: float = 1e-10, tau: float = 1e-12, require_same_d:
     if upto < d_cmp and rerun is not None:
         forced = rerun(list(ref.selected))
         assert list(forced.selected[:ref.d]) == list(ref.selected[:forced.d])
-        return compare(forced, ref, X, tol, tau, require_same_d, diag)
+        return compare(forced, ref, X, tol, tau, require_same_d, diag, col_sq=col_sq)
     if upto == d_cmp and require_same_d:
         assert gpu.d == ref.d, f"d differs: gpu {gpu.d} ref {ref.d}"
     tols = step_tolerances(ref, col_sq, rsteps, tol)

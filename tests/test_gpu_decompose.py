@@ -114,29 +114,6 @@ def test_c1_full_parity_all_steps(cuda):
     assert compare(g, r, X) == r.d == g.d == w.d_max
 
 
-@pytest.mark.slow
-def test_c2_prefix_parity(cuda):
-    """C2 (34 GB) at full size: the first 8 greedy steps against the oracle."""
-    import os
-    import torch
-    w = configs.C2
-    Xd = configs.low_rank_matrix_torch(w.m, w.n, 1024, configs.spectrum("C2", 1024), 1e-8,
-                                       w.seed, device=cuda)
-    g = rbd.decompose(Xd, d_max=8)
-    Xh = torch.empty((w.n, w.m), dtype=torch.float64, pin_memory=True)
-    Xh.copy_(Xd.t())
-    del Xd
-    X = Xh.numpy().T
-    r = oracle.decompose(X, 8, nthreads=os.cpu_count() or 1)
-
-    class P:
-        pass
-    gp = P()
-    gp.Y, gp.T, gp.d = g.Y.cpu().numpy(), g.T.cpu().numpy(), g.d
-    gp.selected, gp.residual_history = g.selected, g.residual_history
-    assert compare(gp, r, X) == 8
-
-
 def test_determinism_bitwise(cuda):
     X = configs.c0_matrix()
     a = basic(X, 64, 1e-6)
@@ -446,3 +423,37 @@ def test_host_many_stops_at_a_failing_matrix(cuda):
         rbd.decompose_many(xs, d_max=5)
     ok = rbd.decompose_many([xs[0], xs[2]], d_max=5)
     assert [g.d for g in ok] == [5, 5]
+
+
+def test_overflowing_column_norms_return_an_error_and_keep_the_context(cuda):
+    """Finite entries near 1e160 overflow ||x_j||^2 to inf. The reference then
+    has max_col_norm = inf, so breakdown_tol = inf (decompose.cpp:70-74) and the
+    first mgs_project of a normal start column breaks down: DegenerateInput
+    (:104-105) — the oracle's outcome below. The B200 path returns that error
+    before its loop starts (no NaN partial can reach the loop's ready-flag
+    protocol), and the context stays usable. (When the start column itself
+    overflows, the reference divides by an infinite norm and returns zero basis
+    vectors with an inf history; the B200 path returns the same error there.)"""
+    import torch
+    rng = np.random.default_rng(5)
+    x = rng.standard_normal((64, 9))
+    x[:, 5] = rng.choice([-1.0, 1.0], size=64) * 1e160
+    with pytest.raises(oracle.OracleError) as ei:
+        oracle.decompose(x, 4)
+    assert ei.value.kind == "DegenerateInput"
+    ctx = rbd.Context(0)
+    with pytest.raises(rbd.DegenerateInput):
+        rbd.decompose(x, d_max=4, ctx=ctx)
+    with pytest.raises(rbd.DegenerateInput):
+        rbd.decompose(x * 0 + 1e160, d_max=4, ctx=ctx)
+    with pytest.raises(rbd.DegenerateInput):
+        rbd.decompose(torch.as_tensor(x, device=cuda), d_max=4, ctx=ctx)
+    # weighted: finite ||x_j||^2 but a_i * ||x_j||^2 overflows
+    xw = rng.choice([-1.0, 1.0], size=(64, 9)) * 1e150
+    with pytest.raises(rbd.InvalidArgument):
+        rbd.decompose(xw, d_max=4, diag=np.full(64, 1e10), ctx=ctx)
+    ok = rbd.decompose(oracle.random_matrix(30, 10, 7), d_max=5, ctx=ctx)
+    r = oracle.decompose(oracle.random_matrix(30, 10, 7), 5)
+    assert ok.selected == r.selected
+    assert np.abs(ok.Y - r.Y).max() < 1e-12
+    torch.cuda.synchronize()

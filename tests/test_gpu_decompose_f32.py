@@ -109,8 +109,8 @@ def test_f32_gating(cuda):
     xi[0, 0] = np.inf
     with pytest.raises(rbd.InvalidArgument):
         rbd.decompose(xi, d_max=2)
-    with pytest.raises(rbd.InvalidArgument):
-        rbd.decompose(x, d_max=2, diag=np.ones(10))
+    with pytest.raises(rbd.InvalidArgument):     # the fp32 mode is identity-only
+        rbd.decompose(x, d_max=2, diag=np.ones(10), storage="f32")
     z = x.copy()
     z[:, 0] = 0.0
     with pytest.raises(rbd.DegenerateInput):
@@ -211,3 +211,19 @@ def test_c2_f32_prefix_parity(cuda):
     gp.Y, gp.T, gp.d = g.Y.cpu().numpy(), g.T.cpu().numpy(), g.d
     gp.selected, gp.residual_history = g.selected, g.residual_history
     assert compare(gp, r, X) == 8
+
+
+def test_f32_input_outside_the_fp32_mode_is_widened(cuda):
+    """float32 input with a diagonal weight (or d_max above the persistent
+    loop's limit) runs the fp64 path on the exactly widened values, as the
+    reference's binding converts any array to a double Matrix
+    (bindings.cpp:69-78); it is not rejected."""
+    x = f32(oracle.random_matrix(40, 12, 311))
+    w = oracle.random_positive(40, 312)
+    a = rbd.decompose(x, d_max=6, diag=w)
+    b = rbd.decompose(x.astype(np.float64), d_max=6, diag=w)
+    assert a.selected == b.selected
+    np.testing.assert_array_equal(a.Y, b.Y)
+    np.testing.assert_array_equal(a.T, b.T)
+    clf = rbd.fit(x, list(range(12)), d_max=6, diag=w)
+    assert clf.predict(x[:, 3].astype(np.float64)) == 3
