@@ -1,18 +1,30 @@
 #!/usr/bin/env python
 """Benchmark of the B200 RBD greedy loop (BASELINE.json metric: effective HBM
-GB/s = X bytes x greedy steps / time).
+GB/s = X bytes x greedy steps / time; end-to-end seconds alongside).
 
-One bench "step" = one full rbd::decompose of the workload (default C1, the
-BASELINE config the metric is quoted on). `value` is device-resident (X in
-HBM before the timed region); `e2e` goes through the reference-facing host
-entry (numpy X in pinned memory -> H2D -> loop -> D2H of Y and T).
+One bench "step" = one full rbd::decompose of the workload. Workloads
+(BASELINE.json configs, seeded synthetic inputs, paper_1503_05947_b200/configs.py):
+
+* N = 1 (default): C2-tall, 1,048,576 x 4,096 fp64 (32 GiB), d = 512 — the
+  largest configuration that is a single-GPU workload (BASELINE.json names no
+  config for the metric). `value` is device-resident (X in HBM before the
+  timed region); `e2e` goes through the reference-facing host entry
+  (rbd_decompose_host_many: pinned host X -> H2D -> loop -> D2H of Y and T,
+  the upload of matrix i+1 overlapping the loop of matrix i).
+* N > 1 (torchrun): C3-sharded, 262,144 x 65,536 (128 GiB), d = 1024, X split
+  by contiguous column blocks over the ranks, Y replicated (strong scaling;
+  `--workload C3-sharded` runs the same line at N = 1).
+
+Secondary figures (C1 image-like, the fp32 storage mode, C4 out-of-sample)
+ride along in `secondary` and never enter `value`.
 
 Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
-For N > 1 launch under torchrun; C1 does not shard (replicas only).
+                       [--workload NAME]
 """
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import subprocess
@@ -25,20 +37,28 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+METRIC = "rbd_effective_hbm_gbs"
+
 
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--steps", type=int, default=5)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    p.add_argument("--workload", default="C1-image-like")
-    p.add_argument("--cpu-seconds", type=float, default=15.0)
+    p.add_argument("--workload", default=None,
+                   help="default: C2-tall at N=1, C3-sharded under torchrun (N>1)")
+    p.add_argument("--cpu-seconds", type=float, default=20.0,
+                   help="cpu_baseline: bounded single-thread oracle sample (seconds)")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
-    p.add_argument("--no-f32", action="store_true", help="skip the fp32 storage-mode line")
+    p.add_argument("--e2e-steps", type=int, default=6,
+                   help="matrices per timed rbd_decompose_host_many call (capped at --steps)")
+    p.add_argument("--aux-steps", type=int, default=3,
+                   help="timed decompositions of each secondary figure")
+    p.add_argument("--no-secondary", action="store_true")
     p.add_argument("--d-max", type=int, default=None, help="override d_max (quick runs)")
-    p.add_argument("--ref-seconds", type=float, default=6.0,
+    p.add_argument("--ref-seconds", type=float, default=3.0,
                    help="reference arm: CPU seconds of greedy steps per bench step")
     return p.parse_args()
 
@@ -48,6 +68,23 @@ def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return rank, world, local
+
+
+def default_workload(args, world):
+    if args.workload:
+        return args.workload
+    return "C2-tall" if world == 1 else "C3-sharded"
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 class ClockSampler:
@@ -121,13 +158,16 @@ def peak_hbm():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic():
+def ncu_traffic(workload):
+    """dram bytes per launch of the loop kernel from one `ncu --set full`
+    capture of the same workload (profiles/traffic.json, keyed by workload)."""
     path = os.path.join(ROOT, "profiles", "traffic.json")
     try:
         with open(path) as f:
-            return json.load(f)
+            t = json.load(f)
     except Exception:
         return None
+    return t.get(workload)
 
 
 def read_peak_gbs(dev, gib: int = 4, reps: int = 10):
@@ -152,173 +192,268 @@ def read_peak_gbs(dev, gib: int = 4, reps: int = 10):
     return nbytes / (best / 1e3) / 1e9
 
 
-def make_workload(name, device):
+# ---------------------------------------------------------------- workloads
+
+NOISE = {"C2": 1e-8, "C3": 1e-10, "C4": 1e-6}
+RANK = {"C2": 1024, "C3": 2048, "C4": 512}
+
+
+def make_workload(name, device, offset=0, n_local=None):
+    """(workload, X column-major view on `device`, absolute eps_R). C3 is built
+    by column blocks (any shard of it regenerates alone)."""
     import torch
     from paper_1503_05947_b200 import configs
     w = configs.WORKLOADS[name]
-    if name.startswith("C1"):
+    key = name.split("-")[0]
+    if key == "C1":
         Xd = configs.c1_matrix(n=w.n, seed=w.seed, device=device)
-    elif name.startswith("C0"):
-        Xh = configs.c0_matrix()
-        Xd = torch.as_tensor(Xh.T.copy(), device=device).t()
+    elif key == "C0":
+        Xd = torch.as_tensor(configs.c0_matrix().T.copy(), device=device).t()
+    elif key == "C3":
+        Xd = configs.low_rank_shard_torch(w.m, w.n, RANK[key], configs.spectrum(key, RANK[key]),
+                                          NOISE[key], w.seed, offset,
+                                          w.n if n_local is None else n_local, device=device)
     else:
-        rank = {"C2-tall": 1024, "C3-sharded": 2048, "C4-out-of-sample": 512}[name]
-        key = name.split("-")[0]
-        Xd = configs.low_rank_matrix_torch(w.m, w.n, rank, configs.spectrum(key, rank),
-                                           {"C2": 1e-8, "C3": 1e-10, "C4": 1e-6}[key], w.seed,
-                                           device=device)
+        Xd = configs.low_rank_matrix_torch(w.m, w.n, RANK[key], configs.spectrum(key, RANK[key]),
+                                           NOISE[key], w.seed, device=device)
     if torch.device(device).type == "cuda":
         torch.cuda.synchronize(device)
-    colmax = float(Xd.norm(dim=0).max())
-    return w, Xd, configs.eps_for(w, colmax)
+    eps = w.eps_abs
+    if w.eps_rel != 0.0:
+        eps = configs.eps_for(w, float(Xd.norm(dim=0).max()))
+    return w, Xd, eps
 
 
-def cpu_baseline_sample(X_host, w, eps, seconds, nthreads):
-    """Oracle (restated reference path, two X passes per step) on the first
-    greedy steps of the same workload, bounded to ~`seconds` of CPU work."""
-    import oracle
-    t0 = time.perf_counter()
-    oracle.decompose(X_host, w.d_max, eps, nthreads=nthreads, max_steps=2)
-    per = max((time.perf_counter() - t0) / 2.0, 1e-4)
-    steps = int(max(2, min(w.d_max, seconds / per)))
-    t0 = time.perf_counter()
-    r = oracle.decompose(X_host, w.d_max, eps, nthreads=nthreads, max_steps=steps)
-    dt = time.perf_counter() - t0
-    return r.d, dt
+def workload_config(w, eps, world, d_max):
+    """The `config` object of BOTH arms (identical dicts)."""
+    sharded = w.name.startswith("C3")
+    xbytes = w.m * w.n * 8
+    return {"workload": w.name, "m": w.m, "n": w.n, "d_max": d_max, "eps_R": eps,
+            "dtype_X": "f64", "parallelism": (f"colshard{world}" if sharded else f"replicas{world}"),
+            "l2": f"inputs larger than L2 (X {xbytes / 1e9:.1f} GB vs 126 MB L2)",
+            "describe": w.describe}
 
+
+# ---------------------------------------------------------------- reference arm
 
 def run_reference(args):
+    """The reference's CPU path on the box's host cores: the oracle port
+    (restating decompose.cpp / workspace.cpp with the reference's two X passes
+    per step), all host threads, on our arm's workload and config. Each bench
+    step is a bounded sample: the first S greedy steps of the full workload."""
     rank, world, local = dist_env()
     if rank != 0:
         return
     import torch
-    from paper_1503_05947_b200 import configs
-    w = configs.WORKLOADS[args.workload]
+    wname = default_workload(args, world)
     dev = torch.device("cuda", local) if torch.cuda.is_available() else torch.device("cpu")
-    _, Xd, eps = make_workload(args.workload, dev)
+    w, Xd, eps = make_workload(wname, dev)
+    d_max = args.d_max or w.d_max
     X = np.asfortranarray(Xd.cpu().numpy())
     del Xd
+    if dev.type == "cuda":
+        torch.cuda.empty_cache()
     cores = os.cpu_count() or 1
     import oracle
-    # bounded sample per step: the first S greedy steps of the full workload
-    t0 = time.perf_counter()
-    oracle.decompose(X, w.d_max, eps, nthreads=cores, max_steps=2)
-    per = max((time.perf_counter() - t0) / 2.0, 1e-4)
-    S = int(max(2, min(w.d_max, args.ref_seconds / per)))
+    per_est = 2.0 * w.m * w.n * 8 / (8e9 * cores)      # two X passes per greedy step
+    S = int(max(1, min(d_max, args.ref_seconds / max(per_est, 1e-6))))
     for _ in range(args.warmup):
-        oracle.decompose(X, w.d_max, eps, nthreads=cores, max_steps=S)
+        oracle.decompose(X, d_max, eps, nthreads=cores, max_steps=S)
+    loops, inits, done = 0.0, 0.0, 0
     t0 = time.perf_counter()
-    done = 0
     for _ in range(args.steps):
-        r = oracle.decompose(X, w.d_max, eps, nthreads=cores, max_steps=S)
+        r = oracle.decompose(X, d_max, eps, nthreads=cores, max_steps=S)
+        loops += r.t_loop_s
+        inits += r.t_init_s
         done += r.d
-    dt = time.perf_counter() - t0
+    wall = time.perf_counter() - t0
     bytes_per = w.m * w.n * 8
-    val = bytes_per * done / dt / 1e9
-    sample = f"first {S} greedy steps of {w.name} per bench step ({w.m}x{w.n} fp64)"
+    val = bytes_per * done / loops / 1e9
+    sample = (f"first {S} of {d_max} greedy steps of {w.name} ({w.m}x{w.n} fp64) per bench step, "
+              f"oracle port (decompose.cpp:53-111, two X passes per step), {cores} threads; "
+              f"value = X bytes x steps / greedy-loop time (the per-call validation + "
+              f"workspace_init pass, {inits / max(args.steps, 1):.2f} s, is excluded: a full "
+              f"decompose runs it once per {d_max} steps)")
     line = {
-        "impl": "reference", "metric": "rbd_effective_hbm_gbs", "value": val, "unit": "GB/s",
+        "impl": "reference", "metric": METRIC, "value": val, "unit": "GB/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": wall / max(args.steps, 1) * 1e3, "higher_is_better": True,
+        "scaling": "strong" if w.name.startswith("C3") else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": w.name, "m": w.m, "n": w.n, "d_max": w.d_max, "eps_R": eps},
+        "config": workload_config(w, eps, world, d_max),
         "cpu_baseline": {"value": val, "unit": "GB/s", "cores": cores, "kind": "port",
-                         "sample": sample},
+                         "sample": sample, "cpu_model": cpu_model()},
         "e2e": {"value": val, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "greedy_steps_timed": done,
     }
     print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- our arm (one GPU per workload)
+
+def cpu_baseline_leg(X_host, w, eps, d_max, seconds):
+    """Oracle port (two X passes per step), ONE thread, on the first S greedy
+    steps of the same workload (S sized for ~`seconds` of CPU work)."""
+    import oracle
+    per_est = 2.0 * w.m * w.n * 8 / 8e9
+    S = int(max(1, min(d_max, seconds / max(per_est, 1e-6))))
+    r = oracle.decompose(X_host, d_max, eps, nthreads=1, max_steps=S)
+    xb = w.m * w.n * 8
+    loop_rate = xb * r.d / r.t_loop_s / 1e9
+    full_s = r.t_init_s + d_max * r.t_loop_s / r.d
+    return {"value": loop_rate, "unit": "GB/s", "cores": 1, "kind": "port",
+            "sample": (f"first {r.d} of {d_max} greedy steps of {w.name} ({w.m}x{w.n} fp64), "
+                       f"single-thread oracle restating decompose.cpp (two X passes per step): "
+                       f"{r.t_loop_s:.1f} s of greedy loop (value = X bytes x steps / loop time) "
+                       f"after a {r.t_init_s:.1f} s validation + workspace_init pass"),
+            "steps_sampled": r.d, "loop_s": r.t_loop_s, "init_s": r.t_init_s,
+            "extrapolated_full_decompose_s": full_s,
+            "cpu_model": cpu_model(), "nproc": os.cpu_count()}
+
+
+def time_decomposes(rbd, X, d_max, eps, ctx, steps, stream, dev):
+    import torch
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize(dev)
+    e0.record(stream)
+    ds, loops = [], []
+    for _ in range(steps):
+        g = rbd.decompose(X, d_max=d_max, eps_r=eps, ctx=ctx)
+        ds.append(g.d)
+        loops.append(g.result.loop_ms)
+        del g
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    return e0.elapsed_time(e1), ds, loops
+
+
+def secondary_c1(rbd, ctx, dev, stream, args, peak):
+    w, Xd, eps = make_workload("C1-image-like", dev)
+    for _ in range(3):
+        rbd.decompose(Xd, d_max=w.d_max, eps_r=eps, ctx=ctx)
+    K = max(args.aux_steps, 5)
+    ms, ds, loops = time_decomposes(rbd, Xd, w.d_max, eps, ctx, K, stream, dev)
+    xb = w.m * w.n * 8
+    lm = float(np.mean(loops))
+    out = {"workload": w.name, "m": w.m, "n": w.n, "d_max": w.d_max,
+           "value": xb * sum(ds) / (ms / 1e3) / 1e9, "unit": "GB/s", "ms_per_step": ms / K,
+           "loop_ms_mean": lm, "roofline_frac": xb * float(np.mean(ds)) / (lm / 1e3) / 1e9 / peak,
+           "d_reached": int(np.mean(ds))}
+    del Xd
+    gc.collect()
+    return out
+
+
+def f32_leg(rbd, Xd, w, d_max, eps, ctx, dev, stream, args, peak):
+    """fp32 storage mode on the same workload rounded to fp32 (half the X
+    bytes per sweep, fp64 arithmetic): device-resident and e2e."""
+    import torch
+    m, n = Xd.shape
+    Xf = Xd.float()
+    gf = rbd.decompose(Xf, d_max=d_max, eps_r=eps, ctx=ctx)
+    K = max(1, args.aux_steps)
+    ms, fd, fl = time_decomposes(rbd, Xf, d_max, eps, ctx, K, stream, dev)
+    fbytes = m * n * 4
+    floop = float(np.mean(fl))
+    out = {"storage": "f32 X, f64 arithmetic (rbd_decompose_device_f32)",
+           "value": fbytes * sum(fd) / (ms / 1e3) / 1e9, "unit": "GB/s",
+           "ms_per_step": ms / K, "loop_ms_mean": floop,
+           "roofline_frac": fbytes * float(np.mean(fd)) / (floop / 1e3) / 1e9 / peak,
+           "d_reached": int(np.mean(fd))}
+    if not args.no_e2e:
+        Xh_t = torch.empty((n, m), dtype=torch.float32, pin_memory=True)
+        Xh_t.copy_(Xf.t())
+        Xh32 = Xh_t.numpy().T
+        del Xf
+        torch.cuda.empty_cache()
+        Ke = max(1, min(args.e2e_steps, args.steps))
+        from paper_1503_05947_b200.api import output_buffers
+        obufs = output_buffers(m, n, d_max, Ke)
+        warm = rbd.decompose_many([Xh32] * 2, d_max=d_max, eps_r=eps, ctx=ctx, out=obufs[:2])
+        del warm
+        gc.collect()
+        t0 = time.perf_counter()
+        outs = rbd.decompose_many([Xh32] * Ke, d_max=d_max, eps_r=eps, ctx=ctx, out=obufs)
+        te = time.perf_counter() - t0
+        del obufs
+        fe = [o.d for o in outs]
+        del outs
+        gc.collect()
+        out["e2e"] = {"value": fbytes * sum(fe) / te / 1e9, "unit": "GB/s",
+                      "ms_per_step": te * 1e3 / Ke, "h2d_bytes_per_step": m * n * 4,
+                      "entry": "rbd_decompose_host_many_f32 (numpy float32, pinned)"}
+        del Xh_t, Xh32
+    else:
+        del Xf
+    del gf
+    gc.collect()
+    torch.cuda.empty_cache()
+    return out
 
 
 def run_b200(args):
     import torch
     rank, world, local = dist_env()
-    if world > 1:
-        import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     import paper_1503_05947_b200 as rbd
-    from paper_1503_05947_b200._lib import load_library
+    from paper_1503_05947_b200._lib import check, load_library
     import ctypes as C
 
-    w, Xd, eps = make_workload(args.workload, dev)
+    wname = default_workload(args, world)
+    w, Xd, eps = make_workload(wname, dev)
+    d_max = args.d_max or w.d_max
     ctx = rbd.Context(local)
     lib = load_library()
     m, n = Xd.shape
     bytes_per_gstep = m * n * 8
-
-    def barrier():
-        if world > 1:
-            import torch.distributed as dist
-            dist.barrier()
+    stream = torch.cuda.ExternalStream(ctx.stream, device=dev)
 
     for _ in range(max(args.warmup, 0)):
-        g = rbd.decompose(Xd, d_max=w.d_max, eps_r=eps, ctx=ctx)
-    stream = torch.cuda.ExternalStream(ctx.stream, device=dev)
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
+        rbd.decompose(Xd, d_max=d_max, eps_r=eps, ctx=ctx)
     clocks = ClockSampler(local)
-    barrier()
     torch.cuda.synchronize(dev)
     clocks.start()
     clocks.wait_first()
     launches0 = ctx.launches
-    e0.record(stream)
-    ds = []
-    loop_ms = []
-    for _ in range(args.steps):
-        g = rbd.decompose(Xd, d_max=w.d_max, eps_r=eps, ctx=ctx)
-        ds.append(g.d)
-        loop_ms.append(g.result.loop_ms)
-    e1.record(stream)
-    torch.cuda.synchronize(dev)
-    barrier()
+    ms, ds, loop_ms = time_decomposes(rbd, Xd, d_max, eps, ctx, args.steps, stream, dev)
     clk = clocks.stop()
     launches = ctx.launches - launches0
-    ms = e0.elapsed_time(e1)
-    t_max = ms
-    if world > 1:
-        import torch.distributed as dist
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        t_max = float(t.item())
-    total_bytes = bytes_per_gstep * sum(ds) * world
-    value = total_bytes / (t_max / 1e3) / 1e9
+    value = bytes_per_gstep * sum(ds) / (ms / 1e3) / 1e9
 
     # ---- roofline of the dominant kernel ----
     # Inside the timed region the only kernels are K1 (init, 2 launches) and
     # k_rbd_persistent (the whole greedy loop, 1 launch per decompose). Its
     # algorithmic bytes per launch = m*n*8 per greedy step (X read once) x d;
-    # its duration is the CUDA-event time around the launch (loop_ms).
+    # its duration is the CUDA-event time around the launch on the context
+    # stream (result.loop_ms).
     peak, peak_src = peak_hbm()
     d_mean = float(np.mean(ds))
     loop_mean = float(np.mean(loop_ms))
     alg_bytes = bytes_per_gstep * d_mean
     ach = alg_bytes / (loop_mean / 1e3) / 1e9
-    traffic = ncu_traffic()
+    traffic = ncu_traffic(w.name) or {}
     roofline = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
-                "traffic": (traffic or {}).get("bytes_per_launch"),
+                "traffic": traffic.get("bytes_per_launch"),
                 "kernel": "k_rbd_persistent<2> (whole greedy loop, 1 launch/decompose)",
                 "algorithmic_bytes_per_launch": alg_bytes,
                 "algorithmic_bytes_note": "m*n*8 per greedy step x d (X read once per step); "
                                           "Y passes and bookkeeping not credited",
-                "ms_per_launch": loop_mean, "peak_source": peak_src,
-                "traffic_source": (traffic or {}).get("source")}
+                "ms_per_launch": loop_mean, "loop_share_of_step": loop_mean / (ms / args.steps),
+                "peak_source": peak_src, "traffic_source": traffic.get("source")}
     # the fused sweep phase alone, as a standalone kernel (K2), CUDA events
     y = torch.randn(m, dtype=torch.float64, device=dev)
     y /= y.norm()
     torch.cuda.synchronize(dev)
     ms_sweep = C.c_double()
-    from paper_1503_05947_b200._lib import check
     check(lib.rbd_time_sweep(ctx.handle, C.c_void_p(Xd.data_ptr()), m, n, Xd.stride(1),
                              C.c_void_p(y.data_ptr()), 20, C.byref(ms_sweep)))
     sw = bytes_per_gstep / (ms_sweep.value / 1e3) / 1e9
     roofline["sweep_kernel"] = {"kernel": "k_sweep<2,MODE_DOT,stream> (K2 standalone)",
                                 "achieved": sw, "frac": sw / peak, "ms_per_launch": ms_sweep.value,
                                 "bytes_per_launch": bytes_per_gstep}
-    # read-only HBM peak (SURVEY §8(d): the copy-based peak under-states a pure
-    # read stream): a stock reduction over 4 GiB of fp64, best of 10
+    del y
     rp = read_peak_gbs(dev)
     if rp:
         roofline["read_peak"] = {"gbs": rp, "frac": ach / rp,
@@ -327,156 +462,84 @@ def run_b200(args):
     roofline["frac_of_nominal"] = {"gbs": 7700.0, "frac": ach / 7700.0,
                                    "note": "nominal HBM3e 7.7 TB/s (HGX), B200_PROFILING.md"}
 
-    # ---- fp32 storage mode (rbd_decompose_device_f32), same workload rounded
-    #      to fp32: half the X bytes per sweep, fp64 arithmetic; reported beside
-    #      the fp64 headline (metric bytes at 4 B/element) ----
-    f32_mode = None
-    if not args.no_f32:
-        Xf = Xd.float()
-        for _ in range(2):
-            gf = rbd.decompose(Xf, d_max=w.d_max, eps_r=eps, ctx=ctx)
-        torch.cuda.synchronize(dev)
-        e0.record(stream)
-        fl, fd = [], []
-        for _ in range(max(1, args.steps)):
-            gf = rbd.decompose(Xf, d_max=w.d_max, eps_r=eps, ctx=ctx)
-            fd.append(gf.d)
-            fl.append(gf.result.loop_ms)
-        e1.record(stream)
-        torch.cuda.synchronize(dev)
-        msf = e0.elapsed_time(e1)
-        fbytes = m * n * 4
-        floop = float(np.mean(fl))
-        f32_mode = {"storage": "f32 X, f64 arithmetic (rbd_decompose_device_f32)",
-                    "value": fbytes * sum(fd) / (msf / 1e3) / 1e9, "unit": "GB/s",
-                    "ms_per_step": msf / len(fd), "loop_ms_mean": floop,
-                    "roofline_frac": fbytes * float(np.mean(fd)) / (floop / 1e3) / 1e9 / peak,
-                    "d_reached": int(np.mean(fd)),
-                    "same_selection_as_f64_run_on_f32_values": None}
-        g64 = rbd.decompose(Xf.double(), d_max=w.d_max, eps_r=eps, ctx=ctx)
-        f32_mode["same_selection_as_f64_run_on_f32_values"] = g64.selected == gf.selected
-        if not args.no_e2e:   # host entry with a pinned float32 X (half the PCIe bytes)
-            Xh32_t = torch.empty((n, m), dtype=torch.float32, pin_memory=True)
-            Xh32_t.copy_(Xf.t())
-            Xh32 = Xh32_t.numpy().T
-            K = max(1, args.steps)
-            import gc
-            warm = rbd.decompose_many([Xh32] * K, d_max=w.d_max, eps_r=eps, ctx=ctx)
-            del warm
-            gc.collect()
-            t0 = time.perf_counter()
-            outs = rbd.decompose_many([Xh32] * K, d_max=w.d_max, eps_r=eps, ctx=ctx)
-            te = (time.perf_counter() - t0) * 1e3
-            fe = [o.d for o in outs]
-            del outs
-            gc.collect()
-            f32_mode["e2e"] = {"value": fbytes * sum(fe) / (te / 1e3) / 1e9, "unit": "GB/s",
-                               "ms_per_step": te / len(fe), "h2d_bytes_per_step": m * n * 4,
-                               "entry": "rbd_decompose_host_many_f32 (numpy float32, pinned)"}
-            del Xh32_t, Xh32
-        del Xf, g64
-        torch.cuda.empty_cache()
-
     # ---- e2e through the reference-facing host entry (pinned host X) ----
     e2e = None
-    if not args.no_e2e:
+    Xh = None
+    Xh_t = None
+    if not args.no_e2e or not args.no_cpu:
         Xh_t = torch.empty((n, m), dtype=torch.float64, pin_memory=True)
         Xh_t.copy_(Xd.t())
         Xh = Xh_t.numpy().T  # (m, n) Fortran view, pinned
         assert Xh.flags["F_CONTIGUOUS"]
-        # warm-up: device buffers and the pinned host outputs (the caching host
-        # allocator serves the alternating output sets from its cache afterwards)
-        for _ in range(max(3, args.warmup)):
-            g2 = rbd.decompose(Xh, d_max=w.d_max, eps_r=eps, ctx=ctx)
-        barrier()
-        torch.cuda.synchronize(dev)
-        e0.record(stream)
-        t0 = time.perf_counter()
-        d2 = []
-        for _ in range(max(1, args.steps)):
-            g2 = rbd.decompose(Xh, d_max=w.d_max, eps_r=eps, ctx=ctx)
-            d2.append(g2.d)
-        e1.record(stream)
-        torch.cuda.synchronize(dev)
-        wall = time.perf_counter() - t0
-        ms2 = e0.elapsed_time(e1)
-        t2 = max(ms2, wall * 1e3)
-        if world > 1:
-            import torch.distributed as dist
-            t = torch.tensor([t2], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            t2 = float(t.item())
-        dmean = float(np.mean(d2))
-        single = {"value": bytes_per_gstep * sum(d2) * world / (t2 / 1e3) / 1e9, "unit": "GB/s",
-                  "ms_per_step": t2 / len(d2),
-                  "entry": "rbd_decompose_host, one call per step (upload, loop, download in series)"}
-        # the stream of inputs through the pipelined host entry: K matrices (the
-        # pinned X, uploaded again for every step) in one rbd_decompose_host_many
-        # call; the upload of matrix i+1 overlaps the loop of matrix i
-        K = max(1, args.steps)
-        import gc
-        warm = rbd.decompose_many([Xh] * K, d_max=w.d_max, eps_r=eps, ctx=ctx)
+    if not args.no_e2e:
+        Ke = max(1, min(args.e2e_steps, args.steps))
+        # the caller's page-locked output buffers, allocated once and reused
+        from paper_1503_05947_b200.api import output_buffers
+        obufs = output_buffers(m, n, d_max, Ke)
+        warm = rbd.decompose_many([Xh] * 2, d_max=d_max, eps_r=eps, ctx=ctx, out=obufs[:2])
         del warm
         gc.collect()
-        barrier()
         torch.cuda.synchronize(dev)
-        e0.record(stream)
         t0 = time.perf_counter()
-        outs = rbd.decompose_many([Xh] * K, d_max=w.d_max, eps_r=eps, ctx=ctx)
-        e1.record(stream)
-        torch.cuda.synchronize(dev)
+        outs = rbd.decompose_many([Xh] * Ke, d_max=d_max, eps_r=eps, ctx=ctx, out=obufs)
         wall = time.perf_counter() - t0
-        t3 = max(e0.elapsed_time(e1), wall * 1e3)
         d3 = [o.d for o in outs]
         del outs
         gc.collect()
-        if world > 1:
-            import torch.distributed as dist
-            t = torch.tensor([t3], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            t3 = float(t.item())
-        e2e = {"value": bytes_per_gstep * sum(d3) * world / (t3 / 1e3) / 1e9, "unit": "GB/s",
+        dmean = float(np.mean(d3))
+        e2e = {"value": bytes_per_gstep * sum(d3) / wall / 1e9, "unit": "GB/s",
                "h2d_bytes_per_step": m * n * 8,
                "d2h_bytes_per_step": int(8 * (m * dmean + dmean * n + 2 * dmean)),
-               "ms_per_step": t3 / len(d3),
-               "entry": "rbd_decompose_host_many (numpy, pinned; upload of step i+1 overlaps "
-                        "the loop of step i)",
-               "single_call": single}
+               "ms_per_step": wall * 1e3 / Ke, "steps": Ke,
+               "seconds_per_decompose": wall / Ke,
+               "entry": "rbd_decompose_host_many (numpy, pinned; upload of matrix i+1 overlaps "
+                        "the loop of matrix i; Y and T stream back during the loop into the "
+                        "caller's page-locked output buffers, allocated before the timed region)"}
+        del obufs
 
-    # ---- CPU baseline: oracle port, one thread, bounded sample (rank 0, N=1) ----
+    # ---- CPU baseline: oracle port, one thread, bounded sample ----
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
-        X_host = np.asfortranarray(Xd.cpu().numpy())
-        steps, dt = cpu_baseline_sample(X_host, w, eps, args.cpu_seconds, 1)
-        cpu = {"value": bytes_per_gstep * steps / dt / 1e9, "unit": "GB/s", "cores": 1,
-               "kind": "port",
-               "sample": f"first {steps} greedy steps of {w.name} ({m}x{n} fp64), single-thread "
-                         f"oracle restating decompose.cpp (two X passes per step), {dt:.1f}s"}
+    if not args.no_cpu:
+        cpu = cpu_baseline_leg(Xh, w, eps, d_max, args.cpu_seconds)
+    del Xh, Xh_t
+    gc.collect()
 
-    if rank == 0:
-        line = {
-            "metric": "rbd_effective_hbm_gbs", "value": value, "unit": "GB/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic",
-            "config": {"workload": w.name, "m": m, "n": n, "d_max": w.d_max, "eps_R": eps,
-                       "d_reached": int(np.mean(ds)), "parallelism": f"replicas{world}",
-                       "l2": "inputs larger than L2 (X 627 MB vs 126 MB L2)",
-                       "describe": w.describe},
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-            "clocks": clk, "loop_ms_mean": float(np.mean(loop_ms)),
-            "d_per_step": ds, "f32_mode": f32_mode,
-        }
-        print(json.dumps(line), flush=True)
+    # ---- secondary figures (never part of `value`) ----
+    secondary = {}
+    if not args.no_secondary:
+        try:
+            secondary["f32_mode"] = f32_leg(rbd, Xd, w, d_max, eps, ctx, dev, stream, args, peak)
+        except Exception as ex:   # reported, not fatal: the headline is already measured
+            secondary["f32_mode"] = {"error": repr(ex)[:300]}
+        del Xd
+        gc.collect()
+        torch.cuda.empty_cache()
+        if not w.name.startswith("C1"):
+            try:
+                secondary["C1-image-like"] = secondary_c1(rbd, ctx, dev, stream, args, peak)
+            except Exception as ex:
+                secondary["C1-image-like"] = {"error": repr(ex)[:300]}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": workload_config(w, eps, world, d_max),
+        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+        "clocks": clk, "loop_ms_mean": loop_mean, "d_per_step": ds,
+        "seconds_per_decompose": ms / 1e3 / args.steps,
+        "secondary": secondary,
+    }
+    print(json.dumps(line), flush=True)
     ctx.close()
-    if world > 1:
-        import torch.distributed as dist
-        dist.destroy_process_group()
 
+
+# ---------------------------------------------------------------- sharded (C3, N GPUs)
 
 def run_sharded(args):
-    """C3: X sharded by contiguous column blocks over the ranks (NCCL payload
-    allgather inside the library); weak per-GPU data, strong on the job."""
+    """C3: X sharded by contiguous column blocks over the ranks (the exchange
+    runs inside the library over NCCL); strong scaling on the whole job."""
     import torch
     rank, world, local = dist_env()
     dev = torch.device("cuda", local)
@@ -486,15 +549,11 @@ def run_sharded(args):
         dist.init_process_group("nccl", device_id=dev)
     import paper_1503_05947_b200 as rbd
     from paper_1503_05947_b200 import configs, distributed as rd
-    w = configs.WORKLOADS[args.workload]
-    key = w.name.split("-")[0]
-    rank_r = {"C2": 1024, "C3": 2048, "C4": 512}.get(key, 64)
-    plan = rd.plan_shards(w.n, world)
+    wname = default_workload(args, world)
+    w0 = configs.WORKLOADS[wname]
+    plan = rd.plan_shards(w0.n, world)
     o, nl = plan.offsets[rank], plan.n_locals[rank]
-    X = configs.low_rank_shard_torch(w.m, w.n, rank_r, configs.spectrum(key, rank_r),
-                                     {"C2": 1e-8, "C3": 1e-10, "C4": 1e-6}.get(key, 1e-6), w.seed,
-                                     o, nl, device=dev)
-    torch.cuda.synchronize(dev)
+    w, X, eps = make_workload(wname, dev, o, nl)
     d_max = args.d_max or w.d_max
     ctx = rbd.Context(local)
     if world > 1:
@@ -513,7 +572,7 @@ def run_sharded(args):
             dist.barrier()
 
     for _ in range(max(args.warmup, 0)):
-        r = rd.decompose_sharded(X, plan, rank, d_max, 0.0, ctx=ctx)
+        r = rd.decompose_sharded(X, plan, rank, d_max, eps, ctx=ctx)
     clocks = ClockSampler(local)
     barrier()
     torch.cuda.synchronize(dev)
@@ -526,7 +585,7 @@ def run_sharded(args):
     e0.record(stream)
     ds = []
     for _ in range(args.steps):
-        r = rd.decompose_sharded(X, plan, rank, d_max, 0.0, ctx=ctx)
+        r = rd.decompose_sharded(X, plan, rank, d_max, eps, ctx=ctx)
         ds.append(r.d)
     e1.record(stream)
     torch.cuda.synchronize(dev)
@@ -545,19 +604,17 @@ def run_sharded(args):
         peak, src = peak_hbm()
         per_gpu = value / world
         line = {
-            "metric": "rbd_effective_hbm_gbs", "value": value, "unit": "GB/s", "n_gpus": world,
+            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": w.name, "m": w.m, "n": w.n, "d_max": d_max,
-                       "d_reached": int(np.mean(ds)), "parallelism": f"colshard{world}",
-                       "shard_cols": list(plan.n_locals), "describe": w.describe},
+            "config": workload_config(w, eps, world, d_max),
             "roofline": {"bound": "hbm", "achieved": per_gpu, "peak": peak, "unit": "GB/s",
                          "frac": per_gpu / peak, "traffic": None,
-                         "kernel": "k_rbd_persistent<2,true> per step + payload allgather",
+                         "kernel": "k_rbd_persistent<2,true> per step + NCCL exchange",
                          "note": "per-GPU X bytes x steps / time", "peak_source": src},
             "cpu_baseline": None, "e2e": None, "gpu_launches": ctx.launches - launches0,
-            "clocks": clk,
+            "clocks": clk, "shard_cols": list(plan.n_locals), "d_per_step": ds,
         }
         print(json.dumps(line), flush=True)
     ctx.close()
@@ -568,9 +625,10 @@ def run_sharded(args):
 
 def main():
     args = parse()
+    rank, world, _ = dist_env()
     if args.impl == "reference":
         run_reference(args)
-    elif args.workload.startswith(("C2", "C3")):
+    elif default_workload(args, world).startswith("C3"):
         run_sharded(args)
     else:
         run_b200(args)

@@ -5,6 +5,7 @@
 #define RBD_B200_DECOMPOSE_HPP
 
 #include <cstdint>
+#include <mutex>
 #include <optional>
 #include <vector>
 
@@ -33,6 +34,51 @@ struct RbdConfig {                                   // decompose.hpp:25-36
   double breakdown_tol = -1.0;
 };
 
+namespace detail {
+inline rbd_ctx_t context();
+inline void check(int status);
+
+// A model's device-resident Y (rbd_model_t), created by the first project /
+// reconstruct and reused by the later ones, so the reference's per-vector
+// callers (classify.cpp:22-23, tools/main.cpp:149-158) upload Y once instead
+// of per call. Copies of a model start with an empty cache; the key (Y's
+// buffer and shape) rebuilds it if Y was replaced.
+class ResidentCache {
+ public:
+  ResidentCache() = default;
+  ResidentCache(const ResidentCache&) {}
+  ResidentCache& operator=(const ResidentCache&) {
+    std::lock_guard<std::mutex> g(mu_);
+    drop();
+    return *this;
+  }
+  ~ResidentCache() { drop(); }
+  rbd_model_t get(const Matrix& Y, Index d) const {
+    std::lock_guard<std::mutex> g(mu_);
+    if (h_ && key_ == Y.data() && m_ == Y.rows() && d_ == d) return h_;
+    drop();
+    rbd_model_t h = nullptr;
+    check(rbd_model_create(context(), Y.rows(), d, d, Y.data(), Y.rows(), nullptr, 0, nullptr,
+                           0.0, &h));
+    h_ = h;
+    key_ = Y.data();
+    m_ = Y.rows();
+    d_ = d;
+    return h_;
+  }
+
+ private:
+  void drop() const {
+    if (h_) rbd_model_free(h_);
+    h_ = nullptr;
+  }
+  mutable std::mutex mu_;
+  mutable rbd_model_t h_ = nullptr;
+  mutable const double* key_ = nullptr;
+  mutable Index m_ = 0, d_ = 0;
+};
+}  // namespace detail
+
 struct RbdModel {                                    // decompose.hpp:39-46
   Matrix Y;                                          // m x d
   Matrix T;                                          // d x n
@@ -40,6 +86,7 @@ struct RbdModel {                                    // decompose.hpp:39-46
   std::vector<double> residual_history;
   Index d = 0;
   WeightSpec weight{};
+  detail::ResidentCache resident{};                  // B200: device copy of Y (not in the reference)
 };
 
 struct MgsResult {                                   // decompose.hpp:48-51
@@ -178,16 +225,17 @@ inline Vector project(const RbdModel& model, const VectorRef& v) {     // decomp
   if (v.size() != model.Y.rows()) throw DimensionMismatch("project: vector length != m");
   Vector c(model.d);
   if (model.d == 0) return c;
-  detail::check(rbd_project_host(detail::context(), model.Y.data(), model.Y.rows(), model.d,
-                                 v.data(), 1, c.data(), nullptr));
+  detail::check(rbd_project_model(detail::context(), model.resident.get(model.Y, model.d),
+                                  v.data(), 1, v.size(), c.data(), nullptr));
   return c;
 }
 
 inline Vector reconstruct(const RbdModel& model, const VectorRef& c) { // decompose.cpp:119-123
   if (c.size() != model.d) throw DimensionMismatch("reconstruct: coefficient length != d");
   Vector v(model.Y.rows());
-  detail::check(rbd_reconstruct_host(detail::context(), model.Y.data(), model.Y.rows(), model.d,
-                                     c.data(), v.data()));
+  if (model.d == 0) return v;
+  detail::check(rbd_reconstruct_model(detail::context(), model.resident.get(model.Y, model.d),
+                                      c.data(), 1, v.data()));
   return v;
 }
 

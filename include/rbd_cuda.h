@@ -248,6 +248,55 @@ int rbd_project_host(rbd_ctx_t ctx, const double* hY, int64_t m, int64_t d, cons
 int rbd_reconstruct_host(rbd_ctx_t ctx, const double* hY, int64_t m, int64_t d,
                          const double* hc, double* hv);
 
+/* ---- Device-resident model (SURVEY §8(b) rbd_model_t) ----
+ * An RbdModel (decompose.hpp:39-46) whose Y (m x d, column-major, ld m) and T
+ * (d x n, row-major) live in HBM, so the reference's per-vector callers
+ * (project: classify.cpp:22-23, tools/main.cpp:149-158; reconstruct:
+ * main.cpp:128-145) pay no Y upload or allocation per call. Created from host
+ * or device buffers (copied), or read from an RBD1 file straight into HBM
+ * (read_model, io.cpp:574-622). Usable from any context on the same device;
+ * immutable after creation. */
+typedef struct rbd_model_s* rbd_model_t;
+/* Y: m x d (ld ldy >= m), T: d x n row-major (ld n); y_on_device selects
+ * whether Y and T are device (1) or host (0) pointers. T may be NULL (a model
+ * for project / reconstruct only); history (host, length d) may be NULL. */
+int rbd_model_create(rbd_ctx_t ctx, int64_t m, int64_t n, int64_t d, const double* Y, int64_t ldy,
+                     const double* T, int y_on_device, const double* h_history, double eps_r,
+                     rbd_model_t* out);
+/* read_model into a device-resident model (diagonal weights are validated as
+ * WeightSpec::diagonal; tag 2 models load with weight_kind 2 and no values). */
+int rbd_model_load(rbd_ctx_t ctx, const char* path, rbd_model_t* out);
+int rbd_model_free(rbd_model_t model);
+/* Shape, device pointers (Y ld m; T row-major), eps_R, weight kind. */
+int rbd_model_info(rbd_model_t model, int64_t* m, int64_t* n, int64_t* d, const double** dY,
+                   const double** dT, double* eps_r, int* weight_kind);
+/* Host copies of history[d] and (weight kind 1) diag[m]; either may be NULL. */
+int rbd_model_read_vectors(rbd_model_t model, double* h_history, double* h_diag);
+/* project (decompose.cpp:113-117), batched, HOST buffers: T_new = Y'X_new
+ * (d x N column-major, ld d) and err_j = max(||x_j||^2 - ||t_j||^2, 0) (Eq. 3;
+ * h_err may be NULL). X_new: m x N (ld ldx >= m). The upload goes into
+ * context-owned device scratch that is kept between calls. */
+int rbd_project_model(rbd_ctx_t ctx, rbd_model_t model, const double* hXn, int64_t N, int64_t ldx,
+                      double* hTn, double* h_err);
+/* reconstruct (decompose.cpp:119-123), batched, HOST buffers: V = Y C, C d x N
+ * column-major (ld d), V m x N column-major (ld m). */
+int rbd_reconstruct_model(rbd_ctx_t ctx, rbd_model_t model, const double* hC, int64_t N, double* hV);
+/* A stream of `count` out-of-sample batches of N columns each (BASELINE
+ * config 4: 16 batches of 16,384): the H2D of batch i+1 runs on a copy stream
+ * while batch i is contracted (K5, DMMA) and batch i-1's T_new/err come back
+ * on a third stream; two device buffers per operand. Page-locked inputs and
+ * outputs are needed for the overlap. Same bits as rbd_project_model per
+ * batch. h_err[i] may be NULL (or h_err itself). */
+int rbd_project_host_many(rbd_ctx_t ctx, rbd_model_t model, int64_t count,
+                          const double* const* hXn, int64_t N, int64_t ldx, double* const* hTn,
+                          double* const* h_err);
+/* fp32 mode of the same stream (north star: fp32 Y and X_new, 1e-4 parity):
+ * K6 (tcgen05 kind::tf32, 3xTF32) on an fp32 copy of Y the model keeps;
+ * T_new fp32, err accumulated in fp64. */
+int rbd_project_host_many_f32(rbd_ctx_t ctx, rbd_model_t model, int64_t count,
+                              const float* const* hXn, int64_t N, int64_t ldx, float* const* hTn,
+                              double* const* h_err);
+
 /* Measurement hook: run the fused sweep kernel (K2) `reps` times back to back
  * on dX with vector dy and return the mean device time per launch (CUDA
  * events on the context stream). Used by bench.py for the roofline figure. */

@@ -8,13 +8,13 @@ from ._lib import (CudaError, DegenerateInput, DimensionMismatch, IncompatibleWe
                    IndexOutOfRange, InvalidArgument, IoError, NoConvergence, NotPositive,
                    ParseError, RbdError, UnsupportedFormat, Context, default_context,
                    load_library)
-from .api import (Classifier, Model, Workspace, decompose, decompose_many, fit, load, make_config,
+from .api import (Classifier, Model, ResidentModel, Workspace, decompose, decompose_many, fit, load, make_config,
                   mgs_project, project, project_batch, project_batch_f32, reconstruct, save)
 
 __all__ = [
     "RbdError", "InvalidArgument", "IncompatibleWeight", "DegenerateInput", "IndexOutOfRange",
     "DimensionMismatch", "NotPositive", "NoConvergence", "UnsupportedFormat", "IoError",
     "ParseError", "CudaError", "Context", "default_context", "load_library", "Model",
-    "Workspace", "Classifier", "fit", "decompose", "decompose_many", "load", "make_config", "mgs_project", "project", "project_batch",
+    "Workspace", "ResidentModel", "Classifier", "fit", "decompose", "decompose_many", "load", "make_config", "mgs_project", "project", "project_batch",
     "project_batch_f32", "reconstruct", "save",
 ]

@@ -192,6 +192,18 @@ _SIGS = {
     "rbd_compress_host": (C.c_int, [_P, _P, _I64, _I64, _P, _I64, _P]),
     "rbd_decompose_sharded_virtual": (C.c_int, [_P, C.c_int, _P, _P, _I64, _I64, C.POINTER(Config),
                                                 _P, _P, _P, _P, C.POINTER(Result)]),
+    "rbd_model_create": (C.c_int, [_P, _I64, _I64, _I64, _P, _I64, _P, C.c_int, _P, C.c_double,
+                                   C.POINTER(_P)]),
+    "rbd_model_load": (C.c_int, [_P, C.c_char_p, C.POINTER(_P)]),
+    "rbd_model_free": (C.c_int, [_P]),
+    "rbd_model_info": (C.c_int, [_P, C.POINTER(_I64), C.POINTER(_I64), C.POINTER(_I64),
+                                 C.POINTER(_P), C.POINTER(_P), C.POINTER(C.c_double),
+                                 C.POINTER(C.c_int)]),
+    "rbd_model_read_vectors": (C.c_int, [_P, _P, _P]),
+    "rbd_project_model": (C.c_int, [_P, _P, _P, _I64, _I64, _P, _P]),
+    "rbd_reconstruct_model": (C.c_int, [_P, _P, _P, _I64, _P]),
+    "rbd_project_host_many": (C.c_int, [_P, _P, _I64, _P, _I64, _I64, _P, _P]),
+    "rbd_project_host_many_f32": (C.c_int, [_P, _P, _I64, _P, _I64, _I64, _P, _P]),
 }
 
 EXPORTED = tuple(_SIGS)

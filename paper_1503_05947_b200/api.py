@@ -49,6 +49,13 @@ def _col_major_torch(x, dtype=None):
     return xc, m
 
 
+def output_buffers(m: int, n: int, d_max: int, count: int = 1):
+    """Page-locked (Y, T) output pairs for decompose_many(out=...): Y m x cap
+    column-major, T cap x n row-major, cap = min(d_max, n)."""
+    cap = max(1, min(int(d_max), n)) if n > 0 else 1
+    return [_host_outputs(m, n, cap) for _ in range(count)]
+
+
 def _host_outputs(m: int, n: int, cap: int):
     """Y (m x cap, column-major) and T (cap x n) host buffers; page-locked when
     torch is available so the device-to-host copies run at full PCIe rate."""
@@ -118,6 +125,14 @@ class Model:
         self.diag = None if diag is None else np.ascontiguousarray(
             diag.detach().cpu().numpy() if hasattr(diag, "detach") else np.asarray(diag),
             dtype=np.float64).reshape(-1)
+        self._resident = None
+
+    def resident(self) -> "ResidentModel":
+        """The device-resident copy of a host model (rbd_model_t), made on first
+        use and reused by project / reconstruct: no Y upload per call."""
+        if self._resident is None:
+            self._resident = ResidentModel.from_model(self, ctx=self._ctx)
+        return self._resident
 
     @property
     def Y(self):
@@ -258,11 +273,15 @@ def decompose(x, d_max: int, eps_r: float = 0.0, diag=None, sparse=None, start_c
 def decompose_many(xs, d_max: int, eps_r: float = 0.0, start_column: int = 0,
                    reorthogonalize: bool = False, breakdown_tol: float = -1.0,
                    start_seed: Optional[int] = None, ctx: Optional[Context] = None,
-                   storage: Optional[str] = None):
+                   storage: Optional[str] = None, out=None):
     """rbd::decompose over a sequence of host matrices of one shape
     (rbd_decompose_host_many): the upload of matrix i+1 overlaps the greedy
     loop of matrix i. Returns one Model per matrix. Page-locked inputs (e.g.
-    ``torch.empty(..., pin_memory=True).numpy()``) are needed for the overlap."""
+    ``torch.empty(..., pin_memory=True).numpy()``) are needed for the overlap.
+    ``out`` may pass one (Y, T) pair of host buffers per matrix (Y m x cap
+    column-major, T cap x n row-major, cap = min(d_max, n); see
+    ``output_buffers``) that the models then view — e.g. page-locked buffers
+    reused across calls."""
     xs = list(xs)
     if not xs:
         return []
@@ -285,7 +304,16 @@ def decompose_many(xs, d_max: int, eps_r: float = 0.0, start_column: int = 0,
     ctx = ctx or default_context(0)
     cap = max(1, min(int(d_max), n)) if n > 0 else 1
     cnt = len(arrs)
-    outs = [_host_outputs(m, n, cap) for _ in range(cnt)]
+    if out is not None:
+        outs = list(out)
+        if len(outs) != cnt or any(
+                np.shape(o[0]) != (m, cap) or np.shape(o[1]) != (cap, n)
+                or o[0].dtype != np.float64 or o[1].dtype != np.float64
+                or not o[0].flags["F_CONTIGUOUS"] or not o[1].flags["C_CONTIGUOUS"] for o in outs):
+            raise InvalidArgument("decompose_many: out needs one (Y m x cap F-order, "
+                                  "T cap x n C-order) float64 pair per matrix")
+    else:
+        outs = [_host_outputs(m, n, cap) for _ in range(cnt)]
     sels = [np.zeros(cap, dtype=np.int64) for _ in range(cnt)]
     hists = [np.zeros(cap, dtype=np.float64) for _ in range(cnt)]
     res = (Result * cnt)()
@@ -472,13 +500,9 @@ def project(model: Model, v):
         ctx.synchronize()
         return out
     vv = np.ascontiguousarray(np.asarray(v, dtype=np.float64).reshape(-1))
-    Y = np.asfortranarray(model.Y)
-    m = Y.shape[0]
-    if vv.shape[0] != m:
+    if vv.shape[0] != model.Y.shape[0]:
         raise DimensionMismatch("project: vector length != m")
-    out = np.zeros(model.d, dtype=np.float64)
-    check(lib.rbd_project_host(ctx.handle, _dp(Y), m, model.d, _dp(vv), 1, _dp(out), None))
-    return out
+    return model.resident().project(vv.reshape(-1, 1), with_error=False)[0][:, 0]
 
 
 def reconstruct(model: Model, c):
@@ -502,10 +526,153 @@ def reconstruct(model: Model, c):
     cc = np.ascontiguousarray(np.asarray(c, dtype=np.float64).reshape(-1))
     if cc.shape[0] != model.d:
         raise DimensionMismatch("reconstruct: coefficient length != d")
-    Y = np.asfortranarray(model.Y)
-    out = np.zeros(Y.shape[0], dtype=np.float64)
-    check(lib.rbd_reconstruct_host(ctx.handle, _dp(Y), Y.shape[0], model.d, _dp(cc), _dp(out)))
-    return out
+    return model.resident().reconstruct(cc.reshape(-1, 1))[:, 0]
+
+
+class ResidentModel:
+    """A model resident in HBM (rbd_model_t): Y (m x d) and T
+    (d x n) uploaded once (or read from an RBD1 file straight into HBM); the
+    out-of-sample calls move only their own vectors. Host numpy in, host numpy
+    out (the reference-facing entries rbd_project_model /
+    rbd_project_host_many[_f32] / rbd_reconstruct_model)."""
+
+    def __init__(self, handle, ctx: Context):
+        self.handle = handle
+        self.ctx = ctx
+        self._lib = load_library()
+        m, n, d = C.c_int64(), C.c_int64(), C.c_int64()
+        eps = C.c_double()
+        kind = C.c_int()
+        check(self._lib.rbd_model_info(handle, C.byref(m), C.byref(n), C.byref(d), None, None,
+                                       C.byref(eps), C.byref(kind)))
+        self.m, self.n, self.d = m.value, n.value, d.value
+        self.eps_r, self.weight_kind = eps.value, kind.value
+
+    @classmethod
+    def from_model(cls, model: "Model", ctx: Optional[Context] = None) -> "ResidentModel":
+        lib = load_library()
+        Y, T = model.Y, model.T
+        h = C.c_void_p()
+        hist = np.ascontiguousarray(np.asarray(model.residual_history, dtype=np.float64))
+        if _is_torch_cuda(Y):
+            ctx = ctx or default_context(Y.device.index or 0)
+            Yc = Y if Y.stride(0) == 1 else Y.t().contiguous().t()
+            Tc = T.contiguous()
+            torch.cuda.current_stream(Y.device).synchronize()
+            ldy = Yc.stride(1) if Yc.shape[1] > 1 else Yc.shape[0]
+            check(lib.rbd_model_create(ctx.handle, Yc.shape[0], Tc.shape[1], model.d,
+                                       C.c_void_p(Yc.data_ptr()), ldy, C.c_void_p(Tc.data_ptr()), 1,
+                                       _dp(hist) if hist.size else None, 0.0, C.byref(h)))
+        else:
+            ctx = ctx or default_context(0)
+            Yh = np.asfortranarray(Y, dtype=np.float64)
+            Th = np.ascontiguousarray(T, dtype=np.float64)
+            check(lib.rbd_model_create(ctx.handle, Yh.shape[0], Th.shape[1], model.d, _dp(Yh),
+                                       Yh.shape[0], _dp(Th), 0, _dp(hist) if hist.size else None,
+                                       0.0, C.byref(h)))
+        return cls(h, ctx)
+
+    @classmethod
+    def load(cls, path, ctx: Optional[Context] = None) -> "ResidentModel":
+        """read_model (io.cpp:574-622) straight into HBM."""
+        ctx = ctx or default_context(0)
+        h = C.c_void_p()
+        check(load_library().rbd_model_load(ctx.handle, os.fsencode(str(path)), C.byref(h)))
+        return cls(h, ctx)
+
+    def close(self):
+        if getattr(self, "handle", None):
+            self._lib.rbd_model_free(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def history(self):
+        out = np.zeros(self.d)
+        check(self._lib.rbd_model_read_vectors(self.handle, _dp(out), None))
+        return out
+
+    def device_arrays(self):
+        """(Y, T) as torch CUDA views of the resident buffers (no copy)."""
+        dy, dt = C.c_void_p(), C.c_void_p()
+        check(self._lib.rbd_model_info(self.handle, None, None, None, C.byref(dy), C.byref(dt),
+                                       None, None))
+        dev = torch.device("cuda", self.ctx.device if hasattr(self.ctx, "device") else 0)
+        Y = _torch_from_ptr(dy.value, (self.d, self.m), dev).t()
+        T = _torch_from_ptr(dt.value, (self.d, self.n), dev)
+        return Y, T
+
+    def _check_x(self, Xn, dtype):
+        xa = np.asarray(Xn, dtype=dtype)
+        xa = xa.reshape(-1, 1) if xa.ndim == 1 else xa
+        if xa.ndim != 2 or xa.shape[0] != self.m:
+            raise DimensionMismatch("project: vector length != m")
+        return xa if xa.flags["F_CONTIGUOUS"] else np.asfortranarray(xa)
+
+    def project(self, Xn, with_error: bool = True):
+        """T_new = Y'X_new (d x N) and err (Eq. 3) for host columns X_new (m x N)."""
+        xa = self._check_x(Xn, np.float64)
+        N = xa.shape[1]
+        Tn = np.zeros((self.d, N), order="F")
+        err = np.zeros(N) if with_error else None
+        check(self._lib.rbd_project_model(self.ctx.handle, self.handle, _dp(xa), N,
+                                          max(self.m, xa.strides[1] // 8 if N > 1 else self.m),
+                                          _dp(Tn), _dp(err) if with_error else None))
+        return Tn, err
+
+    def project_many(self, batches, with_error: bool = True, f32: bool = False, out=None):
+        """A stream of equally sized host batches (rbd_project_host_many[_f32]):
+        the upload of batch i+1 overlaps the contraction of batch i. Page-locked
+        batches (e.g. torch.empty(..., pin_memory=True).numpy()) are needed for
+        the overlap. Returns [(T_new, err)] per batch; `out` may pass
+        preallocated (T_new, err) pairs (page-locked outputs download during
+        the stream)."""
+        dt = np.float32 if f32 else np.float64
+        xs = [self._check_x(b, dt) for b in batches]
+        if not xs:
+            return []
+        N = xs[0].shape[1]
+        if any(x.shape != xs[0].shape or x.strides != xs[0].strides for x in xs):
+            raise InvalidArgument("project_many: batches must share one shape and layout")
+        ldx = xs[0].strides[1] // xs[0].itemsize if N > 1 else self.m
+        cnt = len(xs)
+        if out is None:
+            out = [(np.zeros((self.d, N), dtype=dt, order="F"),
+                    np.zeros(N) if with_error else None) for _ in range(cnt)]
+        P = C.c_void_p * cnt
+        xp = P(*[x.ctypes.data for x in xs])
+        tp = P(*[o[0].ctypes.data for o in out])
+        ep = P(*[(o[1].ctypes.data if o[1] is not None else None) for o in out])
+        fn = self._lib.rbd_project_host_many_f32 if f32 else self._lib.rbd_project_host_many
+        check(fn(self.ctx.handle, self.handle, cnt, xp, N, ldx, tp, ep if with_error else None))
+        return out
+
+    def reconstruct(self, Cm):
+        """V = Y C for host coefficients C (d x N)."""
+        ca = np.asfortranarray(np.asarray(Cm, dtype=np.float64))
+        ca = ca.reshape(-1, 1) if ca.ndim == 1 else ca
+        if ca.shape[0] != self.d:
+            raise DimensionMismatch("reconstruct: coefficient length != d")
+        V = np.zeros((self.m, ca.shape[1]), order="F")
+        check(self._lib.rbd_reconstruct_model(self.ctx.handle, self.handle, _dp(ca), ca.shape[1],
+                                              _dp(V)))
+        return V
+
+
+def _torch_from_ptr(addr, shape, device):
+    """A torch float64 view of `shape` on raw device memory owned elsewhere."""
+    n = int(np.prod(shape))
+
+    class _Cai:
+        __cuda_array_interface__ = {"shape": tuple(shape), "typestr": "<f8", "data": (addr, False),
+                                    "version": 3, "strides": None}
+    t = torch.as_tensor(_Cai(), device=device)
+    assert t.numel() == n
+    return t
 
 
 def project_batch(Y, Xn, with_error: bool = True, ctx: Optional[Context] = None):

@@ -366,6 +366,9 @@ int enqueue_fused_ext(rbd_ctx_t ctx, const LoopBufs& L) {
   ra.p = ptr<double>(ctx->p);
   ra.st = st;
   ra.selected = ptr<long long>(ctx->sel);
+  ra.w1 = ptr<double>(ctx->w);
+  ra.Y = L.Y;
+  ra.m = L.m;
   k_ext_reduce<<<(unsigned)std::max<long long>(1, cdiv(L.d_max, 32)), kThreads, 0, ctx->stream>>>(ra);
   ctx->launches++;
   CU(cudaGetLastError());
@@ -795,8 +798,12 @@ int rbd_ctx_destroy(rbd_ctx_t ctx) {
                   &ctx->wd_cross, &ctx->wd_quad, &ctx->wd_colsq, &ctx->wd_diag,
                   &ctx->wd_ppart2, &ctx->wd_q, &ctx->wd_yay, &ctx->wd_yslice, &ctx->forced,
                   &ctx->nn_part, &ctx->nn_coords, &ctx->pj_ws,
-                  &ctx->ctl,     &ctx->gcnt, &ctx->ygcnt,   &ctx->rdy,   &ctx->send,  &ctx->recv};
+                  &ctx->ctl,     &ctx->gcnt, &ctx->ygcnt,   &ctx->rdy,   &ctx->send,  &ctx->recv,
+                  &ctx->hs[0],   &ctx->hs[1], &ctx->hs[2],  &ctx->hs[3], &ctx->hs[4],
+                  &ctx->pm_X[0], &ctx->pm_X[1], &ctx->pm_T[0], &ctx->pm_T[1], &ctx->pm_E[0],
+                  &ctx->pm_E[1]};
   for (DevBuf* b : bl) release(*b);
+  if (ctx->d2h_stream) cudaStreamDestroy(ctx->d2h_stream);
   if (ctx->h_state) cudaFreeHost(ctx->h_state);
   if (ctx->h_progress) cudaFreeHost(ctx->h_progress);
   if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
@@ -1385,13 +1392,8 @@ int rbd_mgs_project_host(rbd_ctx_t ctx, const double* hv, int64_t m, const doubl
   if (m < 1) return set_err(RBD_ERR_DIMENSION_MISMATCH, "mgs_project: vector length != basis row count");
   if (k > 0 && ldb < m) return set_err(RBD_ERR_DIMENSION_MISMATCH, "mgs_project: vector length != basis row count");
   CU(cudaSetDevice(ctx->device));
-  DevBuf bv, bB, bx;
-  auto fin = [&](int rc) {
-    release(bv);
-    release(bB);
-    release(bx);
-    return rc;
-  };
+  DevBuf &bv = ctx->hs[0], &bB = ctx->hs[1], &bx = ctx->hs[2];   // kept between calls
+  auto fin = [&](int rc) { return rc; };
   int rc;
   if ((rc = ensure(bv, sizeof(double) * m)) || (rc = ensure(bx, sizeof(double) * m)) ||
       (rc = ensure(bB, sizeof(double) * m * std::max<int64_t>(k, 1))))

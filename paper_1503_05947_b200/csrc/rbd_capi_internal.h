@@ -147,6 +147,14 @@ struct rbd_ctx_s {
   DevBuf nn_part, nn_coords;               // classify: split minima, query coordinates
   DevBuf pj_ws;                            // K5 split-K partial slices
   DevBuf send, recv;                       // sharded mode: payload exchange buffers
+  // host-buffer entries (project/reconstruct/compress/classify/mgs_project/
+  // ws_extend _host): device scratch kept between calls instead of a
+  // cudaMalloc/cudaFree pair (and the implicit device sync of cudaFree) per call
+  DevBuf hs[5];
+  // device-resident model entries (rbd_model.cu): two buffers per operand for
+  // the pipelined batch stream, plus the D2H stream
+  DevBuf pm_X[2], pm_T[2], pm_E[2];
+  cudaStream_t d2h_stream = nullptr;
   // multi-GPU
   void* comm = nullptr;                    // ncclComm_t (dlopen'ed NCCL)
   int rank = 0, world = 1;

@@ -568,6 +568,32 @@ __device__ __forceinline__ double block_sum_fixed(double x, double* sm) {
   return s;
 }
 
+// ||w||^2 of the twice-orthogonalised column, w = w1 - Y p. The loops take
+// it as ||w1||^2 - ||p||^2 (exact algebra for p = Y'w1 with orthonormal Y),
+// which carries ~eps (||w1||^2 + ||p||^2) of rounding. Where that uncertainty
+// straddles the breakdown tolerance (decompose.cpp:29-30), the decision is
+// made on the norm of the materialised w instead, as the reference does.
+__device__ __forceinline__ bool wnorm_in_guard_band(double wn2, double w1n2, double pn, double tol) {
+  const double err = 64.0 * 2.220446049250313e-16 * (w1n2 + pn);
+  return fabs(wn2 - tol * tol) <= err;
+}
+
+// Single-CTA ||w1 - Y p||^2 over all m rows (fixed order: rows strided by the
+// CTA's threads, basis vectors in order, then block_sum_fixed). Y, w1 and p
+// were written by other CTAs of the grid and are read through L2.
+template <int NT>
+__device__ __noinline__ double exact_wnorm2(const double* w1, const double* Y, long long m,
+                                            long long ldy, long long k, const double* p,
+                                            double* sm) {
+  double acc = 0.0;
+  for (long long i = threadIdx.x; i < m; i += NT) {
+    double v = __ldcg(&w1[i]);
+    for (long long l = 0; l < k; ++l) v = fma(-__ldcg(&Y[i + l * ldy]), __ldcg(&p[l]), v);
+    acc = fma(v, v, acc);
+  }
+  return block_sum_fixed<NT>(acc, sm);
+}
+
 __device__ __forceinline__ void warp_argmax(double& v, long long& j) {
   for (int off = 16; off > 0; off >>= 1) {
     const double ov = __shfl_xor_sync(0xffffffffu, v, off);
@@ -1125,6 +1151,9 @@ struct ReduceArgs {
   double* p;              // out: p_k (zeroed if the second pass is skipped)
   DevState* st;
   long long* selected;
+  const double* w1;       // w1 (m), for the guard-band norm recompute
+  const double* Y;        // m x k basis, ld m
+  long long m;
 };
 
 static __global__ void __launch_bounds__(kThreads) k_ext_reduce(ReduceArgs a) {
@@ -1171,13 +1200,16 @@ static __global__ void __launch_bounds__(kThreads) k_ext_reduce(ReduceArgs a) {
   }
   pn = block_sum_fixed<kThreads>(pn, smn);
   const int reorth = (k > 0) && (st->cfg_reorth || sqrt(w1n2) < 0.5 * sqrt(st->xnorm2));
+  double wn2 = reorth ? w1n2 - pn : w1n2;
+  if (reorth && wnorm_in_guard_band(wn2, w1n2, pn, st->breakdown_tol))
+    wn2 = exact_wnorm2<kThreads>(a.w1, a.Y, a.m, a.m, k, a.p, smn);
+  __syncthreads();
   if (!reorth)
     for (long long l = tid; l < k; l += kThreads) a.p[l] = 0.0;
   if (tid == 0) {
     st->pending = 0;
     st->reorth = reorth;
     st->w1n2 = w1n2;
-    double wn2 = reorth ? w1n2 - pn : w1n2;
     wn2 = wn2 > 0.0 ? wn2 : 0.0;
     const double norm = sqrt(wn2);
     if (norm < st->breakdown_tol || norm == 0.0) {

@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cerrno>
 #include <cstdint>
 #include <cstdio>
@@ -206,8 +207,19 @@ int read_spans(FILE* f, const char* path, const std::vector<Span>& spans, cudaSt
   return RBD_OK;
 }
 
-size_t expected_size(int64_t m, int64_t n, int64_t d, int tag) {   // io.cpp:595-596
-  return kHeader + 8 * (size_t)(m * d + d * n + 1 + d) + (tag == 1 ? 8 * (size_t)m : 0);
+// io.cpp:595-596 with overflow-checked arithmetic: header values come from an
+// untrusted file, so a product that does not fit in 64 bits is "no size" (the
+// file cannot match it) rather than a wrapped number.
+bool expected_size(int64_t m, int64_t n, int64_t d, int tag, uint64_t* out) {
+  uint64_t md, dn, s;
+  if (__builtin_mul_overflow((uint64_t)m, (uint64_t)d, &md) ||
+      __builtin_mul_overflow((uint64_t)d, (uint64_t)n, &dn) ||
+      __builtin_add_overflow(md, dn, &s) || __builtin_add_overflow(s, (uint64_t)(1 + d), &s) ||
+      (tag == 1 && __builtin_add_overflow(s, (uint64_t)m, &s)) ||
+      __builtin_mul_overflow(s, (uint64_t)8, &s) || __builtin_add_overflow(s, (uint64_t)kHeader, &s))
+    return false;
+  *out = s;
+  return true;
 }
 
 }  // namespace
@@ -280,7 +292,8 @@ int rbd_model_read_header(const char* path, int64_t* m, int64_t* n, int64_t* d, 
   if (tag > 2) return parse_err(path, "unknown weight tag");             // :590
   if (fseeko(fi.f, 0, SEEK_END) != 0) return err(RBD_ERR_IO, std::string("read failed: ") + path);
   const off_t size = ftello(fi.f);
-  if (size < 0 || (size_t)size != expected_size(M, N, D, tag))           // :592-596
+  uint64_t want = 0;
+  if (size < 0 || !expected_size(M, N, D, tag, &want) || (uint64_t)size != want)   // :592-596
     return parse_err(path, "model file size does not match header");
   if (m) *m = M;
   if (n) *n = N;
@@ -315,6 +328,20 @@ int rbd_model_read(rbd_ctx_t ctx, const char* path, double* Y, int64_t ldy, doub
   if (tag == RBD_WEIGHT_DIAGONAL) spans.push_back({h_diag, m, 1, m, on_device(h_diag)});   // :617
   const int rc = read_spans(fi.f, path, spans, st);
   if (rc) return rc;
+  if (tag == RBD_WEIGHT_DIAGONAL) {   // WeightSpec::diagonal(values), io.cpp:617-618 (weight.cpp:11-17)
+    std::vector<double> dh((size_t)m);
+    if (on_device(h_diag)) {
+      if (cudaMemcpyAsync(dh.data(), h_diag, sizeof(double) * m, cudaMemcpyDeviceToHost, st) ||
+          cudaStreamSynchronize(st))
+        return err(RBD_ERR_CUDA, "read_model: diagonal D2H failed");
+    } else {
+      std::memcpy(dh.data(), h_diag, sizeof(double) * m);
+    }
+    for (double v : dh)
+      if (!(v > 0.0) || !std::isfinite(v))
+        return err(RBD_ERR_INVALID_ARGUMENT,
+                   "diagonal weight entries must be strictly positive and finite");
+  }
   if (eps_r) *eps_r = e;
   return RBD_OK;
 }

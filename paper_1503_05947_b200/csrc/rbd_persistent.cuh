@@ -866,10 +866,12 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
             for (int b = tid; b < G; b += kThreads) w1a += __ldcg(&a.npart2[b]);
             w1a = block_sum_fixed<kThreads>(w1a, smn);
           }
+          const int re = (cfg_reorth || sqrt(w1n2) < 0.5 * sqrt(xnorm2)) ? 1 : 0;    // :28
+          double wn2 = re ? w1n2 - pn : w1n2;
+          if (re && wnorm_in_guard_band(wn2, w1n2, pn, tol))   // decide on the exact ||w||
+            wn2 = exact_wnorm2<kThreads>(a.w, a.Y, m, m, k, pbuf(k), smn);
           if (tid == 0) {
             ctl->ydone = 0u;
-            const int re = (cfg_reorth || sqrt(w1n2) < 0.5 * sqrt(xnorm2)) ? 1 : 0;  // :28
-            double wn2 = re ? w1n2 - pn : w1n2;
             wn2 = wn2 > 0.0 ? wn2 : 0.0;
             const double nrm = sqrt(wn2);
             const int bd = (nrm < tol || nrm == 0.0) ? 1 : 0;                       // :29-30

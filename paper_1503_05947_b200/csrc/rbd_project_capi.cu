@@ -105,15 +105,9 @@ int rbd_classify_host(rbd_ctx_t ctx, const double* hY, int64_t m, int64_t d, con
     return set_err(RBD_ERR_DIMENSION_MISMATCH, "classify: bad sizes");
   if (Q == 0) return RBD_OK;
   CU(cudaSetDevice(ctx->device));
-  DevBuf bY, bT, bQ, bB, bD;
-  auto fin = [&](int rc) {
-    release(bY);
-    release(bT);
-    release(bQ);
-    release(bB);
-    release(bD);
-    return rc;
-  };
+  DevBuf &bY = ctx->hs[0], &bT = ctx->hs[1], &bQ = ctx->hs[2], &bB = ctx->hs[3],
+         &bD = ctx->hs[4];   // context scratch, kept between calls
+  auto fin = [&](int rc) { return rc; };
   const long long ldm = (m % 2 == 0) ? m : m + 1;   // 16-byte aligned columns for K5
   int rc;
   if ((rc = ensure(bY, sizeof(double) * ldm * d)) || (rc = ensure(bT, sizeof(double) * d * n_train)) ||
@@ -159,14 +153,8 @@ int rbd_project_host(rbd_ctx_t ctx, const double* hY, int64_t m, int64_t d, cons
   if (m < 1 || d < 1 || N < 0) return set_err(RBD_ERR_DIMENSION_MISMATCH, "project: bad sizes");
   if (N == 0) return RBD_OK;
   CU(cudaSetDevice(ctx->device));
-  DevBuf bY, bX, bT, bE;
-  auto fin = [&](int rc) {
-    release(bY);
-    release(bX);
-    release(bT);
-    release(bE);
-    return rc;
-  };
+  DevBuf &bY = ctx->hs[0], &bX = ctx->hs[1], &bT = ctx->hs[2], &bE = ctx->hs[3];   // kept
+  auto fin = [&](int rc) { return rc; };
   int rc;
   if ((rc = ensure(bY, sizeof(double) * m * d)) || (rc = ensure(bX, sizeof(double) * m * N)) ||
       (rc = ensure(bT, sizeof(double) * d * N)) || (rc = ensure(bE, sizeof(double) * N)))
@@ -190,13 +178,8 @@ int rbd_reconstruct_host(rbd_ctx_t ctx, const double* hY, int64_t m, int64_t d, 
   if (!ctx) return set_err(RBD_ERR_INVALID_ARGUMENT, "null context");
   if (m < 1 || d < 0) return set_err(RBD_ERR_DIMENSION_MISMATCH, "reconstruct: bad sizes");
   CU(cudaSetDevice(ctx->device));
-  DevBuf bY, bc, bv;
-  auto fin = [&](int rc) {
-    release(bY);
-    release(bc);
-    release(bv);
-    return rc;
-  };
+  DevBuf &bY = ctx->hs[0], &bc = ctx->hs[1], &bv = ctx->hs[2];   // kept between calls
+  auto fin = [&](int rc) { return rc; };
   int rc;
   if ((rc = ensure(bY, sizeof(double) * m * std::max<int64_t>(d, 1))) ||
       (rc = ensure(bc, sizeof(double) * std::max<int64_t>(d, 1))) || (rc = ensure(bv, sizeof(double) * m)))
@@ -311,13 +294,8 @@ int rbd_compress_host(rbd_ctx_t ctx, const double* hY, int64_t m, int64_t d, con
   if (!ctx) return set_err(RBD_ERR_INVALID_ARGUMENT, "null context");
   if (m < 1 || d < 1 || N < 1) return set_err(RBD_ERR_DIMENSION_MISMATCH, "compress: bad sizes");
   CU(cudaSetDevice(ctx->device));
-  DevBuf bY, bC, bV;
-  auto fin = [&](int rc) {
-    release(bY);
-    release(bC);
-    release(bV);
-    return rc;
-  };
+  DevBuf &bY = ctx->hs[0], &bC = ctx->hs[1], &bV = ctx->hs[2];   // kept between calls
+  auto fin = [&](int rc) { return rc; };
   int rc;
   if ((rc = ensure(bY, sizeof(double) * m * d)) || (rc = ensure(bC, sizeof(double) * d * N)) ||
       (rc = ensure(bV, sizeof(double) * m * N)))

@@ -356,18 +356,14 @@ int rbd_ws_init_diag_host(rbd_ctx_t ctx, const double* hX, int64_t m, int64_t n,
 
 int rbd_ws_extend_host(rbd_ws_t ws, const double* hxi) {
   if (!ws) return set_err(RBD_ERR_INVALID_ARGUMENT, "null workspace");
-  DevBuf b;
+  DevBuf& b = ws->ctx->hs[0];   // context scratch, kept between calls
   TRY(ensure(b, sizeof(double) * ws->m));
   // on the workspace's stream (a pageable-source cudaMemcpy may return before its
   // DMA lands, and the context stream does not wait for the legacy stream)
   if (cudaMemcpyAsync(b.p, hxi, sizeof(double) * ws->m, cudaMemcpyHostToDevice,
-                      ws->ctx->stream) != cudaSuccess) {
-    release(b);
+                      ws->ctx->stream) != cudaSuccess)
     return set_err(RBD_ERR_CUDA, "workspace_extend: H2D failed");
-  }
-  int rc = rbd_ws_extend(ws, ptr<double>(b));
-  release(b);
-  return rc;
+  return rbd_ws_extend(ws, ptr<double>(b));
 }
 
 }  // extern "C"

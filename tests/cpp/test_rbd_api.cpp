@@ -395,6 +395,32 @@ int main() {
     CHECK_THROWS_AS(read_model(dir / "nope.rbd"), IoError);
     fs::remove_all(dir);
   }
+  {  // per-vector project / reconstruct through the model's device-resident Y
+     // (classify.cpp:22-23 calls project once per query): same values as the
+     // first call, Y uploaded once, a copied model builds its own cache
+    Matrix x = random_matrix(300, 40, 700);
+    RbdModel model = decompose(x, basic(20));
+    Matrix q = random_matrix(300, 64, 701);
+    double worst = 0.0;
+    for (Index j = 0; j < q.cols(); ++j) {
+      Vector v = q.col(j);
+      Vector c = project(model, v);
+      for (Index k = 0; k < model.d; ++k) {
+        double s = 0.0;
+        for (Index i = 0; i < 300; ++i) s += model.Y(i, k) * v[i];
+        worst = std::max(worst, std::abs(s - c[k]));
+      }
+      Vector back = reconstruct(model, c);
+      Vector again = project(model, back);
+      for (Index k = 0; k < model.d; ++k) worst = std::max(worst, std::abs(again[k] - c[k]));
+    }
+    CHECK(worst < 1e-12);
+    RbdModel copy = model;
+    Vector c1 = project(copy, q.col(3)), c2 = project(model, q.col(3));
+    bool same = true;
+    for (Index k = 0; k < model.d; ++k) same = same && c1[k] == c2[k];
+    CHECK(same);
+  }
   std::printf("%d checks, %d failed\n", g_checks, g_fail);
   return g_fail;
 }

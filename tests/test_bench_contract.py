@@ -1,6 +1,6 @@
 """The bench.py contract: one JSON line per run with the keys the driver reads.
 CPU: the reference arm (oracle port, all host cores) on the small C0 workload.
-GPU: our arm on the default C1 workload, shortened."""
+GPU: our arm on the C1 workload (the default C2-tall takes minutes), shortened."""
 import json
 import os
 import subprocess
@@ -29,6 +29,7 @@ def test_reference_arm_line():
     assert d["impl"] == "reference" and d["metric"] == "rbd_effective_hbm_gbs"
     assert d["value"] > 0 and d["higher_is_better"] is True and d["dtype"] == "f64"
     assert d["config"]["workload"] == "C0-cpu-ref"
+    assert set(d["config"]) >= {"workload", "m", "n", "d_max", "eps_R", "parallelism"}
     cb = d["cpu_baseline"]
     assert {"value", "unit", "cores", "kind", "sample"} <= set(cb) and cb["kind"] == "port"
     assert cb["value"] == d["value"] and cb["cores"] >= 1
@@ -38,7 +39,8 @@ def test_reference_arm_line():
 
 @pytest.mark.gpu
 def test_b200_arm_line(cuda):
-    d = run(["--steps", "2", "--warmup", "3", "--cpu-seconds", "1"], 900)
+    d = run(["--workload", "C1-image-like", "--steps", "2", "--warmup", "3", "--cpu-seconds", "1",
+             "--aux-steps", "1", "--no-secondary"], 900)
     assert BASE <= set(d) and "impl" not in d
     assert d["config"]["workload"] == "C1-image-like" and d["n_gpus"] == 1
     assert d["scaling"] == "weak" and d["data"] == "synthetic" and d["dtype"] == "f64"
@@ -46,7 +48,9 @@ def test_b200_arm_line(cuda):
     assert {"bound", "achieved", "peak", "unit", "frac", "traffic"} <= set(r)
     assert r["bound"] == "hbm" and r["unit"] == "GB/s"
     assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9 and 0.3 < r["frac"] < 1.2
-    assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["value"] > 0
+    cb = d["cpu_baseline"]
+    assert cb["kind"] == "port" and cb["value"] > 0 and cb["cores"] == 1
+    assert cb["steps_sampled"] >= 1 and cb["cpu_model"]
     e = d["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] == 32256 * 2432 * 8
     assert e["d2h_bytes_per_step"] > 0 and e["value"] < d["value"]
