@@ -170,6 +170,17 @@ def ncu_traffic(workload):
     return t.get(workload)
 
 
+def host_mem_available():
+    try:
+        with open("/proc/meminfo") as f:
+            for ln in f:
+                if ln.startswith("MemAvailable:"):
+                    return int(ln.split()[1]) * 1024
+    except OSError:
+        pass
+    return None
+
+
 def read_peak_gbs(dev, gib: int = 4, reps: int = 10):
     import torch
     try:
@@ -247,7 +258,14 @@ def run_reference(args):
     import torch
     wname = default_workload(args, world)
     dev = torch.device("cuda", local) if torch.cuda.is_available() else torch.device("cpu")
-    w, Xd, eps = make_workload(wname, dev)
+    from paper_1503_05947_b200 import configs
+    wfull = configs.WORKLOADS[wname]
+    block = None
+    if wfull.m * wfull.n * 8 > 64e9:   # C3 (137 GB): a column block of the same X
+        block = 2048
+        w, Xd, eps = make_workload(wname, dev, 0, block)
+    else:
+        w, Xd, eps = make_workload(wname, dev)
     d_max = args.d_max or w.d_max
     X = np.asfortranarray(Xd.cpu().numpy())
     del Xd
@@ -255,8 +273,8 @@ def run_reference(args):
         torch.cuda.empty_cache()
     cores = os.cpu_count() or 1
     import oracle
-    per_est = 2.0 * w.m * w.n * 8 / (8e9 * cores)      # two X passes per greedy step
-    S = int(max(1, min(d_max, args.ref_seconds / max(per_est, 1e-6))))
+    per_est = 2.0 * w.m * (block or w.n) * 8 / (8e9 * cores)   # two X passes per greedy step
+    S = int(max(1, min(d_max, block or d_max, args.ref_seconds / max(per_est, 1e-6))))
     for _ in range(args.warmup):
         oracle.decompose(X, d_max, eps, nthreads=cores, max_steps=S)
     loops, inits, done = 0.0, 0.0, 0
@@ -267,9 +285,11 @@ def run_reference(args):
         inits += r.t_init_s
         done += r.d
     wall = time.perf_counter() - t0
-    bytes_per = w.m * w.n * 8
+    ncols = block or w.n
+    bytes_per = w.m * ncols * 8
     val = bytes_per * done / loops / 1e9
-    sample = (f"first {S} of {d_max} greedy steps of {w.name} ({w.m}x{w.n} fp64) per bench step, "
+    sample = (f"first {S} of {d_max} greedy steps of {w.name} ({w.m}x{ncols} fp64"
+              f"{f', the first {block} of its {w.n} columns' if block else ''}) per bench step, "
               f"oracle port (decompose.cpp:53-111, two X passes per step), {cores} threads; "
               f"value = X bytes x steps / greedy-loop time (the per-call validation + "
               f"workspace_init pass, {inits / max(args.steps, 1):.2f} s, is excluded: a full "
@@ -280,7 +300,7 @@ def run_reference(args):
         "ms_per_step": wall / max(args.steps, 1) * 1e3, "higher_is_better": True,
         "scaling": "strong" if w.name.startswith("C3") else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": workload_config(w, eps, world, d_max),
+        "config": workload_config(wfull, eps, world, d_max),
         "cpu_baseline": {"value": val, "unit": "GB/s", "cores": cores, "kind": "port",
                          "sample": sample, "cpu_model": cpu_model()},
         "e2e": {"value": val, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -550,6 +570,7 @@ def run_sharded(args):
     import paper_1503_05947_b200 as rbd
     from paper_1503_05947_b200 import configs, distributed as rd
     wname = default_workload(args, world)
+    r = None
     w0 = configs.WORKLOADS[wname]
     plan = rd.plan_shards(w0.n, world)
     o, nl = plan.offsets[rank], plan.n_locals[rank]
@@ -600,6 +621,55 @@ def run_sharded(args):
         t_max = float(t.item())
     total = w.m * w.n * 8 * sum(ds)
     value = total / (t_max / 1e3) / 1e9
+
+    # ---- e2e: this rank's shard from pinned host memory -> HBM, the sharded
+    #      decompose, Y and T_local back; only where the host can pin the shards ----
+    e2e = None
+    shard_bytes = w.m * nl * 8
+    avail = host_mem_available()
+    local_ranks = int(os.environ.get("LOCAL_WORLD_SIZE", world))
+    if not args.no_e2e and avail and avail > 2.0 * shard_bytes * local_ranks:
+        Xh_t = torch.empty((nl, w.m), dtype=torch.float64, pin_memory=True)
+        Xh_t.copy_(X.t())
+        Xd_t = X.t()                         # the device shard buffer, refilled every step
+        Ke = max(1, min(args.e2e_steps, args.steps))
+        barrier()
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        de = []
+        for _ in range(Ke):
+            Xd_t.copy_(Xh_t, non_blocking=True)
+            torch.cuda.current_stream(dev).synchronize()
+            r = rd.decompose_sharded(X, plan, rank, d_max, eps, ctx=ctx)
+            Yh = r.Y.cpu()
+            Th = r.T_local.cpu()
+            de.append(r.d)
+        te = time.perf_counter() - t0
+        if world > 1:
+            import torch.distributed as dist
+            t = torch.tensor([te], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            te = float(t.item())
+        e2e = {"value": w.m * w.n * 8 * sum(de) / te / 1e9, "unit": "GB/s",
+               "h2d_bytes_per_step": shard_bytes,
+               "d2h_bytes_per_step": int(Yh.numel() * 8 + Th.numel() * 8),
+               "ms_per_step": te * 1e3 / Ke, "steps": Ke,
+               "entry": "pinned host shard -> HBM (copy engine), rd.decompose_sharded, Y and "
+                        "T_local -> host; per rank, max over ranks"}
+        del Xh_t
+    elif not args.no_e2e:
+        e2e = {"skipped": f"host RAM: {(avail or 0) / 1e9:.0f} GB available, the pinned shards "
+                          f"need {2.0 * shard_bytes * local_ranks / 1e9:.0f} GB (2x {local_ranks} x "
+                          f"{shard_bytes / 1e9:.1f} GB)"}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        # single-thread oracle on a column block of the same X (the whole 137 GB
+        # does not fit the host): the first 2048 columns
+        nb = min(nl, 2048)
+        Xs = np.asfortranarray(X[:, :nb].cpu().numpy())
+        ws = configs.Workload(w.name + f"[:, :{nb}]", w.m, nb, w.d_max, 0.0, 0.0, w.seed, w.describe)
+        cpu = cpu_baseline_leg(Xs, ws, eps, min(d_max, nb), args.cpu_seconds)
+        del Xs
     if rank == 0:
         peak, src = peak_hbm()
         per_gpu = value / world
@@ -611,10 +681,12 @@ def run_sharded(args):
             "config": workload_config(w, eps, world, d_max),
             "roofline": {"bound": "hbm", "achieved": per_gpu, "peak": peak, "unit": "GB/s",
                          "frac": per_gpu / peak, "traffic": None,
-                         "kernel": "k_rbd_persistent<2,true> per step + NCCL exchange",
+                         "kernel": "k_rbd_persistent<2,true> per step + NCCL record allgather + "
+                                   "payload allreduce, 8-step CUDA graph",
                          "note": "per-GPU X bytes x steps / time", "peak_source": src},
-            "cpu_baseline": None, "e2e": None, "gpu_launches": ctx.launches - launches0,
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": ctx.launches - launches0,
             "clocks": clk, "shard_cols": list(plan.n_locals), "d_per_step": ds,
+            "step_graph": bool(r.result.reserved),
         }
         print(json.dumps(line), flush=True)
     ctx.close()

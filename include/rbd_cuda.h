@@ -306,11 +306,21 @@ int rbd_time_sweep(rbd_ctx_t ctx, const double* dX, int64_t m, int64_t n, int64_
 /* ---- multi-GPU (one process per GPU; X sharded by contiguous column blocks,
  *      Y replicated) ---- */
 #define RBD_UNIQUE_ID_BYTES 128
+/* The winner rule of the per-step record exchange (host-callable; the device
+ * kernels run the same code, csrc/rbd_select.h): recs[2r] = rank r's best
+ * residual, recs[2r+1] = its GLOBAL column index as int64 bits (-1: none).
+ * Largest residual, ties to the smallest global index (the reference's strict
+ * '>' scan, workspace.cpp:107-113). *owner = -1 when no rank has a candidate. */
+int rbd_shard_pick(const double* recs, int nranks, double* best_r, int64_t* best_j, int* owner);
 int rbd_comm_unique_id(char out[RBD_UNIQUE_ID_BYTES]);
 int rbd_ctx_init_comm(rbd_ctx_t ctx, int rank, int world, const char id[RBD_UNIQUE_ID_BYTES]);
 /* Sharded decompose: this rank owns global columns [col_offset, col_offset+n_local)
  * of an m x n_global X. dT_local: d_max x n_local row-major. selected holds
- * GLOBAL column indices; Y/selected/history are identical on every rank. */
+ * GLOBAL column indices; Y/selected/history are identical on every rank. Per
+ * step: the local fused sweep, an ncclAllGather of 16-byte records, the
+ * owner's payload {col_sq, x_j, T[0:k+1, j]} by a -0.0-padded ncclAllReduce
+ * (exact), replayed from a CUDA graph of 8 steps (RBD_SHARD_GRAPH=0: eager;
+ * result->reserved = 1 when the graph ran). */
 int rbd_decompose_sharded(rbd_ctx_t ctx, const double* dX_local, int64_t m, int64_t n_local,
                           int64_t ldx, int64_t col_offset, int64_t n_global,
                           const rbd_config_t* cfg, double* dY, double* dT_local,

@@ -181,6 +181,8 @@ _SIGS = {
     "rbd_reconstruct_host": (C.c_int, [_P, _P, _I64, _I64, _P, _P]),
     "rbd_time_sweep": (C.c_int, [_P, _P, _I64, _I64, _I64, _P, C.c_int, _DP]),
     "rbd_comm_unique_id": (C.c_int, [C.c_char_p]),
+    "rbd_shard_pick": (C.c_int, [_P, C.c_int, C.POINTER(C.c_double), C.POINTER(_I64),
+                                 C.POINTER(C.c_int)]),
     "rbd_ctx_init_comm": (C.c_int, [_P, C.c_int, C.c_int, C.c_char_p]),
     "rbd_decompose_sharded": (C.c_int, [_P, _P, _I64, _I64, _I64, _I64, _I64, C.POINTER(Config),
                                         _P, _P, _P, _P, C.POINTER(Result)]),

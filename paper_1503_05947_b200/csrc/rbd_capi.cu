@@ -799,11 +799,13 @@ int rbd_ctx_destroy(rbd_ctx_t ctx) {
                   &ctx->wd_ppart2, &ctx->wd_q, &ctx->wd_yay, &ctx->wd_yslice, &ctx->forced,
                   &ctx->nn_part, &ctx->nn_coords, &ctx->pj_ws,
                   &ctx->ctl,     &ctx->gcnt, &ctx->ygcnt,   &ctx->rdy,   &ctx->send,  &ctx->recv,
+                  &ctx->srec,    &ctx->rrec,
                   &ctx->hs[0],   &ctx->hs[1], &ctx->hs[2],  &ctx->hs[3], &ctx->hs[4],
                   &ctx->pm_X[0], &ctx->pm_X[1], &ctx->pm_T[0], &ctx->pm_T[1], &ctx->pm_E[0],
                   &ctx->pm_E[1]};
   for (DevBuf* b : bl) release(*b);
   if (ctx->d2h_stream) cudaStreamDestroy(ctx->d2h_stream);
+  if (ctx->h_done) cudaFreeHost(ctx->h_done);
   if (ctx->h_state) cudaFreeHost(ctx->h_state);
   if (ctx->h_progress) cudaFreeHost(ctx->h_progress);
   if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);

@@ -146,7 +146,9 @@ struct rbd_ctx_s {
   std::vector<long long> forced_h;
   DevBuf nn_part, nn_coords;               // classify: split minima, query coordinates
   DevBuf pj_ws;                            // K5 split-K partial slices
-  DevBuf send, recv;                       // sharded mode: payload exchange buffers
+  DevBuf send, recv;                       // sharded mode: payload (-0.0-padded) and its allreduce
+  DevBuf srec, rrec;                       // sharded mode: 16-byte records and their allgather
+  double* h_done = nullptr;                // sharded mode: pinned done flags of the graph replays
   // host-buffer entries (project/reconstruct/compress/classify/mgs_project/
   // ws_extend _host): device scratch kept between calls instead of a
   // cudaMalloc/cudaFree pair (and the implicit device sync of cudaFree) per call

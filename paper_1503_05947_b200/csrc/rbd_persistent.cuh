@@ -32,6 +32,7 @@
 // (the decider forms the YAY row; the finaliser carries cross/quad).
 #pragma once
 
+#include "rbd_select.h"
 #include "rbd_weighted.cuh"
 
 namespace rbdk {
@@ -61,9 +62,9 @@ struct PersistArgs {
   unsigned long long* phase_ns;  // optional [8] accumulated phase times (CTA 0)
   unsigned long long* trace;     // optional per-CTA timeline [G][kTraceWords] for steps
   long long trace_step;          //   trace_step .. trace_step+1
-  // sharded mode (one step per launch; see rbd_capi.cu's sharded driver)
-  const double* recv;            // gathered payloads [nranks][pay_stride]
-  double* send;                  // this rank's payload
+  // sharded mode (one step per launch; see rbd_shard.cu)
+  const double* recv;            // the winner's payload (allreduced: owner's values + -0.0)
+  double* send;                  // this rank's 16-byte record {best residual, global index}
   long long pay_stride;          // doubles per payload
   long long col_offset;          // global index of local column 0
   struct StepCtl* ctl;           // queue / publish words
@@ -287,7 +288,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
     reorth_prev = st->reorth;
     wnorm_prev = st->wnorm;
     xnorm2 = st->xnorm2;
-    pay = a.recv + (long long)st->rank_owner * a.pay_stride;
+    pay = a.recv;
   } else {
     xnorm2 = a.col_sq[jstar];
   }
@@ -988,24 +989,17 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
       }
       block_argmax<kThreads>(gv, gj, smr);
       if constexpr (SHARD) {
-        // pack this rank's candidate: record, x_{gj}, T[0:k+1, gj]; the select
-        // kernel picks the winner after the allgather
+        // this rank's 16-byte record {best residual, global index}; after the
+        // record allgather the owner of the winner packs x_j and T[0:k+1, j]
+        // (k_shard_pack) for the payload allreduce
         const bool have = gj != 0x7fffffffffffffffLL;
         if (cta == 0 && tid == 0) {
           a.send[0] = have ? gv : -2.0;
           a.send[1] = __longlong_as_double(have ? a.col_offset + gj : -1LL);
-          a.send[2] = have ? a.col_sq[gj] : 0.0;
-          a.send[3] = 0.0;
+          st->jlocal = have ? gj : -1;
           st->reorth = re;
           st->wnorm = nrm;
           st->pending = 0;
-        }
-        if (have) {
-          const double* xs = a.X + gj * a.ldx;
-          for (long long i = (long long)cta * kThreads + tid; i < m; i += (long long)G * kThreads)
-            a.send[kPayHead + i] = xs[i];
-          for (long long l = (long long)cta * kThreads + tid; l <= k; l += (long long)G * kThreads)
-            a.send[kPayHead + m + l] = __ldcg(&a.T[l * n + gj]);
         }
         break;
       } else {
@@ -1039,24 +1033,41 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
   }
 }
 
-// Sharded mode: winner selection after the payload allgather (every rank runs
-// it on identical data, so every rank takes the same decision).
-static __global__ void k_shard_select(DevState* st, const double* recv, long long pay_stride, int nranks,
-                               double* history, long long* selected) {
-  if (threadIdx.x != 0 || st->done) return;
-  double bv = -1.0;
-  long long bj = 0x7fffffffffffffffLL;
-  int br = -1;
-  for (int r = 0; r < nranks; ++r) {
-    const double* h = recv + (long long)r * pay_stride;
-    const long long j = __double_as_longlong(h[1]);
-    if (j < 0) continue;
-    if (rec_better(h[0], j, bv, bj)) {
-      bv = h[0];
-      bj = j;
-      br = r;
+// Sharded mode, after the record allgather: every rank applies the winner
+// rule to the same records (rbd_select.h); the owner packs the winner's
+// payload {col_sq, x_j, T[0:k+1, j]} and every other rank contributes -0.0
+// (x + -0.0 == x for every x, signed zeros included, so the sum allreduce that
+// follows moves the owner's bits exactly, in any order and at any rank count).
+static __global__ void k_shard_pack(const DevState* st, const double* rrec, int nranks, int rank,
+                                    const double* X, long long ldx, long long m, const double* T,
+                                    long long n_local, const double* col_sq, double* pay,
+                                    long long pay_count) {
+  double bv;
+  long long bj;
+  const int br = rbdsel::pick(rrec, nranks, 2, &bv, &bj);
+  const bool own = !st->done && br == rank;
+  const long long jl = own ? st->jlocal : -1;
+  const long long k = st->d;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < pay_count; t += stride) {
+    double v = -0.0;
+    if (own) {
+      if (t == 2) v = col_sq[jl];
+      else if (t >= kPayHead && t < kPayHead + m) v = X[jl * ldx + (t - kPayHead)];
+      else if (t >= kPayHead + m && t <= kPayHead + m + k) v = T[(t - kPayHead - m) * n_local + jl];
     }
+    pay[t] = v;
   }
+}
+
+// Sharded mode, after the payload allreduce: the step's bookkeeping
+// (decompose.cpp:94-101), identical on every rank.
+static __global__ void k_shard_select(DevState* st, const double* rrec, const double* pay,
+                                      int nranks, double* history, long long* selected) {
+  if (threadIdx.x != 0 || st->done) return;
+  double bv;
+  long long bj;
+  rbdsel::pick(rrec, nranks, 2, &bv, &bj);
   const long long k = st->d;
   const double e_cur = sqrt(bv > 0.0 ? bv : 0.0);      // workspace.cpp:123
   history[k] = e_cur;                                   // decompose.cpp:99
@@ -1065,36 +1076,44 @@ static __global__ void k_shard_select(DevState* st, const double* recv, long lon
   st->d = k + 1;                                        // :96
   st->pending = 1;
   st->jstar = bj;                                       // :101
-  st->rank_owner = br;
-  st->xnorm2 = recv[(long long)br * pay_stride + 2];
+  st->rank_owner = 0;
+  st->xnorm2 = pay[2];
   st->done = !((k + 1) < st->d_max && e_cur > st->eps_R) ? 1 : 0;  // :87
 }
 
-// Sharded mode, before step 0: the owner of the start column publishes it.
+// Sharded mode, before step 0: the owner of the start column publishes it
+// ({col_sq, x_j0} through the same -0.0-padded allreduce).
 static __global__ void k_shard_seed_pack(const double* X, long long ldx, long long m, long long jlocal,
-                                  long long col_offset, const double* col_sq, double* send) {
-  const long long i0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i0 == 0) {
-    send[0] = 0.0;
-    send[1] = __longlong_as_double(jlocal >= 0 ? col_offset + jlocal : -1LL);
-    send[2] = jlocal >= 0 ? col_sq[jlocal] : 0.0;
-    send[3] = 0.0;
+                                         const double* col_sq, double* pay, long long pay_count) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < pay_count; t += stride) {
+    double v = -0.0;
+    if (jlocal >= 0) {
+      if (t == 2) v = col_sq[jlocal];
+      else if (t >= kPayHead && t < kPayHead + m) v = X[jlocal * ldx + (t - kPayHead)];
+    }
+    pay[t] = v;
   }
-  if (jlocal < 0) return;
-  for (long long i = i0; i < m; i += (long long)gridDim.x * blockDim.x)
-    send[kPayHead + i] = X[jlocal * ldx + i];
 }
 
-static __global__ void k_shard_seed_select(DevState* st, const double* recv, long long pay_stride,
-                                    int nranks) {
+static __global__ void k_shard_seed_select(DevState* st, const double* pay) {
   if (threadIdx.x != 0) return;
-  for (int r = 0; r < nranks; ++r) {
-    const double* h = recv + (long long)r * pay_stride;
-    if (__double_as_longlong(h[1]) >= 0) {
-      st->rank_owner = r;
-      st->xnorm2 = h[2];
-      return;
-    }
+  st->rank_owner = 0;
+  st->xnorm2 = pay[2];
+}
+
+// Virtual ranks (one device): the sum allreduce of the R payloads, in rank
+// order, into every rank's receive buffer.
+struct PayPtrs {
+  const double* in[16];
+  double* out[16];
+};
+static __global__ void k_sum_payloads(PayPtrs p, int nranks, long long count) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < count; t += stride) {
+    double v = p.in[0][t];
+    for (int r = 1; r < nranks; ++r) v += p.in[r][t];
+    for (int r = 0; r < nranks; ++r) p.out[r][t] = v;
   }
 }
 

@@ -74,6 +74,21 @@ def exchange_unique_id(rank: int, group=None) -> bytes:
     return obj[0]
 
 
+def pick_winner(records):
+    """The per-step winner rule of the record exchange, run by the library's own
+    code (rbd_shard_pick, csrc/rbd_select.h — the same function the device
+    kernels call): records = [(best residual, global index or -1)] per rank.
+    Returns (value, global index, owner rank); owner -1 when nobody has one."""
+    recs = np.zeros(2 * len(records))
+    for r, (v, j) in enumerate(records):
+        recs[2 * r] = float(v)
+        recs[2 * r + 1] = np.array([int(j)], dtype=np.int64).view(np.float64)[0]
+    bv, bj, own = C.c_double(), C.c_int64(), C.c_int()
+    check(load_library().rbd_shard_pick(recs.ctypes.data_as(C.c_void_p), len(records),
+                                        C.byref(bv), C.byref(bj), C.byref(own)))
+    return bv.value, bj.value, own.value
+
+
 def init_comm(ctx: Context, rank: int, world: int, uid: bytes) -> None:
     check(load_library().rbd_ctx_init_comm(ctx.handle, rank, world, uid))
 

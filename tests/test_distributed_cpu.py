@@ -1,8 +1,9 @@
 """Host-side logic of the multi-GPU path with world_size 2 on CPU (gloo):
 shard planning, NCCL unique-id exchange over torch.distributed, assembly of
-the sharded T, and the winner-selection rule of the payload protocol
-(value desc, GLOBAL index asc — the reference's strict '>' scan,
-workspace.cpp:107-113, must survive sharding)."""
+the sharded T, and the winner rule of the per-step record exchange (value
+desc, GLOBAL index asc — the reference's strict '>' scan,
+workspace.cpp:107-113, must survive sharding), run by the library's own code
+(rbd_shard_pick: csrc/rbd_select.h, the function the device kernels call)."""
 import os
 import socket
 
@@ -24,14 +25,9 @@ def _free_port():
 
 
 def select_winner(records):
-    """The k_shard_select rule on gathered (value, global index) records."""
-    best = None
-    for v, j in records:
-        if j < 0:
-            continue
-        if best is None or v > best[0] or (v == best[0] and j < best[1]):
-            best = (v, j)
-    return best
+    """(value, global index) of the winner, by the library's rule."""
+    v, j, owner = rd.pick_winner(records)
+    return None if owner < 0 else (v, j)
 
 
 def _worker(rank, world, port, q):
@@ -57,7 +53,27 @@ def _worker(rank, world, port, q):
         recs = [torch.empty(2, dtype=torch.float64) for _ in range(world)]
         dist.all_gather(recs, rec)
         win = select_winner([(float(t[0]), int(t[1])) for t in recs])
-        q.put((rank, plan, len(uid), ids[0] == ids[-1], bool(torch.equal(Tg, T)), win))
+        # the greedy loop's steps over two shards: every rank scans its own
+        # columns of the oracle's residual bookkeeping (workspace.cpp:52-53,
+        # 107-113) and the exchanged records pick the whole-matrix argmax
+        import oracle
+        X = oracle.random_matrix(40, 23, 77)
+        X[:, 17] = X[:, 4]                       # an exact tie across the two shards
+        ref = oracle.decompose(X, 6)
+        plan2 = rd.plan_shards(23, world)
+        o2, n2 = plan2.offsets[rank], plan2.n_locals[rank]
+        r_all = oracle.column_sq(X)
+        steps_ok = True
+        for kk in range(ref.d - 1):
+            r_all = np.maximum(r_all - ref.T[kk] * ref.T[kk], 0.0)
+            loc = r_all[o2:o2 + n2]
+            lj = int(np.argmax(loc))
+            mine = torch.tensor([loc[lj], float(o2 + lj)], dtype=torch.float64)
+            got = [torch.empty(2, dtype=torch.float64) for _ in range(world)]
+            dist.all_gather(got, mine)
+            v, j, owner = rd.pick_winner([(float(t[0]), int(t[1])) for t in got])
+            steps_ok = steps_ok and j == ref.selected[kk + 1] and owner == plan2.owner(j)
+        q.put((rank, plan, len(uid), ids[0] == ids[-1], bool(torch.equal(Tg, T)), win, steps_ok))
     finally:
         dist.destroy_process_group()
 
@@ -73,11 +89,12 @@ def test_gloo_world2_host_protocol():
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    for rank, plan, uid_len, same_uid, t_ok, win in out:
+    for rank, plan, uid_len, same_uid, t_ok, win, steps_ok in out:
         assert plan.offsets == (0, 6) and plan.n_locals == (6, 5)
         assert uid_len == 128 and same_uid
         assert t_ok
         assert win == (7.0, 3)
+        assert steps_ok
 
 
 def test_plan_shards():
@@ -93,3 +110,5 @@ def test_plan_shards():
 def test_select_rule():
     assert select_winner([(1.0, 5), (1.0, 2), (0.5, 1)]) == (1.0, 2)
     assert select_winner([(-2.0, -1), (0.0, 7)]) == (0.0, 7)
+    assert rd.pick_winner([(-2.0, -1), (-2.0, -1)])[2] == -1
+    assert rd.pick_winner([(3.0, 9), (3.0, 9 + 2**40)]) == (3.0, 9, 0)

@@ -1,7 +1,8 @@
-"""Sharded (multi-GPU) path on one B200: the same kernels and payload protocol
-with R column shards stepped in lockstep in one process. Results must be
-bit-identical to the single-GPU loop for any R (per-column
-sums depend on m only; the allgather moves bits, never adds them)."""
+"""Sharded (multi-GPU) path on one B200: the same kernels and exchange protocol
+(16-byte record allgather, -0.0-padded payload allreduce, CUDA-graph replay of
+8 steps) with R column shards stepped in lockstep in one process. Results must
+be bit-identical to the single-GPU loop for any R (per-column
+sums depend on m only; the exchanges move bits, never round them)."""
 import numpy as np
 import pytest
 
@@ -95,7 +96,40 @@ def test_nccl_world1_matches_single_gpu(cuda):
     distributed.init_comm(ctx, 0, 1, bytes(buf.raw))
     plan = distributed.plan_shards(300, 1)
     r = distributed.decompose_sharded(X, plan, 0, 50, ctx=ctx)
+    assert r.result.reserved == 1                    # NCCL calls captured in the step graph
     assert r.d == ref[2] and r.selected == ref[3] and r.residual_history == ref[4]
     assert np.array_equal(r.Y.cpu().numpy(), ref[0])
     assert np.array_equal(r.T_local.cpu().numpy(), ref[1])
     ctx.close()
+
+
+@pytest.mark.parametrize("R", [1, 3])
+def test_graph_replay_and_eager_steps_agree(cuda, monkeypatch, R):
+    """The steps are replayed from a CUDA graph (result.reserved == 1); the eager
+    host-driven loop (RBD_SHARD_GRAPH=0) gives the same bits, including a stop
+    in the middle of a replay (d = 13 is not a multiple of 8)."""
+    X = dev(oracle.random_matrix(3000, 120, 12), cuda)
+    ref = single(X, 13)
+    g = distributed.decompose_virtual(X, R, 13)
+    assert g[5].reserved == 1
+    check_same(ref, *g[:5])
+    monkeypatch.setenv("RBD_SHARD_GRAPH", "0")
+    e = distributed.decompose_virtual(X, R, 13)
+    assert e[5].reserved == 0
+    check_same(ref, *e[:5])
+
+
+def test_signed_zero_columns_survive_the_payload_allreduce(cuda):
+    """The owner's payload travels through a sum with -0.0 from every other rank:
+    exact for every value, -0.0 entries of x included."""
+    x = oracle.random_matrix(256, 24, 13)
+    x[::3, :] = -0.0
+    X = dev(x, cuda)
+    ref = single(X, 10)
+    bits = lambda a: np.asarray(a).view(np.int64)   # noqa: E731  (tells -0.0 from +0.0)
+    for R in (2, 4):
+        out = distributed.decompose_virtual(X, R, 10)
+        check_same(ref, *out[:5])
+        for Y in out[0]:
+            assert np.array_equal(bits(Y.cpu().numpy()), bits(ref[0]))
+        assert np.array_equal(bits(out[1].cpu().numpy()), bits(ref[1]))

@@ -1,6 +1,7 @@
-"""Per-step cost of the sharded mode (one persistent-kernel launch + NCCL payload
-allgather + select per step) against the single-GPU persistent loop, on C1 at
-world 1 (NCCL with one rank). Prints one JSON line."""
+"""Per-step cost of the sharded mode (step kernel, NCCL record allgather, pack,
+NCCL payload allreduce, select; replayed from a CUDA graph, or eager with
+RBD_SHARD_GRAPH=0) against the single-GPU persistent loop, on C1 at world 1
+(NCCL with one rank). Prints one JSON line."""
 import ctypes as C
 import json
 import os
@@ -22,8 +23,18 @@ check(load_library().rbd_comm_unique_id(buf))
 rd.init_comm(ctx, 0, 1, bytes(buf.raw))
 plan = rd.plan_shards(n, 1)
 out = {}
+def eager():
+    os.environ["RBD_SHARD_GRAPH"] = "0"
+    try:
+        return rd.decompose_sharded(X, plan, 0, w.d_max, 0.0, ctx=ctx)
+    finally:
+        os.environ.pop("RBD_SHARD_GRAPH")
+
+
 for name, fn in (("persistent", lambda: rbd.decompose(X, d_max=w.d_max, ctx=ctx)),
-                 ("sharded_world1", lambda: rd.decompose_sharded(X, plan, 0, w.d_max, 0.0, ctx=ctx))):
+                 ("sharded_world1_graph", lambda: rd.decompose_sharded(X, plan, 0, w.d_max, 0.0,
+                                                                       ctx=ctx)),
+                 ("sharded_world1_eager", eager)):
     fn()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
