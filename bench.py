@@ -365,6 +365,100 @@ def secondary_c1(rbd, ctx, dev, stream, args, peak):
     return out
 
 
+def secondary_c4(rbd, ctx, dev, stream, args):
+    """BASELINE config 4: RBD on the 65,536 x 8,192 stage, then the out-of-sample
+    stream of 16 batches x 16,384 columns (T_new = Y'X_new + Eq. 3 error
+    indicator). Device-resident K5 / K6 rates, and e2e through
+    rbd_project_host_many[_f32] from pinned host batches (two distinct pinned
+    buffers alternate: 16 distinct 8 GiB batches would need 128 GiB of host RAM;
+    every batch is uploaded, contracted and downloaded)."""
+    import torch
+    from paper_1503_05947_b200 import configs
+    w = configs.C4
+    X = configs.c4_stage_matrix(dev)
+    for _ in range(2):
+        g = rbd.decompose(X, d_max=w.d_max, ctx=ctx)
+    K = max(args.aux_steps, 3)
+    ms, ds, loops = time_decomposes(rbd, X, w.d_max, 0.0, ctx, K, stream, dev)
+    xb = w.m * w.n * 8
+    out = {"stage": {"workload": "C4 RBD stage 65536x8192", "d": int(ds[0]),
+                     "value": xb * sum(ds) / (ms / 1e3) / 1e9, "unit": "GB/s", "ms_per_step": ms / K}}
+    g = rbd.decompose(X, d_max=w.d_max, ctx=ctx)
+    del X
+    rm = rbd.ResidentModel.from_model(g, ctx=ctx)
+    Yd = g.Y.t().contiguous().t()
+    U, sv = configs.c4_basis(dev)
+    B = configs.C4_BATCH
+    nb = configs.C4_NEW_COLUMNS // B
+    flops = 2.0 * w.m * g.d * B
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # device-resident K5 (fp64 DMMA) and K6 (fp32 tcgen05 3xTF32) on one batch
+    Xn = configs.c4_new_batch(U, sv, 0, device=dev)
+    rbd.project_batch(Yd, Xn, ctx=ctx)
+    torch.cuda.synchronize(dev)
+    e0.record(stream)
+    for _ in range(3):
+        rbd.project_batch(Yd, Xn, ctx=ctx)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    k5 = e0.elapsed_time(e1) / 3
+    Y32 = Yd.float().t().contiguous().t()
+    X32 = Xn.float().t().contiguous().t()
+    rbd.project_batch_f32(Y32, X32, ctx=ctx)
+    torch.cuda.synchronize(dev)
+    e0.record(stream)
+    for _ in range(3):
+        rbd.project_batch_f32(Y32, X32, ctx=ctx)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    k6 = e0.elapsed_time(e1) / 3
+    out["device_fp64"] = {"kernel": "K5 k_project_dmma (FP64 DMMA) + Eq. 3", "ms_per_batch": k5,
+                          "tflops": flops / (k5 / 1e3) / 1e12}
+    out["device_fp32"] = {"kernel": "K6 k_project_tf32x3 (tcgen05 kind::tf32, 3xTF32) + Eq. 3",
+                          "ms_per_batch": k6, "tflops_fp32_equivalent": flops / (k6 / 1e3) / 1e12}
+    # e2e: the pinned host stream through the resident model
+    for f32, dt, tdt in ((False, torch.float64, np.float64), (True, torch.float32, np.float32)):
+        bufs = []
+        for b in range(2):
+            xb_dev = configs.c4_new_batch(U, sv, b, device=dev)
+            h = torch.empty((B, w.m), dtype=dt, pin_memory=True)
+            h.copy_(xb_dev.t())
+            bufs.append(h.numpy().T)
+            del xb_dev
+        outs = [(torch.empty((B, g.d), dtype=dt, pin_memory=True).numpy().T,
+                 torch.empty(B, dtype=torch.float64, pin_memory=True).numpy()) for _ in range(nb)]
+        batches = [bufs[i % 2] for i in range(nb)]
+        rm.project_many(batches[:2], f32=f32, out=outs[:2])   # warm
+        t0 = time.perf_counter()
+        rm.project_many(batches, f32=f32, out=outs)
+        te = time.perf_counter() - t0
+        hb = B * w.m * (4 if f32 else 8)
+        out["e2e_fp32" if f32 else "e2e_fp64"] = {
+            "entry": f"rbd_project_host_many{'_f32' if f32 else ''} ({nb} batches of {B}, pinned)",
+            "seconds_all_batches": te, "ms_per_batch": te * 1e3 / nb,
+            "tflops": flops * nb / te / 1e12, "h2d_gbs": hb * nb / te / 1e9,
+            "h2d_bytes_per_batch": hb, "d2h_bytes_per_batch": B * g.d * (4 if f32 else 8) + 8 * B}
+        del bufs, outs, batches
+        gc.collect()
+    # CPU: the reference's per-vector project (decompose.cpp:113-117), one thread
+    import oracle
+    ns = 64
+    Yh = np.asfortranarray(Yd.cpu().numpy())
+    Xs = np.asfortranarray(Xn[:, :ns].cpu().numpy())
+    t0 = time.perf_counter()
+    for j in range(ns):
+        oracle.project(Yh, Xs[:, j])
+    tc = time.perf_counter() - t0
+    out["cpu_baseline"] = {"value": 2.0 * w.m * g.d * ns / tc / 1e12, "unit": "TFLOP/s",
+                           "cores": 1, "kind": "port", "seconds": tc,
+                           "sample": f"oracle per-vector project (decompose.cpp:113-117, Y re-read "
+                                     f"per vector, one thread) on {ns} of the batch's columns"}
+    del Xn, X32, Y32, Yd, U, rm, g
+    gc.collect()
+    torch.cuda.empty_cache()
+    return out
+
+
 def f32_leg(rbd, Xd, w, d_max, eps, ctx, dev, stream, args, peak):
     """fp32 storage mode on the same workload rounded to fp32 (half the X
     bytes per sweep, fp64 arithmetic): device-resident and e2e."""
@@ -539,6 +633,11 @@ def run_b200(args):
                 secondary["C1-image-like"] = secondary_c1(rbd, ctx, dev, stream, args, peak)
             except Exception as ex:
                 secondary["C1-image-like"] = {"error": repr(ex)[:300]}
+        if not w.name.startswith("C4"):
+            try:
+                secondary["C4-out-of-sample"] = secondary_c4(rbd, ctx, dev, stream, args)
+            except Exception as ex:
+                secondary["C4-out-of-sample"] = {"error": repr(ex)[:300]}
 
     line = {
         "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world,

@@ -70,6 +70,7 @@ def lib():
         L.orc_ws_error_sq.restype = I
         L.orc_ws_scan.argtypes = [P, P, P]
         L.orc_project.argtypes = [P, I64, I64, P, P]
+        L.orc_project.restype = None
         L.orc_reconstruct.argtypes = [P, I64, I64, P, P]
         L.orc_project_batch.argtypes = [P, I64, I64, P, I64, I64, I, P, P]
         L.orc_random_matrix.argtypes = [I64, I64, C.c_uint64, P]
@@ -332,6 +333,17 @@ class Workspace:
         j = C.c_int64()
         lib().orc_ws_scan(self.h, C.byref(e), C.byref(j))
         return e.value, j.value
+
+
+def project(Y, v):
+    """rbd::project (decompose.cpp:113-117): c = Y'v for one vector, the
+    reference's per-vector call (Y re-read per vector)."""
+    Ya = np.asfortranarray(np.asarray(Y, dtype=np.float64))
+    va = np.ascontiguousarray(np.asarray(v, dtype=np.float64).reshape(-1))
+    m, d = Ya.shape
+    c = np.zeros(d)
+    lib().orc_project(_p(Ya), m, d, _p(va), _p(c))
+    return c
 
 
 def project_batch(Y, Xn, nthreads: int = 1):
