@@ -339,6 +339,17 @@ size_t persist_smem(long long dcap, bool diag) {
          (diag ? (size_t)kSvBytes : 0);   // DIAG: X-tile vector slots (rbd_weighted.cuh)
 }
 
+// X tiles claimed ahead of the Y'w1 groups in every step of the fp64 identity
+// loop (RBD_YDELAY overrides, in tiles): half a wave lets the first claimers
+// stream X instead of waiting for the slowest CTA's P1. Measured (A/B in one
+// process, tools/ab_env.py): C1 46.18 -> 45.89 ms at grid/2, 46.09 at one
+// wave, 46.46 at two; C2 unchanged (2930.8 / 2931.0 / 2933.3 ms); the fp32
+// loop slower (33.81 -> 34.11 ms at one wave), so it keeps 0.
+long long y_delay(int grid, bool xf32) {
+  if (const char* e = getenv("RBD_YDELAY")) return atoll(e);
+  return xf32 ? 0 : grid / 2;
+}
+
 // Materialise a pending column / clear the pending flag (used after the loop).
 int enqueue_fused_ext(rbd_ctx_t ctx, const LoopBufs& L) {
   DevState* st = ptr<DevState>(ctx->state);
@@ -486,6 +497,7 @@ int launch_persistent(rbd_ctx_t ctx, const LoopBufs& L, const double* diag = nul
   a.rdy = ptr<unsigned long long>(ctx->rdy);
   a.forced = ctx->forced_h.empty() ? nullptr : ptr<long long>(ctx->forced);
   a.nforced = (long long)ctx->forced_h.size();
+  a.ydelay = y_delay(grid, xf32);
   if (diag) {
     TRY(ensure(ctx->wd_ppart2, sizeof(double) * (size_t)std::max<long long>(grid, S) * L.d_max));
     TRY(ensure(ctx->wd_q, sizeof(double) * (size_t)(L.d_max + 1)));

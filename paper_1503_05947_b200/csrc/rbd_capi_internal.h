@@ -188,6 +188,7 @@ int enqueue_init(rbd_ctx_t ctx, const double* X, long long m, long long n, long 
                  double* partial, double* colsq, double* resid, DevState* st);
 int diag_vec_grid(rbd_ctx_t ctx, long long m);
 size_t persist_smem(long long dcap, bool diag = false);
+long long y_delay(int grid, bool xf32 = false);
 int persistent_grid(rbd_ctx_t ctx, int vec, long long d_max, bool diag = false, bool xf32 = false);
 int ensure_loop_buffers(rbd_ctx_t ctx, long long m, long long n, long long d_max);
 int validate_after_init(const rbd_config_t* cfg, long long m, long long n, const DevState& hs,

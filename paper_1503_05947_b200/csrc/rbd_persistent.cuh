@@ -89,6 +89,10 @@ struct PersistArgs {
   double* quad;                  // [n] T[:,j]' YAY T[:,j]
   const double* colsq_a;         // [n] ||x_j||_A^2
   double* yslice;                // [d_max / kYSlice + 2][2] per-slice (p.q, p.v) of the YAY row
+  // identity loops: the first ydelay claims of a step are X tiles, then the
+  // Y'w1 groups, then the rest (CTAs that claim first then stream X instead
+  // of waiting for every CTA's P1; the decision comes a tile later)
+  long long ydelay;
 };
 
 __device__ __forceinline__ void red_release_add_u64(unsigned long long* p, unsigned long long v) {
@@ -488,6 +492,22 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
         if ((++spins & 0xfffu) == 0 && globaltimer() - t0 > 30000000000ull) __trap();
       } while (ld_acquire_u64(c) < want);
     };
+    // claim index t -> Y'w1 group (t_y >= 0) or X tile index (t_x >= 0), for a
+    // step with gyv Y'w1 groups and totv claims in all
+    auto split = [&](long long t, long long gyv, long long totv, long long& t_y, long long& t_x) {
+      const long long nxv = totv - gyv;
+      const long long yo = DIAG ? 0 : (a.ydelay < nxv ? a.ydelay : nxv);
+      if (t < yo) {
+        t_y = -1;
+        t_x = t;
+      } else if (t < yo + gyv) {
+        t_y = t - yo;
+        t_x = -1;
+      } else {
+        t_y = -1;
+        t_x = t - gyv;
+      }
+    };
     // (tid 0, before publishing tile t to the CTA) the P1 rows tile t reads
     auto wait_inputs = [&](long long t, long long gy_, long long total_) {
       if (t >= total_ || all_rdy) return;
@@ -495,12 +515,14 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
         all_rdy = true;
         return;
       }
-      if (t < gy_) {
+      long long t_y, t_x;
+      split(t, gy_, total_, t_y, t_x);
+      if (t_y >= 0) {
         wait_ge(&a.rdy[0], (unsigned long long)G * ord);
         all_rdy = true;
       } else {
         long long gx, sc;
-        x_tile(t - gy_, gx, sc);
+        x_tile(t_x, gx, sc);
         const long long rows = (m - sc * kChunk < kChunk) ? m - sc * kChunk : kChunk;
         wait_ge(&a.rdy[1 + sc], (unsigned long long)rows * ord);
       }
@@ -814,15 +836,19 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
       mark(9);
       if (tid == 0) {
         wait_inputs(next, gy, total);   // acquire by tid 0, published by the barrier below
-        sh_tile = next;
+        // published as: -1 - g for Y'w1 group g, the X tile index, or total (end)
+        long long t_y, t_x;
+        split(next, gy, total, t_y, t_x);
+        sh_tile = next >= total ? total : (t_y >= 0 ? -1 - t_y : t_x);
       }
       __syncthreads();
-      const long long t = sh_tile;
+      const long long code = sh_tile;
       mark(5);
-      if (t >= total) break;
-      trace(k, 4 | ((unsigned long long)t << 8));
+      if (code >= total) break;
+      trace(k, 4 | ((unsigned long long)(code < 0 ? -1 - code : code + gy) << 8));
       if (tid == 0) next = (long long)(atomicAdd(&ctl->tile_ctr, 1ull) - tile_base);
-      if (t < gy) {
+      if (code < 0) {
+        const long long t = -1 - code;   // the Y'w1 group
         for (long long s = 0; s < S; ++s) {
           if constexpr (DIAG)
             sweep_tile_dot2<VEC, LOAD_CG, true, 2>(a.Y, m, m, k, a.w, a.aw, a.ppart, a.ppart2,
@@ -895,7 +921,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
         // the siblings are long done and finalisation never piles up at the
         // end of the queue
         long long g, s;
-        x_tile(t - gy, g, s);
+        x_tile(code, g, s);
         if constexpr (DIAG && VEC == 2)
           sweep_tile_dot2_sv(a.X, a.ldx, m, n, a.w, a.aw, a.partial, a.partial2, n, s * ngx + g,
                              red2, svec);

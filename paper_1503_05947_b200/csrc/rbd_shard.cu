@@ -158,6 +158,7 @@ int shard_step_launch(rbd_ctx_t c, const Shard& sh, long long m, long long ldx, 
   a.send = ptr<double>(c->srec);   // this rank's record
   a.pay_stride = pay_stride;
   a.col_offset = sh.col_offset;
+  a.ydelay = y_delay(grid);
   void* args[] = {&a};
   const size_t smem = persist_smem(d_max);
   cudaError_t e = vec == 2 ? cudaLaunchCooperativeKernel((void*)k_rbd_persistent<2, true>, grid,
