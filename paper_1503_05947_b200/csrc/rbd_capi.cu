@@ -879,6 +879,7 @@ int decompose_device_impl(rbd_ctx_t ctx, const double* dX, int64_t m, int64_t n,
                      "decompose: fp32 storage mode runs on the persistent loop (d_max <= 4096)");
   }
   const long long d_cap = std::max<long long>(1, std::min<long long>(cfg->d_max, n));
+  NvtxRange nv_all("rbd.decompose");
   TRY(ensure_loop_buffers(ctx, m, n, d_cap));
   DevState* st = ptr<DevState>(ctx->state);
 
@@ -896,6 +897,7 @@ int decompose_device_impl(rbd_ctx_t ctx, const double* dX, int64_t m, int64_t n,
     }
   } evg{ev0, ev1, ev2};
   // ---- K1 ----
+  NvtxRange nv_k1("rbd.init (K1: validation, workspace_init)");
   CU(cudaMemsetAsync(st, 0, sizeof(DevState), ctx->stream));
   CU(cudaEventRecord(ev0, ctx->stream));
   if (dXf)
@@ -914,6 +916,7 @@ int decompose_device_impl(rbd_ctx_t ctx, const double* dX, int64_t m, int64_t n,
   CU(cudaMemsetAsync(ctx->counter.p, 0, 64, ctx->stream));
   CU(cudaMemcpyAsync(ctx->h_state, st, sizeof(DevState), cudaMemcpyDeviceToHost, ctx->stream));
   CU(cudaStreamSynchronize(ctx->stream));
+  nv_k1.end();
   DevState hs = *ctx->h_state;
   double init_ms = 0.0;
   {
@@ -957,6 +960,7 @@ int decompose_device_impl(rbd_ctx_t ctx, const double* dX, int64_t m, int64_t n,
   CU(cudaMemcpyAsync(st, ctx->h_state, sizeof(DevState), cudaMemcpyHostToDevice, ctx->stream));
 
   LoopBufs L{dX, m, n, ldx, cfg->d_max, dY, dT, dXf};
+  NvtxRange nv_loop("rbd.loop (greedy steps)");
   if (diag) {
     const long long S = cdiv(m, kChunk);
     TRY(ensure(ctx->wd_axi, sizeof(double) * m));

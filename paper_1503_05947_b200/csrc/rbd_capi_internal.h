@@ -22,6 +22,7 @@
 #include "rbd_internal.h"
 #include "rbd_device.cuh"   // shared types (DevState, Rec, SweepArgs); each unit includes its kernels
 #include <cudaTypedefs.h>
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX v3: phase ranges for nsys / ncu --nvtx
 
 using namespace rbdk;
 
@@ -48,6 +49,20 @@ inline int set_err(int code, const std::string& msg) {
     int s_ = (expr);         \
     if (s_ != RBD_OK) return s_; \
   } while (0)
+
+// NVTX range over a host-side phase (the reference times its phases
+// with steady_clock in tools/main.cpp:31-33,171-177). Free when no tool attaches.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  void end() {
+    if (open) nvtxRangePop();
+    open = false;
+  }
+  ~NvtxRange() { end(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+  bool open = true;
+};
 
 struct DevBuf {
   void* p = nullptr;

@@ -75,6 +75,7 @@ int project_stream(rbd_ctx_t ctx, rbd_model_t md, int64_t count, const TX* const
   for (int64_t i = 0; i < count; ++i)
     if (!hXn[i]) return set_err(RBD_ERR_INVALID_ARGUMENT, "project: null input batch");
   CU(cudaSetDevice(ctx->device));
+  NvtxRange nv(f32 ? "rbd.project_stream_f32" : "rbd.project_stream");
   const int64_t m = md->m, d = md->d;
   if (f32) TRY(ensure_y32(ctx, md));
   const int64_t ldd = f32 ? md->ld32 : m;

@@ -205,6 +205,7 @@ int sharded_decompose(std::vector<rbd_ctx_t>& R, Exchange& ex, std::vector<Shard
                       int64_t* h_selected, double* h_history, rbd_result_t* result,
                       const std::vector<int>& ranks_id) {
   if (m < 1 || n_global < 1) return set_err(RBD_ERR_INVALID_ARGUMENT, "decompose: matrix must be non-empty");
+  NvtxRange nv("rbd.decompose_sharded");
   const int nl = (int)R.size();
   const long long d_cap = std::max<long long>(1, std::min<long long>(cfg->d_max, n_global));
   if (d_cap > kFMaxCoef)
