@@ -108,9 +108,19 @@ static __global__ void k_reconstruct(const double* __restrict__ Y, long long m, 
 // by 2 points more (its combine pass and workspace are not free). E.g. C4's
 // 8 x 256 tiles -> 2 (6.92 waves), classify's 7 x 256 -> 4 (12.1 waves, 93 %
 // instead of 3.03 waves at 76 %).
+// K5 tile shape: 0 = 64 x 64 CTA tiles of 2 x 2 warps (32 x 32 each), 4 CTAs
+// per SM; 1 = 64 x 128 tiles of 2 x 2 warps (32 x 64 each: twice the DMMAs per
+// fragment load and per CTA barrier), 2 CTAs per SM. RBD_K5_TILE overrides.
+inline int project_tile() {
+  const char* e = getenv("RBD_K5_TILE");
+  return e ? atoi(e) : 0;
+}
+
 inline int project_splitk(long long m, long long d, long long N, int nsm) {
-  const long long ctas = ((d + 63) / 64) * ((N + 63) / 64);
-  const long long slots = 4LL * nsm;
+  const int tile = project_tile();
+  const long long bn = tile == 1 ? 128 : 64;
+  const long long ctas = ((d + 63) / 64) * ((N + bn - 1) / bn);
+  const long long slots = (tile == 1 ? 2LL : 4LL) * nsm;
   int best = 1;
   double best_eff = 0.0;
   for (int s = 1; s <= 4; ++s) {
@@ -135,11 +145,12 @@ inline int launch_project_f64(const double* Y, long long m, long long d, long lo
                        ((reinterpret_cast<uintptr_t>(Y) | reinterpret_cast<uintptr_t>(Xn)) & 15) == 0;
   *nlaunch = 0;
   if (dmma_ok) {
-    constexpr int BM = 64, BN = 64, WM = 2, WN = 2;
     static bool attr = false;
     if (!attr) {
-      cudaFuncSetAttribute(k_project_dmma<BM, BN, WM, WN>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dm_smem_bytes<BM, BN>());
+      cudaFuncSetAttribute(k_project_dmma<64, 64, 2, 2>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dm_smem_bytes<64, 64>());
+      cudaFuncSetAttribute(k_project_dmma<64, 128, 2, 2, 2>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dm_smem_bytes<64, 128>());
       attr = true;
     }
     double* xn = err ? xnorm_scratch : nullptr;
@@ -148,9 +159,15 @@ inline int launch_project_f64(const double* Y, long long m, long long d, long lo
     double* Tws = splitk_ws;
     double* xws = splitk_ws ? splitk_ws + (long long)(sk - 1) * d * N : nullptr;
     const long long kc = ((m + sk - 1) / sk + 15) / 16 * 16;
-    dim3 grid((unsigned)((d + BM - 1) / BM), (unsigned)((N + BN - 1) / BN), (unsigned)sk);
-    k_project_dmma<BM, BN, WM, WN><<<grid, WM * WN * 32, dm_smem_bytes<BM, BN>(), s>>>(
-        Y, m, d, ldy, Xn, N, ldx, Tn, xn, kc, Tws, xws);
+    if (project_tile() == 1) {
+      dim3 grid((unsigned)((d + 63) / 64), (unsigned)((N + 127) / 128), (unsigned)sk);
+      k_project_dmma<64, 128, 2, 2, 2><<<grid, 128, dm_smem_bytes<64, 128>(), s>>>(
+          Y, m, d, ldy, Xn, N, ldx, Tn, xn, kc, Tws, xws);
+    } else {
+      dim3 grid((unsigned)((d + 63) / 64), (unsigned)((N + 63) / 64), (unsigned)sk);
+      k_project_dmma<64, 64, 2, 2><<<grid, 128, dm_smem_bytes<64, 64>(), s>>>(
+          Y, m, d, ldy, Xn, N, ldx, Tn, xn, kc, Tws, xws);
+    }
     *nlaunch += 1;
     if (sk > 1) {
       k_splitk_sum<<<1184, 256, 0, s>>>(Tn, Tws, d * N, sk - 1, xn, xws, N);

@@ -77,8 +77,8 @@ __device__ __forceinline__ void dm_load_tile(double* s, const double* __restrict
   }
 }
 
-template <int BM, int BN, int WARPS_M, int WARPS_N>
-__global__ void __launch_bounds__(WARPS_M * WARPS_N * 32, RBD_DM_MINB)
+template <int BM, int BN, int WARPS_M, int WARPS_N, int MINB = RBD_DM_MINB>
+__global__ void __launch_bounds__(WARPS_M * WARPS_N * 32, MINB)
     k_project_dmma(const double* __restrict__ Y, long long m, long long d, long long ldy,
                    const double* __restrict__ Xn, long long N, long long ldx,
                    double* __restrict__ Tn, double* __restrict__ xnorm2, long long kc,
@@ -118,10 +118,13 @@ __global__ void __launch_bounds__(WARPS_M * WARPS_N * 32, RBD_DM_MINB)
     for (int b = 0; b < NT; ++b)
 #pragma unroll
       for (int e = 0; e < 4; ++e) acc[a][b][e] = 0.0;
-  // ||x_j||^2 (l-tile 0 only): every thread takes half a B row (8 stored
-  // doubles) of column (tid % BN) in two chains; halves combined in order
-  static_assert(NTHREADS == 2 * BN, "two threads per B row");
-  double xa = 0.0, xb = 0.0;
+  // ||x_j||^2 (l-tile 0 only): each half of a B row (8 stored doubles) of
+  // column (tid % BN) in two chains, halves combined in order. With 2 threads
+  // per B row every thread takes one half; with one, a thread takes both halves
+  // (separate chains), so the sum has the same bits for either tile shape.
+  static_assert(NTHREADS == 2 * BN || NTHREADS == BN, "one or two threads per B row");
+  constexpr int kHalves = 2 * BN / NTHREADS;   // halves per thread
+  double xa = 0.0, xb = 0.0, xa2 = 0.0, xb2 = 0.0;
   __shared__ double xn_half[BN];
   const long long nk = (m + kDmBK - 1) / kDmBK;
   auto load_stage = [&](int st, long long kt) {
@@ -175,7 +178,7 @@ __global__ void __launch_bounds__(WARPS_M * WARPS_N * 32, RBD_DM_MINB)
     if (do_norm) {
       // stored positions p = 2q + h (the row's half h), rotated by the row so the
       // lanes of a warp spread over 8 bank pairs instead of one (rows are 128 B)
-      const int row = tid % BN, h = tid / BN;
+      const int row = tid % BN, h = (kHalves == 1) ? tid / BN : 0;
       const double* xr = B + row * kDmBK;
 #pragma unroll
       for (int q = 0; q < kDmBK / 2; q += 2) {
@@ -183,6 +186,12 @@ __global__ void __launch_bounds__(WARPS_M * WARPS_N * 32, RBD_DM_MINB)
         const double v1 = xr[(2 * q + 2 + h + 2 * row) & (kDmBK - 1)];
         xa = fma(v0, v0, xa);
         xb = fma(v1, v1, xb);
+        if (kHalves == 2) {
+          const double u0 = xr[(2 * q + 1 + 2 * row) & (kDmBK - 1)];
+          const double u1 = xr[(2 * q + 3 + 2 * row) & (kDmBK - 1)];
+          xa2 = fma(u0, u0, xa2);
+          xb2 = fma(u1, u1, xb2);
+        }
       }
     }
   }
@@ -199,9 +208,13 @@ __global__ void __launch_bounds__(WARPS_M * WARPS_N * 32, RBD_DM_MINB)
         if (l < d && j < N) Tn[l + j * d] = acc[a][b][e];
       }
   if (do_norm) {
-    if (tid >= BN) xn_half[tid - BN] = xa + xb;
-    __syncthreads();
-    if (tid < BN && j0 + tid < N) xnorm2[j0 + tid] = (xa + xb) + xn_half[tid];
+    if (kHalves == 2) {
+      if (j0 + tid < N) xnorm2[j0 + tid] = (xa + xb) + (xa2 + xb2);
+    } else {
+      if (tid >= BN) xn_half[tid - BN] = xa + xb;
+      __syncthreads();
+      if (tid < BN && j0 + tid < N) xnorm2[j0 + tid] = (xa + xb) + xn_half[tid];
+    }
   }
 }
 
