@@ -94,6 +94,40 @@ __global__ void __launch_bounds__(kT, 2) k_p1(const double* __restrict__ Y, long
   if (acc == 12345.0) out[cta] = acc;
 }
 
+// P1 pattern with wider per-column segments: a lane owns RPL row pairs of a
+// half (2*RPL rows), so each column segment of a block is 64*RPL*8*2 bytes;
+// 16 loads in flight per lane (16/RPL columns per batch).
+template <int RPL>
+__global__ void __launch_bounds__(kT, 2) k_p1w(const double* __restrict__ Y, long long m, int k,
+                                              const double* __restrict__ c, double* out) {
+  const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int HR = 64 * RPL;          // rows per half
+  constexpr int CB = 16 / RPL;          // columns per batch per warp
+  const long long lo = ((m * cta / G) + 1) & ~1LL, hi = (cta + 1 == G) ? m : (((m * (cta + 1) / G) + 1) & ~1LL);
+  double acc = 0.0;
+  for (long long rb = lo; rb < hi; rb += 2 * HR) {
+    const int half = warp / 4, wh = warp % 4;
+    const long long i0 = rb + half * HR + 2 * lane;
+    for (int l = wh; l < k; l += 4 * CB) {
+      double2 v[CB][RPL];
+#pragma unroll
+      for (int q = 0; q < CB; ++q)
+#pragma unroll
+        for (int r = 0; r < RPL; ++r) {
+          const long long i = i0 + 64 * r;
+          v[q][r] = (l + q * 4 < k && i + 1 < hi)
+                        ? __ldcg(reinterpret_cast<const double2*>(Y + i + (long long)(l + q * 4) * m))
+                        : make_double2(0, 0);
+        }
+#pragma unroll
+      for (int q = 0; q < CB; ++q)
+#pragma unroll
+        for (int r = 0; r < RPL; ++r) acc = fma(v[q][r].x + v[q][r].y, c[(l + q * 4) & 511], acc);
+    }
+  }
+  if (acc == 12345.0) out[cta] = acc;
+}
+
 int main(int argc, char** argv) {
   const long long m = argc > 1 ? atoll(argv[1]) : (1 << 20);
   const int k = argc > 2 ? atoi(argv[2]) : 512;
@@ -127,6 +161,10 @@ int main(int argc, char** argv) {
            e == cudaSuccess ? "" : cudaGetErrorString(e));
   };
   timeit([&] { k_p1<<<2 * nsm, kT>>>(Y, m, k, c, out); }, "P1 pattern (128-row blocks, regs)");
+  timeit([&] { k_p1w<1><<<2 * nsm, kT>>>(Y, m, k, c, out); }, "P1 RPL=1 (1 KB segments)");
+  timeit([&] { k_p1w<2><<<2 * nsm, kT>>>(Y, m, k, c, out); }, "P1 RPL=2 (2 KB segments)");
+  timeit([&] { k_p1w<4><<<2 * nsm, kT>>>(Y, m, k, c, out); }, "P1 RPL=4 (4 KB segments)");
+  timeit([&] { k_p1w<8><<<2 * nsm, kT>>>(Y, m, k, c, out); }, "P1 RPL=8 (8 KB segments)");
 #define RUN(R, NB, CPS, CO)                                                                \
   {                                                                                        \
     const size_t smb = sizeof(double) * (size_t)NB * k * R;                                \
