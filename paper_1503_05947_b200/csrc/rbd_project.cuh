@@ -116,11 +116,11 @@ inline int project_tile() {
   return e ? atoi(e) : 0;
 }
 
-inline int project_splitk(long long m, long long d, long long N, int nsm) {
+inline int project_splitk(long long m, long long d, long long N, int nsm, int per_sm = 0) {
   const int tile = project_tile();
   const long long bn = tile == 1 ? 128 : 64;
   const long long ctas = ((d + 63) / 64) * ((N + bn - 1) / bn);
-  const long long slots = (tile == 1 ? 2LL : 4LL) * nsm;
+  const long long slots = (per_sm > 0 ? per_sm : (tile == 1 ? 2LL : 4LL)) * nsm;
   int best = 1;
   double best_eff = 0.0;
   for (int s = 1; s <= 4; ++s) {

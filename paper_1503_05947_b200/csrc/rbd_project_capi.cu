@@ -6,6 +6,84 @@
 #include "rbd_project_tc.cuh"
 #include "rbd_classify.cuh"
 #include "rbd_compress_dmma.cuh"
+#include "rbd_project_dmma_tma.cuh"
+
+namespace {
+
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return (PFN_cuTensorMapEncodeTiled_v12000) nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }();
+  return fn;
+}
+
+// 2-D fp64 column-major operand for K5-TMA: rows (the K dimension, length
+// `inner`) contiguous, `outer` columns of leading dimension ld; box 16 x 64,
+// 128-byte swizzle (one 16-double row per 128 bytes).
+int make_map_f64(CUtensorMap* map, const double* base, long long inner, long long outer, long long ld) {
+  auto enc = tensor_map_encoder();
+  if (!enc) return set_err(RBD_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * sizeof(double)};
+  cuuint32_t box[2] = {(cuuint32_t)rbdk::kDmBK, 64u};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_err(RBD_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  return RBD_OK;
+}
+
+// K5 staging: 0 = per-thread cp.async (k_project_dmma), 1 = TMA, 3 stages, 4
+// CTAs per SM (128 registers), 2 = TMA, 4 stages, 3 CTAs per SM (162
+// registers, no spill). Measured on a C4 batch (tools/ab_k5.py, with the error
+// indicator): 34.63 / 32.57 / 31.82 ms; ncu of mode 2: DMMA pipe active 97.3 %
+// of active cycles (cuBLAS DGEMM, same operands: 30.41 ms). RBD_K5_TMA overrides.
+int k5_tma_mode() {
+  const char* e = getenv("RBD_K5_TMA");
+  return e ? atoi(e) : 2;
+}
+
+// T_new (and ||x_j||^2) through k_project_dmma_tma; the caller combines
+// split-K slices and forms the error indicator as for the cp.async kernel.
+int launch_project_tma(rbd_ctx_t ctx, int mode, const double* dY, long long m, long long d, long long ldy,
+                       const double* dXn, long long N, long long ldx, double* dTn, double* xn, int sk,
+                       double* Tws, double* xws) {
+  CUtensorMap mY, mX;
+  TRY(make_map_f64(&mY, dY, m, d, ldy));
+  TRY(make_map_f64(&mX, dXn, m, N, ldx));
+  const long long kc = ((m + sk - 1) / sk + 15) / 16 * 16;
+  dim3 grid((unsigned)cdiv(d, 64), (unsigned)cdiv(N, 64), (unsigned)sk);
+  if (mode == 2) {
+    static bool attr = false;
+    if (!attr) {
+      CU(cudaFuncSetAttribute(rbdk::k_project_dmma_tma<4, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)rbdk::dt_smem_bytes<4>()));
+      attr = true;
+    }
+    rbdk::k_project_dmma_tma<4, 3><<<grid, 128, rbdk::dt_smem_bytes<4>(), ctx->stream>>>(
+        mY, mX, m, d, N, dTn, xn, kc, Tws, xws);
+  } else {
+    static bool attr = false;
+    if (!attr) {
+      CU(cudaFuncSetAttribute(rbdk::k_project_dmma_tma<3, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)rbdk::dt_smem_bytes<3>()));
+      attr = true;
+    }
+    rbdk::k_project_dmma_tma<3, 4><<<grid, 128, rbdk::dt_smem_bytes<3>(), ctx->stream>>>(
+        mY, mX, m, d, N, dTn, xn, kc, Tws, xws);
+  }
+  ctx->launches++;
+  CU(cudaGetLastError());
+  return RBD_OK;
+}
+
+}  // namespace
 
 extern "C" {
 
@@ -22,9 +100,28 @@ int rbd_project_batch(rbd_ctx_t ctx, const double* dY, int64_t m, int64_t d, int
   long long nl = 0;
   if (d_err) TRY(ensure(ctx->scratch1, sizeof(double) * (size_t)std::max<int64_t>(N, 32)));
   // split the K = m reduction when the DMMA grid would leave a partial last wave
-  int sk = rbdk::project_splitk(m, d, N, ctx->nsm);
+  const int tma = k5_tma_mode();
+  int sk = rbdk::project_splitk(m, d, N, ctx->nsm, tma == 2 ? 3 : (tma == 1 ? 4 : 0));
   if (sk > 1 && ensure(ctx->pj_ws, sizeof(double) * (size_t)(sk - 1) * (size_t)(d * N + N)) != RBD_OK)
     sk = 1;
+  const bool tma_ok = tma > 0 && ldy % 2 == 0 && ldx % 2 == 0 && aligned16(dY) && aligned16(dXn) &&
+                      m < (1LL << 31) && d < (1LL << 31) && N < (1LL << 31);
+  if (tma_ok) {
+    double* xn = d_err ? ptr<double>(ctx->scratch1) : nullptr;
+    double* Tws = sk > 1 ? ptr<double>(ctx->pj_ws) : nullptr;
+    double* xws = sk > 1 ? Tws + (long long)(sk - 1) * d * N : nullptr;
+    TRY(launch_project_tma(ctx, tma, dY, m, d, ldy, dXn, N, ldx, dTn, xn, sk, Tws, xws));
+    if (sk > 1) {
+      rbdk::k_splitk_sum<<<1184, 256, 0, ctx->stream>>>(dTn, Tws, d * N, sk - 1, xn, xws, N);
+      ctx->launches++;
+    }
+    if (d_err) {
+      rbdk::k_project_err_fused<<<(unsigned)cdiv(N, 8), 256, 0, ctx->stream>>>(xn, dTn, d, N, d_err);
+      ctx->launches++;
+    }
+    CU(cudaGetLastError());
+    return RBD_OK;
+  }
   int rc = rbdk::launch_project_f64(dY, m, d, ldy, dXn, N, ldx, dTn, d_err, ctx->stream, &nl,
                                     d_err ? ptr<double>(ctx->scratch1) : nullptr, sk,
                                     sk > 1 ? ptr<double>(ctx->pj_ws) : nullptr);
@@ -317,18 +414,6 @@ int rbd_compress_host(rbd_ctx_t ctx, const double* hY, int64_t m, int64_t d, con
 // fp32 out-of-sample compression on tcgen05 (K6)
 // ===========================================================================
 namespace {
-
-PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
-        q != cudaDriverEntryPointSuccess)
-      return (PFN_cuTensorMapEncodeTiled_v12000) nullptr;
-    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-  }();
-  return fn;
-}
 
 // 2-D fp32 column-major operand (rows = contiguous dim of length `inner`,
 // `outer` columns, leading dimension ld), box 32 x 128, 128-byte swizzle.

@@ -1,4 +1,4 @@
-"""A/B of the K5 tile shapes (RBD_K5_TILE) on one C4 batch (Y 65 536 x 512,
+"""A/B of a K5 knob (default RBD_K5_TILE; argv[3] names another, e.g. RBD_K5_TMA) on one C4 batch (Y 65 536 x 512,
 X_new 65 536 x 16 384, fp64): alternating runs, CUDA events, plus a bitwise
 comparison of T_new and the error indicator across the shapes."""
 import os
@@ -17,13 +17,14 @@ Y = Y.t().contiguous().t()
 X = torch.randn(N, m, dtype=torch.float64, device="cuda", generator=g).t()
 tiles = sys.argv[1].split(",") if len(sys.argv) > 1 else ["0", "1"]
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 5
+var = sys.argv[3] if len(sys.argv) > 3 else "RBD_K5_TILE"
 ctx = rbd.Context(0)
 st = torch.cuda.ExternalStream(ctx.stream)
 res = {t: [] for t in tiles}
 outs = {}
 for it in range(reps + 1):
     for t in tiles:
-        os.environ["RBD_K5_TILE"] = t
+        os.environ[var] = t
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
         e0.record(st)
@@ -36,10 +37,10 @@ for it in range(reps + 1):
 flops = 2.0 * m * d * N
 for t, v in res.items():
     ms = float(np.median(v))
-    print(f"tile {t}: {ms:.2f} ms  {flops / ms / 1e9:.1f} TFLOP/s  runs {np.round(v, 2)}")
+    print(f"{var}={t}: {ms:.2f} ms  {flops / ms / 1e9:.1f} TFLOP/s  runs {np.round(v, 2)}")
 a = outs[tiles[0]]
 for t in tiles[1:]:
-    print(f"tile {t} bitwise equal to tile {tiles[0]}: T {np.array_equal(a[0], outs[t][0])} "
+    print(f"{var}={t} bitwise equal to {var}={tiles[0]}: T {np.array_equal(a[0], outs[t][0])} "
           f"err {np.array_equal(a[1], outs[t][1])}")
 Yt = Y.t().contiguous()
 ref = Yt @ X
