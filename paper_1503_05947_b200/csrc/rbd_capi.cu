@@ -333,10 +333,27 @@ int fused_grid(rbd_ctx_t ctx, long long m) {
 size_t fused_smem(long long dcap) { return sizeof(double) * 3 * (size_t)std::max<long long>(dcap, 1); }
 // c and p vectors, each zero-padded by one P1 batch (16 loads x kWarps columns);
 // weighted: + p_k and the YAY row for the finaliser
-size_t persist_smem(long long dcap, bool diag) {
+// fold: + this CTA's share of p_k (d doubles per P1 half)
+size_t persist_smem(long long dcap, bool diag, bool fold) {
   const size_t d = (size_t)std::max<long long>(dcap, 1);
-  return sizeof(double) * (2 * (d + 16 * kWarps) + (diag ? 2 * (d + 1) + 2 : 0)) +
+  const size_t halves = RBD_FOLD_ROWS / 64;
+  return sizeof(double) * (2 * (d + 16 * kWarps) + (diag ? 2 * (d + 1) + 2 : 0) + (fold ? halves * d : 0)) +
          (diag ? (size_t)kSvBytes : 0);   // DIAG: X-tile vector slots (rbd_weighted.cuh)
+}
+
+// The fp64 identity loop forms p_k = Y'w1_k inside P1 (FOLD instantiation)
+// when Y outgrows L2, so each step reads Y from HBM once instead of twice
+// (P1 + the Y'w1 groups); steps with k above fold_kmax keep the Y'w1 sweep,
+// since the 296 CTAs' 64-row blocks (64 k doubles each) must stay L2-resident
+// between P1's read and the fold's re-read. RBD_FOLD=0/1 and RBD_FOLD_KMAX
+// override (tools/microbench/p1_fold.cu).
+bool use_fold(long long m, long long d_max) {
+  if (const char* e = getenv("RBD_FOLD")) return atoi(e) != 0;
+  return (double)m * (double)d_max * 8.0 > 192.0 * (1 << 20);
+}
+long long fold_kmax(int grid) {
+  if (const char* e = getenv("RBD_FOLD_KMAX")) return atoll(e);
+  return (long long)(80.0e6 / (8.0 * 64.0 * std::max(grid, 1)));
 }
 
 // X tiles claimed ahead of the Y'w1 groups in every step of the fp64 identity
@@ -425,10 +442,13 @@ int enqueue_step_fused(rbd_ctx_t ctx, const LoopBufs& L) {
   return RBD_OK;
 }
 
-int persistent_grid(rbd_ctx_t ctx, int vec, long long d_max, bool diag, bool xf32) {
+int persistent_grid(rbd_ctx_t ctx, int vec, long long d_max, bool diag, bool xf32, bool fold) {
   int occ = 0;
-  const size_t smem = persist_smem(d_max, diag);
-  if (xf32)
+  const size_t smem = persist_smem(d_max, diag, fold);
+  if (fold)
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_rbd_persistent<2, false, false, false, true>,
+                                                  kThreads, smem);
+  else if (xf32)
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(
         &occ, vec == 2 ? k_rbd_persistent<2, false, false, true> : k_rbd_persistent<1, false, false, true>,
         kThreads, smem);
@@ -454,7 +474,8 @@ int launch_persistent(rbd_ctx_t ctx, const LoopBufs& L, const double* diag = nul
   const bool xpairs = xf32 || (L.ldx % 2 == 0 && aligned16(L.X));
   const int vec = (xpairs && L.m % 2 == 0 && aligned16(L.Y) && aligned16(ctx->w.p) &&
                    (!diag || aligned16(ctx->wd_axi.p))) ? 2 : 1;
-  const int grid = persistent_grid(ctx, vec, L.d_max, diag != nullptr, xf32);
+  const bool fold = !xf32 && !diag && vec == 2 && use_fold(L.m, L.d_max);
+  const int grid = persistent_grid(ctx, vec, L.d_max, diag != nullptr, xf32, fold);
   if (grid < 1) return set_err(RBD_ERR_CUDA, "persistent kernel: zero occupancy");
   const long long S = cdiv(L.m, kChunk);
   const long long ngx = cdiv(L.n, kCols);
@@ -498,6 +519,7 @@ int launch_persistent(rbd_ctx_t ctx, const LoopBufs& L, const double* diag = nul
   a.forced = ctx->forced_h.empty() ? nullptr : ptr<long long>(ctx->forced);
   a.nforced = (long long)ctx->forced_h.size();
   a.ydelay = y_delay(grid, xf32);
+  a.fold_kmax = fold ? fold_kmax(grid) : 0;
   if (diag) {
     TRY(ensure(ctx->wd_ppart2, sizeof(double) * (size_t)std::max<long long>(grid, S) * L.d_max));
     TRY(ensure(ctx->wd_q, sizeof(double) * (size_t)(L.d_max + 1)));
@@ -536,12 +558,16 @@ int launch_persistent(rbd_ctx_t ctx, const LoopBufs& L, const double* diag = nul
     a.trace_step = atoll(ts);
   }
   void* args[] = {&a};
-  const size_t smem = persist_smem(L.d_max, diag != nullptr);
-  void* fn = xf32 ? (vec == 2 ? (void*)k_rbd_persistent<2, false, false, true>
+  const size_t smem = persist_smem(L.d_max, diag != nullptr, fold);
+  void* fn = fold ? (void*)k_rbd_persistent<2, false, false, false, true>
+             : xf32 ? (vec == 2 ? (void*)k_rbd_persistent<2, false, false, true>
                               : (void*)k_rbd_persistent<1, false, false, true>)
              : diag ? (vec == 2 ? (void*)k_rbd_persistent<2, false, true>
                               : (void*)k_rbd_persistent<1, false, true>)
                   : (vec == 2 ? (void*)k_rbd_persistent<2, false> : (void*)k_rbd_persistent<1, false>);
+  if (getenv("RBD_DEBUG_LAUNCH"))
+    fprintf(stderr, "[launch] persistent vec=%d fold=%d diag=%d xf32=%d grid=%d smem=%zu fold_kmax=%lld\n", vec,
+            (int)fold, diag != nullptr, (int)xf32, grid, smem, a.fold_kmax);
   cudaError_t e = cudaLaunchCooperativeKernel(fn, grid, kThreads, args, smem, ctx->stream);
   ctx->launches++;
   if (e != cudaSuccess)
@@ -784,6 +810,9 @@ int rbd_ctx_create(int device, rbd_ctx_t* out) {
                          cudaFuncAttributeMaxDynamicSharedMemorySize, sm_f32);
     cudaFuncSetAttribute(k_rbd_persistent<1, false, false, true>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, sm_f32);
+    cudaFuncSetAttribute(k_rbd_persistent<2, false, false, false, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)persist_smem(kFMaxCoef, false, true));
   }
   cudaFuncSetAttribute(k_rbd_persistent<2, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)persist_smem(kFMaxCoef, true));

@@ -202,9 +202,10 @@ long long gemv_grid(long long m);
 int enqueue_init(rbd_ctx_t ctx, const double* X, long long m, long long n, long long ldx,
                  double* partial, double* colsq, double* resid, DevState* st);
 int diag_vec_grid(rbd_ctx_t ctx, long long m);
-size_t persist_smem(long long dcap, bool diag = false);
+size_t persist_smem(long long dcap, bool diag = false, bool fold = false);
 long long y_delay(int grid, bool xf32 = false);
-int persistent_grid(rbd_ctx_t ctx, int vec, long long d_max, bool diag = false, bool xf32 = false);
+int persistent_grid(rbd_ctx_t ctx, int vec, long long d_max, bool diag = false, bool xf32 = false,
+                    bool fold = false);
 int ensure_loop_buffers(rbd_ctx_t ctx, long long m, long long n, long long d_max);
 int validate_after_init(const rbd_config_t* cfg, long long m, long long n, const DevState& hs,
                         bool diag_supplied = false, double diag_max = 0.0);

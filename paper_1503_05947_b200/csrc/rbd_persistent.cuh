@@ -93,6 +93,10 @@ struct PersistArgs {
   // Y'w1 groups, then the rest (CTAs that claim first then stream X instead
   // of waiting for every CTA's P1; the decision comes a tile later)
   long long ydelay;
+  // FOLD instantiation: steps with k <= fold_kmax form p_k = Y'w1_k inside P1
+  // (each CTA's share from the row block it just read, re-read from L2) and
+  // the Y'w1 groups only sum the G shares; larger k sweep Y as before
+  long long fold_kmax;
 };
 
 __device__ __forceinline__ void red_release_add_u64(unsigned long long* p, unsigned long long v) {
@@ -233,12 +237,105 @@ constexpr int kTraceWords = 256;  // per CTA: [0] count, then (tag<<40 | time) w
 // column x_j, [4+m, 4+m+k+1) the column T[0:k+1, j].
 constexpr int kPayHead = 4;
 
-template <int VEC, bool SHARD, bool DIAG = false, bool XF32 = false>
+#ifndef RBD_FOLD_ROWS
+#define RBD_FOLD_ROWS 64   // FOLD P1 block height (64: one half of 8 warps; 128: two halves)
+#endif
+// Columns of p_k summed per Y'w1 group in a FOLD step (the G CTA shares).
+constexpr int kFoldCols = 32;
+
+// One level of the FOLD transposing butterfly: S values per lane; the lane
+// keeps the half selected by its lane bit BIT and adds the partner's copy of
+// that half (one shuffle per kept value).
+template <int S, int BIT>
+__device__ __forceinline__ void fold_butterfly(double* t, int lane) {
+  const bool upper = (lane & BIT) != 0;
+#pragma unroll
+  for (int q = 0; q < S; ++q) {
+    const double send = upper ? t[q] : t[q + S];
+    const double keep = upper ? t[q + S] : t[q];
+    t[q] = keep + __shfl_xor_sync(0xffffffffu, send, BIT);
+  }
+}
+
+// FOLD, P1: one row block's share of p_k = Y[:, 0:k]' w1_k, added into psh
+// (shared). The block is re-read from L2 (column k-1 was just written by P1);
+// a lane holds two rows (yb = Y + its first row; wa, wb their w1), and a
+// transposing butterfly leaves lane pair 2c..2c+1 with column c of the
+// 16-column batch summed over the half's 64 rows. The most recently read
+// batches are re-read first (fewer L2 misses: C2 3058 -> 3055 ms against
+// in-order re-reads below k = 448).
+template <int PW>
+__device__ __forceinline__ void fold_block_share(const double* __restrict__ yb, long long m, long long k,
+                                              int wh, int lane, double wa, double wb, bool rows,
+                                              double* psh) {
+  constexpr int kStep = kPLoads * PW;
+  const long long nb = (k - wh + kStep - 1) / kStep;
+  for (long long bi = 0; bi < nb; ++bi) {
+    const long long l = wh + (nb - 1 - bi) * kStep;
+    double t[kPLoads];
+#pragma unroll
+    for (int q = 0; q < kPLoads; ++q) {
+      const long long col = l + q * PW;
+      double2 v = make_double2(0.0, 0.0);
+      if (rows && col < k) v = __ldcg(reinterpret_cast<const double2*>(yb + col * m));
+      t[q] = fma(v.y, wb, v.x * wa);
+    }
+    fold_butterfly<8, 16>(t, lane);
+    fold_butterfly<4, 8>(t, lane);
+    fold_butterfly<2, 4>(t, lane);
+    fold_butterfly<1, 2>(t, lane);
+    t[0] += __shfl_xor_sync(0xffffffffu, t[0], 1);
+    const int qs = (((lane >> 4) & 1) << 3) | (((lane >> 3) & 1) << 2) | (((lane >> 2) & 1) << 1) |
+                   ((lane >> 1) & 1);
+    const long long col = l + qs * PW;
+    if ((lane & 1) == 0 && col < k) psh[col] += t[0];   // (warp, lane pair) owns col
+  }
+}
+
+// FOLD, Y'w1 group t: p_k[l] = sum of the G CTA shares (ppart[b][l]) for
+// the group's kFoldCols columns, in a fixed order: 8 strided partial sums per
+// column, then the partials in order (rp: kThreads doubles of shared memory).
+static __device__ __noinline__ void fold_group_sum(const double* ppart, long long d_max, int G, long long k,
+                                            long long t, double* rp, double* pk) {
+  constexpr int kParts = kThreads / kFoldCols;
+  const int tid = threadIdx.x;
+  const int cl = tid % kFoldCols, part = tid / kFoldCols;
+  const long long l = t * kFoldCols + cl;
+  double v = 0.0;
+  if (l < k)
+    for (int b = part; b < G; b += kParts) v += __ldcg(&ppart[(long long)b * d_max + l]);
+  rp[part * kFoldCols + cl] = v;
+  __syncthreads();
+  if (tid < kFoldCols && l < k) {
+    double sum = rp[cl];
+#pragma unroll
+    for (int pp = 1; pp < kParts; ++pp) sum += rp[pp * kFoldCols + cl];
+    pk[l] = sum;
+  }
+}
+
+template <int VEC, bool SHARD, bool DIAG = false, bool XF32 = false, bool FOLD = false>
 __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
   static_assert(!(SHARD && DIAG), "the weighted loop is single-GPU");
   static_assert(!XF32 || (!SHARD && !DIAG), "fp32 storage: single-GPU identity loop");
+  static_assert(!FOLD || (VEC == 2 && !DIAG && !XF32), "fold: fp64 identity loop, row pairs");
+  // The fold lives in its own instantiation: compiled into the base kernel
+  // (runtime-gated) it cost that kernel's X-tile stream 4-9% on C1/C2
+  // (ptxas then consumed a batch's first loads before issuing the rest).
+  constexpr bool FC = FOLD;
   extern __shared__ __align__(128) double dsm[];
-  constexpr int kPBatch = kPLoads * kWarps / 2;   // columns per P1 batch of a half
+  // P1 block: halves of 32*VEC rows (warps 0-3 / 4-7); within a half the kPW
+  // warps split the columns (l = wh mod kPW), so every row's sum runs in the
+  // same order whichever half it falls in. FOLD: one 64-row half of all 8
+  // warps, so the 296 CTAs' blocks (64 x k doubles each) stay L2-resident
+  // until the block's Y'w1 share re-reads them (tools/microbench/p1_fold.cu:
+  // 128-row blocks miss L2 at k >= 256)
+  constexpr bool kOneHalf = FOLD && RBD_FOLD_ROWS == 64;
+  constexpr int kPW = kOneHalf ? kWarps : kWarps / 2;   // warps per half
+  constexpr int kPHalf = 32 * VEC;
+  constexpr int kPRows = kOneHalf ? kPHalf : 2 * kPHalf;  // rows per P1 block
+  constexpr int kNHalf = kPRows / kPHalf;
+  constexpr int kPBatch = kPLoads * kPW;   // columns per P1 batch of a half
   static_assert(kPBatch <= 16 * kWarps, "P1 batch padding (persist_smem) too small");
   double* cs = dsm;                        // c = T[0:k, j*], zero-padded to a batch multiple
   double* ps = cs + a.d_max + kPBatch;     // p_{k-1} (pending column), zero-padded
@@ -246,13 +343,11 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
   double* yd = pd + a.d_max + 1;                // DIAG: YAY[k, 0:k+1]
   // DIAG, VEC 2: per-thread cp.async slots of the X tiles' two vectors
   double2* svec = reinterpret_cast<double2*>(cs + ((2 * (a.d_max + 16 * kWarps) + 2 * (a.d_max + 1) + 1) & ~1LL));
+  // FOLD: this CTA's share of p_k, per half (recomputed at each use: nothing
+  // of the fold stays live across the X-tile queue)
+  auto psh = [&] { return dsm + 2 * (a.d_max + 16 * kWarps); };
   __shared__ double red[kWarps][kCols];
-  // P1 block: two warp-halves of 32*VEC rows each (warps 0-3 / 4-7); within a
-  // half the 4 warps split the columns (l = warp%4 mod 4), so every row's sum
-  // runs in the same order whichever half it falls in
-  constexpr int kPHalf = 32 * VEC;
-  constexpr int kPRows = 2 * kPHalf;  // rows per P1 block
-  constexpr int kPW = kWarps / 2;     // warps per half
+  __shared__ double w1s[FC ? kPRows : 1];         // FOLD: w1 of the block's rows
   __shared__ double red_c[kWarps][kPHalf];
   __shared__ double red_p[kWarps][kPHalf];
   __shared__ double smn[kWarps];
@@ -349,6 +444,11 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
     }
   };
 
+  // the shares start at zero here and are rezeroed as P1 publishes them
+  // (zeroing them at the top of each step made ptxas interleave the X-tile
+  // batch, as above)
+  if (FC && a.fold_kmax > 0)
+    for (long long l = tid; l < kNHalf * a.d_max; l += kThreads) psh()[l] = 0.0;   // read after P1's barriers
   while (true) {
     const int live = !done;
     if (!live && !pending) break;
@@ -362,6 +462,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
                                 : __ldcg(&a.T[l * n + jstar]);
       ps[l] = (pending && reorth_prev && l < kb) ? __ldcg(&pbuf(k - 1)[l]) : 0.0;
     }
+    // FOLD: this step forms p_k in P1 (its Y'w1 groups sum the CTA shares)
+    const bool fold = FC && live && k > 0 && k <= a.fold_kmax;
     const double* x = SHARD ? pay + kPayHead : a.X + jstar * a.ldx;
     const float* xf = XF32 ? a.Xf + jstar * a.ldx : nullptr;
     __syncthreads();
@@ -433,6 +535,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
 #pragma unroll
         for (int v = 0; v < VEC; ++v) {
           const long long i = i0 + v;
+          if constexpr (FC) w1s[half * kPHalf + VEC * lane + v] = 0.0;
           if (i >= iend) break;
           const int w0 = half * kPW;
           double sc = red_c[w0][VEC * lane + v], sp = red_p[w0][VEC * lane + v];
@@ -449,6 +552,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
           if (live) {
             const double w1 = xpre[v] - sc;                  // first pass of column k
             a.w[i] = w1;
+            if constexpr (FC) w1s[half * kPHalf + VEC * lane + v] = w1;
             nacc = fma(w1, w1, nacc);
             if constexpr (DIAG) {
               const double awv = apre[v] * w1;               // a o w1 (weight.cpp:83)
@@ -459,9 +563,34 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
         }
       }
       __syncthreads();
+      if constexpr (FC) {
+        // the block's share of p_k = Y[:, 0:k]' w1_k: re-read the block (L2;
+        // column k-1 was just written above), a lane's two rows times w1, and a
+        // transposing butterfly leaves lane pair 2c..2c+1 with column c of the
+        // 16-column batch summed over the half's 64 rows. The most recently
+        // read batches are re-read first once k is large (fewer L2 misses).
+        if (fold)
+          fold_block_share<kPW>(a.Y + i0, m, k, wh, lane, w1s[half * kPHalf + VEC * lane],
+                                w1s[half * kPHalf + VEC * lane + 1], nv == 2, psh() + half * a.d_max);
+        __syncthreads();
+      }
     }
     pending = 0;
     if (!live) continue;   // materialisation-only pass after the stop
+    if constexpr (FC) {
+      if (fold)   // published by the release-adds below
+        for (long long l = tid; l < k; l += kThreads) {
+          // read and rezero (the shares start at zero: kernel entry, then here)
+          double v = psh()[l];
+          psh()[l] = 0.0;
+#pragma unroll
+          for (int h = 1; h < kNHalf; ++h) {
+            v += psh()[h * a.d_max + l];
+            psh()[h * a.d_max + l] = 0.0;
+          }
+          a.ppart[(long long)cta * a.d_max + l] = v;
+        }
+    }
     {
       const double sblk = block_sum_fixed<kThreads>(warp % kPW == 0 ? nacc : 0.0, smn);
       if constexpr (DIAG) {
@@ -546,7 +675,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
     //                 earlier and finalisation is deferred by one tile, so the
     //                 poll rarely waits, and every wait targets an
     //                 earlier-claimed tile (no deadlock).
-    const long long gy = (k + kCols - 1) / kCols;
+    const long long gy = (FC && k > 0 && k <= a.fold_kmax) ? (k + kFoldCols - 1) / kFoldCols
+                                                            : (k + kCols - 1) / kCols;
     const long long total = gy + nx;
     double bv = -1.0;          // this CTA's best finalised residual (argmax record)
     long long bj = 0x7fffffffffffffffLL;
@@ -849,6 +979,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
       if (tid == 0) next = (long long)(atomicAdd(&ctl->tile_ctr, 1ull) - tile_base);
       if (code < 0) {
         const long long t = -1 - code;   // the Y'w1 group
+        if (FC && k <= a.fold_kmax)   // a FOLD step (k > 0 here)
+          fold_group_sum(a.ppart, a.d_max, G, k, t, &red_c[0][0], pbuf(k));
+        else
         for (long long s = 0; s < S; ++s) {
           if constexpr (DIAG)
             sweep_tile_dot2<VEC, LOAD_CG, true, 2>(a.Y, m, m, k, a.w, a.aw, a.ppart, a.ppart2,
@@ -859,7 +992,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
                                                        dummy_nz);
         }
         // the partials of this group were written by this CTA (CTA-visible)
-        if (tid < kCols && t * kCols + tid < k) {
+        if (!(FC && k <= a.fold_kmax) && tid < kCols && t * kCols + tid < k) {
           const long long l = t * kCols + tid;
           double v = 0.0;
           for (long long s = 0; s < S; ++s) v += a.ppart[s * a.d_max + l];
