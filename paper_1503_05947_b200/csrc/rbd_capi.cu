@@ -446,8 +446,9 @@ int persistent_grid(rbd_ctx_t ctx, int vec, long long d_max, bool diag, bool xf3
   int occ = 0;
   const size_t smem = persist_smem(d_max, diag, fold);
   if (fold)
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_rbd_persistent<2, false, false, false, true>,
-                                                  kThreads, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &occ, xf32 ? k_rbd_persistent<2, false, false, true, true> : k_rbd_persistent<2, false, false, false, true>,
+        kThreads, smem);
   else if (xf32)
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(
         &occ, vec == 2 ? k_rbd_persistent<2, false, false, true> : k_rbd_persistent<1, false, false, true>,
@@ -474,7 +475,7 @@ int launch_persistent(rbd_ctx_t ctx, const LoopBufs& L, const double* diag = nul
   const bool xpairs = xf32 || (L.ldx % 2 == 0 && aligned16(L.X));
   const int vec = (xpairs && L.m % 2 == 0 && aligned16(L.Y) && aligned16(ctx->w.p) &&
                    (!diag || aligned16(ctx->wd_axi.p))) ? 2 : 1;
-  const bool fold = !xf32 && !diag && vec == 2 && use_fold(L.m, L.d_max);
+  const bool fold = !diag && vec == 2 && use_fold(L.m, L.d_max);
   const int grid = persistent_grid(ctx, vec, L.d_max, diag != nullptr, xf32, fold);
   if (grid < 1) return set_err(RBD_ERR_CUDA, "persistent kernel: zero occupancy");
   const long long S = cdiv(L.m, kChunk);
@@ -559,7 +560,8 @@ int launch_persistent(rbd_ctx_t ctx, const LoopBufs& L, const double* diag = nul
   }
   void* args[] = {&a};
   const size_t smem = persist_smem(L.d_max, diag != nullptr, fold);
-  void* fn = fold ? (void*)k_rbd_persistent<2, false, false, false, true>
+  void* fn = fold ? (xf32 ? (void*)k_rbd_persistent<2, false, false, true, true>
+                          : (void*)k_rbd_persistent<2, false, false, false, true>)
              : xf32 ? (vec == 2 ? (void*)k_rbd_persistent<2, false, false, true>
                               : (void*)k_rbd_persistent<1, false, false, true>)
              : diag ? (vec == 2 ? (void*)k_rbd_persistent<2, false, true>
@@ -811,6 +813,9 @@ int rbd_ctx_create(int device, rbd_ctx_t* out) {
     cudaFuncSetAttribute(k_rbd_persistent<1, false, false, true>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, sm_f32);
     cudaFuncSetAttribute(k_rbd_persistent<2, false, false, false, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)persist_smem(kFMaxCoef, false, true));
+    cudaFuncSetAttribute(k_rbd_persistent<2, false, false, true, true>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)persist_smem(kFMaxCoef, false, true));
   }

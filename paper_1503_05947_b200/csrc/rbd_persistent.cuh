@@ -318,7 +318,7 @@ template <int VEC, bool SHARD, bool DIAG = false, bool XF32 = false, bool FOLD =
 __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
   static_assert(!(SHARD && DIAG), "the weighted loop is single-GPU");
   static_assert(!XF32 || (!SHARD && !DIAG), "fp32 storage: single-GPU identity loop");
-  static_assert(!FOLD || (VEC == 2 && !DIAG && !XF32), "fold: fp64 identity loop, row pairs");
+  static_assert(!FOLD || (VEC == 2 && !DIAG && !SHARD), "fold: single-GPU identity loop, row pairs");
   // The fold lives in its own instantiation: compiled into the base kernel
   // (runtime-gated) it cost that kernel's X-tile stream 4-9% on C1/C2
   // (ptxas then consumed a batch's first loads before issuing the rest).
@@ -1065,7 +1065,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
           sweep_tiles_f32<MODE_DOT, true, kXT>(a.Xf, a.ldx, m, n, a.w, a.partial, n, s * ngt + g,
                                                1LL << 40, red2, dummy_nf, dummy_nz, a.xvec4 != 0);
         else
-          sweep_tiles<VEC, MODE_DOT, LOAD_STREAM, true>(a.X, a.ldx, m, n, a.w, a.partial, n,
+          // the sharded instantiation needs the batch fence (its batches
+          // were split: SASS showed FMAs between the X loads); the others
+          // already issue every load of a batch first
+          sweep_tiles<VEC, MODE_DOT, LOAD_STREAM, true, kCols, SHARD>(a.X, a.ldx, m, n, a.w, a.partial, n,
                                                          s * ngx + g, 1LL << 40, red, dummy_nf,
                                                          dummy_nz);
         mark(7);

@@ -78,3 +78,13 @@ def test_fold_rank_deficient_breakdown(cuda, fold_env):
     r = oracle.decompose(A, 20)
     assert g.d == r.d
     assert compare(g, r, A) == r.d
+
+
+@pytest.mark.parametrize("m,n,d", [(8194, 40, 33), (12290, 130, 100)])
+def test_fold_f32_storage_parity(cuda, fold_env, m, n, d):
+    """The fp32 storage mode's FOLD instantiation (X in fp32, Y and the fold
+    in fp64) against the fp64 oracle on the fp32-valued matrix, 1e-10."""
+    X32 = np.asfortranarray(oracle.random_matrix(m, n, 4000 + m).astype(np.float32))
+    g = rbd.decompose(X32, d_max=d)
+    r = oracle.decompose(X32.astype(np.float64), d)
+    assert compare(g, r, X32, rerun=lambda sel: rbd.decompose(X32, d_max=d, forced_selection=sel)) == r.d

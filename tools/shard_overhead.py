@@ -1,7 +1,7 @@
 """Per-step cost of the sharded mode (step kernel, NCCL record allgather, pack,
 NCCL payload allreduce, select; replayed from a CUDA graph, or eager with
-RBD_SHARD_GRAPH=0) against the single-GPU persistent loop, on C1 at world 1
-(NCCL with one rank). Prints one JSON line."""
+RBD_SHARD_GRAPH=0) against the single-GPU persistent loop, on C1 (or the
+workload named by argv[1]) at world 1 (NCCL with one rank). Prints one JSON line."""
 import ctypes as C
 import json
 import os
@@ -14,8 +14,10 @@ import paper_1503_05947_b200 as rbd  # noqa: E402
 from paper_1503_05947_b200 import configs, distributed as rd  # noqa: E402
 from paper_1503_05947_b200._lib import check, load_library  # noqa: E402
 
-w = configs.WORKLOADS["C1-image-like"]
-X = configs.c1_matrix(n=w.n, seed=w.seed, device="cuda")
+import bench  # noqa: E402
+
+name = sys.argv[1] if len(sys.argv) > 1 else "C1-image-like"
+w, X, _ = bench.make_workload(name, torch.device("cuda"))
 m, n = X.shape
 ctx = rbd.Context(0)
 buf = C.create_string_buffer(128)
