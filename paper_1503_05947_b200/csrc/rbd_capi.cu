@@ -341,15 +341,18 @@ size_t persist_smem(long long dcap, bool diag, bool fold) {
          (diag ? (size_t)kSvBytes : 0);   // DIAG: X-tile vector slots (rbd_weighted.cuh)
 }
 
-// The fp64 identity loop forms p_k = Y'w1_k inside P1 (FOLD instantiation)
-// when Y outgrows L2, so each step reads Y from HBM once instead of twice
-// (P1 + the Y'w1 groups); steps with k above fold_kmax keep the Y'w1 sweep,
-// since the 296 CTAs' 64-row blocks (64 k doubles each) must stay L2-resident
-// between P1's read and the fold's re-read. RBD_FOLD=0/1 and RBD_FOLD_KMAX
-// override (tools/microbench/p1_fold.cu).
+// RBD_FOLD=1: the identity loop forms p_k = Y'w1_k inside P1 (FOLD
+// instantiation), so each step reads Y from HBM once instead of twice (P1 +
+// the Y'w1 groups) when Y outgrows L2; steps with k above fold_kmax
+// (RBD_FOLD_KMAX) keep the Y'w1 sweep, since the 296 CTAs' 64-row blocks (64 k
+// doubles each) must stay L2-resident between P1's read and the fold's
+// re-read (tools/microbench/p1_fold.cu).
 bool use_fold(long long m, long long d_max) {
-  if (const char* e = getenv("RBD_FOLD")) return atoi(e) != 0;
-  return (double)m * (double)d_max * 8.0 > 192.0 * (1 << 20);
+  if (const char* e = getenv("RBD_FOLD")) return atoi(e) != 0 && (double)m * (double)d_max > 0.0;
+  // off by default: once the instrumentation checks left the base kernel
+  // (RBD_INSTRUMENT), its C2 loop (2977 ms) beat the FOLD one (3004 ms; fp32
+  // storage 1811 vs 1859 ms): the fold's P1 costs more than the second Y read
+  return false;
 }
 long long fold_kmax(int grid) {
   if (const char* e = getenv("RBD_FOLD_KMAX")) return atoll(e);
@@ -545,14 +548,20 @@ int launch_persistent(rbd_ctx_t ctx, const LoopBufs& L, const double* diag = nul
   a.progress = (ctx->ystream_dst && ctx->d_progress) ? ctx->d_progress : nullptr;
   if (a.progress) *(volatile long long*)ctx->h_progress = 0;
   a.phase_ns = nullptr;
-  if (getenv("RBD_PHASE_TIMING")) {
+  if ((getenv("RBD_PHASE_TIMING") || getenv("RBD_TRACE_STEP")) && !RBD_INSTRUMENT) {
+    static bool warned = false;
+    if (!warned) fprintf(stderr, "[rbd] RBD_PHASE_TIMING / RBD_TRACE_STEP need a build with "
+                                 "RBD_NVCC_DEFS=-DRBD_INSTRUMENT=1; ignored\n");
+    warned = true;
+  }
+  if (RBD_INSTRUMENT && getenv("RBD_PHASE_TIMING")) {
     TRY(ensure(ctx->scratch1, 256));
     cudaMemsetAsync(ctx->scratch1.p, 0, 128, ctx->stream);
     a.phase_ns = ptr<unsigned long long>(ctx->scratch1);
   }
   a.trace = nullptr;
   DevBuf tracebuf;
-  if (const char* ts = getenv("RBD_TRACE_STEP")) {
+  if (const char* ts = RBD_INSTRUMENT ? getenv("RBD_TRACE_STEP") : nullptr) {
     TRY(ensure(tracebuf, sizeof(unsigned long long) * (size_t)grid * kTraceWords));
     cudaMemsetAsync(tracebuf.p, 0, sizeof(unsigned long long) * (size_t)grid * kTraceWords, ctx->stream);
     a.trace = ptr<unsigned long long>(tracebuf);

@@ -237,6 +237,9 @@ constexpr int kTraceWords = 256;  // per CTA: [0] count, then (tag<<40 | time) w
 // column x_j, [4+m, 4+m+k+1) the column T[0:k+1, j].
 constexpr int kPayHead = 4;
 
+#ifndef RBD_INSTRUMENT
+#define RBD_INSTRUMENT 0   // 1: RBD_PHASE_TIMING / RBD_TRACE_STEP work (tools only)
+#endif
 #ifndef RBD_FOLD_ROWS
 #define RBD_FOLD_ROWS 64   // FOLD P1 block height (64: one half of 8 warps; 128: two halves)
 #endif
@@ -417,25 +420,35 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
       g = (tx < nf) ? tx / (S - 1) : tx - nf;
       s = (tx < nf) ? tx - g * (S - 1) : S - 1;
     } else {
-      g = tx / S;
+      // The fenced instantiations (below) divide in 32 bits while nx < 2^32
+      // (a 64-bit division is a long emulated sequence). In the base kernel
+      // the 32-bit form made ptxas split the X batches (C1 +8%), so it
+      // keeps the 64-bit one.
+      constexpr bool kDiv32 = FOLD || SHARD;
+      g = (kDiv32 && nx < (1LL << 32)) ? (long long)((unsigned)tx / (unsigned)S) : tx / S;
       s = tx - g * S;
     }
   };
   unsigned dummy_nf = 0, dummy_nz = 0;
-  const bool timing = (a.phase_ns != nullptr) && cta == 0 && tid == 0;
+  // Phase timing and the step trace (tools/ab_arms.py --phases,
+  // tools/trace_report.py) are compiled in only with -DRBD_INSTRUMENT=1: their
+  // per-call checks were ~3% of the loop's issued instructions (ncu source
+  // counters, C2), on the X-tile path.
+  constexpr bool kInstr = RBD_INSTRUMENT;
+  const bool timing = kInstr && (a.phase_ns != nullptr) && cta == 0 && tid == 0;
   unsigned long long tp = timing ? globaltimer() : 0ull;
   auto mark = [&](int slot) {
-    if (timing) {
+    if (kInstr && timing) {
       const unsigned long long t = globaltimer();
       a.phase_ns[slot] += t - tp;
       tp = t;
     }
   };
-  unsigned long long* trow = a.trace ? a.trace + (size_t)cta * kTraceWords : nullptr;
+  unsigned long long* trow = (kInstr && a.trace) ? a.trace + (size_t)cta * kTraceWords : nullptr;
   // tag: 1 P1 start, 2 P1 end, 3 bar1 out, 4 tile start (|tile<<8), 5 tile end,
   //      6 P2 end, 7 bar2 out, 8 P3 end, 9 bar3 out, 10 step end
   auto trace = [&](long long step, unsigned long long tag) {
-    if (trow && tid == 0 && step >= a.trace_step && step < a.trace_step + 2) {
+    if (kInstr && trow && tid == 0 && step >= a.trace_step && step < a.trace_step + 2) {
       const unsigned long long c = trow[0];
       if (c + 1 < kTraceWords) {
         trow[1 + c] = (tag << 40) | (globaltimer() & 0xFFFFFFFFFFull);
@@ -1065,10 +1078,11 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
           sweep_tiles_f32<MODE_DOT, true, kXT>(a.Xf, a.ldx, m, n, a.w, a.partial, n, s * ngt + g,
                                                1LL << 40, red2, dummy_nf, dummy_nz, a.xvec4 != 0);
         else
-          // the sharded instantiation needs the batch fence (its batches
-          // were split: SASS showed FMAs between the X loads); the others
-          // already issue every load of a batch first
-          sweep_tiles<VEC, MODE_DOT, LOAD_STREAM, true, kCols, SHARD>(a.X, a.ldx, m, n, a.w, a.partial, n,
+          // the load-batch fence keeps each X batch whole where ptxas split
+          // it (sharded, FOLD: FMAs between the loads in SASS); the base
+          // kernel issues whole batches without it, and there the fence's
+          // later start of the FMAs cost C1 2.5% (batch_fence)
+          sweep_tiles<VEC, MODE_DOT, LOAD_STREAM, true, kCols, SHARD || FOLD>(a.X, a.ldx, m, n, a.w, a.partial, n,
                                                          s * ngx + g, 1LL << 40, red, dummy_nf,
                                                          dummy_nz);
         mark(7);

@@ -1,6 +1,7 @@
 """A/B of env-knob combinations of the persistent loop on one workload, arms
 alternated in one process (clock drift hits every arm alike), then one
-RBD_PHASE_TIMING run per arm (CTA 0 phase split, stderr).
+RBD_PHASE_TIMING run per arm (CTA 0 phase split, stderr; needs a library
+built with RBD_NVCC_DEFS=-DRBD_INSTRUMENT=1).
 Usage: tools/ab_arms.py WORKLOAD "A=1,B=2" "A=0" ... [--reps R] [--f32]"""
 import argparse
 import os

@@ -1,4 +1,5 @@
-"""Summarise a persistent-kernel trace (RBD_TRACE_STEP / RBD_TRACE_FILE), per step."""
+"""Summarise a persistent-kernel trace (RBD_TRACE_STEP / RBD_TRACE_FILE; the
+library must be built with RBD_NVCC_DEFS=-DRBD_INSTRUMENT=1), per step."""
 import sys
 
 import numpy as np
