@@ -133,17 +133,17 @@ struct SweepArgs {
 // KC = columns per tile. A column's chunk sum depends only on the row layout
 // (thread -> rows, fma order, reduction tree), never on KC or on how loads are
 // batched, so tiles of different widths give bit-identical partials.
+// One tile (chunk s, column group g); ends with the partials written by
+// tid < KC and no barrier (sweep_tiles adds it; the persistent loop's X tiles
+// pass s, g directly instead of a tile index divided again here).
 template <int VEC, int MODE, int ALOAD, bool VCOH = false, int KC = kCols, bool FENCE = false>
-__device__ __forceinline__ void sweep_tiles(const double* __restrict__ A, long long lda,
-                                            long long m, long long ncols,
-                                            const double* __restrict__ v,
-                                            double* __restrict__ partial, long long pstride,
-                                            long long tile_begin, long long tile_stride,
-                                            double (*red)[kCols], unsigned& nonfinite,
-                                            unsigned& nonzero) {
-  const long long S = (m + kChunk - 1) / kChunk;
-  const long long G = (ncols + KC - 1) / KC;
-  const long long ntiles = S * G;
+__device__ __forceinline__ void sweep_tile(const double* __restrict__ A, long long lda,
+                                           long long m, long long ncols,
+                                           const double* __restrict__ v,
+                                           double* __restrict__ partial, long long pstride,
+                                           long long s, long long g,
+                                           double (*red)[kCols], unsigned& nonfinite,
+                                           unsigned& nonzero) {
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   constexpr int U = kChunk / (VEC * kThreads);  // element groups per thread per column
@@ -151,10 +151,7 @@ __device__ __forceinline__ void sweep_tiles(const double* __restrict__ A, long l
   // loads in flight per thread, capped at the whole chunk
   constexpr int UB0 = ((VEC == 2) ? 4 : 8) * (kCols / KC);
   constexpr int UB = UB0 < U ? UB0 : U;
-
-  for (long long tile = tile_begin; tile < ntiles; tile += tile_stride) {
-    const long long s = tile / G;
-    const long long g = tile - s * G;
+  {
     const long long row0 = s * kChunk;
     const long long col0 = g * KC;
     const long long rows = (m - row0 < kChunk) ? m - row0 : kChunk;
@@ -381,6 +378,25 @@ __device__ __forceinline__ void sweep_tiles(const double* __restrict__ A, long l
       for (int w = 1; w < kWarps; ++w) sum += red[w][tid];
       partial[s * pstride + col0 + tid] = sum;
     }
+  }
+}
+
+template <int VEC, int MODE, int ALOAD, bool VCOH = false, int KC = kCols, bool FENCE = false>
+__device__ __forceinline__ void sweep_tiles(const double* __restrict__ A, long long lda,
+                                            long long m, long long ncols,
+                                            const double* __restrict__ v,
+                                            double* __restrict__ partial, long long pstride,
+                                            long long tile_begin, long long tile_stride,
+                                            double (*red)[kCols], unsigned& nonfinite,
+                                            unsigned& nonzero) {
+  const long long S = (m + kChunk - 1) / kChunk;
+  const long long G = (ncols + KC - 1) / KC;
+  const long long ntiles = S * G;
+  for (long long tile = tile_begin; tile < ntiles; tile += tile_stride) {
+    const long long s = tile / G;
+    const long long g = tile - s * G;
+    sweep_tile<VEC, MODE, ALOAD, VCOH, KC, FENCE>(A, lda, m, ncols, v, partial, pstride, s, g, red,
+                                                  nonfinite, nonzero);
     __syncthreads();
   }
 }

@@ -396,7 +396,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
   }
   const double eps_R = st->eps_R, tol = st->breakdown_tol;
   const int cfg_reorth = st->cfg_reorth;
-  const long long S = (m + kChunk - 1) / kChunk;
+  // (m, n >= 0: unsigned shifts, cheap to rematerialise in the tile loop)
+  const long long S = (long long)((unsigned long long)(m + kChunk - 1) / kChunk);
   // p_k by step parity: a CTA still in P1 of step k reads p_{k-1} while
   // faster CTAs already write p_k
   auto pbuf = [&](long long kk) { return a.p + (kk & 1) * (a.d_max + 1); };
@@ -404,10 +405,11 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
   // row pairs never straddle two CTAs), processed in kPRows-row blocks
   const long long r_lo = ((m * cta / G) + 1) & ~1LL;
   const long long r_hi = (cta + 1 == G) ? m : (((m * (cta + 1) / G) + 1) & ~1LL);
-  const long long ngx = (n + kCols - 1) / kCols;   // X column groups (finalisation unit)
+  const long long ngx = (long long)((unsigned long long)(n + kCols - 1) / kCols);   // X column groups (finalisation unit)
   constexpr int kXT = XF32 ? 2 * kCols : kCols;    // columns per X tile (fp32: 128 KB tiles)
-  const long long ngt = (n + kXT - 1) / kXT;       // X tile columns
+  const long long ngt = (long long)((unsigned long long)(n + kXT - 1) / kXT);       // X tile columns
   const long long nx = ngt * S;                    // X tiles
+  const double rS = 1.0 / (double)S;
   // X claim index tx (counted after the Y'w1 groups) -> column group g and
   // chunk s; used for the tile and for its P1-readiness wait. Group-major; DIAG
   // puts every group's last chunk at the end instead (measured: weighted loop
@@ -420,12 +422,11 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
       g = (tx < nf) ? tx / (S - 1) : tx - nf;
       s = (tx < nf) ? tx - g * (S - 1) : S - 1;
     } else {
-      // The fenced instantiations (below) divide in 32 bits while nx < 2^32
-      // (a 64-bit division is a long emulated sequence). In the base kernel
-      // the 32-bit form made ptxas split the X batches (C1 +8%), so it
-      // keeps the 64-bit one.
-      constexpr bool kDiv32 = FOLD || SHARD;
-      g = (kDiv32 && nx < (1LL << 32)) ? (long long)((unsigned)tx / (unsigned)S) : tx / S;
+      // tx / S by a double reciprocal and a +-1 fix (exact for tx < 2^52);
+      // an integer division is a long emulated sequence per tile
+      g = (long long)((double)tx * rS);
+      if (g * S > tx) --g;
+      else if ((g + 1) * S <= tx) ++g;
       s = tx - g * S;
     }
   };
@@ -1082,9 +1083,11 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
           // it (sharded, FOLD: FMAs between the loads in SASS); the base
           // kernel issues whole batches without it, and there the fence's
           // later start of the FMAs cost C1 2.5% (batch_fence)
-          sweep_tiles<VEC, MODE_DOT, LOAD_STREAM, true, kCols, SHARD || FOLD>(a.X, a.ldx, m, n, a.w, a.partial, n,
-                                                         s * ngx + g, 1LL << 40, red, dummy_nf,
-                                                         dummy_nz);
+        {
+          sweep_tile<VEC, MODE_DOT, LOAD_STREAM, true, kCols, SHARD || FOLD>(a.X, a.ldx, m, n, a.w, a.partial,
+                                                                          n, s, g, red, dummy_nf, dummy_nz);
+          __syncthreads();
+        }
         mark(7);
         if (DIAG) yay_slices(false);   // this CTA's share of the YAY row, once decided
         if (kFinFirst && npend > 0) finalize_pass(false);
