@@ -161,21 +161,25 @@ __device__ __forceinline__ void sweep_tile(const double* __restrict__ A, long lo
     const double* vr = (MODE == MODE_DOT) ? v + row0 : nullptr;
     if (VEC == 2 && MODE == MODE_DOT && rows == kChunk && col0 + KC <= ncols &&
         lda <= (1LL << 27)) {
-      // full tile (the common case): one base pointer and 32-bit column
-      // offsets keep fewer registers live; same loads and fma order as below
-      const double* A0 = A + col0 * lda + row0;
-      const int ld32 = (int)lda;
+      // full tile (the common case): per batch one base pointer per column,
+      // the batch's element groups at immediate offsets (u * 4 KiB), so a load
+      // costs no address arithmetic (it was ~35% of the loop's issued
+      // instructions: ncu source counters, C2); same loads and fma order as below
+      const double* A0 = A + col0 * lda + row0 + 2 * tid;
+      const double* V0 = vr + 2 * tid;
 #pragma unroll 1
       for (int ub = 0; ub < U; ub += UB) {
         double2 yv[UB];
         double2 xv[UB][KC];
+        const double* Ab = A0 + ub * (2 * kThreads);
+        const double* Vb = V0 + ub * (2 * kThreads);
 #pragma unroll
         for (int u = 0; u < UB; ++u) {
-          const int e = (tid + (ub + u) * kThreads) * 2;
-          yv[u] = VCOH ? __ldcg(reinterpret_cast<const double2*>(vr + e)) : ld_keep2(vr + e);
+          const double* pv = Vb + u * (2 * kThreads);
+          yv[u] = VCOH ? __ldcg(reinterpret_cast<const double2*>(pv)) : ld_keep2(pv);
 #pragma unroll
           for (int c = 0; c < KC; ++c) {
-            const double* pc = A0 + (c * ld32 + e);
+            const double* pc = Ab + c * lda + u * (2 * kThreads);
             xv[u][c] = ALOAD == LOAD_STREAM ? ld_stream2(pc)
                        : ALOAD == LOAD_CG   ? __ldcg(reinterpret_cast<const double2*>(pc))
                                             : ld_keep2(pc);
@@ -362,14 +366,33 @@ __device__ __forceinline__ void sweep_tile(const double* __restrict__ A, long lo
     }
     }   // general path
     // CTA reduction in a fixed order: xor-butterfly in the warp, then warps 0..7.
+    if constexpr (KC == 4) {
+      // the same butterfly tree, transposed: at xor 16 a lane keeps two of
+      // the four columns and receives the partner's copies of them, at xor 8
+      // one, then xor 4, 2, 1 on that column; every sum has the butterfly's
+      // operands in the butterfly's order (x + partner), so the values are the
+      // butterfly's bit for bit, with 6 shuffles per warp instead of 20
+      const bool h16 = (lane & 16) != 0, h8 = (lane & 8) != 0;
+      double k0 = h16 ? acc[2] : acc[0], k1 = h16 ? acc[3] : acc[1];
+      const double g0 = h16 ? acc[0] : acc[2], g1 = h16 ? acc[1] : acc[3];
+      k0 += __shfl_xor_sync(0xffffffffu, g0, 16);
+      k1 += __shfl_xor_sync(0xffffffffu, g1, 16);
+      double kk = h8 ? k1 : k0;
+      const double gg = h8 ? k0 : k1;
+      kk += __shfl_xor_sync(0xffffffffu, gg, 8);
 #pragma unroll
-    for (int c = 0; c < KC; ++c) {
+      for (int off = 4; off > 0; off >>= 1) kk += __shfl_xor_sync(0xffffffffu, kk, off);
+      if ((lane & 7) == 0) red[warp][(h16 ? 2 : 0) + (h8 ? 1 : 0)] = kk;
+    } else {
 #pragma unroll
-      for (int off = 16; off > 0; off >>= 1) acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], off);
-    }
-    if (lane == 0) {
+      for (int c = 0; c < KC; ++c) {
 #pragma unroll
-      for (int c = 0; c < KC; ++c) red[warp][c] = acc[c];
+        for (int off = 16; off > 0; off >>= 1) acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], off);
+      }
+      if (lane == 0) {
+#pragma unroll
+        for (int c = 0; c < KC; ++c) red[warp][c] = acc[c];
+      }
     }
     __syncthreads();
     if (tid < KC && col0 + tid < ncols) {
