@@ -520,23 +520,25 @@ __device__ __forceinline__ void sweep_tiles_f32(const float* __restrict__ A, lon
     if (vec4 && rows == kChunk && col0 + KC <= ncols && lda <= (1LL << 27)) {
       // whole tile in range: batches of UB row groups x KC columns in flight;
       // one base pointer and 32-bit column offsets (fewer live registers)
-      const float* A0 = A + col0 * lda + row0;
-      const int ld32 = (int)lda;
+      // per-column base pointers, element groups at immediate offsets (as in
+      // the fp64 sweep: no per-load address arithmetic)
+      const float* A0 = A + col0 * lda + row0 + 4 * tid;
+      const double* V0 = (MODE == MODE_DOT) ? vr + 4 * tid : nullptr;
 #pragma unroll
       for (int ub = 0; ub < U; ub += UB) {
         float4 xv[UB][KC];
         double2 y0[UB], y1[UB];
 #pragma unroll
         for (int u = 0; u < UB; ++u) {
-          const int e = (tid + (ub + u) * kThreads) * 4;
+          const int eo = (ub + u) * kThreads * 4;
           if constexpr (MODE == MODE_DOT) {
-            y0[u] = ldv(vr + e);
-            y1[u] = ldv(vr + e + 2);
+            y0[u] = ldv(V0 + eo);
+            y1[u] = ldv(V0 + eo + 2);
           } else {
             y0[u] = y1[u] = make_double2(0.0, 0.0);
           }
 #pragma unroll
-          for (int c = 0; c < KC; ++c) xv[u][c] = ld_stream4f(A0 + (c * ld32 + e));
+          for (int c = 0; c < KC; ++c) xv[u][c] = ld_stream4f(A0 + c * lda + eo);
         }
 #pragma unroll
         for (int u = 0; u < UB; ++u)

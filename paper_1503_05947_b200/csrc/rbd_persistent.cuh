@@ -1086,7 +1086,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
         {
           sweep_tile<VEC, MODE_DOT, LOAD_STREAM, true, kCols, SHARD || FOLD>(a.X, a.ldx, m, n, a.w, a.partial,
                                                                           n, s, g, red, dummy_nf, dummy_nz);
-          __syncthreads();
+          // the claim barrier orders `red` for the next tile; a barrier here
+          // only when the finalisation attempt below may read this tile's own
+          // chunk partials (the group's last chunk)
+          if (s == S - 1) __syncthreads();
         }
         mark(7);
         if (DIAG) yay_slices(false);   // this CTA's share of the YAY row, once decided
