@@ -1,6 +1,6 @@
 """A/B of two builds of librbd_b200.so on one workload: alternating decompose
 calls through the bare C ABI (rbd_decompose_device), loop_ms medians.
-Usage: tools/ab_lib.py WORKLOAD LIB_A LIB_B [reps] [d_max]"""
+Usage: tools/ab_lib.py WORKLOAD LIB_A LIB_B [reps] [d_max] [--f32]"""
 import ctypes as C
 import os
 import sys
@@ -12,9 +12,14 @@ import torch  # noqa: E402
 import bench  # noqa: E402
 from paper_1503_05947_b200._lib import Config, Result  # noqa: E402
 
+F32 = "--f32" in sys.argv
+if F32:
+    sys.argv.remove("--f32")
 name, la, lb = sys.argv[1], sys.argv[2], sys.argv[3]
 reps = int(sys.argv[4]) if len(sys.argv) > 4 else 5
 w, X, eps = bench.make_workload(name, torch.device("cuda:0"))
+if F32:   # fp32 storage mode: the same values rounded to float32
+    X = X.float()
 d_max = int(sys.argv[5]) if len(sys.argv) > 5 else w.d_max
 m, n = X.shape
 libs = {}
@@ -22,9 +27,10 @@ for tag, path in (("A", la), ("B", lb)):
     L = C.CDLL(os.path.abspath(path))
     L.rbd_ctx_create.argtypes = [C.c_int, C.POINTER(C.c_void_p)]
     L.rbd_config_default.argtypes = [C.POINTER(Config)]
-    L.rbd_decompose_device.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64,
-                                       C.POINTER(Config), C.c_void_p, C.c_void_p, C.c_void_p,
-                                       C.c_void_p, C.POINTER(Result)]
+    for fn in ("rbd_decompose_device", "rbd_decompose_device_f32"):
+        getattr(L, fn).argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64,
+                                   C.POINTER(Config), C.c_void_p, C.c_void_p, C.c_void_p,
+                                   C.c_void_p, C.POINTER(Result)]
     h = C.c_void_p()
     assert L.rbd_ctx_create(0, C.byref(h)) == 0
     libs[tag] = (L, h)
@@ -41,7 +47,7 @@ sels = {}
 for it in range(reps + 1):
     for tag, (L, h) in libs.items():
         r = Result()
-        rc = L.rbd_decompose_device(h, C.c_void_p(X.data_ptr()), m, n, X.stride(1), C.byref(cfg),
+        rc = (L.rbd_decompose_device_f32 if F32 else L.rbd_decompose_device)(h, C.c_void_p(X.data_ptr()), m, n, X.stride(1), C.byref(cfg),
                                     C.c_void_p(Y.data_ptr()), C.c_void_p(T.data_ptr()),
                                     sel.ctypes.data_as(C.c_void_p), hist.ctypes.data_as(C.c_void_p),
                                     C.byref(r))
@@ -49,7 +55,7 @@ for it in range(reps + 1):
         if it:
             out[tag].append(r.loop_ms)
         sels[tag] = sel[:r.d].copy()
-xb = m * n * 8
+xb = m * n * (4 if F32 else 8)
 for tag in ("A", "B"):
     ms = float(np.median(out[tag]))
     print(f"{name} {tag} ({os.path.basename(sys.argv[2 if tag == 'A' else 3])}): loop {ms:9.3f} ms "
