@@ -466,7 +466,54 @@ __device__ __forceinline__ bool is_nonfinite_f(float x) {
 // fp64 tile's bytes, loaded as two batches of 16 float4 per thread — row
 // groups 0-1 then 2-3 — so per-tile costs are amortised as in fp64). A
 // column's sum does not depend on KC.
-template <int MODE, bool VCOH = false, int KC = kCols>
+// Warp + CTA column reduction of sweep_tiles_f32 (KC = 4 or 8): the xor
+// butterfly (16, 8, 4, 2, 1) transposed as in sweep_tile: at xor 16 a lane
+// keeps half of the columns and receives its partner's copies of them, at
+// xor 8 a quarter, ..., down to one column, then xor 2/1 on it. Every sum has
+// the butterfly's operands in its order (mine + partner), so the values are
+// the plain butterfly's bit for bit, with 9 shuffles per warp for 8 columns
+// instead of 40 (4 columns: 6 instead of 20). Lanes (lane & (32/KC - 1)) == 0
+// write red[warp][column].
+template <int KC>
+__device__ __forceinline__ void warp_cols_to_red(const double (&acc)[KC], double (*red)[KC],
+                                                 int lane, int warp) {
+  static_assert(KC == 4 || KC == 8, "transposed butterfly: 4 or 8 columns");
+  const bool h16 = (lane & 16) != 0, h8 = (lane & 8) != 0;
+  double k4[KC / 2];
+#pragma unroll
+  for (int i = 0; i < KC / 2; ++i) {
+    const double send = h16 ? acc[i] : acc[KC / 2 + i];
+    k4[i] = (h16 ? acc[KC / 2 + i] : acc[i]) + __shfl_xor_sync(0xffffffffu, send, 16);
+  }
+  double k2[KC / 4];
+#pragma unroll
+  for (int i = 0; i < KC / 4; ++i) {
+    const double send = h8 ? k4[i] : k4[KC / 4 + i];
+    k2[i] = (h8 ? k4[KC / 4 + i] : k4[i]) + __shfl_xor_sync(0xffffffffu, send, 8);
+  }
+  double q;
+  int col;
+  if constexpr (KC == 8) {
+    const bool h4 = (lane & 4) != 0;
+    const double send = h4 ? k2[0] : k2[1];
+    q = (h4 ? k2[1] : k2[0]) + __shfl_xor_sync(0xffffffffu, send, 4);
+    q += __shfl_xor_sync(0xffffffffu, q, 2);
+    q += __shfl_xor_sync(0xffffffffu, q, 1);
+    col = (h16 ? 4 : 0) + (h8 ? 2 : 0) + (h4 ? 1 : 0);
+    if ((lane & 3) == 0) red[warp][col] = q;
+  } else {
+    q = k2[0];
+#pragma unroll
+    for (int off = 4; off > 0; off >>= 1) q += __shfl_xor_sync(0xffffffffu, q, off);
+    col = (h16 ? 2 : 0) + (h8 ? 1 : 0);
+    if ((lane & 7) == 0) red[warp][col] = q;
+  }
+}
+
+// TRAIL = false: no barrier after the partials are written (single-tile calls
+// from the persistent loop, whose claim barrier orders `red` for the next
+// tile; the caller adds one where a finalisation may read these partials).
+template <int MODE, bool VCOH = false, int KC = kCols, bool TRAIL = true>
 __device__ __forceinline__ void sweep_tiles_f32(const float* __restrict__ A, long long lda,
                                                 long long m, long long ncols,
                                                 const double* __restrict__ v,
@@ -579,15 +626,7 @@ __device__ __forceinline__ void sweep_tiles_f32(const float* __restrict__ A, lon
       }
     }
     // CTA reduction in a fixed order: xor-butterfly in the warp, then warps 0..7.
-#pragma unroll
-    for (int c = 0; c < KC; ++c) {
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], off);
-    }
-    if (lane == 0) {
-#pragma unroll
-      for (int c = 0; c < KC; ++c) red[warp][c] = acc[c];
-    }
+    warp_cols_to_red<KC>(acc, red, lane, warp);
     __syncthreads();
     if (tid < KC && col0 + tid < ncols) {
       double sum = red[0][tid];
@@ -595,7 +634,7 @@ __device__ __forceinline__ void sweep_tiles_f32(const float* __restrict__ A, lon
       for (int w = 1; w < kWarps; ++w) sum += red[w][tid];
       partial[s * pstride + col0 + tid] = sum;
     }
-    __syncthreads();
+    if constexpr (TRAIL) __syncthreads();
   }
 }
 

@@ -1076,8 +1076,12 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
           sweep_tile_dot2<VEC, LOAD_STREAM, true, 2>(a.X, a.ldx, m, n, a.w, a.aw, a.partial,
                                                      a.partial2, n, s * ngx + g, red2);
         else if constexpr (XF32)   // g: an 8-column tile = finalisation groups 2g, 2g+1
-          sweep_tiles_f32<MODE_DOT, true, kXT>(a.Xf, a.ldx, m, n, a.w, a.partial, n, s * ngt + g,
-                                               1LL << 40, red2, dummy_nf, dummy_nz, a.xvec4 != 0);
+        {
+          sweep_tiles_f32<MODE_DOT, true, kXT, false>(a.Xf, a.ldx, m, n, a.w, a.partial, n,
+                                                      s * ngt + g, 1LL << 40, red2, dummy_nf,
+                                                      dummy_nz, a.xvec4 != 0);
+          if (s == S - 1) __syncthreads();   // as below: only before a finalisation of this chunk
+        }
         else
           // the load-batch fence keeps each X batch whole where ptxas split
           // it (sharded, FOLD: FMAs between the loads in SASS); the base
