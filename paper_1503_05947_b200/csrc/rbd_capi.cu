@@ -363,11 +363,13 @@ long long fold_kmax(int grid) {
 // loop (RBD_YDELAY overrides, in tiles): half a wave lets the first claimers
 // stream X instead of waiting for the slowest CTA's P1. Measured (A/B in one
 // process, tools/ab_env.py): C1 46.18 -> 45.89 ms at grid/2, 46.09 at one
-// wave, 46.46 at two; C2 unchanged (2930.8 / 2931.0 / 2933.3 ms); the fp32
-// loop slower (33.81 -> 34.11 ms at one wave), so it keeps 0.
+// wave, 46.46 at two; C2 unchanged (2930.8 / 2931.0 / 2933.3 ms). The fp32
+// loop, once its tiles lost the trailing barrier (tools/ab_arms.py --f32):
+// C1 31.40 -> 31.13 ms at grid/2, 31.61 at one wave; C2 unchanged.
 long long y_delay(int grid, bool xf32) {
   if (const char* e = getenv("RBD_YDELAY")) return atoll(e);
-  return xf32 ? 0 : grid / 2;
+  (void)xf32;
+  return grid / 2;
 }
 
 // Materialise a pending column / clear the pending flag (used after the loop).

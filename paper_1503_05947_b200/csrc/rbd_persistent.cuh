@@ -722,8 +722,14 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
     // (before or after the tile's own group is queued): measured per loop,
     // C1 fp64 46.3 -> 46.1 ms and weighted 55.8 -> 55.3 ms with (2, after);
     // the fp32 loop keeps (4, before): 33.8 ms against 34.6 ms
-    constexpr int kPend = XF32 ? 4 : 2;
-    constexpr bool kFinFirst = XF32;
+#ifndef RBD_F32_PEND
+#define RBD_F32_PEND 4
+#endif
+#ifndef RBD_F32_FINFIRST
+#define RBD_F32_FINFIRST 1
+#endif
+    constexpr int kPend = XF32 ? RBD_F32_PEND : 2;
+    constexpr bool kFinFirst = XF32 && RBD_F32_FINFIRST;
     long long pend[kPend];
 #pragma unroll
     for (int i = 0; i < kPend; ++i) pend[i] = -1;
