@@ -1076,8 +1076,11 @@ __global__ void __launch_bounds__(kThreads, 2) k_rbd_persistent(PersistArgs a) {
         long long g, s;
         x_tile(code, g, s);
         if constexpr (DIAG && VEC == 2)
-          sweep_tile_dot2_sv(a.X, a.ldx, m, n, a.w, a.aw, a.partial, a.partial2, n, s * ngx + g,
-                             red2, svec);
+        {
+          sweep_tile_dot2_sv<LOAD_STREAM, kSvUB, false>(a.X, a.ldx, m, n, a.w, a.aw, a.partial,
+                                                        a.partial2, n, s, g, red2, svec);
+          if (s == S - 1) __syncthreads();   // only before a finalisation of this chunk
+        }
         else if constexpr (DIAG)
           sweep_tile_dot2<VEC, LOAD_STREAM, true, 2>(a.X, a.ldx, m, n, a.w, a.aw, a.partial,
                                                      a.partial2, n, s * ngx + g, red2);

@@ -180,19 +180,23 @@ __device__ __forceinline__ void sweep_tile_dot2(const double* __restrict__ A, lo
 // sweep_tile_dot2, hence the same bits. sv: [UB][2][kThreads] double2.
 constexpr int kSvUB = 4;
 constexpr int kSvBytes = kSvUB * 2 * kThreads * 16;   // 32 KiB per CTA
-template <int ALOAD = LOAD_STREAM, int UB = kSvUB>
+// The persistent loop passes the tile as (chunk s, group g) — no 64-bit
+// division per tile — and TRAIL = false: its claim barrier orders `red` for the
+// next tile, and it adds a barrier itself where a finalisation may read these
+// partials. The two 4-column reductions run as one transposed 8-way butterfly
+// (warp_cols_to_red: 9 shuffles per warp instead of 40, the same sums bit for
+// bit).
+template <int ALOAD = LOAD_STREAM, int UB = kSvUB, bool TRAIL = true>
 __device__ __forceinline__ void sweep_tile_dot2_sv(const double* __restrict__ A, long long lda,
                                                    long long m, long long ncols,
                                                    const double* __restrict__ v,
                                                    const double* __restrict__ v2,
                                                    double* __restrict__ partial,
                                                    double* __restrict__ partial2, long long pstride,
-                                                   long long tile, double (*red)[2 * kCols],
+                                                   long long s, long long g,
+                                                   double (*red)[2 * kCols],
                                                    double2* __restrict__ sv) {
   constexpr int VEC = 2;
-  const long long G = (ncols + kCols - 1) / kCols;
-  const long long s = tile / G;
-  const long long g = tile - s * G;
   const long long row0 = s * kChunk;
   const long long col0 = g * kCols;
   const long long rows = (m - row0 < kChunk) ? m - row0 : kChunk;
@@ -252,19 +256,14 @@ __device__ __forceinline__ void sweep_tile_dot2_sv(const double* __restrict__ A,
       }
     }
   }
-#pragma unroll
-  for (int c = 0; c < kCols; ++c)
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], off);
-      acc2[c] += __shfl_xor_sync(0xffffffffu, acc2[c], off);
-    }
-  if (lane == 0) {
+  {
+    double acc8[2 * kCols];
 #pragma unroll
     for (int c = 0; c < kCols; ++c) {
-      red[warp][c] = acc[c];
-      red[warp][kCols + c] = acc2[c];
+      acc8[c] = acc[c];
+      acc8[kCols + c] = acc2[c];
     }
+    warp_cols_to_red<2 * kCols>(acc8, red, lane, warp);
   }
   __syncthreads();
   if (tid < 2 * kCols) {
@@ -276,7 +275,7 @@ __device__ __forceinline__ void sweep_tile_dot2_sv(const double* __restrict__ A,
       (tid < kCols ? partial : partial2)[s * pstride + col0 + c] = sum;
     }
   }
-  __syncthreads();
+  if constexpr (TRAIL) __syncthreads();
 }
 
 // One X pass for both new rows: T row partials (xi . x_j, decompose.cpp:93) and
