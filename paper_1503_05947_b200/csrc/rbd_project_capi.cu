@@ -4,6 +4,7 @@
 #include "rbd_capi_internal.h"
 #include "rbd_project.cuh"
 #include "rbd_project_tc.cuh"
+#include "rbd_project_tc2.cuh"
 #include "rbd_classify.cuh"
 #include "rbd_compress_dmma.cuh"
 #include "rbd_project_dmma_tma.cuh"
@@ -451,8 +452,13 @@ int rbd_project_batch_f32(rbd_ctx_t ctx, const float* dY, int64_t m, int64_t d, 
   static bool attr = false;
   if (!attr) {
     CU(cudaFuncSetAttribute(k_project_tf32x3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTcSmem));
+    CU(cudaFuncSetAttribute(k_project_tf32x3_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTc2Smem));
     attr = true;
   }
+  // CTA-pair kernel (tcgen05 cta_group::2, 256 x 256 tile per two SMs) once both
+  // tile sides are used beyond a single CTA's 128; RBD_K6_PAIR=0/1 overrides
+  bool pair = d > kTcBM && N > kTcBN;
+  if (const char* e = getenv("RBD_K6_PAIR")) pair = atoi(e) != 0;
   double* xn = nullptr;
   if (d_err) {
     TRY(ensure(ctx->scratch1, sizeof(double) * (size_t)std::max<int64_t>(N, 32)));
@@ -460,20 +466,23 @@ int rbd_project_batch_f32(rbd_ctx_t ctx, const float* dY, int64_t m, int64_t d, 
   }
   // split-K over the k-blocks for the best-filled waves (1 CTA per SM): 2 for C4's 4 x 128 tiles
   const long long nk = cdiv(m, kTcBK);
-  const long long ctas = cdiv(d, kTcBM) * cdiv(N, kTcBN);
+  // (pair: units are clusters, nsm / 2 of them per wave)
+  const long long ctas = pair ? cdiv(d, 2 * kTcBM) * cdiv(N, kTc2BN) : cdiv(d, kTcBM) * cdiv(N, kTcBN);
+  const long long slots = pair ? std::max(ctx->nsm / 2, 1) : ctx->nsm;
   int sk = 1;
   {
     double best_eff = 0.0;
     for (int s = 1; s <= 4; ++s) {
       if (s > 1 && nk / s < 64) break;
-      const long long c = ctas * s, waves = cdiv(c, ctx->nsm);
-      const double eff = (double)c / (double)(waves * ctx->nsm);
+      const long long c = ctas * s, waves = cdiv(c, slots);
+      const double eff = (double)c / (double)(waves * slots);
       if (s == 1 || eff > best_eff + 0.02) {
         sk = s;
         best_eff = eff;
       }
     }
   }
+  if (const char* e = getenv("RBD_K6_SPLITK")) sk = (int)std::min<long long>(std::max(atoi(e), 1), nk);
   const int kb_per = (int)cdiv(nk, sk);
   sk = (int)cdiv(nk, kb_per);   // every split gets at least one k-block
   float* Tws = nullptr;
@@ -484,9 +493,15 @@ int rbd_project_batch_f32(rbd_ctx_t ctx, const float* dY, int64_t m, int64_t d, 
     Tws = ptr<float>(ctx->pj_ws);
     xws = reinterpret_cast<double*>(reinterpret_cast<char*>(ctx->pj_ws.p) + ((tbytes + 15) & ~(size_t)15));
   }
-  dim3 grid((unsigned)cdiv(d, kTcBM), (unsigned)cdiv(N, kTcBN), (unsigned)sk);
-  k_project_tf32x3<<<grid, kTcThreads, kTcSmem, ctx->stream>>>(mY, mX, m, d, N, dTn, xn, kb_per,
-                                                                Tws, xws);
+  if (pair) {
+    dim3 grid((unsigned)(2 * cdiv(d, 2 * kTcBM)), (unsigned)cdiv(N, kTc2BN), (unsigned)sk);
+    k_project_tf32x3_pair<<<grid, kTcThreads, kTc2Smem, ctx->stream>>>(mY, mX, m, d, N, dTn, xn, kb_per,
+                                                                        Tws, xws);
+  } else {
+    dim3 grid((unsigned)cdiv(d, kTcBM), (unsigned)cdiv(N, kTcBN), (unsigned)sk);
+    k_project_tf32x3<<<grid, kTcThreads, kTcSmem, ctx->stream>>>(mY, mX, m, d, N, dTn, xn, kb_per,
+                                                                  Tws, xws);
+  }
   ctx->launches++;
   CU(cudaGetLastError());
   if (sk > 1) {

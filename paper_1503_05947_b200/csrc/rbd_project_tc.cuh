@@ -8,10 +8,17 @@
 // D += A_hi B_hi + A_hi B_lo + A_lo B_hi recovers ~fp32 accuracy; only the lo
 // tiles are computed (by the converter warps, in shared memory).
 //
-// CTA: 6 warps. warp 0 = TMA producer, warp 1 = TMEM owner + MMA issuer,
-// warps 2-5 = converters (lo tiles, ||x_j||^2 in fp64) and then the epilogue
-// (tcgen05.ld of their TMEM lane quarter, warp_id % 4). Tile 128 (l) x 128 (j),
-// K = 32 fp32 rows (one 128-byte swizzle row) per stage, 3 stages.
+// CTA: 12 warps. warp 0 = TMA producer, warp 1 = TMEM owner + MMA issuer,
+// warps 2-9 = converters (lo tiles) and then the epilogue (tcgen05.ld of their
+// TMEM lane quarter, warp_id % 4, one column half each), warps 10-13 = the
+// ||x_j||^2 accumulation in fp64 (Eq. 3), in the CTAs of the first l-tile row
+// only. Tile 128 (l) x 128 (j), K = 32 fp32 rows (one 128-byte swizzle row)
+// per stage, 3 stages.
+// Eight converter warps and the norms in warps of their own: ncu showed the
+// converters, not the tensor pipe or shared memory, pacing a k-block (four
+// warps doing the split AND the fp32->fp64 widening + DFMA chains stalled
+// 6-13 cycles per issued instruction); off the converters' path the norms
+// only have to finish within a k-block's tensor time.
 #pragma once
 
 #include <cuda.h>
@@ -24,7 +31,10 @@ constexpr int kTcBM = 128;
 constexpr int kTcBN = 128;
 constexpr int kTcBK = 32;            // fp32 per 128-byte row
 constexpr int kTcStages = 3;
-constexpr int kTcThreads = 192;
+constexpr int kTcConvWarps = 8;
+constexpr int kTcXnWarps = 4;
+constexpr int kTcXnRows = kTcBN / (32 * kTcXnWarps);   // B rows per norm thread
+constexpr int kTcThreads = 64 + 32 * kTcConvWarps + 32 * kTcXnWarps;   // 448
 constexpr int kTcTileBytes = kTcBM * kTcBK * 4;   // 16 KiB (A and B tiles are both 128 x 32)
 // smem per stage: A raw, A lo, B raw, B lo
 constexpr int kTcStageBytes = 4 * kTcTileBytes;
@@ -122,6 +132,46 @@ __device__ __forceinline__ float tf32_lo(float x) {
   return x - hi;                                                        // exact in fp32
 }
 
+// Converter thread t (0..255) of a stage: row r = t % 128 of the A tile and of
+// the B tile, 16-byte chunks 4h..4h+3 (h = t / 128) of the row's 128 bytes: lo
+// tiles written beside the raw ones.
+__device__ __forceinline__ void tc_convert_half_rows(const uint8_t* A, uint8_t* Alo, const uint8_t* B, uint8_t* Blo,
+                                                     int r, int h) {
+  const float4* ar = reinterpret_cast<const float4*>(A + r * 128);
+  float4* alo = reinterpret_cast<float4*>(Alo + r * 128);
+  const float4* br = reinterpret_cast<const float4*>(B + r * 128);
+  float4* blo = reinterpret_cast<float4*>(Blo + r * 128);
+#pragma unroll
+  for (int cc = 0; cc < 4; ++cc) {
+    // same chunk position in raw and lo tiles; rotated per lane so the 8
+    // lanes of a 128-byte phase hit 8 different bank groups
+    const int c = (cc + 4 * h + r) & 7;
+    const float4 a = ar[c];
+    alo[c] = make_float4(tf32_lo(a.x), tf32_lo(a.y), tf32_lo(a.z), tf32_lo(a.w));
+    const float4 b = br[c];
+    blo[c] = make_float4(tf32_lo(b.x), tf32_lo(b.y), tf32_lo(b.z), tf32_lo(b.w));
+  }
+}
+
+// ||x_j||^2 thread u of a stage: rows u + 32 kTcXnWarps rr of the raw B tile
+// (columns j of X_new), each accumulated in four fp64 chains (the float4
+// components) over the row's eight 16-byte chunks in rotated order.
+__device__ __forceinline__ void tc_xnorm_rows(const uint8_t* B, int u, double (*xn)[4]) {
+#pragma unroll
+  for (int rr = 0; rr < kTcXnRows; ++rr) {
+    const int r = u + 32 * kTcXnWarps * rr;
+    const float4* br = reinterpret_cast<const float4*>(B + r * 128);
+#pragma unroll
+    for (int cc = 0; cc < 8; ++cc) {
+      const float4 b = br[(cc + r) & 7];
+      xn[rr][0] = fma((double)b.x, (double)b.x, xn[rr][0]);
+      xn[rr][1] = fma((double)b.y, (double)b.y, xn[rr][1]);
+      xn[rr][2] = fma((double)b.z, (double)b.z, xn[rr][2]);
+      xn[rr][3] = fma((double)b.w, (double)b.w, xn[rr][3]);
+    }
+  }
+}
+
 // split-K: blockIdx.z takes k-blocks [z * kb_per, min(nk, (z + 1) * kb_per)) (at
 // least one); split 0 writes Tn / xnorm2, split z > 0 its workspace slices
 // (Tws + (z-1) d N, xws + (z-1) N), added in order by k_splitk_sum_f32.
@@ -148,11 +198,12 @@ static __global__ void __launch_bounds__(kTcThreads, 1)
     if (xnorm2) xnorm2 = xws + (long long)(blockIdx.z - 1) * N;
   }
 
+  const bool want_xn = xnorm2 != nullptr && blockIdx.x == 0;   // one l-tile row computes ||x_j||^2
   if (threadIdx.x == 0) {
     for (int s = 0; s < kTcStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&conv[s], 128);
-      mbar_init(&empty[s], 1);
+      mbar_init(&conv[s], kTcConvWarps);   // one arrival per converter warp
+      mbar_init(&empty[s], want_xn ? 1 + kTcXnWarps : 1);   // MMA commit (+ the norm warps)
     }
     mbar_init(tmem_full, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -216,45 +267,44 @@ static __global__ void __launch_bounds__(kTcThreads, 1)
       }
       umma_commit(tmem_full);
     }
+  } else if (warp >= 2 + kTcConvWarps) {
+    // ---------------- ||x_j||^2 in fp64 (warps 10-13, first l-tile row only) ----------------
+    if (want_xn) {
+      const int u = threadIdx.x - 32 * (2 + kTcConvWarps);   // norm thread
+      double xn[kTcXnRows][4] = {};
+      for (int kb = 0; kb < nk; ++kb) {
+        const int s = kb % kTcStages;
+        const uint32_t ph = (kb / kTcStages) & 1;
+        mbar_wait(&full[s], ph);
+        tc_xnorm_rows(stageB(s), u, xn);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);   // this warp is done with the stage's raw B tile
+      }
+#pragma unroll
+      for (int rr = 0; rr < kTcXnRows; ++rr)
+        if (j0 + u + 32 * kTcXnWarps * rr < N) xnorm2[j0 + u + 32 * kTcXnWarps * rr] = (xn[rr][0] + xn[rr][1]) + (xn[rr][2] + xn[rr][3]);
+    }
   } else {
-    // ---------------- converters (warps 2-5): lo tiles, ||x_j||^2 (fp64) ----------------
-    const int r = threadIdx.x - 64;   // 0..127: row r of the A tile and of the B tile
-    double xn0 = 0.0, xn1 = 0.0, xn2 = 0.0, xn3 = 0.0;   // four chains (fixed combination)
+    // ---------------- converters (warps 2-9): lo tiles ----------------
+    const int t = threadIdx.x - 64;   // 0..255
+    const int r = t & 127, h = t >> 7;
     for (int kb = 0; kb < nk; ++kb) {
       const int s = kb % kTcStages;
       const uint32_t ph = (kb / kTcStages) & 1;
       mbar_wait(&full[s], ph);
-      const float4* ar = reinterpret_cast<const float4*>(stageA(s) + r * 128);
-      float4* alo = reinterpret_cast<float4*>(stageAlo(s) + r * 128);
-      const float4* br = reinterpret_cast<const float4*>(stageB(s) + r * 128);
-      float4* blo = reinterpret_cast<float4*>(stageBlo(s) + r * 128);
-#pragma unroll
-      for (int cc = 0; cc < 8; ++cc) {
-        // same chunk position in raw and lo tiles; rotated per lane so the 8
-        // lanes of a 128-byte phase hit 8 different bank groups
-        const int c = (cc + r) & 7;
-        const float4 a = ar[c];
-        alo[c] = make_float4(tf32_lo(a.x), tf32_lo(a.y), tf32_lo(a.z), tf32_lo(a.w));
-        const float4 b = br[c];
-        blo[c] = make_float4(tf32_lo(b.x), tf32_lo(b.y), tf32_lo(b.z), tf32_lo(b.w));
-        xn0 = fma((double)b.x, (double)b.x, xn0);
-        xn1 = fma((double)b.y, (double)b.y, xn1);
-        xn2 = fma((double)b.z, (double)b.z, xn2);
-        xn3 = fma((double)b.w, (double)b.w, xn3);
-      }
+      tc_convert_half_rows(stageA(s), stageAlo(s), stageB(s), stageBlo(s), r, h);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic -> async proxy
-      mbar_arrive(&conv[s]);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&conv[s]);
     }
-    const double xn = (xn0 + xn1) + (xn2 + xn3);
-    if (xnorm2 != nullptr && blockIdx.x == 0 && j0 + r < N) xnorm2[j0 + r] = xn;
-    // ---------------- epilogue: TMEM -> registers -> T_new ----------------
     mbar_wait(tmem_full, 0);
     asm volatile("tcgen05.fence::after_thread_sync;");
+    // ---------------- epilogue: TMEM -> registers -> T_new ----------------
     const int q = warp & 3;                 // TMEM lane quarter of this warp
     const int row = q * 32 + lane;          // accumulator row = basis index l0 + row
     const long long l = l0 + row;
 #pragma unroll 1
-    for (int c0 = 0; c0 < kTcBN; c0 += 32) {
+    for (int c0 = h * (kTcBN / 2); c0 < (h + 1) * (kTcBN / 2); c0 += 32) {   // this warp's column half
       uint32_t v[32];
       const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c0;
       asm volatile(
