@@ -414,7 +414,7 @@ def secondary_c4(rbd, ctx, dev, stream, args):
     k6 = e0.elapsed_time(e1) / 3
     out["device_fp64"] = {"kernel": "K5 k_project_dmma (FP64 DMMA) + Eq. 3", "ms_per_batch": k5,
                           "tflops": flops / (k5 / 1e3) / 1e12}
-    out["device_fp32"] = {"kernel": "K6 k_project_tf32x3 (tcgen05 kind::tf32, 3xTF32) + Eq. 3",
+    out["device_fp32"] = {"kernel": "K6 k_project_tf32x3_pair (tcgen05 cta_group::2 kind::tf32, 3xTF32, 256x256 tile per CTA pair) + Eq. 3",
                           "ms_per_batch": k6, "tflops_fp32_equivalent": flops / (k6 / 1e3) / 1e12}
     # e2e: the pinned host stream through the resident model
     for f32, dt, tdt in ((False, torch.float64, np.float64), (True, torch.float32, np.float32)):

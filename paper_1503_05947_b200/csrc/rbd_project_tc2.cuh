@@ -1,15 +1,17 @@
 // rbd_project_tc2.cuh — K6 on a CTA pair: T_new = Y' X_new (fp32, 3xTF32) with
 // tcgen05.mma.cta_group::2, one 256 (l) x 256 (j) tile per two-SM cluster.
 //
-// Why a pair: the single-CTA kernel (rbd_project_tc.cuh, 128 x 128 tile) is
-// bound by shared-memory bandwidth, not by the tensor pipe. Per 32-row k-block
-// it moves 192 KB through shared memory (TMA writes 32 KB, the lo-tile
-// converters read and write 64 KB, and the twelve 128x128x8 MMAs read 8 KB of
-// operands each) at 128 B/clk: 1500 clk for 768 clk of tensor work, i.e. the
-// ~50 % tensor-pipe activity ncu showed. With cta_group::2 each CTA supplies
-// its 128 rows of A (Y) and only HALF of B (128 of the 256 X_new columns), and
-// a 256x256x8 MMA takes 128 clk per SM: the same 192 KB per k-block now feeds
-// 1536 clk of tensor work.
+// Why a pair: per 32-row k-block the single-CTA kernel (rbd_project_tc.cuh,
+// 128 x 128 tile) moves 192 KB through shared memory (TMA writes 32 KB, the
+// lo-tile converters read and write 64 KB, the twelve 128x128x8 MMAs read 8 KB
+// of operands each) for 768 clk of tensor work at 128 B/clk. With
+// cta_group::2 each CTA supplies its 128 rows of A (Y) and only HALF of B (128
+// of the 256 X_new columns), and a 256x256x8 MMA takes 128 clk per SM: the
+// same 192 KB per k-block feeds 1536 clk of tensor work. ncu on the C4 batch
+// (profiles/r02k6f_*): shared-memory pipe 60 % -> 34 % of peak, tensor pipe
+// 57 % -> 72 % of active cycles, 5.64 -> 4.78 ms with the error indicator.
+// (A 4-deep raw ring + 2-deep lo ring in the same 192 KB measured the same:
+// at this tensor load the clocks sit under the power cap.)
 //
 // Per CTA (rank r of the pair): A rows l0p + 128 r .. +127 (raw + lo tiles),
 // B rows j0p + 128 r .. +127 (raw + lo), accumulator rows 128 r .. of D in its

@@ -34,5 +34,9 @@ ws = rbd.Workspace(torch.from_numpy(np.asfortranarray(rng.standard_normal((200, 
 Y = torch.linalg.qr(torch.randn(1024, 128, device="cuda"))[0].float().t().contiguous().t()
 X = torch.randn(256, 1024, device="cuda", dtype=torch.float32).t()
 rbd.project_batch_f32(Y, X)
+# CTA-pair kernel (d > 128 and N > 128), partial pair tiles in both
+Y2 = torch.linalg.qr(torch.randn(1024, 300, device="cuda"))[0].float().t().contiguous().t()
+X2 = torch.randn(300, 1024, device="cuda", dtype=torch.float32).t()
+rbd.project_batch_f32(Y2, X2)
 torch.cuda.synchronize()
 print("sanitize smoke ok")
