@@ -556,6 +556,13 @@ def run_b200(args):
                                           "Y passes and bookkeeping not credited",
                 "ms_per_launch": loop_mean, "loop_share_of_step": loop_mean / (ms / args.steps),
                 "peak_source": peak_src, "traffic_source": traffic.get("source")}
+    # DRAM rate of the loop = the ncu capture's bytes per launch / this run's
+    # launch time (context only: `frac` above is the algorithmic one)
+    if traffic.get("bytes_per_launch") and abs(d_mean - w.d_max) < 0.5:
+        dr = traffic["bytes_per_launch"] / (loop_mean / 1e3) / 1e9
+        roofline["dram"] = {"gbs": dr, "frac_of_peak": dr / peak,
+                            "note": "ncu dram bytes per launch (traffic) / this run's ms_per_launch: "
+                                    "what the HBM moves, X plus the uncredited Y passes"}
     # the fused sweep phase alone, as a standalone kernel (K2), CUDA events
     y = torch.randn(m, dtype=torch.float64, device=dev)
     y /= y.norm()
