@@ -459,6 +459,29 @@ int rbd_project_batch_f32(rbd_ctx_t ctx, const float* dY, int64_t m, int64_t d, 
   // tile sides are used beyond a single CTA's 128; RBD_K6_PAIR=0/1 overrides
   bool pair = d > kTcBM && N > kTcBN;
   if (const char* e = getenv("RBD_K6_PAIR")) pair = atoi(e) != 0;
+  if (pair) {
+    // a device (or partition) that cannot co-schedule a two-CTA cluster of this
+    // kernel takes the single-CTA kernel instead
+    static int pair_ok = -1;
+    if (pair_ok < 0) {
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(2, 1, 1);
+      cfg.blockDim = dim3(kTcThreads, 1, 1);
+      cfg.dynamicSmemBytes = kTc2Smem;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = 2;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      int nclusters = 0;
+      const cudaError_t ce = cudaOccupancyMaxActiveClusters(&nclusters, k_project_tf32x3_pair, &cfg);
+      if (ce != cudaSuccess) cudaGetLastError();
+      pair_ok = (ce == cudaSuccess && nclusters > 0) ? 1 : 0;
+    }
+    pair = pair_ok == 1;
+  }
   double* xn = nullptr;
   if (d_err) {
     TRY(ensure(ctx->scratch1, sizeof(double) * (size_t)std::max<int64_t>(N, 32)));
